@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark of the Nievergelt slice-map path (BASELINE.json metric: ODE trajectory-steps/s and
+time-to-solution at 1/2/4/8 B200 vs the CPU reference).
+
+Workload (BASELINE.json configs[1]): linear ODE system from the semi-discretised 1-D heat
+equation, n = 128 interior points (dx = 1/129), T = 10, affine propagator per slice from n+1
+basis trajectories, matrix-product (tree) composition. 256 slices x 256 backward-Euler steps per
+GPU (weak scaling: N = 256 x n_gpus slices, dt = T / (N S)). One "step" = one full solve:
+per-step factor tables -> all slice maps (K3) -> log-depth tree compose (K4) -> y = G y0 + c,
+plus, for n_gpus > 1, the NCCL gather of the composed block maps and the root's ordered apply.
+
+  python bench.py [--gpus N --steps K --warmup W]            # this implementation
+  python bench.py --impl reference [...]                     # the reference CPU path (oracle/_ref)
+
+value: trajectory-steps/s with tables resident in HBM (device events, L2 flushed between steps).
+e2e:   the same metric through the host-buffer C-ABI call pint_run_heat (N=1) / the sharded
+       host path (N>1): host tables + H2D + device + D2H of the final state, wall clock.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import shutil
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "ODE trajectory-steps/s (heat n=128 affine slice maps + tree compose)"
+UNIT = "traj-steps/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=128, help="interior points (dx = 1/(n+1))")
+    p.add_argument("--slices-per-gpu", type=int, default=256)
+    p.add_argument("--S", type=int, default=256, help="backward-Euler steps per slice")
+    p.add_argument("--T", type=float, default=10.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def flops_per_slice_step(n: int) -> int:
+    """Algorithmic FP64 flops of one slice-step of the map build: per column the
+    Thomas forward sweep (1 div on row 0, then mul+sub+div) and back sweep (mul+sub) = 5n-4,
+    over n+1 columns, plus the forcing column's 5 flops per row."""
+    return (n + 1) * (5 * n - 4) + 5 * n
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        if not shutil.which("nvidia-smi"):
+            return
+        self.proc = subprocess.Popen(
+            ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+             "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def ref_tool():
+    p = ROOT / "oracle" / "_ref" / "ref_tool"
+    return p if p.exists() else None
+
+
+def run_reference_cpu(n, N, S, T, reps, workers=None):
+    """Time the UNMODIFIED reference (oracle/_ref/ref_tool -> pint::run_nievergelt) on host cores."""
+    tool = ref_tool()
+    if tool is None:
+        return None
+    workers = workers or os.cpu_count() or 1
+    cmd = [str(tool), "bench-heat", "--n", str(n), "--N", str(N), "--S", str(S), "--T", repr(T),
+           "--workers", str(workers), "--reps", str(reps)]
+    out = subprocess.run(cmd, check=True, capture_output=True, text=True, timeout=1800).stdout
+    runs = json.loads(out)
+    return {"runs": runs, "workers": workers, "cmd": " ".join(cmd[1:])}
+
+
+def run_port_cpu(n, N, S, T, slices=4):
+    """Fallback CPU baseline: the C restatement oracle (single thread) on `slices` slices."""
+    import oracle as O
+
+    dx, dt = 1.0 / (n + 1), T / (N * S)
+    tb, te, st, h = O.decompose(0.0, T, N, dt)
+    t0 = time.perf_counter()
+    for j in range(slices):
+        O.heat_build(dx, tb[j], te[j], dt)
+    secs = time.perf_counter() - t0
+    return {"seconds": secs, "traj_steps": slices * (n + 1) * S}
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    N = args.slices_per_gpu * args.gpus
+    for _ in range(args.warmup):
+        pass  # the reference has no device state to warm; each rep is a cold full run
+    res = run_reference_cpu(args.n, N, args.S, args.T, max(1, args.steps))
+    if res is None:
+        rp = run_port_cpu(args.n, N, args.S, args.T)
+        v = rp["traj_steps"] / rp["seconds"]
+        kind, cores, sample, secs = "port", 1, f"oracle heat_build on 4 of {N} slices", rp["seconds"]
+    else:
+        vals = [r["traj_steps"] / r["seconds"] for r in res["runs"]]
+        v = statistics.mean(vals)
+        secs = statistics.mean(r["seconds"] for r in res["runs"])
+        kind, cores, sample = "reference", res["workers"], f"full run_nievergelt (N={N}, S={args.S}, n={args.n})"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "heat n=128 affine slice maps (BASELINE.json configs[1])", "n": args.n,
+                   "slices": N, "steps_per_slice": args.S, "T": args.T, "compose": "chain (reference)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1304_6514_b200 import capi, pint
+    from paper_1304_6514_b200.dist import HeatPlan, HeatTablesHost, apply_chain, gather_maps, slice_block
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    ctx = capi.Context(local, stream=stream)
+    pint.set_context(ctx)
+
+    n, S, T = args.n, args.S, args.T
+    N = args.slices_per_gpu * world
+    dx, dt = 1.0 / (n + 1), T / (N * S)
+    lo, hi = slice_block(N, world, rank)
+    plan = HeatPlan(ctx, dx, dt, T, N, lo, hi)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MB > L2
+
+    peak64 = C.c_double()
+    ctx.check(ctx.lib.pint_probe_peak(ctx.h, capi.F64, C.byref(peak64)))
+
+    def one_step(events=None):
+        if events:
+            events[0].record(stream)
+        P = capi.ptr
+        step_off, slice_dt, r, fa, fb, sx = plan.dev
+        ctx.call("pint_heat_factor_dev", plan.n, plan.Q, P(r), P(plan.factor))
+        if events:
+            events[1].record(stream)
+        ctx.call("pint_heat_build_dev", plan.n, plan.N, P(step_off), P(slice_dt), P(plan.factor), P(r), P(fa),
+                 P(fb), P(sx), P(plan.maps), None)
+        if events:
+            events[2].record(stream)
+        plan.compose_local(capi.COMPOSE_TREE)
+        if world > 1:
+            maps = gather_maps(plan.composed)
+            if rank == 0:
+                apply_chain(ctx, plan.n, torch.cat(maps), plan.y0, plan.y)
+        if events:
+            events[3].record(stream)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    tot = {"step": 0.0, "factor": 0.0, "build": 0.0, "compose": 0.0}
+    launches0 = ctx.launches()
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between timed iterations (outside the events)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        one_step(ev)
+        ev[3].synchronize()
+        tot["step"] += ev[0].elapsed_time(ev[3])
+        tot["factor"] += ev[0].elapsed_time(ev[1])
+        tot["build"] += ev[1].elapsed_time(ev[2])
+        tot["compose"] += ev[2].elapsed_time(ev[3])
+    torch.cuda.synchronize()
+    launches = ctx.launches() - launches0 - 0  # our kernels only (flush is torch's)
+    if world > 1:
+        t = torch.tensor([tot["step"]], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot["step"] = float(t.item())
+        dist.barrier()
+    clocks.stop()
+
+    ms_per_step = tot["step"] / args.steps
+    traj_steps_total = N * (n + 1) * S  # every rank's block: all ranks processed all N slices
+    value = traj_steps_total / (ms_per_step * 1e-3)
+
+    # ---- e2e: host buffers through the public API, H2D + D2H inside the timed region
+    y_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    e2e_secs, h2d, d2h = 0.0, 0, 0
+    if world == 1:
+        y_np = y_host.numpy()
+        rep = capi.Report()
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ctx.check(ctx.lib.pint_run_heat(ctx.h, dx, dt, T, N, capi.COMPOSE_TREE, None, capi.ptr(y_np), None,
+                                            C.byref(rep)))
+            dt_s = time.perf_counter() - t0
+            if i >= args.warmup:
+                e2e_secs += dt_s
+        h2d, d2h = int(rep.h2d_bytes), int(rep.d2h_bytes)
+    else:
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            host = HeatTablesHost(dx, plan.slices)
+            plan.host = host
+            b = plan.upload()
+            one_step()
+            if rank == 0:
+                y_host.copy_(plan.y, non_blocking=True)
+            torch.cuda.synchronize()
+            el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+            if i >= args.warmup:
+                e2e_secs += float(el.item())
+            h2d = b + plan.y0.numel() * 8
+            d2h = n * 8 if rank == 0 else 0
+    e2e_value = traj_steps_total / (e2e_secs / args.steps)
+
+    # ---- roofline of the dominant kernel (the K3 map build)
+    build_ms = tot["build"] / args.steps
+    build_flops = sum(s.steps for s in plan.slices) * flops_per_slice_step(n)
+    achieved = build_flops / (build_ms * 1e-3) / 1e12
+    traffic = None
+    prof = ROOT / "profiles" / "r01_build_traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            res = run_reference_cpu(n, N, S, T, 1)
+            if res is not None:
+                r0 = res["runs"][0]
+                cpu = {"value": r0["traj_steps"] / r0["seconds"], "unit": UNIT, "cores": res["workers"],
+                       "kind": "reference", "sample": f"full pint::run_nievergelt N={N} S={S} n={n} "
+                       f"(T_total, {res['workers']} workers)"}
+            else:
+                rp = run_port_cpu(n, N, S, T)
+                cpu = {"value": rp["traj_steps"] / rp["seconds"], "unit": UNIT, "cores": 1, "kind": "port",
+                       "sample": f"oracle heat_build, 4 of {N} slices"}
+        except Exception as e:  # the baseline is reported, never the target
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "heat n=128 affine slice maps + tree compose (BASELINE.json configs[1])",
+                       "n": n, "slices": N, "slices_per_gpu": args.slices_per_gpu, "steps_per_slice": S, "T": T,
+                       "dt": dt, "compose": "tree (DMMA)" + (" + NCCL gather" if world > 1 else ""),
+                       "parallelism": f"slice blocks x{world}", "l2": "flushed (256 MB write) between steps",
+                       "time_to_solution_ms": ms_per_step, "e2e_time_to_solution_ms": e2e_secs / args.steps * 1e3},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "roofline": {"bound": "fp64", "kernel": "heat_columns_kernel<build>", "achieved": achieved,
+                         "peak": peak64.value, "unit": "TFLOP/s", "frac": achieved / peak64.value,
+                         "traffic": traffic, "peak_source": "measured DFMA probe (pint_probe_peak)",
+                         "flops_per_launch": build_flops, "launch_ms": build_ms,
+                         "share_of_step": build_ms / ms_per_step,
+                         "factor_ms": tot["factor"] / args.steps, "compose_ms": tot["compose"] / args.steps},
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

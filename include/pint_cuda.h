@@ -1,0 +1,220 @@
+/* pint_cuda.h — C ABI of the B200-native Nievergelt slice-map path (libpint_cuda.so).
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary. The C++ drop-in
+ * library (paper_1304_6514_b200/include/pint/*.hpp, libpint_b200.so) and the Python host
+ * (paper_1304_6514_b200/capi.py, ctypes) are both thin callers of these entry points.
+ * Each entry point names the reference interface it replaces (file:line under
+ * /root/reference/proj). Ctypes / C++ bindings a maintainer adds are shown in INTEGRATION.md.
+ *
+ * Conventions
+ *  - `_dev` entry points take DEVICE pointers, enqueue on the context's stream and return
+ *    immediately. Task failures (e.g. NoRealRoot) are latched in the context's device-side
+ *    failure record; read it with pint_fail_read() after pint_ctx_sync().
+ *  - Entry points without `_dev` take HOST pointers, copy in/out and synchronise.
+ *  - Slice maps of a linear problem ("affine maps") are stored as one row-major augmented
+ *    block per slice: rows i < n, columns [0, n) = G, column n = c, leading dimension
+ *    ldm = pint_affine_ldm(n) (n + 1 rounded up to a multiple of 4), slice j at j * n * ldm.
+ *  - Every function returns PINT_OK or a PINT_E_* code; pint_ctx_last_error() has the text.
+ */
+#ifndef PINT_CUDA_H
+#define PINT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: one per reference exception type (errors.hpp:9-43) ---- */
+enum {
+    PINT_OK = 0,
+    PINT_E_NO_REAL_ROOT = 1,        /* NoRealRoot          errors.hpp:10 */
+    PINT_E_SINGULAR = 2,            /* SingularSystem      errors.hpp:15 */
+    PINT_E_BAD_GRID = 3,            /* BadGrid             errors.hpp:20 */
+    PINT_E_NON_INTEGER_STEPS = 4,   /* NonIntegerStepCount errors.hpp:25 */
+    PINT_E_DUPLICATE_NODES = 5,     /* DuplicateNodes      errors.hpp:29 */
+    PINT_E_INVALID = 16,            /* bad argument to this ABI */
+    PINT_E_CUDA = 17,               /* CUDA runtime failure (no CPU fallback exists) */
+    PINT_E_NO_DEVICE = 18
+};
+
+typedef struct pint_ctx pint_ctx;
+
+/* One time slice (ode_core.hpp:42-48). `steps`/`dt` follow decompose (ode_core.cpp:26-45). */
+typedef struct {
+    double t_begin;
+    double t_end;
+    int64_t steps;
+    double dt;
+} pint_slice;
+
+/* Lowest failing task, parallel_map semantics (exec_harness.hpp:88-99). index < 0: none. */
+typedef struct {
+    int64_t index;
+    int32_t code;   /* PINT_E_* of the failing task */
+    int32_t pad;
+    double value;   /* the offending quantity (Riccati discriminant, zero pivot row, ...) */
+} pint_fail;
+
+/* Scalar right-hand sides on the device. The reference integrator ignores ScalarIVP::rhs and
+ * always runs backward-Euler Riccati (nievergelt.cpp:28-35); the others are EXTENSIONS. */
+enum {
+    PINT_RHS_RICCATI_BE = 0,  /* y' = y^2, closed-form backward Euler (ode_core.cpp:47-53) */
+    PINT_RHS_LOGISTIC_RK4 = 1 /* y' = r y (1 - y/K), classical RK4 */
+};
+enum { PINT_F64 = 0, PINT_F32 = 1 };
+enum { PINT_WEIGHTS_PRODUCT = 0, PINT_WEIGHTS_CLOSED2 = 1 };
+enum { PINT_SWEEP_EXACT = 0, PINT_SWEEP_TREE = 1 };        /* barycentric sum order */
+enum { PINT_COMPOSE_CHAIN = 0, PINT_COMPOSE_TREE = 1 };    /* affine composition */
+enum { PINT_NODES_FIRST_KIND = 0, PINT_NODES_SECOND_KIND = 1 };
+
+typedef struct {
+    int32_t kind;      /* PINT_RHS_* */
+    int32_t precision; /* PINT_F64 / PINT_F32 (F32 only for LOGISTIC_RK4) */
+    double r;          /* logistic rate */
+    double K;          /* logistic capacity */
+} pint_scalar_rhs;
+
+/* Report of a full run, the subset of RunReport (nievergelt.hpp:42-62) the device produces. */
+typedef struct {
+    int64_t message_count;
+    int64_t bytes_communicated;
+    int64_t extrapolation_count;
+    double device_ms;        /* CUDA-event time of the device work */
+    double total_ms;         /* host wall time of the call (T_total analogue) */
+    int64_t traj_steps;      /* sum over slices of trajectories x steps */
+    int64_t gpu_launches;    /* kernels this call launched */
+    int64_t h2d_bytes;       /* host->device bytes this call copied */
+    int64_t d2h_bytes;       /* device->host bytes this call copied */
+    double compose_ms;       /* CUDA-event time of the composition sweep alone (apply_cost) */
+} pint_report;
+
+/* ---- context ---- */
+int pint_ctx_create(int device, pint_ctx** out);
+void pint_ctx_destroy(pint_ctx* ctx);
+const char* pint_ctx_last_error(const pint_ctx* ctx);
+int pint_ctx_sync(pint_ctx* ctx);
+/* the cudaStream_t the context enqueues on (as void*); set_stream adopts a caller stream */
+void* pint_ctx_stream(pint_ctx* ctx);
+int pint_ctx_set_stream(pint_ctx* ctx, void* stream);
+/* number of kernels launched through this context so far */
+int64_t pint_ctx_launch_count(const pint_ctx* ctx);
+/* read (and clear) the device-side failure record; syncs the stream */
+int pint_fail_read(pint_ctx* ctx, pint_fail* out);
+const char* pint_version(void);
+
+/* ---- host-side tables (bit-identical to the reference's own host arithmetic) ---- */
+/* steps_for (ode_core.cpp:18-24) */
+int64_t pint_steps_for(double width, double dt);
+/* decompose (ode_core.cpp:26-45): writes N slices */
+int pint_decompose(double t0, double T, int64_t N, double dt, pint_slice* out);
+/* cheb_nodes / cheb_nodes_second_kind (interp.cpp:21-41) */
+int pint_sample_nodes(int kind, int64_t M, double a, double b, double* out);
+/* augmented map leading dimension, see conventions */
+int64_t pint_affine_ldm(int64_t n);
+
+/* ---- K1: scalar ensemble (replaces parallel_map over N*M tasks, nievergelt.cpp:170-182) ----
+ * endpoints[j*M + m] = slice j's end state from nodes[m] after steps[j] steps of dt[j].
+ * nodes/endpoints are double (PINT_F64) or float (PINT_F32). per_slice_ns (may be NULL) gets
+ * the summed device time of the slice's thread blocks (RunReport::per_slice_compute). */
+int pint_scalar_ensemble_dev(pint_ctx* ctx, const pint_scalar_rhs* rhs, int64_t N, int64_t M,
+                             const int64_t* steps, const double* dt, const void* nodes,
+                             void* endpoints, unsigned long long* per_slice_ns);
+
+/* ---- K2: barycentric weights (interp.cpp:43-55, product form; or closed-form EXTENSION) */
+int pint_bary_weights_dev(pint_ctx* ctx, int kind, int64_t M, const double* nodes, double* w);
+
+/* ---- K2: scalar composition sweep (compose_sweep, nievergelt.cpp:68-88 + interp_eval,
+ * interp.cpp:68-80). values[j*M + m]; nodes/weights per slice at stride node_stride (0 = all
+ * slices share one set); a/b per slice at stride ab_stride (0 or 1). Writes lambdas[j]
+ * (may be NULL), *y_out and *extrapolations (device pointers). mode: PINT_SWEEP_EXACT keeps the
+ * reference's sequential sum order (bit-exact); PINT_SWEEP_TREE sums by warp tree. */
+int pint_scalar_sweep_dev(pint_ctx* ctx, int mode, int64_t N, int64_t M, const double* nodes,
+                          int64_t node_stride, const double* weights, const double* values,
+                          const double* a, const double* b, int64_t ab_stride, double y0,
+                          double* lambdas, double* y_out, long long* extrapolations);
+
+/* ---- K3: heat slice maps (build_affine_propagator, nievergelt.cpp:53-66, driving the
+ * make_heat_problem integrate closure, pde_problems.cpp:76-100). Per-step coefficient tables
+ * come from pint_heat_coefficients (host, glibc sin/cos like the reference). ---- */
+/* total steps over the slices */
+int64_t pint_heat_total_steps(const pint_slice* slices, int64_t N);
+/* Host tables: step_off[N+1] (prefix sums of steps); per step q: r[q] = (h a(t)) / dx^2,
+ * fa[q] = -sin t, fb[q] = ((a(t) pi) pi) cos t; sx[i] = sin(pi (i+1) dx). n = interior points. */
+int pint_heat_coefficients(double dx, const pint_slice* slices, int64_t N, int64_t* step_off,
+                           double* r, double* fa, double* fb, double* sx, int64_t* n_out);
+/* Shared tridiagonal factor per step (the Thomas forward pivots, linalg.cpp:77-93):
+ * factor[q*n + i] = {pivot_i, c_i} for every step q < total_steps. */
+int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t total_steps, const double* r,
+                         double* factor /* total_steps * n * 2 */);
+/* Build all N augmented maps into maps (N * n * ldm doubles). slices/step_off are device
+ * copies of the host tables. */
+int pint_heat_build_dev(pint_ctx* ctx, int64_t n, int64_t N, const int64_t* step_off,
+                        const double* slice_dt, const double* factor, const double* r,
+                        const double* fa, const double* fb, const double* sx, double* maps,
+                        unsigned long long* per_slice_ns);
+/* Integrate K state vectors y[k*n ...] in place through the steps [q0, q0+steps) of the
+ * tables (the integrate closure for one slice, or run_serial over one whole-interval slice). */
+int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t q0, int64_t steps,
+                            double h, int with_forcing, const double* factor, const double* r,
+                            const double* fa, const double* fb, const double* sx, double* y);
+
+/* ---- K4: affine composition (compose_sweep, nievergelt.cpp:90-110) ----
+ * CHAIN: y <- G_j y + c_j in slice order, rows as sequential dots (bit-exact vs matvec,
+ * linalg.cpp:17-26). TREE: log-depth pairwise products on FP64 tensor cores (DMMA), then one
+ * apply (EXTENSION, <= 1e-12 relative). maps is consumed (overwritten) by TREE; scratch must hold
+ * ceil(N/2) maps (TREE only; may be NULL for CHAIN). composed (may be NULL) receives the
+ * composed augmented map (TREE only). y0, y: device n-vectors. */
+int pint_affine_compose_dev(pint_ctx* ctx, int mode, int64_t n, int64_t N, double* maps,
+                            double* scratch, const double* y0, double* y, double* composed);
+/* Compose two augmented maps: out = later ∘ earlier (EXTENSION, the tree's pair step). */
+int pint_affine_pair_dev(pint_ctx* ctx, int64_t n, int64_t P, const double* earlier,
+                         const double* later, double* out);
+
+/* ---- EXTENSION: 2-D Lotka-Volterra ensemble + bilinear sweep (config 3) ---- */
+/* endpoints layout (N, 2, Mu, Mv); params = {alpha, beta, delta, gamma} (host) */
+int pint_lv_ensemble_dev(pint_ctx* ctx, int64_t N, int64_t Mu, int64_t Mv, const int64_t* steps,
+                         const double* dt, const double* un, const double* vn,
+                         const double* params, double* endpoints);
+/* chain of bilinear maps; lambdas (N, 2), brackets (N, 2) = (iu, iv) used at each slice */
+int pint_bilinear_sweep_dev(pint_ctx* ctx, int64_t N, int64_t Mu, int64_t Mv, const double* un,
+                            const double* vn, const double* tables, double u0, double v0,
+                            double* lambdas, long long* brackets, long long* extrapolations);
+
+/* ---- full runs with HOST buffers (run_nievergelt, nievergelt.cpp:145-265) ---- */
+/* Scalar: decompose, sample nodes, K1, weights, K2 sweep. y_out[0] = final state.
+ * endpoints_out (N*M, may be NULL) receives the ensemble; lambdas_out (N, may be NULL). */
+int pint_run_scalar(pint_ctx* ctx, const pint_scalar_rhs* rhs, double t0, double T, double y0,
+                    int64_t N, double dt, int node_kind, int64_t M, double a, double b,
+                    int weight_kind, int sweep_mode, double* y_out, double* endpoints_out,
+                    double* lambdas_out, double* per_slice_seconds, pint_report* report,
+                    pint_fail* fail);
+/* Heat: make_heat_problem(dx, dt, T) with y0 = heat_initial, N slices, K3 + K4. */
+int pint_run_heat(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int compose_mode,
+                  const double* y0, double* y_out, double* per_slice_seconds, pint_report* report);
+/* Heat slice maps to host: G row-major N x n x n, c N x n (build_affine_propagator for all). */
+int pint_heat_maps(pint_ctx* ctx, double dx, double dt, const pint_slice* slices, int64_t N,
+                   double* G, double* c);
+/* Heat integrate closure on host vectors: K states y[k*n..] over one slice, in place. */
+int pint_heat_integrate(pint_ctx* ctx, double dx, const pint_slice* slice, double dt_nominal,
+                        int with_forcing, int64_t K, double* y);
+/* Scalar integrate (integrate_scalar, nievergelt.cpp:29-35) for K initial values on one slice. */
+int pint_scalar_integrate(pint_ctx* ctx, const pint_scalar_rhs* rhs, const pint_slice* slice,
+                          int64_t K, const double* y0, double* y_out, pint_fail* fail);
+/* Host-buffer affine chain / tree over maps given as G (N x n x n row-major) and c (N x n). */
+int pint_affine_compose(pint_ctx* ctx, int mode, int64_t n, int64_t N, const double* G,
+                        const double* c, const double* y0, double* y_out);
+/* Host-buffer scalar sweep over N interpolants (general: per-slice nodes/weights/a/b). */
+int pint_scalar_sweep(pint_ctx* ctx, int mode, int64_t N, int64_t M, const double* nodes,
+                      int64_t node_stride, const double* weights, const double* values,
+                      const double* a, const double* b, int64_t ab_stride, double y0,
+                      double* lambdas, double* y_out, long long* extrapolations);
+
+/* ---- roofline probe: measured FMA throughput (TFLOP/s) of this GPU for PINT_F64 / PINT_F32 */
+int pint_probe_peak(pint_ctx* ctx, int precision, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,806 @@
+// The C ABI (include/pint_cuda.h): context, host-side tables and the full-run pipelines.
+//
+// Host tables are computed with the reference's own arithmetic (same operation order, glibc
+// sin/cos, no FMA contraction: -Xcompiler -ffp-contract=off), so slice assignment, step counts
+// and per-step coefficients are bit-identical to what the reference computes inside its loops.
+// There is no CPU fallback anywhere: without a device every entry point returns an error.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "pint_internal.cuh"
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+
+const char* cuda_name(cudaError_t e) { return cudaGetErrorString(e); }
+
+bool ok(pint_ctx* ctx, cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return true;
+    pint_set_error(ctx, PINT_E_CUDA, std::string(what) + ": " + cuda_name(e));
+    return false;
+}
+
+struct HostTimer {
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    double ms() const {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+};
+
+// integrate_slice's integrality check (ode_core.hpp:77-80) for a slice run at step h
+int check_integral(pint_ctx* ctx, double span, double h) {
+    const double ratio = span / h;
+    const long long n = std::llround(ratio);
+    if (n == 0 || std::fabs(ratio - static_cast<double>(n)) > 1e-9 * std::max(1.0, std::fabs(ratio))) {
+        char buf[128];
+        std::snprintf(buf, sizeof buf, "integrate_slice: (t_end - t_start)/dt = %f", ratio);
+        return pint_set_error(ctx, PINT_E_NON_INTEGER_STEPS, buf);
+    }
+    return PINT_OK;
+}
+
+// interior_points (pde_problems.cpp:14-21)
+int heat_dim(pint_ctx* ctx, double dx, int64_t* n) {
+    const double inv = 1.0 / dx;
+    const long long m = std::llround(inv);
+    if (m < 2 || std::fabs(inv - static_cast<double>(m)) > 1e-9 * inv) {
+        char buf[160];
+        std::snprintf(buf, sizeof buf, "make_heat_system: 1/dx must be an integer >= 2, got dx = %f", dx);
+        return pint_set_error(ctx, PINT_E_BAD_GRID, buf);
+    }
+    *n = m - 1;
+    return PINT_OK;
+}
+
+// Slices as the heat integrate closure sees them: steps = steps_for(width, dt_nominal),
+// h = width / steps (pde_problems.cpp:88-89).
+void closure_slices(const pint_slice* in, int64_t N, double dt_nominal, std::vector<pint_slice>& out) {
+    out.resize(static_cast<size_t>(N));
+    for (int64_t j = 0; j < N; ++j) {
+        pint_slice s = in[j];
+        s.steps = pint_steps_for(s.t_end - s.t_begin, dt_nominal);
+        s.dt = (s.t_end - s.t_begin) / static_cast<double>(s.steps);
+        out[static_cast<size_t>(j)] = s;
+    }
+}
+
+// Pinned staging buffer owned by the context for the host-buffer entry points.
+struct Pinned {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+thread_local Pinned t_pinned;
+
+void* pinned(size_t bytes) {
+    if (t_pinned.bytes < bytes) {
+        if (t_pinned.p) cudaFreeHost(t_pinned.p);
+        t_pinned.p = nullptr;
+        t_pinned.bytes = 0;
+        if (cudaHostAlloc(&t_pinned.p, bytes, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+        t_pinned.bytes = bytes;
+    }
+    return t_pinned.p;
+}
+
+// Bump allocator over one scratch arena.
+struct Carve {
+    char* base;
+    size_t off = 0;
+    template <class T>
+    T* take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T* p = reinterpret_cast<T*>(base + off);
+        off += sizeof(T) * count;
+        return p;
+    }
+};
+
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+}  // namespace
+
+// ---- internal helpers shared with the kernel files ------------------------------------------
+
+int pint_set_error(pint_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->last_error = msg;
+    return code;
+}
+
+int pint_check_launch(pint_ctx* ctx, const char* what) {
+    ++ctx->launches;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return pint_set_error(ctx, PINT_E_CUDA, std::string(what) + ": " + cuda_name(e));
+    return PINT_OK;
+}
+
+void* pint_scratch(pint_ctx* ctx, int slot, size_t bytes) {
+    if (ctx->scratch_bytes[slot] < bytes) {
+        if (ctx->scratch[slot]) cudaFree(ctx->scratch[slot]);
+        ctx->scratch[slot] = nullptr;
+        ctx->scratch_bytes[slot] = 0;
+        if (cudaMalloc(&ctx->scratch[slot], bytes) != cudaSuccess) {
+            pint_set_error(ctx, PINT_E_CUDA, "scratch allocation of " + std::to_string(bytes) + " bytes failed");
+            return nullptr;
+        }
+        ctx->scratch_bytes[slot] = bytes;
+    }
+    return ctx->scratch[slot];
+}
+
+// ---- context -----------------------------------------------------------------------------------
+
+extern "C" {
+
+const char* pint_version(void) { return "pint-b200 0.1 (sm_100a)"; }
+
+int pint_ctx_create(int device, pint_ctx** out) {
+    if (!out) return PINT_E_INVALID;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return PINT_E_NO_DEVICE;
+    if (device < 0 || device >= count) return PINT_E_INVALID;
+    auto* ctx = new pint_ctx();
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete ctx;
+        return PINT_E_CUDA;
+    }
+    cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc(&ctx->d_fail, sizeof(FailRec)) != cudaSuccess ||
+        cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
+        cudaEventCreate(&ctx->evc) != cudaSuccess) {
+        delete ctx;
+        return PINT_E_CUDA;
+    }
+    ctx->own_stream = true;
+    FailRec init{pint_dev::kNoFail, 0, 0, 0.0};
+    cudaMemcpy(ctx->d_fail, &init, sizeof init, cudaMemcpyHostToDevice);
+    *out = ctx;
+    return PINT_OK;
+}
+
+void pint_ctx_destroy(pint_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (int i = 0; i < 4; ++i)
+        if (ctx->scratch[i]) cudaFree(ctx->scratch[i]);
+    if (ctx->d_fail) cudaFree(ctx->d_fail);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->evc) cudaEventDestroy(ctx->evc);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* pint_ctx_last_error(const pint_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+
+int pint_ctx_sync(pint_ctx* ctx) {
+    return ok(ctx, cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize") ? PINT_OK : PINT_E_CUDA;
+}
+
+void* pint_ctx_stream(pint_ctx* ctx) { return ctx ? reinterpret_cast<void*>(ctx->stream) : nullptr; }
+
+int pint_ctx_set_stream(pint_ctx* ctx, void* stream) {
+    if (!ctx) return PINT_E_INVALID;
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    ctx->stream = reinterpret_cast<cudaStream_t>(stream);
+    ctx->own_stream = false;
+    return PINT_OK;
+}
+
+int64_t pint_ctx_launch_count(const pint_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int pint_fail_read(pint_ctx* ctx, pint_fail* out) {
+    FailRec rec{};
+    if (!ok(ctx, cudaMemcpyAsync(&rec, ctx->d_fail, sizeof rec, cudaMemcpyDeviceToHost, ctx->stream), "fail read") ||
+        !ok(ctx, cudaStreamSynchronize(ctx->stream), "fail read sync"))
+        return PINT_E_CUDA;
+    FailRec init{pint_dev::kNoFail, 0, 0, 0.0};
+    if (rec.index != pint_dev::kNoFail &&
+        !ok(ctx, cudaMemcpyAsync(ctx->d_fail, &init, sizeof init, cudaMemcpyHostToDevice, ctx->stream), "fail reset"))
+        return PINT_E_CUDA;
+    cudaStreamSynchronize(ctx->stream);
+    if (out) {
+        out->index = rec.index == pint_dev::kNoFail ? -1 : static_cast<int64_t>(rec.index);
+        out->code = rec.index == pint_dev::kNoFail ? 0 : rec.code;
+        out->pad = 0;
+        out->value = rec.value;
+    }
+    return PINT_OK;
+}
+
+// ---- host tables ---------------------------------------------------------------------------------
+
+int64_t pint_steps_for(double width, double dt) {
+    const double ratio = width / dt;
+    const double snapped = ratio - 1e-9 * std::max(1.0, ratio);
+    const auto n = static_cast<long long>(std::ceil(snapped));
+    return n < 1 ? 1 : n;
+}
+
+int pint_decompose(double t0, double T, int64_t N, double dt, pint_slice* out) {
+    if (N <= 0 || !(T > t0) || !(dt > 0.0) || !out) return PINT_E_BAD_GRID;
+    const double width = (T - t0) / static_cast<double>(N);
+    for (int64_t j = 0; j < N; ++j) {
+        pint_slice s;
+        s.t_begin = t0 + static_cast<double>(j) * width;
+        s.t_end = (j + 1 == N) ? T : t0 + static_cast<double>(j + 1) * width;
+        s.steps = pint_steps_for(s.t_end - s.t_begin, dt);
+        s.dt = (s.t_end - s.t_begin) / static_cast<double>(s.steps);
+        out[j] = s;
+    }
+    return PINT_OK;
+}
+
+int pint_sample_nodes(int kind, int64_t M, double a, double b, double* out) {
+    if (M <= 0 || !out) return PINT_E_BAD_GRID;
+    if (M == 1) {
+        out[0] = 0.5 * (a + b);
+        return PINT_OK;
+    }
+    for (int64_t k = 0; k < M; ++k) {
+        const double kd = static_cast<double>(k);
+        out[k] = (kind == PINT_NODES_FIRST_KIND)
+                     ? std::cos((2.0 * kd + 1.0) * kPi / (2.0 * static_cast<double>(M)))
+                     : std::cos(kd * kPi / static_cast<double>(M - 1));
+    }
+    for (int64_t k = 0; k < M; ++k) out[k] = a + (b - a) * (out[k] + 1.0) / 2.0;
+    std::sort(out, out + M);
+    return PINT_OK;
+}
+
+int64_t pint_affine_ldm(int64_t n) { return ((n + 1) + 3) / 4 * 4; }
+
+int64_t pint_heat_total_steps(const pint_slice* slices, int64_t N) {
+    int64_t t = 0;
+    for (int64_t j = 0; j < N; ++j) t += slices[j].steps;
+    return t;
+}
+
+int pint_heat_coefficients(double dx, const pint_slice* slices, int64_t N, int64_t* step_off,
+                           double* r, double* fa, double* fb, double* sx, int64_t* n_out) {
+    int64_t n = 0;
+    if (const int rc = heat_dim(nullptr, dx, &n)) return rc;
+    if (n_out) *n_out = n;
+    step_off[0] = 0;
+    for (int64_t j = 0; j < N; ++j) step_off[j + 1] = step_off[j] + slices[j].steps;
+    const double inv_dx2 = 1.0 / (dx * dx);  // pde_problems.cpp:33
+    // per step: heat_coefficient (pde_problems.cpp:24), solve_implicit's r (:54), forcing (:26-29)
+    auto fill = [&](int64_t j0, int64_t j1) {
+        for (int64_t j = j0; j < j1; ++j) {
+            const double tb = slices[j].t_begin, h = slices[j].dt;
+            const int64_t base = step_off[j];
+            for (int64_t i = 1; i <= slices[j].steps; ++i) {
+                const double t = tb + static_cast<double>(i) * h;  // ode_core.hpp:83
+                const double st = std::sin(t);
+                const double a = 1.0 + 0.25 * st;
+                const int64_t q = base + i - 1;
+                r[q] = h * a * inv_dx2;
+                fa[q] = -st;
+                fb[q] = a * kPi * kPi * std::cos(t);
+            }
+        }
+    };
+    const int64_t total = step_off[N];
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    if (total < 16384 || hw == 1 || N < 2) {
+        fill(0, N);
+    } else {
+        std::vector<std::thread> pool;
+        const int64_t per = (N + hw - 1) / hw;
+        for (int64_t j0 = 0; j0 < N; j0 += per) pool.emplace_back(fill, j0, std::min(N, j0 + per));
+        for (auto& t : pool) t.join();
+    }
+    if (sx)
+        for (int64_t i = 0; i < n; ++i) sx[i] = std::sin(kPi * (static_cast<double>(i + 1) * dx));
+    return PINT_OK;
+}
+
+// ---- device-pointer entry points -----------------------------------------------------------------
+
+int pint_scalar_ensemble_dev(pint_ctx* ctx, const pint_scalar_rhs* rhs, int64_t N, int64_t M,
+                             const int64_t* steps, const double* dt, const void* nodes,
+                             void* endpoints, unsigned long long* per_slice_ns) {
+    if (!ctx) return PINT_E_INVALID;
+    return launch_scalar_ensemble(ctx, rhs, N, M, steps, dt, nodes, endpoints, per_slice_ns);
+}
+
+int pint_bary_weights_dev(pint_ctx* ctx, int kind, int64_t M, const double* nodes, double* w) {
+    if (!ctx) return PINT_E_INVALID;
+    return launch_bary_weights(ctx, kind, M, nodes, w);
+}
+
+int pint_scalar_sweep_dev(pint_ctx* ctx, int mode, int64_t N, int64_t M, const double* nodes,
+                          int64_t node_stride, const double* weights, const double* values,
+                          const double* a, const double* b, int64_t ab_stride, double y0,
+                          double* lambdas, double* y_out, long long* extrapolations) {
+    if (!ctx) return PINT_E_INVALID;
+    return launch_scalar_sweep(ctx, mode, N, M, nodes, node_stride, weights, values, a, b, ab_stride,
+                               y0, lambdas, y_out, extrapolations);
+}
+
+int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t total_steps, const double* r, double* factor) {
+    if (!ctx) return PINT_E_INVALID;
+    return launch_heat_factor(ctx, n, total_steps, r, factor);
+}
+
+int pint_heat_build_dev(pint_ctx* ctx, int64_t n, int64_t N, const int64_t* step_off,
+                        const double* slice_dt, const double* factor, const double* r,
+                        const double* fa, const double* fb, const double* sx, double* maps,
+                        unsigned long long* per_slice_ns) {
+    if (!ctx) return PINT_E_INVALID;
+    return launch_heat_build(ctx, n, N, step_off, slice_dt, factor, r, fa, fb, sx, maps, per_slice_ns);
+}
+
+int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t q0, int64_t steps,
+                            double h, int with_forcing, const double* factor, const double* r,
+                            const double* fa, const double* fb, const double* sx, double* y) {
+    if (!ctx) return PINT_E_INVALID;
+    return launch_heat_integrate(ctx, n, K, q0, steps, h, with_forcing, factor, r, fa, fb, sx, y);
+}
+
+int pint_affine_compose_dev(pint_ctx* ctx, int mode, int64_t n, int64_t N, double* maps,
+                            double* scratch, const double* y0, double* y, double* composed) {
+    if (!ctx) return PINT_E_INVALID;
+    if (mode == PINT_COMPOSE_CHAIN) return launch_affine_chain(ctx, n, N, maps, y0, y);
+    if (mode == PINT_COMPOSE_TREE) {
+        if (!scratch && N > 1) return pint_set_error(ctx, PINT_E_INVALID, "affine tree needs scratch");
+        return launch_affine_tree(ctx, n, N, maps, scratch, y0, y, composed);
+    }
+    return pint_set_error(ctx, PINT_E_INVALID, "affine_compose: unknown mode");
+}
+
+int pint_affine_pair_dev(pint_ctx* ctx, int64_t n, int64_t P, const double* earlier,
+                         const double* later, double* out) {
+    if (!ctx) return PINT_E_INVALID;
+    return launch_affine_pair(ctx, n, P, earlier, later, out);
+}
+
+int pint_lv_ensemble_dev(pint_ctx* ctx, int64_t N, int64_t Mu, int64_t Mv, const int64_t* steps,
+                         const double* dt, const double* un, const double* vn,
+                         const double* params, double* endpoints) {
+    if (!ctx) return PINT_E_INVALID;
+    return launch_lv_ensemble(ctx, N, Mu, Mv, steps, dt, un, vn, params, endpoints);
+}
+
+int pint_bilinear_sweep_dev(pint_ctx* ctx, int64_t N, int64_t Mu, int64_t Mv, const double* un,
+                            const double* vn, const double* tables, double u0, double v0,
+                            double* lambdas, long long* brackets, long long* extrapolations) {
+    if (!ctx) return PINT_E_INVALID;
+    return launch_bilinear_sweep(ctx, N, Mu, Mv, un, vn, tables, u0, v0, lambdas, brackets, extrapolations);
+}
+
+// ---- full runs with host buffers -----------------------------------------------------------------
+
+int pint_run_scalar(pint_ctx* ctx, const pint_scalar_rhs* rhs, double t0, double T, double y0,
+                    int64_t N, double dt, int node_kind, int64_t M, double a, double b,
+                    int weight_kind, int sweep_mode, double* y_out, double* endpoints_out,
+                    double* lambdas_out, double* per_slice_seconds, pint_report* report,
+                    pint_fail* fail) {
+    if (!ctx || !rhs || !y_out) return PINT_E_INVALID;
+    HostTimer wall;
+    const long long launches0 = ctx->launches;
+    if (fail) *fail = pint_fail{-1, 0, 0, 0.0};
+    if (N < 1) N = 1;
+    const bool serial = (N == 1);  // run_nievergelt with N <= 1 is run_serial (nievergelt.cpp:146-152)
+    const bool f32 = rhs->precision == PINT_F32;
+    const size_t esz = f32 ? sizeof(float) : sizeof(double);
+
+    std::vector<pint_slice> sl(static_cast<size_t>(N));
+    if (pint_decompose(t0, T, N, dt, sl.data()) != PINT_OK)
+        return pint_set_error(ctx, PINT_E_BAD_GRID, "decompose: need N >= 1, T > t0, dt > 0");
+    for (const auto& s : sl)
+        if (const int rc = check_integral(ctx, s.t_end - s.t_begin, s.dt)) return rc;
+    const int64_t Mn = serial ? 1 : M;
+    std::vector<double> nodes(static_cast<size_t>(Mn));
+    if (serial) {
+        nodes[0] = y0;
+    } else if (pint_sample_nodes(node_kind, M, a, b, nodes.data()) != PINT_OK) {
+        return pint_set_error(ctx, PINT_E_BAD_GRID, "cheb_nodes: M >= 1 required");
+    }
+
+    // staging: steps[N] | dt[N] | nodes[M] (as the kernel's precision) | {a, b}
+    const size_t b_steps = align256(sizeof(int64_t) * N), b_dt = align256(sizeof(double) * N);
+    const size_t b_nodes = align256(esz * Mn), b_ab = align256(2 * sizeof(double));
+    const size_t in_bytes = b_steps + b_dt + b_nodes + b_ab;
+    char* h_in = static_cast<char*>(pinned(in_bytes));
+    if (!h_in) return pint_set_error(ctx, PINT_E_CUDA, "pinned staging allocation failed");
+    for (int64_t j = 0; j < N; ++j) {
+        reinterpret_cast<int64_t*>(h_in)[j] = sl[j].steps;
+        reinterpret_cast<double*>(h_in + b_steps)[j] = sl[j].dt;
+    }
+    for (int64_t m = 0; m < Mn; ++m) {
+        if (f32) reinterpret_cast<float*>(h_in + b_steps + b_dt)[m] = static_cast<float>(nodes[m]);
+        else reinterpret_cast<double*>(h_in + b_steps + b_dt)[m] = nodes[m];
+    }
+    reinterpret_cast<double*>(h_in + b_steps + b_dt + b_nodes)[0] = a;
+    reinterpret_cast<double*>(h_in + b_steps + b_dt + b_nodes)[1] = b;
+
+    const size_t b_ends = align256(esz * N * Mn);
+    const size_t total = in_bytes + b_ends + align256(sizeof(double) * Mn) + align256(sizeof(double) * N) +
+                         align256(sizeof(unsigned long long) * N) + 512;
+    char* dbase = static_cast<char*>(pint_scratch(ctx, 0, total));
+    if (!dbase) return PINT_E_CUDA;
+    Carve cv{dbase};
+    char* d_in = cv.take<char>(in_bytes);
+    void* d_ends = cv.take<char>(b_ends);
+    double* d_w = cv.take<double>(Mn);
+    double* d_lam = cv.take<double>(N);
+    auto* d_ns = cv.take<unsigned long long>(N);
+    double* d_y = cv.take<double>(1);
+    auto* d_ext = cv.take<long long>(1);
+    const auto* d_steps = reinterpret_cast<const int64_t*>(d_in);
+    const auto* d_dt = reinterpret_cast<const double*>(d_in + b_steps);
+    const void* d_nodes = d_in + b_steps + b_dt;
+    const auto* d_ab = reinterpret_cast<const double*>(d_in + b_steps + b_dt + b_nodes);
+
+    cudaEventRecord(ctx->ev0, ctx->stream);
+    if (!ok(ctx, cudaMemcpyAsync(d_in, h_in, in_bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D inputs"))
+        return PINT_E_CUDA;
+    if (per_slice_seconds) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
+    int rc = launch_scalar_ensemble(ctx, rhs, N, Mn, d_steps, d_dt, d_nodes, d_ends,
+                                    per_slice_seconds ? d_ns : nullptr);
+    if (rc) return rc;
+    long long ext = 0;
+    double y = 0.0;
+    if (serial) {
+        if (!ok(ctx, cudaMemcpyAsync(d_y, d_ends, esz, cudaMemcpyDeviceToDevice, ctx->stream), "copy"))
+            return PINT_E_CUDA;
+    } else {
+        if (f32) return pint_set_error(ctx, PINT_E_INVALID, "FP32 runs support the ensemble only; sweep in FP64");
+        if ((rc = launch_bary_weights(ctx, weight_kind, M, reinterpret_cast<const double*>(d_nodes), d_w))) return rc;
+        cudaEventRecord(ctx->evc, ctx->stream);
+        rc = launch_scalar_sweep(ctx, sweep_mode, N, M, reinterpret_cast<const double*>(d_nodes), 0, d_w,
+                                 static_cast<const double*>(d_ends), d_ab, d_ab + 1, 0, y0, d_lam, d_y, d_ext);
+        if (rc) return rc;
+    }
+    cudaEventRecord(ctx->ev1, ctx->stream);
+    int64_t d2h = 0;
+    if (!ok(ctx, cudaMemcpyAsync(&y, d_y, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H y"))
+        return PINT_E_CUDA;
+    d2h += sizeof(double);
+    if (!serial) {
+        cudaMemcpyAsync(&ext, d_ext, sizeof ext, cudaMemcpyDeviceToHost, ctx->stream);
+        d2h += sizeof ext;
+    }
+    if (endpoints_out) {
+        cudaMemcpyAsync(endpoints_out, d_ends, esz * N * Mn, cudaMemcpyDeviceToHost, ctx->stream);
+        d2h += esz * N * Mn;
+    }
+    if (lambdas_out && !serial) {
+        cudaMemcpyAsync(lambdas_out, d_lam, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream);
+        d2h += sizeof(double) * N;
+    }
+    std::vector<unsigned long long> ns;
+    if (per_slice_seconds) {
+        ns.resize(static_cast<size_t>(N));
+        cudaMemcpyAsync(ns.data(), d_ns, sizeof(unsigned long long) * N, cudaMemcpyDeviceToHost, ctx->stream);
+    }
+    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "run_scalar sync")) return PINT_E_CUDA;
+    if (f32) y = static_cast<double>(*reinterpret_cast<float*>(&y));
+    pint_fail fr;
+    if ((rc = pint_fail_read(ctx, &fr))) return rc;
+    if (fail) *fail = fr;
+    if (fr.index >= 0) {
+        char buf[160];
+        if (fr.code == PINT_E_NO_REAL_ROOT)
+            std::snprintf(buf, sizeof buf, "be_step_scalar_riccati: 1 - 4 dt y = %f", fr.value);
+        else
+            std::snprintf(buf, sizeof buf, "barycentric_weights: repeated node");
+        return pint_set_error(ctx, fr.code, buf);
+    }
+    *y_out = y;
+    if (per_slice_seconds)
+        for (int64_t j = 0; j < N; ++j) per_slice_seconds[j] = static_cast<double>(ns[j]) * 1e-9;
+    if (report) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        report->message_count = serial ? 0 : N - 1;
+        report->bytes_communicated = serial ? 0 : (N - 1) * static_cast<int64_t>(sizeof(double));
+        report->extrapolation_count = ext;
+        report->device_ms = ms;
+        report->traj_steps = 0;
+        for (int64_t j = 0; j < N; ++j) report->traj_steps += sl[j].steps * Mn;
+        report->gpu_launches = ctx->launches - launches0;
+        report->h2d_bytes = static_cast<int64_t>(in_bytes);
+        report->d2h_bytes = d2h;
+        float cms = 0.f;
+        if (!serial) cudaEventElapsedTime(&cms, ctx->evc, ctx->ev1);
+        report->compose_ms = cms;
+        report->total_ms = wall.ms();
+    }
+    return PINT_OK;
+}
+
+int pint_scalar_integrate(pint_ctx* ctx, const pint_scalar_rhs* rhs, const pint_slice* slice,
+                          int64_t K, const double* y0, double* y_out, pint_fail* fail) {
+    if (!ctx || !rhs || !slice || K < 0) return PINT_E_INVALID;
+    if (fail) *fail = pint_fail{-1, 0, 0, 0.0};
+    if (K == 0) return PINT_OK;
+    if (rhs->precision != PINT_F64) return pint_set_error(ctx, PINT_E_INVALID, "scalar_integrate: FP64 only");
+    // integrate_scalar (nievergelt.cpp:29-35): steps_for + dt_eff from the slice bounds
+    const int64_t steps = slice->steps;
+    const double h = slice->dt;
+    if (const int rc = check_integral(ctx, slice->t_end - slice->t_begin, h)) return rc;
+    const size_t bytes = align256(sizeof(double) * K) * 2 + 512;
+    char* d = static_cast<char*>(pint_scratch(ctx, 0, bytes));
+    if (!d) return PINT_E_CUDA;
+    Carve cv{d};
+    auto* d_steps = cv.take<int64_t>(1);
+    auto* d_h = cv.take<double>(1);
+    auto* d_y0 = cv.take<double>(K);
+    auto* d_out = cv.take<double>(K);
+    cudaMemcpyAsync(d_steps, &steps, sizeof steps, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(d_h, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(d_y0, y0, sizeof(double) * K, cudaMemcpyHostToDevice, ctx->stream);
+    int rc = launch_scalar_ensemble(ctx, rhs, 1, K, d_steps, d_h, d_y0, d_out, nullptr);
+    if (rc) return rc;
+    cudaMemcpyAsync(y_out, d_out, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream);
+    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "scalar_integrate sync")) return PINT_E_CUDA;
+    pint_fail fr;
+    if ((rc = pint_fail_read(ctx, &fr))) return rc;
+    if (fail) *fail = fr;
+    if (fr.index >= 0) {
+        char buf[128];
+        std::snprintf(buf, sizeof buf, "be_step_scalar_riccati: 1 - 4 dt y = %f", fr.value);
+        return pint_set_error(ctx, fr.code, buf);
+    }
+    return PINT_OK;
+}
+
+// Device tables for a set of (closure-normalised) heat slices; returns device pointers.
+namespace {
+struct HeatDev {
+    int64_t n = 0, N = 0, Q = 0;
+    int64_t* step_off = nullptr;
+    double *slice_dt = nullptr, *r = nullptr, *fa = nullptr, *fb = nullptr, *sx = nullptr;
+    double* factor = nullptr;
+    size_t h2d = 0;
+};
+
+int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, HeatDev& H) {
+    int64_t n = 0;
+    if (const int rc = heat_dim(ctx, dx, &n)) return rc;
+    for (const auto& s : sl)
+        if (const int rc = check_integral(ctx, s.t_end - s.t_begin, s.dt)) return rc;
+    const int64_t N = static_cast<int64_t>(sl.size());
+    const int64_t Q = pint_heat_total_steps(sl.data(), N);
+    const size_t b_off = align256(sizeof(int64_t) * (N + 1)), b_dt = align256(sizeof(double) * N);
+    const size_t b_q = align256(sizeof(double) * Q), b_sx = align256(sizeof(double) * n);
+    const size_t in_bytes = b_off + b_dt + 3 * b_q + b_sx;
+    char* h = static_cast<char*>(pinned(in_bytes));
+    if (!h) return pint_set_error(ctx, PINT_E_CUDA, "pinned staging allocation failed");
+    auto* h_off = reinterpret_cast<int64_t*>(h);
+    auto* h_dt = reinterpret_cast<double*>(h + b_off);
+    auto* h_r = reinterpret_cast<double*>(h + b_off + b_dt);
+    auto* h_fa = reinterpret_cast<double*>(h + b_off + b_dt + b_q);
+    auto* h_fb = reinterpret_cast<double*>(h + b_off + b_dt + 2 * b_q);
+    auto* h_sx = reinterpret_cast<double*>(h + b_off + b_dt + 3 * b_q);
+    for (int64_t j = 0; j < N; ++j) h_dt[j] = sl[j].dt;
+    pint_heat_coefficients(dx, sl.data(), N, h_off, h_r, h_fa, h_fb, h_sx, nullptr);
+    char* d = static_cast<char*>(pint_scratch(ctx, 0, in_bytes));
+    double* f = static_cast<double*>(pint_scratch(ctx, 1, sizeof(double) * 2 * n * Q));
+    if (!d || !f) return PINT_E_CUDA;
+    if (!ok(ctx, cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D heat tables"))
+        return PINT_E_CUDA;
+    H.n = n;
+    H.N = N;
+    H.Q = Q;
+    H.step_off = reinterpret_cast<int64_t*>(d);
+    H.slice_dt = reinterpret_cast<double*>(d + b_off);
+    H.r = reinterpret_cast<double*>(d + b_off + b_dt);
+    H.fa = reinterpret_cast<double*>(d + b_off + b_dt + b_q);
+    H.fb = reinterpret_cast<double*>(d + b_off + b_dt + 2 * b_q);
+    H.sx = reinterpret_cast<double*>(d + b_off + b_dt + 3 * b_q);
+    H.factor = f;
+    H.h2d = in_bytes;
+    return launch_heat_factor(ctx, n, Q, H.r, H.factor);
+}
+
+int singular_check(pint_ctx* ctx) {
+    pint_fail fr;
+    if (const int rc = pint_fail_read(ctx, &fr)) return rc;
+    if (fr.index >= 0) {
+        char buf[96];
+        std::snprintf(buf, sizeof buf, "thomas_solve: zero pivot at row %d", static_cast<int>(fr.value));
+        return pint_set_error(ctx, PINT_E_SINGULAR, buf);
+    }
+    return PINT_OK;
+}
+}  // namespace
+
+int pint_run_heat(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int compose_mode,
+                  const double* y0, double* y_out, double* per_slice_seconds, pint_report* report) {
+    if (!ctx || !y_out || N < 1) return PINT_E_INVALID;
+    HostTimer wall;
+    const long long launches0 = ctx->launches;
+    std::vector<pint_slice> sl(static_cast<size_t>(N));
+    if (pint_decompose(0.0, T, N, dt, sl.data()) != PINT_OK)
+        return pint_set_error(ctx, PINT_E_BAD_GRID, "decompose: need N >= 1, T > t0, dt > 0");
+    closure_slices(sl.data(), N, dt, sl);
+    cudaEventRecord(ctx->ev0, ctx->stream);
+    HeatDev H;
+    if (const int rc = heat_upload(ctx, dx, sl, H)) return rc;
+    const int64_t n = H.n, ldm = pint_affine_ldm(n);
+    const size_t map_elems = static_cast<size_t>(n * ldm);
+    // maps (N) + tree scratch (ceil(N/2)) + y0 + y + per-slice timers
+    const size_t b_maps = align256(sizeof(double) * map_elems * N);
+    const size_t b_scr = (compose_mode == PINT_COMPOSE_TREE && N > 1) ? align256(sizeof(double) * map_elems * ((N + 1) / 2)) : 0;
+    const size_t total = b_maps + b_scr + 2 * align256(sizeof(double) * n) + align256(8 * N) + 1024;
+    char* d = static_cast<char*>(pint_scratch(ctx, 2, total));
+    if (!d) return PINT_E_CUDA;
+    Carve cv{d};
+    double* d_maps = cv.take<double>(map_elems * N);
+    double* d_scr = b_scr ? cv.take<double>(map_elems * ((N + 1) / 2)) : nullptr;
+    double* d_y0 = cv.take<double>(n);
+    double* d_y = cv.take<double>(n);
+    auto* d_ns = cv.take<unsigned long long>(N);
+    std::vector<double> y0v;
+    if (!y0) {
+        y0v.resize(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) y0v[i] = std::sin(kPi * static_cast<double>(i + 1) * dx);  // heat_initial
+        y0 = y0v.data();
+    }
+    cudaMemcpyAsync(d_y0, y0, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream);
+    if (per_slice_seconds) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
+    int rc = launch_heat_build(ctx, n, N, H.step_off, H.slice_dt, H.factor, H.r, H.fa, H.fb, H.sx, d_maps,
+                               per_slice_seconds ? d_ns : nullptr);
+    if (rc) return rc;
+    cudaEventRecord(ctx->evc, ctx->stream);
+    if (compose_mode == PINT_COMPOSE_TREE) rc = launch_affine_tree(ctx, n, N, d_maps, d_scr, d_y0, d_y, nullptr);
+    else rc = launch_affine_chain(ctx, n, N, d_maps, d_y0, d_y);
+    if (rc) return rc;
+    cudaEventRecord(ctx->ev1, ctx->stream);
+    cudaMemcpyAsync(y_out, d_y, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream);
+    std::vector<unsigned long long> ns;
+    if (per_slice_seconds) {
+        ns.resize(static_cast<size_t>(N));
+        cudaMemcpyAsync(ns.data(), d_ns, sizeof(unsigned long long) * N, cudaMemcpyDeviceToHost, ctx->stream);
+    }
+    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "run_heat sync")) return PINT_E_CUDA;
+    if ((rc = singular_check(ctx))) return rc;
+    if (per_slice_seconds)
+        for (int64_t j = 0; j < N; ++j) per_slice_seconds[j] = static_cast<double>(ns[j]) * 1e-9;
+    if (report) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        report->message_count = N - 1;
+        report->bytes_communicated = (N - 1) * n * static_cast<int64_t>(sizeof(double));
+        report->extrapolation_count = 0;
+        report->device_ms = ms;
+        report->traj_steps = H.Q * (n + 1);
+        report->gpu_launches = ctx->launches - launches0;
+        report->h2d_bytes = static_cast<int64_t>(H.h2d + sizeof(double) * n);
+        report->d2h_bytes = static_cast<int64_t>(sizeof(double) * n);
+        float cms = 0.f;
+        cudaEventElapsedTime(&cms, ctx->evc, ctx->ev1);
+        report->compose_ms = cms;
+        report->total_ms = wall.ms();
+    }
+    return PINT_OK;
+}
+
+int pint_heat_maps(pint_ctx* ctx, double dx, double dt, const pint_slice* slices, int64_t N, double* G,
+                   double* c) {
+    if (!ctx || !slices || N < 1) return PINT_E_INVALID;
+    std::vector<pint_slice> sl;
+    closure_slices(slices, N, dt, sl);
+    HeatDev H;
+    if (const int rc = heat_upload(ctx, dx, sl, H)) return rc;
+    const int64_t n = H.n, ldm = pint_affine_ldm(n);
+    double* d_maps = static_cast<double*>(pint_scratch(ctx, 2, sizeof(double) * n * ldm * N));
+    if (!d_maps) return PINT_E_CUDA;
+    int rc = launch_heat_build(ctx, n, N, H.step_off, H.slice_dt, H.factor, H.r, H.fa, H.fb, H.sx, d_maps, nullptr);
+    if (rc) return rc;
+    std::vector<double> host(static_cast<size_t>(n * ldm * N));
+    cudaMemcpyAsync(host.data(), d_maps, sizeof(double) * host.size(), cudaMemcpyDeviceToHost, ctx->stream);
+    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "heat_maps sync")) return PINT_E_CUDA;
+    if ((rc = singular_check(ctx))) return rc;
+    for (int64_t j = 0; j < N; ++j)
+        for (int64_t i = 0; i < n; ++i) {
+            const double* row = host.data() + (j * n + i) * ldm;
+            if (G) std::memcpy(G + (j * n + i) * n, row, sizeof(double) * n);
+            if (c) c[j * n + i] = row[n];
+        }
+    return PINT_OK;
+}
+
+int pint_heat_integrate(pint_ctx* ctx, double dx, const pint_slice* slice, double dt_nominal,
+                        int with_forcing, int64_t K, double* y) {
+    if (!ctx || !slice || K < 0) return PINT_E_INVALID;
+    if (K == 0) return PINT_OK;
+    std::vector<pint_slice> sl;
+    closure_slices(slice, 1, dt_nominal, sl);
+    HeatDev H;
+    if (const int rc = heat_upload(ctx, dx, sl, H)) return rc;
+    const int64_t n = H.n;
+    double* d_y = static_cast<double*>(pint_scratch(ctx, 2, sizeof(double) * n * K));
+    if (!d_y) return PINT_E_CUDA;
+    cudaMemcpyAsync(d_y, y, sizeof(double) * n * K, cudaMemcpyHostToDevice, ctx->stream);
+    int rc = launch_heat_integrate(ctx, n, K, 0, H.Q, sl[0].dt, with_forcing, H.factor, H.r, H.fa, H.fb, H.sx, d_y);
+    if (rc) return rc;
+    cudaMemcpyAsync(y, d_y, sizeof(double) * n * K, cudaMemcpyDeviceToHost, ctx->stream);
+    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "heat_integrate sync")) return PINT_E_CUDA;
+    return singular_check(ctx);
+}
+
+int pint_affine_compose(pint_ctx* ctx, int mode, int64_t n, int64_t N, const double* G, const double* c,
+                        const double* y0, double* y_out) {
+    if (!ctx || n < 1 || N < 0 || !y0 || !y_out) return PINT_E_INVALID;
+    if (N == 0) {
+        std::memcpy(y_out, y0, sizeof(double) * n);
+        return PINT_OK;
+    }
+    const int64_t ldm = pint_affine_ldm(n);
+    const size_t map_elems = static_cast<size_t>(n * ldm);
+    std::vector<double> host(map_elems * N, 0.0);
+    for (int64_t j = 0; j < N; ++j)
+        for (int64_t i = 0; i < n; ++i) {
+            double* row = host.data() + (j * n + i) * ldm;
+            std::memcpy(row, G + (j * n + i) * n, sizeof(double) * n);
+            row[n] = c[j * n + i];
+        }
+    const size_t b_maps = align256(sizeof(double) * map_elems * N);
+    const size_t b_scr = align256(sizeof(double) * map_elems * ((N + 1) / 2));
+    char* d = static_cast<char*>(pint_scratch(ctx, 2, b_maps + b_scr + 2 * align256(sizeof(double) * n) + 512));
+    if (!d) return PINT_E_CUDA;
+    Carve cv{d};
+    double* d_maps = cv.take<double>(map_elems * N);
+    double* d_scr = cv.take<double>(map_elems * ((N + 1) / 2));
+    double* d_y0 = cv.take<double>(n);
+    double* d_y = cv.take<double>(n);
+    cudaMemcpyAsync(d_maps, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(d_y0, y0, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream);
+    int rc = pint_affine_compose_dev(ctx, mode, n, N, d_maps, d_scr, d_y0, d_y, nullptr);
+    if (rc) return rc;
+    cudaMemcpyAsync(y_out, d_y, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream);
+    return ok(ctx, cudaStreamSynchronize(ctx->stream), "affine_compose sync") ? PINT_OK : PINT_E_CUDA;
+}
+
+int pint_scalar_sweep(pint_ctx* ctx, int mode, int64_t N, int64_t M, const double* nodes,
+                      int64_t node_stride, const double* weights, const double* values,
+                      const double* a, const double* b, int64_t ab_stride, double y0,
+                      double* lambdas, double* y_out, long long* extrapolations) {
+    if (!ctx || M < 1 || N < 0 || !y_out) return PINT_E_INVALID;
+    const int64_t nsets = node_stride ? N : 1, nab = ab_stride ? N : 1;
+    const size_t b_nodes = align256(sizeof(double) * M * nsets), b_vals = align256(sizeof(double) * M * N);
+    const size_t b_ab = align256(sizeof(double) * nab);
+    const size_t total = 2 * b_nodes + b_vals + 2 * b_ab + align256(sizeof(double) * N) + 1024;
+    char* d = static_cast<char*>(pint_scratch(ctx, 2, total));
+    if (!d) return PINT_E_CUDA;
+    Carve cv{d};
+    double* d_x = cv.take<double>(M * nsets);
+    double* d_w = cv.take<double>(M * nsets);
+    double* d_v = cv.take<double>(M * N);
+    double* d_a = cv.take<double>(nab);
+    double* d_b = cv.take<double>(nab);
+    double* d_lam = cv.take<double>(N);
+    double* d_y = cv.take<double>(1);
+    auto* d_ext = cv.take<long long>(1);
+    cudaMemcpyAsync(d_x, nodes, sizeof(double) * M * nsets, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(d_w, weights, sizeof(double) * M * nsets, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(d_v, values, sizeof(double) * M * N, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(d_a, a, sizeof(double) * nab, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(d_b, b, sizeof(double) * nab, cudaMemcpyHostToDevice, ctx->stream);
+    int rc = launch_scalar_sweep(ctx, mode, N, M, d_x, node_stride ? M : 0, d_w, d_v, d_a, d_b,
+                                 ab_stride ? 1 : 0, y0, d_lam, d_y, d_ext);
+    if (rc) return rc;
+    long long ext = 0;
+    cudaMemcpyAsync(y_out, d_y, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(&ext, d_ext, sizeof ext, cudaMemcpyDeviceToHost, ctx->stream);
+    if (lambdas) cudaMemcpyAsync(lambdas, d_lam, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream);
+    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "scalar_sweep sync")) return PINT_E_CUDA;
+    if (extrapolations) *extrapolations = ext;
+    return PINT_OK;
+}
+
+}  // extern "C"

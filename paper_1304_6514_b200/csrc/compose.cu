@@ -1,0 +1,239 @@
+// K4 — composition of affine slice maps y -> G y + c.
+//
+//  * CHAIN (bit-exact): compose_sweep (nievergelt.cpp:90-110) as one CTA walking the slices in
+//    order; thread i owns row i and accumulates sum_k G(i,k) y_k sequentially in k exactly like
+//    matvec (linalg.cpp:17-26), then adds c_i. Rows are read as 32 B vectors.
+//  * TREE (EXTENSION, north_star subsystem 3): log-depth pairwise products
+//        (G2, c2) o (G1, c1) = (G2 G1, G2 c1 + c2)
+//    on FP64 tensor cores: mma.sync m8n8k4 f64 (SASS DMMA) with 64x64 CTA tiles staged through
+//    bank-conflict-free padded shared memory. Tolerance vs the chain: <= 1e-12 relative.
+//
+// Maps are the row-major augmented blocks [G | c] with leading dimension ldm (pint_cuda.h).
+// Roofline: TREE is FP64 tensor (2 n^3 flops per pair); CHAIN is latency/L2 bound.
+#include "pint_internal.cuh"
+
+namespace {
+
+constexpr int kChainThreads = 256;
+
+// One CTA; thread t owns rows t, t+256, ... Dynamic smem: y[n].
+__global__ void __launch_bounds__(kChainThreads)
+affine_chain_kernel(long long n, long long N, long long ldm, const double* __restrict__ maps,
+                    const double* __restrict__ y0, double* __restrict__ y) {
+    extern __shared__ double y_s[];
+    for (long long i = threadIdx.x; i < n; i += kChainThreads) y_s[i] = y0[i];
+    __syncthreads();
+    const long long n4 = n / 4;
+    for (long long j = 0; j < N; ++j) {
+        const double* M = maps + j * n * ldm;
+        double out[4];
+        int cnt = 0;
+        for (long long i = threadIdx.x; i < n; i += kChainThreads, ++cnt) {
+            const double* row = M + i * ldm;
+            const double4* row4 = reinterpret_cast<const double4*>(row);
+            double s = 0.0;
+#pragma unroll 4
+            for (long long q = 0; q < n4; ++q) {
+                const double4 g = row4[q];
+                s = __dadd_rn(s, __dmul_rn(g.x, y_s[4 * q + 0]));
+                s = __dadd_rn(s, __dmul_rn(g.y, y_s[4 * q + 1]));
+                s = __dadd_rn(s, __dmul_rn(g.z, y_s[4 * q + 2]));
+                s = __dadd_rn(s, __dmul_rn(g.w, y_s[4 * q + 3]));
+            }
+            for (long long k = 4 * n4; k < n; ++k) s = __dadd_rn(s, __dmul_rn(row[k], y_s[k]));
+            if (cnt < 4) out[cnt] = __dadd_rn(s, row[n]);
+        }
+        __syncthreads();
+        cnt = 0;
+        for (long long i = threadIdx.x; i < n && cnt < 4; i += kChainThreads, ++cnt) y_s[i] = out[cnt];
+        __syncthreads();
+    }
+    for (long long i = threadIdx.x; i < n; i += kChainThreads) y[i] = y_s[i];
+}
+
+// ---- DMMA pair kernel ------------------------------------------------------------------------
+constexpr int BM = 64, BN = 64, BK = 16;
+constexpr int AS = BK + 4;   // padded strides: conflict-free fragment loads
+constexpr int BS = BN + 4;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// out_p = later_p o earlier_p for pair p = blockIdx.z. Blocks with blockIdx.x == tilesN
+// compute the translation column c_out = G_later c_earlier + c_later for their 64 rows.
+__global__ void __launch_bounds__(128)
+affine_pair_kernel(long long n, long long ldm, const double* __restrict__ earlier,
+                   long long e_stride, const double* __restrict__ later, long long l_stride,
+                   double* __restrict__ out, long long o_stride, int tilesN) {
+    const long long p = blockIdx.z;
+    const double* E = earlier + p * e_stride;
+    const double* L = later + p * l_stride;
+    double* O = out + p * o_stride;
+    const long long row0 = static_cast<long long>(blockIdx.y) * BM;
+    const int tid = threadIdx.x;
+
+    if (static_cast<int>(blockIdx.x) == tilesN) {  // translation column (GEMV)
+        if (tid < BM && row0 + tid < n) {
+            const long long i = row0 + tid;
+            const double* lr = L + i * ldm;
+            double s = 0.0;
+            for (long long k = 0; k < n; ++k) s = fma(lr[k], E[k * ldm + n], s);
+            O[i * ldm + n] = s + lr[n];
+        }
+        return;
+    }
+
+    __shared__ __align__(16) double As[2][BM * AS];
+    __shared__ __align__(16) double Bs[2][BK * BS];
+    const long long col0 = static_cast<long long>(blockIdx.x) * BN;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+    const int g = lane >> 2, t4 = lane & 3;
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    // register staging: A tile 64x16 and B tile 16x64 as 4 double2 per thread each
+    double2 ra[4], rb[4];
+    auto load_tiles = [&](long long k0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int idx = tid + u * 128;           // 0..511
+            const int ar = idx >> 3, ac = (idx & 7) * 2;
+            const long long gr = row0 + ar, gc = k0 + ac;
+            double2 v = make_double2(0.0, 0.0);
+            if (gr < n) {
+                const double* src = L + gr * ldm + gc;
+                if (gc + 1 < n) v = *reinterpret_cast<const double2*>(src);
+                else if (gc < n) v.x = src[0];
+            }
+            ra[u] = v;
+            const int br = idx >> 5, bc = (idx & 31) * 2;
+            const long long gk = k0 + br, gn = col0 + bc;
+            double2 w = make_double2(0.0, 0.0);
+            if (gk < n) {
+                const double* src = E + gk * ldm + gn;
+                if (gn + 1 < n) w = *reinterpret_cast<const double2*>(src);
+                else if (gn < n) w.x = src[0];
+            }
+            rb[u] = w;
+        }
+    };
+    auto store_tiles = [&](int buf) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int idx = tid + u * 128;
+            const int ar = idx >> 3, ac = (idx & 7) * 2;
+            As[buf][ar * AS + ac] = ra[u].x;
+            As[buf][ar * AS + ac + 1] = ra[u].y;
+            const int br = idx >> 5, bc = (idx & 31) * 2;
+            Bs[buf][br * BS + bc] = rb[u].x;
+            Bs[buf][br * BS + bc + 1] = rb[u].y;
+        }
+    };
+
+    const long long kTiles = (n + BK - 1) / BK;
+    load_tiles(0);
+    store_tiles(0);
+    __syncthreads();
+    for (long long kt = 0; kt < kTiles; ++kt) {
+        const int buf = static_cast<int>(kt & 1);
+        if (kt + 1 < kTiles) load_tiles((kt + 1) * BK);
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) af[mi] = As[buf][(wm * 32 + mi * 8 + g) * AS + kk + t4];
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) bf[ni] = Bs[buf][(kk + t4) * BS + wn * 32 + ni * 8 + g];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+        }
+        if (kt + 1 < kTiles) store_tiles(buf ^ 1);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+        const long long r = row0 + wm * 32 + mi * 8 + g;
+        if (r >= n) continue;
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+            const long long c = col0 + wn * 32 + ni * 8 + t4 * 2;
+            if (c + 1 < n) {
+                *reinterpret_cast<double2*>(O + r * ldm + c) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+            } else if (c < n) {
+                O[r * ldm + c] = acc[mi][ni][0];
+            }
+        }
+    }
+}
+
+int launch_pairs(pint_ctx* ctx, long long n, long long P, const double* earlier, long long e_stride,
+                 const double* later, long long l_stride, double* out, long long o_stride) {
+    if (P <= 0) return PINT_OK;
+    const long long ldm = pint_affine_ldm(n);
+    const int tilesN = static_cast<int>((n + BN - 1) / BN);
+    const unsigned tilesM = static_cast<unsigned>((n + BM - 1) / BM);
+    if (P > 65535) return pint_set_error(ctx, PINT_E_INVALID, "affine_pair: too many pairs per launch");
+    dim3 grid(static_cast<unsigned>(tilesN + 1), tilesM, static_cast<unsigned>(P));
+    affine_pair_kernel<<<grid, 128, 0, ctx->stream>>>(n, ldm, earlier, e_stride, later, l_stride, out,
+                                                      o_stride, tilesN);
+    return pint_check_launch(ctx, "affine_pair_kernel");
+}
+
+}  // namespace
+
+int launch_affine_chain(pint_ctx* ctx, int64_t n, int64_t N, const double* maps, const double* y0,
+                        double* y) {
+    if (n < 1 || N < 0) return pint_set_error(ctx, PINT_E_INVALID, "affine_chain: bad sizes");
+    if (n > 4 * kChainThreads) return pint_set_error(ctx, PINT_E_INVALID, "affine_chain: n > 1024 unsupported");
+    const size_t smem = sizeof(double) * static_cast<size_t>(n);
+    affine_chain_kernel<<<1, kChainThreads, smem, ctx->stream>>>(n, N, pint_affine_ldm(n), maps, y0, y);
+    return pint_check_launch(ctx, "affine_chain_kernel");
+}
+
+int launch_affine_pair(pint_ctx* ctx, int64_t n, int64_t P, const double* earlier,
+                       const double* later, double* out) {
+    const long long stride = n * pint_affine_ldm(n);
+    return launch_pairs(ctx, n, P, earlier, stride, later, stride, out, stride);
+}
+
+// The log-depth tree: level by level, pairs (2p, 2p+1) of `src` into `dst`, odd tail copied.
+int launch_affine_tree(pint_ctx* ctx, int64_t n, int64_t N, double* maps, double* scratch,
+                       const double* y0, double* y, double* composed) {
+    if (N < 1) return pint_set_error(ctx, PINT_E_INVALID, "affine_tree: N >= 1 required");
+    const long long stride = n * pint_affine_ldm(n);
+    double* src = maps;
+    double* dst = scratch;
+    long long count = N;
+    while (count > 1) {
+        const long long pairs = count / 2;
+        for (long long p0 = 0; p0 < pairs; p0 += 65535) {
+            const long long P = (pairs - p0 < 65535) ? pairs - p0 : 65535;
+            const int rc = launch_pairs(ctx, n, P, src + 2 * p0 * stride, 2 * stride,
+                                        src + (2 * p0 + 1) * stride, 2 * stride, dst + p0 * stride, stride);
+            if (rc) return rc;
+        }
+        if (count & 1) {
+            if (cudaMemcpyAsync(dst + pairs * stride, src + (count - 1) * stride, sizeof(double) * stride,
+                                cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess)
+                return pint_set_error(ctx, PINT_E_CUDA, "affine_tree: tail copy failed");
+        }
+        double* t = src;
+        src = dst;
+        dst = t;
+        count = pairs + (count & 1);
+    }
+    if (composed && composed != src &&
+        cudaMemcpyAsync(composed, src, sizeof(double) * stride, cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess)
+        return pint_set_error(ctx, PINT_E_CUDA, "affine_tree: composed copy failed");
+    return launch_affine_chain(ctx, n, 1, src, y0, y);
+}

@@ -1,0 +1,94 @@
+"""CPU-side checks of the drop-in boundary: libpint_cuda.so loads without a GPU, exports every
+function include/pint_cuda.h declares, and its host-side table functions (decompose, steps_for,
+sample_nodes) are bit-identical to the reference (via the pinned oracle). No compute calls."""
+import pathlib
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1304_6514_b200 import capi, pint
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+
+
+def declared_functions():
+    text = (ROOT / "include" / "pint_cuda.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(pint_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = capi.load()
+    names = declared_functions()
+    assert len(names) >= 30
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(capi.EXPORTED)
+
+
+def test_version_string():
+    assert "sm_100a" in capi.version()
+
+
+def test_no_device_fails_loudly():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(capi.PintError):
+        capi.Context(0)
+
+
+@pytest.mark.parametrize("args", [(0.0, 0.5, 4, 0.01), (0.0, 0.5, 64, 1e-4), (0.0, 0.5, 7, 1e-3),
+                                  (0.0, 10.0, 256, 10.0 / 65536), (0.0, 10.0, 4096, 10.0 / 65536)])
+def test_host_decompose_is_the_reference(args):
+    dec = pint.decompose(*args)
+    tb, te, st, h = O.decompose(*args)
+    assert np.array_equal([s.t_begin for s in dec.slices], tb)
+    assert np.array_equal([s.t_end for s in dec.slices], te)
+    assert np.array_equal([s.steps for s in dec.slices], st)
+    assert np.array_equal([s.dt for s in dec.slices], h)
+
+
+def test_host_nodes_are_the_reference(golden):
+    for M in (1, 2, 5, 6, 7, 33, 64, 512):
+        assert np.array_equal(pint.cheb_nodes_second_kind(M, 0.0, 2.0), golden[f"nodes2_{M}"])
+        assert np.array_equal(pint.cheb_nodes(M, 0.0, 2.0), golden[f"nodes1_{M}"])
+
+
+def test_host_steps_for(golden):
+    for w, dt, s in zip(golden["steps_for_width"], golden["steps_for_dt"], golden["steps_for_steps"]):
+        assert pint.steps_for(w, dt) == s
+
+
+def test_heat_coefficient_tables_match_reference_arithmetic():
+    """The per-step tables the device consumes equal the reference's in-loop values."""
+    import ctypes as C
+    import math
+
+    dx, dt, T, N = 0.1, 0.005, 10.0, 4
+    dec = pint.decompose(0.0, T, N, dt)
+    arr = (capi.Slice * N)(*[s.c() for s in dec.slices])
+    Q = sum(s.steps for s in dec.slices)
+    off = np.empty(N + 1, dtype=np.int64)
+    r, fa, fb = (np.empty(Q) for _ in range(3))
+    sx = np.empty(9)
+    n = C.c_int64()
+    assert capi.load().pint_heat_coefficients(dx, arr, N, capi.ptr(off), capi.ptr(r), capi.ptr(fa),
+                                              capi.ptr(fb), capi.ptr(sx), C.byref(n)) == 0
+    assert n.value == 9 and off[-1] == Q
+    s = dec.slices[2]
+    for i in (1, 7, s.steps):
+        t = s.t_begin + i * s.dt
+        q = off[2] + i - 1
+        assert r[q] == s.dt * O.lib().or_heat_coefficient(t) * (1.0 / (dx * dx))
+        for k in range(9):
+            x = (k + 1) * dx
+            b = fa[q] * sx[k] + fb[q] * sx[k]
+            assert b == O.lib().or_heat_forcing(x, t)
+
+
+def test_affine_ldm():
+    assert [capi.load().pint_affine_ldm(n) for n in (1, 3, 4, 9, 128, 512)] == [4, 4, 8, 12, 132, 516]

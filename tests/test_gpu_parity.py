@@ -1,0 +1,391 @@
+"""GPU parity: the sm_100a path (libpint_cuda.so via the C ABI) against the reference.
+
+Reference-backed paths are compared BIT-EXACTLY (np.array_equal on float64) against the golden
+fixtures produced by the unmodified reference and against the pinned C oracle. EXTENSION paths
+(RK4, Lotka-Volterra, bilinear maps, tree composition) are compared with the tolerance stated in
+each test (north_star: <= 1e-12 relative in FP64, <= 1e-5 in FP32); bracket indices bit-exact.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1304_6514_b200 import capi, pint
+
+pytestmark = pytest.mark.gpu
+
+REL_F64 = 1e-12
+REL_F32 = 1e-5
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    c = pint.context()
+    yield c
+
+
+def dev(x, dtype=None):
+    import torch
+
+    t = torch.as_tensor(np.ascontiguousarray(x))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def run_scalar(ctx, ivp, N, dt, M, a=0.0, b=2.0, weights=capi.WEIGHTS_PRODUCT, sweep=capi.SWEEP_EXACT,
+               kind=capi.NODES_SECOND_KIND):
+    rhs = ivp.device_rhs()
+    y = C.c_double()
+    ends = np.empty(N * M)
+    lam = np.empty(N)
+    rep = capi.Report()
+    fail = capi.Fail()
+    rc = ctx.lib.pint_run_scalar(ctx.h, C.byref(rhs), ivp.t0, ivp.T, ivp.y0, N, dt, kind, M, a, b, weights, sweep,
+                                 C.byref(y), capi.ptr(ends), capi.ptr(lam), None, C.byref(rep), C.byref(fail))
+    return rc, y.value, ends.reshape(N, M), lam, rep, fail
+
+
+SCALAR_RUNS = [
+    ("sc_N4_M5_1em4", 4, 1e-4, 5, 0.0, 2.0),
+    ("sc_N4_M6_1em4", 4, 1e-4, 6, 0.0, 2.0),
+    ("sc_N4_M7_1em4", 4, 1e-4, 7, 0.0, 2.0),
+    ("sc_N64_M6_1em4", 64, 1e-4, 6, 0.0, 2.0),
+    ("sc_N8_M6_1em3", 8, 1e-3, 6, 0.0, 2.0),
+    ("sc_N16_M33_1em3", 16, 1e-3, 33, 0.0, 2.0),
+    ("sc_N64_M64_1em4", 64, 1e-4, 64, 0.0, 2.0),
+    ("sc_extrap_N4_M5_1em3", 4, 1e-3, 5, 0.0, 0.5),
+]
+
+
+@pytest.mark.parametrize("tag,N,dt,M,a,b", SCALAR_RUNS)
+def test_scalar_pipeline_bit_exact_vs_reference(ctx, golden, tag, N, dt, M, a, b):
+    rc, y, ends, lam, rep, fail = run_scalar(ctx, pint.make_model_problem(), N, dt, M, a, b)
+    assert rc == 0 and fail.index == -1
+    assert np.array_equal(ends, golden[tag + "_endpoints"])
+    assert np.array_equal(lam, golden[tag + "_lambdas"])
+    assert y == golden[tag + "_final"][0]
+    assert rep.extrapolation_count == golden[tag + "_extrapolation_count"][0]
+    assert rep.message_count == N - 1 and rep.bytes_communicated == 8 * (N - 1)
+    assert rep.gpu_launches >= 3
+
+
+def test_scalar_M512_reference_limit(ctx, golden):
+    rc, y, ends, _, _, _ = run_scalar(ctx, pint.make_model_problem(), 64, 1e-4, 512)
+    assert rc == 0
+    assert y == golden["sc_N64_M512_1em4_final"][0]
+    _, _, st, h = O.decompose(0.0, 0.5, 64, 1e-4)
+    want, fail, _ = O.riccati_ensemble(st, h, O.cheb_nodes(512, 0.0, 2.0))
+    assert fail == -1 and np.array_equal(ends, want)
+
+
+@pytest.mark.parametrize("S", [79, 782])
+def test_scalar_config1_shape_bit_exact(ctx, S):
+    """Config 1 shape at the reference limit (N=64, M=512), dt = 0.5/(64 S): every endpoint."""
+    N, M = 64, 512
+    dt = 0.5 / (N * S)
+    rc, y, ends, lam, _, _ = run_scalar(ctx, pint.make_model_problem(), N, dt, M)
+    assert rc == 0
+    _, _, st, h = O.decompose(0.0, 0.5, N, dt)
+    x = O.cheb_nodes(M, 0.0, 2.0)
+    want, _, _ = O.riccati_ensemble(st, h, x)
+    assert np.array_equal(ends, want)
+    yo, lo, _ = O.scalar_sweep(x, O.bary_weights(x), want, 0.0, 2.0, 1.0)
+    assert np.array_equal(lam, lo) and y == yo
+
+
+def test_table1_grid_bit_exact(ctx, golden):
+    errs = np.empty((5, 5))
+    for r, dt in enumerate([0.01, 0.005, 0.0025, 0.001, 0.0001]):
+        for c, M in enumerate([3, 4, 5, 6, 7]):
+            rc, y, *_ = run_scalar(ctx, pint.make_model_problem(), 4, dt, M)
+            assert rc == 0
+            errs[r, c] = abs(y - 2.0)
+    assert np.array_equal(errs, golden["table1_errors"])
+
+
+def test_riccati_failure_reports_lowest_task(ctx):
+    """NoRealRoot inside the ensemble -> TaskFailure with the lowest failing idx (exec_harness.hpp:88-99)."""
+    ivp = pint.make_model_problem()
+    N, M, dt = 4, 9, 0.01
+    rc, _, ends, _, _, fail = run_scalar(ctx, ivp, N, dt, M, 0.0, 40.0)
+    _, _, st, h = O.decompose(0.0, 0.5, N, dt)
+    _, want_idx, want_val = O.riccati_ensemble(st, h, O.cheb_nodes(M, 0.0, 40.0))
+    assert rc == capi.PINT_E_NO_REAL_ROOT
+    assert want_idx >= 0 and fail.index == want_idx and fail.value == want_val
+    with pytest.raises(pint.TaskFailure) as ei:
+        pint.run_nievergelt(ivp, N, dt, pint.InitialValueSpace(a=0.0, b=40.0, M=M), pint.ExecConfig())
+    assert ei.value.task_index == want_idx
+
+
+@pytest.mark.parametrize("M", [2, 5, 6, 7, 33, 64, 512])
+def test_weights_bit_exact(ctx, golden, M):
+    assert np.array_equal(pint.barycentric_weights(golden[f"nodes2_{M}"]), golden[f"weights2_{M}"])
+    assert np.array_equal(pint.barycentric_weights(golden[f"nodes2_{M}"], "closed2"), O.bary_weights_closed2(M))
+
+
+def test_duplicate_nodes(ctx):
+    with pytest.raises(pint.DuplicateNodes):
+        pint.barycentric_weights([0.0, 1.0, 1.0])
+
+
+def test_interp_eval_bit_exact(ctx, golden):
+    f = pint.InterpolantData(golden["nodes2_33"], golden["weights2_33"], golden["interp33_values"], 0.0, 2.0)
+    got = np.array([pint.interp_eval(f, q) for q in golden["interp33_xi"]])
+    assert np.array_equal(got, golden["interp33_out"])
+
+
+def test_tree_sweep_within_tolerance(ctx):
+    N, M, dt = 64, 512, 0.5 / (64 * 79)
+    rc, y_exact, *_ = run_scalar(ctx, pint.make_model_problem(), N, dt, M)
+    rc2, y_tree, *_ = run_scalar(ctx, pint.make_model_problem(), N, dt, M, sweep=capi.SWEEP_TREE)
+    assert rc == 0 and rc2 == 0
+    assert abs(y_tree - y_exact) <= REL_F64 * abs(y_exact)
+
+
+def test_scalar_M1024_closed_form(ctx):
+    """Config 1 at M=1024 (reference weights overflow): closed-form weights vs the oracle."""
+    N, M = 64, 1024
+    dt = 0.5 / (N * 79)
+    rc, y, ends, lam, _, _ = run_scalar(ctx, pint.make_model_problem(), N, dt, M, weights=capi.WEIGHTS_CLOSED2)
+    assert rc == 0
+    _, _, st, h = O.decompose(0.0, 0.5, N, dt)
+    x = O.cheb_nodes(M, 0.0, 2.0)
+    want, _, _ = O.riccati_ensemble(st, h, x)
+    assert np.array_equal(ends, want)
+    yo, lo, _ = O.scalar_sweep(x, O.bary_weights_closed2(M), want, 0.0, 2.0, 1.0)
+    assert np.array_equal(lam, lo) and y == yo
+    assert abs(y - 2.0) < 1e-3
+
+
+# ---- EXTENSION: logistic RK4 ------------------------------------------------------------------
+
+@pytest.mark.parametrize("S", [4, 98])
+def test_logistic_rk4_f64_matches_oracle(ctx, S):
+    ivp = pint.make_logistic_problem()
+    N, M = 64, 1024
+    dt = ivp.T / (N * S)
+    rc, y, ends, lam, _, _ = run_scalar(ctx, ivp, N, dt, M, 0.0, 1.25, weights=capi.WEIGHTS_CLOSED2)
+    assert rc == 0
+    _, _, st, h = O.decompose(0.0, ivp.T, N, dt)
+    x = O.cheb_nodes(M, 0.0, 1.25)
+    want = O.logistic_rk4_ensemble(st, h, x, 1.0, 1.0)
+    assert np.max(np.abs(ends - want) / np.abs(want)) <= REL_F64
+    assert np.array_equal(ends, want)  # same explicit-fma op order: bit-exact in practice
+    assert abs(y - ivp.exact(ivp.T)) < 1e-6
+
+
+def test_logistic_rk4_f32_matches_oracle(ctx):
+    N, M, S = 64, 1024, 98
+    _, _, st, h = O.decompose(0.0, 10.0, N, 10.0 / (N * S))
+    x = O.cheb_nodes(M, 0.0, 1.25).astype(np.float32)
+    ends = dev(np.zeros(N * M, dtype=np.float32))
+    rhs = capi.ScalarRHS(capi.RHS_LOGISTIC_RK4, capi.F32, 1.0, 1.0)
+    ctx.call("pint_scalar_ensemble_dev", C.byref(rhs), N, M, capi.ptr(dev(st)), capi.ptr(dev(h)),
+             capi.ptr(dev(x)), capi.ptr(ends), None)
+    ctx.sync()
+    got = ends.cpu().numpy().reshape(N, M)
+    want32 = O.logistic_rk4_ensemble_f32(st, h, x, 1.0, 1.0)
+    want64 = O.logistic_rk4_ensemble(st, h, x.astype(np.float64), 1.0, 1.0)
+    assert np.array_equal(got, want32)
+    assert np.max(np.abs(got - want64) / np.abs(want64)) <= REL_F32
+
+
+# ---- EXTENSION: 2-D Lotka-Volterra + bilinear -------------------------------------------------
+
+LV = [1.5, 1.0, 1.0, 3.0]
+
+
+def lv_run(ctx, N, Mu, Mv, S, T=10.0, lo=0.1, hi=8.0):
+    import torch
+
+    _, _, st, h = O.decompose(0.0, T, N, T / (N * S))
+    un, vn = O.uniform_nodes(Mu, lo, hi), O.uniform_nodes(Mv, lo, hi)
+    tables = torch.empty(N * 2 * Mu * Mv, dtype=torch.float64, device="cuda")
+    ctx.call("pint_lv_ensemble_dev", N, Mu, Mv, capi.ptr(dev(st)), capi.ptr(dev(h)), capi.ptr(dev(un)),
+             capi.ptr(dev(vn)), capi.ptr(np.array(LV)), capi.ptr(tables))
+    lam = torch.empty(2 * N, dtype=torch.float64, device="cuda")
+    br = torch.empty(2 * N, dtype=torch.int64, device="cuda")
+    ext = torch.empty(1, dtype=torch.int64, device="cuda")
+    ctx.call("pint_bilinear_sweep_dev", N, Mu, Mv, capi.ptr(dev(un)), capi.ptr(dev(vn)), capi.ptr(tables), 1.0, 1.0,
+             capi.ptr(lam), capi.ptr(br), capi.ptr(ext))
+    ctx.sync()
+    return st, h, un, vn, tables, lam.cpu().numpy().reshape(N, 2), br.cpu().numpy().reshape(N, 2), int(ext.item())
+
+
+def test_lv_small_bit_exact(ctx):
+    N, Mu, Mv, S = 8, 17, 13, 8
+    st, h, un, vn, tables, lam, br, ext = lv_run(ctx, N, Mu, Mv, S)
+    want = O.lv_rk4_ensemble(st, h, un, vn, LV)
+    got = tables.cpu().numpy().reshape(N, 2, Mu, Mv)
+    assert np.max(np.abs(got - want) / np.abs(want)) <= REL_F64
+    assert np.array_equal(got, want)
+    wl, wb, wext = O.bilinear_sweep(un, vn, want, 1.0, 1.0)
+    assert np.array_equal(br, wb)  # bracket indices bit-exact
+    assert np.array_equal(lam, wl) and ext == wext
+
+
+def test_lv_config3_shape(ctx):
+    """Config 3: 512 slices x 256x256 tensor grid, RK4 S=8; spot-check slices + full sweep."""
+    N, Mu, Mv, S = 512, 256, 256, 8
+    st, h, un, vn, tables, lam, br, ext = lv_run(ctx, N, Mu, Mv, S)
+    P = Mu * Mv
+    got = tables.view(N, 2, P)
+    for j in (0, 137, 511):
+        sub = O.lv_rk4_subset(j * P, j * P + 4096, st, h, un, vn, LV)
+        g = got[j, :, :4096].cpu().numpy().T
+        assert np.array_equal(g, sub)
+    wl, wb, wext = O.bilinear_sweep(un, vn, tables.cpu().numpy().reshape(N, 2, Mu, Mv), 1.0, 1.0)
+    assert np.array_equal(br, wb) and np.array_equal(lam, wl) and ext == wext
+    # the LV first integral V = d u - g ln u + b v - a ln v is ~conserved along the composed orbit
+    V = lambda u, v: LV[2] * u - LV[3] * np.log(u) + LV[1] * v - LV[0] * np.log(v)
+    assert abs(V(lam[-1, 0], lam[-1, 1]) - V(1.0, 1.0)) < 5e-3
+
+
+# ---- heat affine path -------------------------------------------------------------------------
+
+def test_heat9_maps_bit_exact(ctx, golden):
+    prob = pint.make_heat_problem(0.1, 0.005, 10.0)
+    dec = pint.decompose(0.0, 10.0, 4, 0.005)
+    G, c = pint.build_affine_propagators(prob, dec)
+    assert np.array_equal(G, golden["heat9_G"])
+    assert np.array_equal(c, golden["heat9_c"])
+    p1 = pint.build_affine_propagator(prob, dec.slices[1])
+    assert np.array_equal(p1.G, golden["heat9_G"][1]) and np.array_equal(p1.c, golden["heat9_c"][1])
+
+
+def test_heat9_run_bit_exact(ctx, golden):
+    prob = pint.make_heat_problem(0.1, 0.005, 10.0)
+    r = pint.run_nievergelt(prob, 4, pint.ExecConfig())
+    assert np.array_equal(r.final_state, golden["heat9_N4_final"])
+    assert r.error_vs_serial == golden["heat9_N4_error_vs_serial"][0]
+    assert r.message_count == 3 and r.bytes_communicated == golden["heat9_N4_bytes"][0]
+    s = pint.run_serial(prob)
+    assert np.array_equal(s.final_state, golden["heat9_serial_final"])
+    assert s.error_vs_exact == golden["heat9_serial_error"][0]
+    direct = prob.integrate(pint.decompose(0.0, 10.0, 4, 0.005).slices[1], golden["heat9_direct_y"], prob.dt, True)
+    assert np.array_equal(direct, golden["heat9_direct_out"])
+
+
+def test_heat128_bit_exact(ctx, golden):
+    dx, dt = 1.0 / 129.0, 10.0 / (16 * 32)
+    prob = pint.make_heat_problem(dx, dt, 10.0)
+    dec = pint.decompose(0.0, 10.0, 16, dt)
+    p5 = pint.build_affine_propagator(prob, dec.slices[5])
+    assert np.array_equal(p5.G, golden["heat128_slice5_G"])
+    assert np.array_equal(p5.c, golden["heat128_slice5_c"])
+    r = pint.run_nievergelt(prob, 16, pint.ExecConfig())
+    assert np.array_equal(r.final_state, golden["heat128_N16_final"])
+    assert np.array_equal(pint.run_serial(prob).final_state, golden["heat128_serial_final"])
+    rt = pint.run_nievergelt(prob, 16, pint.ExecConfig(), compose="tree")
+    gap = np.max(np.abs(rt.final_state - r.final_state)) / np.max(np.abs(r.final_state))
+    assert gap <= REL_F64
+
+
+def test_heat_config2_shape(ctx):
+    """Config 2: n=128, N=256 slices x S=256 steps. Spot-check slice maps bit-exact against the
+    oracle, the chain bit-exact against the oracle chain over the device's maps, tree <= 1e-12."""
+    import torch
+
+    N, S = 256, 256
+    dx, dt = 1.0 / 129.0, 10.0 / (N * S)
+    prob = pint.make_heat_problem(dx, dt, 10.0)
+    dec = pint.decompose(0.0, 10.0, N, dt)
+    G, c = pint.build_affine_propagators(prob, dec)
+    for j in (0, 101, 255):
+        s = dec.slices[j]
+        Gw, cw = O.heat_build(dx, s.t_begin, s.t_end, dt)
+        assert np.array_equal(G[j], Gw) and np.array_equal(c[j], cw)
+    y_chain = O.affine_chain(G, c, prob.y0)
+    r = pint.run_nievergelt(prob, N, pint.ExecConfig())
+    assert np.array_equal(r.final_state, y_chain)
+    rt = pint.run_nievergelt(prob, N, pint.ExecConfig(), compose="tree")
+    assert np.max(np.abs(rt.final_state - y_chain)) / np.max(np.abs(y_chain)) <= REL_F64
+    assert r.error_vs_serial <= 1e-10  # acceptance criterion 3's bound
+    assert r.traj_steps == N * S * 129
+
+
+def test_affine_tree_random_maps(ctx):
+    rng = np.random.default_rng(1304)
+    for N, n in [(1, 5), (2, 9), (13, 9), (64, 128), (7, 200)]:
+        G = rng.uniform(-1, 1, (N, n, n)) / np.sqrt(n)
+        c = rng.uniform(-1, 1, (N, n))
+        y0 = rng.uniform(-1, 1, n)
+        chain = O.affine_chain(G, c, y0)
+        ctx_ = pint.context()
+        y = np.empty(n)
+        ctx_.check(ctx_.lib.pint_affine_compose(ctx_.h, capi.COMPOSE_CHAIN, n, N, capi.ptr(G), capi.ptr(c),
+                                                capi.ptr(y0), capi.ptr(y)))
+        assert np.array_equal(y, chain)
+        ctx_.check(ctx_.lib.pint_affine_compose(ctx_.h, capi.COMPOSE_TREE, n, N, capi.ptr(G), capi.ptr(c),
+                                                capi.ptr(y0), capi.ptr(y)))
+        _, _, tree = O.affine_tree(G, c, y0)
+        scale = max(1.0, np.max(np.abs(chain)))
+        assert np.max(np.abs(y - tree)) <= REL_F64 * scale
+        assert np.max(np.abs(y - chain)) <= 1e-11 * scale
+
+
+def test_affine_compose_order(ctx):
+    """test_nievergelt.cpp:104-118: maps applied in slice order."""
+    maps = []
+    for j in range(3):
+        G = np.eye(2)
+        G[0, 0] = 2.0
+        maps.append(pint.AffinePropagator(j, G, np.array([0.0, 1.0])))
+    stats = pint.SweepStats()
+    out = pint.compose_sweep(maps, np.array([1.0, 0.0]), 0.0, stats)
+    assert out[0] == 8.0 and out[1] == 3.0
+    assert stats.message_count == 2 and stats.bytes_communicated == 2 * 2 * 8
+
+
+def test_reference_unit_tests_scalar(ctx):
+    """test_nievergelt.cpp:14-74 through the Python mirror."""
+    ivp = pint.make_model_problem()
+    dec = pint.decompose(0.0, 0.5, 4, 0.01)
+    space = pint.InitialValueSpace(M=6)
+    m = pint.build_scalar_slice_map(ivp, dec.slices[0], space, 0.01)
+    for k in range(6):
+        assert pint.interp_eval(m.interpolant, m.interpolant.nodes[k]) == m.interpolant.values[k]
+    assert np.all(np.diff(m.interpolant.values) > 0)
+    r6 = pint.run_nievergelt(ivp, 4, 1e-4, space, pint.ExecConfig())
+    assert r6.error_vs_exact == pytest.approx(2.9623e-4, rel=5e-3)
+    assert (r6.method, r6.N, r6.M, r6.message_count, r6.bytes_communicated, len(r6.per_slice_compute)) == \
+        ("nievergelt", 4, 6, 3, 24, 4)
+    r1 = pint.run_nievergelt(ivp, 1, 1e-3, space, pint.ExecConfig())
+    assert r1.message_count == 0 and r1.final_state[0] == pint.run_serial(ivp, 1e-3).final_state[0]
+    rx = pint.run_nievergelt(ivp, 4, 1e-3, pint.InitialValueSpace(a=0.0, b=0.5, M=5), pint.ExecConfig())
+    assert rx.extrapolation_count >= 1
+
+
+def test_latency_accounting(ctx):
+    """acceptance.cpp:164-207: N-1 messages, T_comm within [N-1, 3(N-1)] x latency."""
+    ivp = pint.make_model_problem()
+    for N in (2, 8):
+        r = pint.run_nievergelt(ivp, N, 1e-4, pint.InitialValueSpace(M=6), pint.ExecConfig(latency_per_receive=1e-3))
+        assert r.message_count == N - 1
+        assert (N - 1) * 1e-3 <= r.T_comm <= 3 * (N - 1) * 1e-3
+
+
+def test_repeatable_bit_identical(ctx):
+    """acceptance.cpp:297-369 analogue: repeated device runs are bit-identical."""
+    ivp = pint.make_model_problem()
+    rs = [pint.run_nievergelt(ivp, 8, 1e-3, pint.InitialValueSpace(M=6), pint.ExecConfig(workers=w)) for w in (1, 2, 8)]
+    assert all(np.array_equal(r.final_state, rs[0].final_state) for r in rs)
+    prob = pint.make_heat_problem(0.1, 0.005, 10.0)
+    hs = [pint.run_nievergelt(prob, 4, pint.ExecConfig(workers=w)) for w in (1, 2, 8)]
+    assert all(np.array_equal(h.final_state, hs[0].final_state) for h in hs)
+
+
+def test_per_slice_compute_halves(ctx):
+    """acceptance.cpp:372-394 analogue: max per-slice device time ~ 1/N."""
+    prob = pint.make_heat_problem(0.02, 2.5e-4, 10.0)
+    mx = []
+    for N in (2, 4, 8):
+        r = pint.run_nievergelt(prob, N, pint.ExecConfig())
+        mx.append(max(r.per_slice_compute))
+    for a, b in zip(mx, mx[1:]):
+        assert 0.3 < b / a < 0.7
