@@ -144,21 +144,23 @@ int64_t pint_heat_total_steps(const pint_slice* slices, int64_t N);
  * fa[q] = -sin t, fb[q] = ((a(t) pi) pi) cos t; sx[i] = sin(pi (i+1) dx). n = interior points. */
 int pint_heat_coefficients(double dx, const pint_slice* slices, int64_t N, int64_t* step_off,
                            double* r, double* fa, double* fb, double* sx, int64_t* n_out);
-/* Shared tridiagonal factor per step (the Thomas forward pivots, linalg.cpp:77-93):
- * factor[q*n + i] = {pivot_i, c_i} for every step q < total_steps. */
+/* doubles per step record (see pint_heat_factor_dev) */
+int64_t pint_heat_record_stride(int64_t n);
+/* Shared tridiagonal factor per step — the Thomas forward pivots (linalg.cpp:77-93), computed
+ * once per (slice, step) instead of once per trajectory. records[q * stride ...] =
+ * {-r, fa, fb, 0, p[0..n), RN(1/p)[0..n), c[0..n)} for every step q < total_steps. */
 int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t total_steps, const double* r,
-                         double* factor /* total_steps * n * 2 */);
-/* Build all N augmented maps into maps (N * n * ldm doubles). slices/step_off are device
- * copies of the host tables. */
+                         const double* fa, const double* fb, double* records);
+/* Build all N augmented maps into maps (N * n * ldm doubles). step_off/slice_dt/sx are device
+ * copies of the host tables; per_slice_ns (may be NULL) accumulates per-slice device time. */
 int pint_heat_build_dev(pint_ctx* ctx, int64_t n, int64_t N, const int64_t* step_off,
-                        const double* slice_dt, const double* factor, const double* r,
-                        const double* fa, const double* fb, const double* sx, double* maps,
-                        unsigned long long* per_slice_ns);
+                        const double* slice_dt, const double* records, const double* sx,
+                        double* maps, unsigned long long* per_slice_ns);
 /* Integrate K state vectors y[k*n ...] in place through the steps [q0, q0+steps) of the
- * tables (the integrate closure for one slice, or run_serial over one whole-interval slice). */
+ * records (the integrate closure for one slice, or run_serial over one whole-interval slice). */
 int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t q0, int64_t steps,
-                            double h, int with_forcing, const double* factor, const double* r,
-                            const double* fa, const double* fb, const double* sx, double* y);
+                            double h, int with_forcing, const double* records, const double* sx,
+                            double* y);
 
 /* ---- K4: affine composition (compose_sweep, nievergelt.cpp:90-110) ----
  * CHAIN: y <- G_j y + c_j in slice order, rows as sequential dots (bit-exact vs matvec,

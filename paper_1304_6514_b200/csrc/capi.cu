@@ -328,24 +328,26 @@ int pint_scalar_sweep_dev(pint_ctx* ctx, int mode, int64_t N, int64_t M, const d
                                y0, lambdas, y_out, extrapolations);
 }
 
-int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t total_steps, const double* r, double* factor) {
+int64_t pint_heat_record_stride(int64_t n) { return heat_record_stride(n); }
+
+int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t total_steps, const double* r, const double* fa,
+                         const double* fb, double* records) {
     if (!ctx) return PINT_E_INVALID;
-    return launch_heat_factor(ctx, n, total_steps, r, factor);
+    return launch_heat_factor(ctx, n, total_steps, r, fa, fb, records);
 }
 
 int pint_heat_build_dev(pint_ctx* ctx, int64_t n, int64_t N, const int64_t* step_off,
-                        const double* slice_dt, const double* factor, const double* r,
-                        const double* fa, const double* fb, const double* sx, double* maps,
-                        unsigned long long* per_slice_ns) {
+                        const double* slice_dt, const double* records, const double* sx,
+                        double* maps, unsigned long long* per_slice_ns) {
     if (!ctx) return PINT_E_INVALID;
-    return launch_heat_build(ctx, n, N, step_off, slice_dt, factor, r, fa, fb, sx, maps, per_slice_ns);
+    return launch_heat_build(ctx, n, N, step_off, slice_dt, records, sx, maps, per_slice_ns);
 }
 
 int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t q0, int64_t steps,
-                            double h, int with_forcing, const double* factor, const double* r,
-                            const double* fa, const double* fb, const double* sx, double* y) {
+                            double h, int with_forcing, const double* records, const double* sx,
+                            double* y) {
     if (!ctx) return PINT_E_INVALID;
-    return launch_heat_integrate(ctx, n, K, q0, steps, h, with_forcing, factor, r, fa, fb, sx, y);
+    return launch_heat_integrate(ctx, n, K, q0, steps, h, with_forcing, records, sx, y);
 }
 
 int pint_affine_compose_dev(pint_ctx* ctx, int mode, int64_t n, int64_t N, double* maps,
@@ -588,7 +590,7 @@ int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, Hea
     for (int64_t j = 0; j < N; ++j) h_dt[j] = sl[j].dt;
     pint_heat_coefficients(dx, sl.data(), N, h_off, h_r, h_fa, h_fb, h_sx, nullptr);
     char* d = static_cast<char*>(pint_scratch(ctx, 0, in_bytes));
-    double* f = static_cast<double*>(pint_scratch(ctx, 1, sizeof(double) * 2 * n * Q));
+    double* f = static_cast<double*>(pint_scratch(ctx, 1, sizeof(double) * heat_record_stride(n) * Q));
     if (!d || !f) return PINT_E_CUDA;
     if (!ok(ctx, cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D heat tables"))
         return PINT_E_CUDA;
@@ -603,7 +605,7 @@ int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, Hea
     H.sx = reinterpret_cast<double*>(d + b_off + b_dt + 3 * b_q);
     H.factor = f;
     H.h2d = in_bytes;
-    return launch_heat_factor(ctx, n, Q, H.r, H.factor);
+    return launch_heat_factor(ctx, n, Q, H.r, H.fa, H.fb, H.factor);
 }
 
 int singular_check(pint_ctx* ctx) {
@@ -652,7 +654,7 @@ int pint_run_heat(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int 
     }
     cudaMemcpyAsync(d_y0, y0, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream);
     if (per_slice_seconds) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
-    int rc = launch_heat_build(ctx, n, N, H.step_off, H.slice_dt, H.factor, H.r, H.fa, H.fb, H.sx, d_maps,
+    int rc = launch_heat_build(ctx, n, N, H.step_off, H.slice_dt, H.factor, H.sx, d_maps,
                                per_slice_seconds ? d_ns : nullptr);
     if (rc) return rc;
     cudaEventRecord(ctx->evc, ctx->stream);
@@ -699,7 +701,7 @@ int pint_heat_maps(pint_ctx* ctx, double dx, double dt, const pint_slice* slices
     const int64_t n = H.n, ldm = pint_affine_ldm(n);
     double* d_maps = static_cast<double*>(pint_scratch(ctx, 2, sizeof(double) * n * ldm * N));
     if (!d_maps) return PINT_E_CUDA;
-    int rc = launch_heat_build(ctx, n, N, H.step_off, H.slice_dt, H.factor, H.r, H.fa, H.fb, H.sx, d_maps, nullptr);
+    int rc = launch_heat_build(ctx, n, N, H.step_off, H.slice_dt, H.factor, H.sx, d_maps, nullptr);
     if (rc) return rc;
     std::vector<double> host(static_cast<size_t>(n * ldm * N));
     cudaMemcpyAsync(host.data(), d_maps, sizeof(double) * host.size(), cudaMemcpyDeviceToHost, ctx->stream);
@@ -726,7 +728,7 @@ int pint_heat_integrate(pint_ctx* ctx, double dx, const pint_slice* slice, doubl
     double* d_y = static_cast<double*>(pint_scratch(ctx, 2, sizeof(double) * n * K));
     if (!d_y) return PINT_E_CUDA;
     cudaMemcpyAsync(d_y, y, sizeof(double) * n * K, cudaMemcpyHostToDevice, ctx->stream);
-    int rc = launch_heat_integrate(ctx, n, K, 0, H.Q, sl[0].dt, with_forcing, H.factor, H.r, H.fa, H.fb, H.sx, d_y);
+    int rc = launch_heat_integrate(ctx, n, K, 0, H.Q, sl[0].dt, with_forcing, H.factor, H.sx, d_y);
     if (rc) return rc;
     cudaMemcpyAsync(y, d_y, sizeof(double) * n * K, cudaMemcpyDeviceToHost, ctx->stream);
     if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "heat_integrate sync")) return PINT_E_CUDA;

@@ -87,7 +87,8 @@ class HeatPlan:
         self.ldm = int(capi.load().pint_affine_ldm(self.n))
         dev = torch.device("cuda", ctx.device)
         self.dev = [t.to(dev) for t in self.host.tensors()]
-        self.factor = torch.empty(self.Q * self.n * 2, dtype=torch.float64, device=dev)
+        stride_rec = int(capi.load().pint_heat_record_stride(self.n))
+        self.factor = torch.empty(self.Q * stride_rec, dtype=torch.float64, device=dev)
         stride = self.n * self.ldm
         self.maps = torch.zeros(self.N * stride, dtype=torch.float64, device=dev)
         self.scratch = torch.zeros(max(1, (self.N + 1) // 2) * stride, dtype=torch.float64, device=dev)
@@ -108,9 +109,9 @@ class HeatPlan:
     def factor_and_build(self):
         c, P = self.ctx, capi.ptr
         step_off, slice_dt, r, fa, fb, sx = self.dev
-        c.call("pint_heat_factor_dev", self.n, self.Q, P(r), P(self.factor))
-        c.call("pint_heat_build_dev", self.n, self.N, P(step_off), P(slice_dt), P(self.factor), P(r), P(fa), P(fb),
-               P(sx), P(self.maps), None)
+        c.call("pint_heat_factor_dev", self.n, self.Q, P(r), P(fa), P(fb), P(self.factor))
+        c.call("pint_heat_build_dev", self.n, self.N, P(step_off), P(slice_dt), P(self.factor), P(sx),
+               P(self.maps), None)
 
     def compose_local(self, mode: int = capi.COMPOSE_TREE):
         """Compose this block's maps; the composed augmented map lands in self.composed (TREE),
@@ -162,13 +163,3 @@ def sharded_heat_step(plan: HeatPlan, group=None) -> None:
         cat = torch.cat(maps)
         apply_chain(plan.ctx, plan.n, cat, plan.y0, plan.y)
 
-
-def compose_blocks_host(maps_per_rank: List[np.ndarray], y0: np.ndarray, n: int) -> np.ndarray:
-    """Host-side reference for the root's compose of gathered augmented maps (tests only use it
-    against the oracle; the product path is apply_chain on the device)."""
-    ldm = int(capi.load().pint_affine_ldm(n))
-    y = np.asarray(y0, dtype=np.float64)
-    for m in maps_per_rank:
-        A = np.asarray(m).reshape(n, ldm)
-        y = A[:, :n] @ y + A[:, n]
-    return y

@@ -174,7 +174,7 @@ def test_logistic_rk4_f64_matches_oracle(ctx, S):
     _, _, st, h = O.decompose(0.0, ivp.T, N, dt)
     x = O.cheb_nodes(M, 0.0, 1.25)
     want = O.logistic_rk4_ensemble(st, h, x, 1.0, 1.0)
-    assert np.max(np.abs(ends - want) / np.abs(want)) <= REL_F64
+    assert np.max(np.abs(ends - want) / np.maximum(np.abs(want), 1e-300)) <= REL_F64
     assert np.array_equal(ends, want)  # same explicit-fma op order: bit-exact in practice
     assert abs(y - ivp.exact(ivp.T)) < 1e-6
 
@@ -192,7 +192,7 @@ def test_logistic_rk4_f32_matches_oracle(ctx):
     want32 = O.logistic_rk4_ensemble_f32(st, h, x, 1.0, 1.0)
     want64 = O.logistic_rk4_ensemble(st, h, x.astype(np.float64), 1.0, 1.0)
     assert np.array_equal(got, want32)
-    assert np.max(np.abs(got - want64) / np.abs(want64)) <= REL_F32
+    assert np.max(np.abs(got - want64) / np.maximum(np.abs(want64), 1e-30)) <= REL_F32
 
 
 # ---- EXTENSION: 2-D Lotka-Volterra + bilinear -------------------------------------------------
@@ -222,7 +222,7 @@ def test_lv_small_bit_exact(ctx):
     st, h, un, vn, tables, lam, br, ext = lv_run(ctx, N, Mu, Mv, S)
     want = O.lv_rk4_ensemble(st, h, un, vn, LV)
     got = tables.cpu().numpy().reshape(N, 2, Mu, Mv)
-    assert np.max(np.abs(got - want) / np.abs(want)) <= REL_F64
+    assert np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-300)) <= REL_F64
     assert np.array_equal(got, want)
     wl, wb, wext = O.bilinear_sweep(un, vn, want, 1.0, 1.0)
     assert np.array_equal(br, wb)  # bracket indices bit-exact
