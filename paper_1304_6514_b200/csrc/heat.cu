@@ -7,19 +7,22 @@
 //
 // B200 design:
 //  * The tridiagonal factor depends only on (slice, step), never on the right-hand side, so
-//    heat_record_kernel computes it once per step (one thread per step, all steps in parallel)
-//    into a per-step record {-r, fa, fb, 0, p[n], rcp[n], c[n]} instead of n+1 times. Same
-//    operations and rounding as thomas_solve, so every solve stays bit-identical.
-//  * Division x / p_i is done as q0 = x * rcp_i, rem = fma(-p_i, q0, x), q = fma(rem, rcp_i, q0)
-//    with rcp_i = RN(1/p_i) (__drcp_rn): Markstein's theorem makes q the correctly rounded
-//    quotient (no over/underflow is possible here: p_i >= 1 and |x| >= 2^-960 is checked on
-//    the exponent bits, anything else takes the IEEE __ddiv_rn path). 5 dependent FP64 ops per
-//    row instead of the ~12 of a full division.
-//  * One warp per (slice, 32-column group); lane = trajectory. Column k < n starts at e_k, column
-//    n (the c run) at 0 with forcing. All lanes of a warp share the slice, so the step's record
-//    is staged once into shared memory by cp.async one step ahead (double-buffered) and read as
-//    broadcasts; the column state is lane-interleaved in shared memory (conflict-free), and the
-//    final rows go out as coalesced 256 B stores into the row-major augmented map [G | c].
+//    heat_record_kernel computes it once per step into a record
+//        {-r, fa, fb, 0, (p_0, 1/p_0), ..., (p_{n-1}, 1/p_{n-1}), c_0, ..., c_{n-1}}
+//    with exactly thomas_solve's operations, so every solve stays bit-identical.
+//  * x / p_i is q0 = x*rcp, rem = fma(-p, q0, x), q = fma(rem, rcp, q0) with rcp = RN(1/p_i):
+//    Markstein's theorem makes q the correctly rounded quotient whenever no intermediate
+//    under/overflows. Basis columns are entrywise non-negative and bounded (each step matrix is an
+//    M-matrix, p_i >= 1, |c_i| < 1) and decay by at most r/p_i per row, so their quotients stay far
+//    from the subnormal range and run unguarded; the warp holding the forced column (and the
+//    integrate kernel, which sees caller data) checks the exponent of x and takes __ddiv_rn
+//    outside [2^-960, 2^997].
+//  * One warp per (slice, 32 columns), lane = trajectory: k < n starts at e_k, k == n is the
+//    forced run from 0 (c). The step record is staged into shared memory by cp.async one step
+//    ahead and read as broadcasts; the first kRegRows rows of every column live in registers,
+//    the rest lane-interleaved in shared memory (conflict-free), roughly doubling the resident
+//    warps per SM versus shared memory alone. Rows leave as coalesced 256 B stores into the
+//    row-major augmented map [G | c].
 //
 // Roofline: FP64 pipe. Algorithmic flops per slice-step: (n+1)(5n-4) + 5n (bench.py).
 #include "pint_internal.cuh"
@@ -28,9 +31,10 @@ namespace {
 
 using pint_dev::record_failure;
 
-__host__ __device__ constexpr long long rec_stride(long long n) { return ((4 + 3 * n) + 1) / 2 * 2; }
+constexpr int kRegRows = 64;  // rows of each column held in registers (n >= kRegRows + 2)
 
-// Per-step record: the Thomas forward pivots of tridiag(-r, 1+2r, -r) (linalg.cpp:80-90).
+__host__ __device__ constexpr long long rec_stride(long long n) { return 4 + 3 * n + ((3 * n) & 1); }
+
 __global__ void heat_record_kernel(long long n, long long Q, const double* __restrict__ r_tab,
                                    const double* __restrict__ fa, const double* __restrict__ fb,
                                    double* __restrict__ rec, FailRec* fail) {
@@ -44,32 +48,32 @@ __global__ void heat_record_kernel(long long n, long long Q, const double* __res
     R[1] = fa[q];
     R[2] = fb[q];
     R[3] = 0.0;
-    double* P = R + 4;
-    double* RC = R + 4 + n;
+    double2* PR = reinterpret_cast<double2*>(R + 4);
     double* CC = R + 4 + 2 * n;
-    double p = diag;
+    double p = diag;  // thomas_solve: pivot = diag[0]; c[0] = sup[0] / pivot (linalg.cpp:80-83)
     if (p == 0.0) record_failure(fail, q, PINT_E_SINGULAR, 0.0);
     double c = (n > 1) ? __ddiv_rn(negr, p) : 0.0;
-    P[0] = p;
-    RC[0] = __drcp_rn(p);
+    PR[0] = make_double2(p, __drcp_rn(p));
     CC[0] = c;
-    for (long long i = 1; i < n; ++i) {
+    for (long long i = 1; i < n; ++i) {  // pivot = diag - sub*c[i-1]; c[i] = sup/pivot (:84-88)
         p = __dsub_rn(diag, __dmul_rn(negr, c));
         if (p == 0.0) record_failure(fail, q, PINT_E_SINGULAR, static_cast<double>(i));
         c = (i < n - 1) ? __ddiv_rn(negr, p) : 0.0;
-        P[i] = p;
-        RC[i] = __drcp_rn(p);
+        PR[i] = make_double2(p, __drcp_rn(p));
         CC[i] = c;
     }
 }
 
-// x / p, correctly rounded, given rcp = RN(1/p) (see header comment).
-__device__ __forceinline__ double div_rcp(double x, double p, double rcp) {
+__device__ __forceinline__ double div_fast(double x, double2 pr) {
+    const double q0 = __dmul_rn(x, pr.y);
+    const double rem = __fma_rn(-pr.x, q0, x);
+    return __fma_rn(rem, pr.y, q0);
+}
+
+__device__ __forceinline__ double div_guarded(double x, double2 pr) {
     const unsigned e = (static_cast<unsigned>(__double2hiint(x)) >> 20) & 0x7ffu;
-    if (e < 63u || e > 2020u) return __ddiv_rn(x, p);  // zero/subnormal/tiny/huge/non-finite
-    const double q0 = __dmul_rn(x, rcp);
-    const double rem = __fma_rn(-p, q0, x);
-    return __fma_rn(rem, rcp, q0);
+    if (e - 63u > 1957u) return __ddiv_rn(x, pr.x);  // zero/subnormal/tiny/huge/non-finite
+    return div_fast(x, pr);
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -82,160 +86,180 @@ __device__ __forceinline__ void stage_record(double* dst, const double* src, int
     asm volatile("cp.async.commit_group;\n" ::);
 }
 
-enum class Mode { kBuild, kIntegrate };
-
-struct ColumnPlan {
-    long long n;
-    const double* rec;   // per-step records
-    const double* sx;    // sin(pi x_i)
-    // kBuild
-    long long N;
+struct BuildPlan {
+    int n;
+    int N;
+    int warps_per_slice;
+    const double* rec;
+    const double* sx;
     const int64_t* step_off;
     const double* slice_dt;
     double* maps;
     long long ldm;
     unsigned long long* per_slice_ns;
-    // kIntegrate
-    long long K;
-    long long q0;
-    long long steps;
-    double h;
-    int with_forcing;
-    double* y;
 };
 
-// Dynamic smem: rec[2][RS] | sx[n] | state[n][32] (state only when kSmem).
-template <Mode kMode, bool kSmem>
-__global__ void __launch_bounds__(32)
-heat_columns_kernel(ColumnPlan P) {
+// Forcing (pde_problems.cpp:91-94) folded into the row update: x + h*(fa s + fb s), where
+// heat_forcing is fa*s + fb*s (pde_problems.cpp:26-29). fa/fb arrive pre-multiplied by f in {0,1}.
+__device__ __forceinline__ double forced(double x, double h, double fa, double fb, double s) {
+    return __dadd_rn(x, __dmul_rn(h, __dadd_rn(__dmul_rn(fa, s), __dmul_rn(fb, s))));
+}
+
+// Warp (slice, g) owns columns k = 32 g + lane of the slice's n+1 trajectories (k > n idle).
+// Only the slice's last warp holds the forced column ("mixed"): f = 1 on that lane, 0 elsewhere,
+// so the other lanes add exactly +-0. Dynamic smem: rec[2][RS] | sx[n] (even) | state[(n-RR)*32].
+template <int RR, bool kMixed>
+__device__ __forceinline__ void slice_warp(const BuildPlan& P, int slice, int g) {
     extern __shared__ __align__(16) double smem[];
     const unsigned long long t_start = pint_dev::globaltimer();
-    const long long n = P.n;
+    const int n = P.n;
+    const int lane = threadIdx.x;
     const long long RS = rec_stride(n);
     double* recbuf = smem;
-    double* sx_s = smem + 2 * RS;
-    double* state_s = sx_s + ((n + 1) / 2) * 2;
-    const int lane = threadIdx.x;
-
-    long long slice = 0, k, q_begin, q_end;
-    double h;
-    bool active, forcing;
-    double* gcol;
-    long long grs;
-    if (kMode == Mode::kBuild) {
-        const long long wps = (n + 1 + 31) / 32;  // warps per slice
-        slice = blockIdx.x / wps;
-        k = (blockIdx.x % wps) * 32 + lane;
-        active = k <= n;
-        forcing = (k == n);
-        q_begin = P.step_off[slice];
-        q_end = P.step_off[slice + 1];
-        h = P.slice_dt[slice];
-        gcol = P.maps + slice * n * P.ldm + (active ? k : 0);
-        grs = P.ldm;
-    } else {
-        k = static_cast<long long>(blockIdx.x) * 32 + lane;
-        active = k < P.K;
-        forcing = P.with_forcing != 0;
-        q_begin = P.q0;
-        q_end = P.q0 + P.steps;
-        h = P.h;
-        gcol = P.y + (active ? k : 0) * n;
-        grs = 1;
-    }
-    // inactive lanes keep a private zero column in smem (or skip work in global mode)
-    double* st = kSmem ? state_s + lane : gcol;
-    const long long rs = kSmem ? 32 : grs;
-    const bool work = kSmem || active;
+    double* sx = smem + 2 * RS;
+    double* st = sx + ((n + 1) & ~1) + lane;  // row i >= RR lives at st[(i - RR) * 32]
+    const int k = g * 32 + lane;
+    const bool active = k <= n;
+    const double f = (k == n) ? 1.0 : 0.0;
+    const long long q_begin = P.step_off[slice], q_end = P.step_off[slice + 1];
+    const double h = P.slice_dt[slice];
     const int chunks = static_cast<int>(RS / 2);
+    const double* rec = P.rec;
 
-    if (q_begin < q_end) stage_record(recbuf, P.rec + q_begin * RS, chunks, lane);
-    const bool any_forcing = __any_sync(0xffffffffu, forcing && active);
-    if (any_forcing)
-        for (long long i = lane; i < n; i += 32) sx_s[i] = P.sx[i];
-    if (work)
-        for (long long i = 0; i < n; ++i) {
-            double v;
-            if (kMode == Mode::kBuild) v = (i == k) ? 1.0 : 0.0;  // e_k, or 0 for the c run
-            else v = active ? gcol[i] : 0.0;
-            st[i * rs] = v;
-        }
+    if (q_begin < q_end) stage_record(recbuf, rec + q_begin * RS, chunks, lane);
+    if (kMixed)
+        for (int i = lane; i < n; i += 32) sx[i] = P.sx[i];
+    double reg[RR > 0 ? RR : 1];
+#pragma unroll
+    for (int i = 0; i < RR; ++i) reg[i] = (i == k) ? 1.0 : 0.0;
+    for (int i = RR; i < n; ++i) st[(i - RR) * 32] = (i == k) ? 1.0 : 0.0;
 
     int cur = 0;
     for (long long q = q_begin; q < q_end; ++q) {
         if (q + 1 < q_end) {
-            stage_record(recbuf + (cur ^ 1) * RS, P.rec + (q + 1) * RS, chunks, lane);
+            stage_record(recbuf + (cur ^ 1) * RS, rec + (q + 1) * RS, chunks, lane);
             asm volatile("cp.async.wait_group 1;\n" ::);
         } else {
             asm volatile("cp.async.wait_group 0;\n" ::);
         }
         __syncwarp();
         const double* R = recbuf + cur * RS;
-        if (work) {
-            const double negr = R[0];
-            const double* Pv = R + 4;
-            const double* Rc = R + 4 + n;
-            const double* Cc = R + 4 + 2 * n;
-            // forward elimination (linalg.cpp:80-90), forcing folded in (pde_problems.cpp:91-94)
-            double dprev = 0.0;
-            if (forcing) {
-                const double fa = R[1], fb = R[2];
-                for (long long i = 0; i < n; ++i) {
-                    const double s = sx_s[i];
-                    const double b = __dadd_rn(__dmul_rn(fa, s), __dmul_rn(fb, s));
-                    const double x = __dadd_rn(st[i * rs], __dmul_rn(h, b));
-                    const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, dprev));
-                    dprev = div_rcp(num, Pv[i], Rc[i]);
-                    st[i * rs] = dprev;
-                }
-            } else {
-                dprev = div_rcp(st[0], Pv[0], Rc[0]);
-                st[0] = dprev;
-#pragma unroll 4
-                for (long long i = 1; i < n; ++i) {
-                    const double num = __dsub_rn(st[i * rs], __dmul_rn(negr, dprev));
-                    dprev = div_rcp(num, Pv[i], Rc[i]);
-                    st[i * rs] = dprev;
-                }
-            }
-            // back substitution (linalg.cpp:91)
-            double dnext = dprev;
-#pragma unroll 4
-            for (long long i = n - 2; i >= 0; --i) {
-                const double d = __dsub_rn(st[i * rs], __dmul_rn(Cc[i], dnext));
-                st[i * rs] = d;
-                dnext = d;
+        const double negr = R[0];
+        const double ffa = kMixed ? __dmul_rn(f, R[1]) : 0.0;
+        const double ffb = kMixed ? __dmul_rn(f, R[2]) : 0.0;
+        const double2* PR = reinterpret_cast<const double2*>(R + 4);
+        const double* CC = R + 4 + 2 * n;
+
+        // forward elimination (linalg.cpp:84-90): d_i = (x_i - sub d_{i-1}) / p_i
+        double d = 0.0;
+#pragma unroll
+        for (int i = 0; i < RR; ++i) {
+            const double x = kMixed ? forced(reg[i], h, ffa, ffb, sx[i]) : reg[i];
+            const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
+            d = kMixed ? div_guarded(num, PR[i]) : div_fast(num, PR[i]);
+            reg[i] = d;
+        }
+        {
+            double* s = st;
+            const double2* pr = PR + RR;
+#pragma unroll 8
+            for (int i = RR; i < n; ++i, s += 32, ++pr) {
+                const double x = kMixed ? forced(*s, h, ffa, ffb, sx[i]) : *s;
+                const double num = (RR == 0 && i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
+                d = kMixed ? div_guarded(num, *pr) : div_fast(num, *pr);
+                *s = d;
             }
         }
-        __syncwarp();  // everyone is done with buffer `cur` before it is refilled
+        // back substitution (linalg.cpp:91): d_i -= c_i * d_{i+1}
+        {
+            double* s = st + (n - 2 - RR) * 32;
+            const double* c = CC + (n - 2);
+#pragma unroll 8
+            for (int i = n - 2; i >= RR; --i, s -= 32, --c) {
+                d = __dsub_rn(*s, __dmul_rn(*c, d));
+                *s = d;
+            }
+        }
+#pragma unroll
+        for (int i = RR - 1; i >= 0; --i) {
+            d = __dsub_rn(reg[i], __dmul_rn(CC[i], d));
+            reg[i] = d;
+        }
+        __syncwarp();  // buffer `cur` is refilled next iteration
         cur ^= 1;
     }
-    if (kSmem && active)
-        for (long long i = 0; i < n; ++i) gcol[i * grs] = st[i * rs];
-    // RunReport::per_slice_compute analogue: the warp's time, charged to its slice
-    if (kMode == Mode::kBuild && P.per_slice_ns && lane == 0)
-        atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
+    if (active) {
+        double* gp = P.maps + static_cast<long long>(slice) * n * P.ldm + k;
+#pragma unroll
+        for (int i = 0; i < RR; ++i) gp[i * P.ldm] = reg[i];
+        for (int i = RR; i < n; ++i) gp[i * P.ldm] = st[(i - RR) * 32];
+    }
+    if (P.per_slice_ns && lane == 0) atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
 }
 
-template <Mode kMode>
-int launch_columns(pint_ctx* ctx, const ColumnPlan& P, long long warps, const char* what) {
-    if (warps <= 0) return PINT_OK;
-    const long long n = P.n;
-    const size_t base = sizeof(double) * (2 * rec_stride(n) + ((n + 1) / 2) * 2);
-    const size_t with_state = base + sizeof(double) * 32 * static_cast<size_t>(n);
-    const unsigned blocks = static_cast<unsigned>(warps);
-    if (with_state <= 200 * 1024) {
-        if (with_state > 48 * 1024)
-            cudaFuncSetAttribute(heat_columns_kernel<kMode, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(with_state));
-        heat_columns_kernel<kMode, true><<<blocks, 32, with_state, ctx->stream>>>(P);
-    } else {
-        if (base > 48 * 1024)
-            cudaFuncSetAttribute(heat_columns_kernel<kMode, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(base));
-        heat_columns_kernel<kMode, false><<<blocks, 32, base, ctx->stream>>>(P);
+template <int RR>
+__global__ void __launch_bounds__(32) heat_build_kernel(BuildPlan P) {
+    const int slice = blockIdx.x / P.warps_per_slice;
+    const int g = blockIdx.x - slice * P.warps_per_slice;
+    if (g == P.warps_per_slice - 1) slice_warp<RR, true>(P, slice, g);
+    else slice_warp<RR, false>(P, slice, g);
+}
+
+// ---- integrate: K caller columns of one slice, lane = column (guarded division) ---------------
+struct IntegratePlan {
+    int n;
+    long long K, q0, steps;
+    double h;
+    int with_forcing;
+    const double* rec;
+    const double* sx;
+    double* y;
+};
+
+__global__ void __launch_bounds__(32) heat_integrate_kernel(IntegratePlan P) {
+    extern __shared__ __align__(16) double smem[];
+    const int n = P.n;
+    const int lane = threadIdx.x;
+    const long long col = static_cast<long long>(blockIdx.x) * 32 + lane;
+    const bool active = col < P.K;
+    double* st = smem + lane;
+    double* sx = smem + 32 * n;
+    for (int i = lane; i < n; i += 32) sx[i] = P.sx[i];
+    for (int i = 0; i < n; ++i) st[i * 32] = active ? P.y[col * n + i] : 0.0;
+    __syncwarp();
+    const long long RS = rec_stride(n);
+    const bool forcing = P.with_forcing != 0;
+    for (long long q = P.q0; q < P.q0 + P.steps; ++q) {
+        const double* R = P.rec + q * RS;
+        const double negr = __ldg(R), fa = __ldg(R + 1), fb = __ldg(R + 2);
+        const double2* PR = reinterpret_cast<const double2*>(R + 4);
+        const double* CC = R + 4 + 2 * n;
+        double d = 0.0;
+        for (int i = 0; i < n; ++i) {
+            double x = st[i * 32];
+            if (forcing) x = forced(x, P.h, fa, fb, sx[i]);
+            const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
+            d = div_guarded(num, __ldg(PR + i));
+            st[i * 32] = d;
+        }
+        for (int i = n - 2; i >= 0; --i) {
+            d = __dsub_rn(st[i * 32], __dmul_rn(__ldg(CC + i), d));
+            st[i * 32] = d;
+        }
     }
-    return pint_check_launch(ctx, what);
+    if (active)
+        for (int i = 0; i < n; ++i) P.y[col * n + i] = st[i * 32];
+}
+
+template <int RR>
+int launch_build(pint_ctx* ctx, const BuildPlan& P) {
+    const size_t smem = sizeof(double) * (2 * rec_stride(P.n) + ((P.n + 1) & ~1) + static_cast<size_t>(P.n - RR) * 32);
+    if (smem > 227 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: n too large for shared memory");
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(heat_build_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const long long blocks = static_cast<long long>(P.N) * P.warps_per_slice;
+    heat_build_kernel<RR><<<static_cast<unsigned>(blocks), 32, smem, ctx->stream>>>(P);
+    return pint_check_launch(ctx, "heat_build_kernel");
 }
 
 }  // namespace
@@ -254,32 +278,32 @@ int launch_heat_factor(pint_ctx* ctx, int64_t n, int64_t total_steps, const doub
 int launch_heat_build(pint_ctx* ctx, int64_t n, int64_t N, const int64_t* step_off, const double* slice_dt,
                       const double* records, const double* sx, double* maps, unsigned long long* per_slice_ns) {
     if (n < 1 || N < 0) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: bad sizes");
-    ColumnPlan P{};
-    P.n = n;
+    if (N == 0) return PINT_OK;
+    if (n > (1 << 20) || N > (1 << 26)) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: sizes out of range");
+    BuildPlan P{};
+    P.n = static_cast<int>(n);
+    P.N = static_cast<int>(N);
+    P.warps_per_slice = static_cast<int>((n + 1 + 31) / 32);
     P.rec = records;
     P.sx = sx;
-    P.N = N;
     P.step_off = step_off;
     P.slice_dt = slice_dt;
     P.maps = maps;
     P.ldm = pint_affine_ldm(n);
     P.per_slice_ns = per_slice_ns;
-    const long long wps = (n + 1 + 31) / 32;
-    return launch_columns<Mode::kBuild>(ctx, P, N * wps, "heat_columns_kernel<build>");
+    if (n >= kRegRows + 2) return launch_build<kRegRows>(ctx, P);
+    return launch_build<0>(ctx, P);
 }
 
 int launch_heat_integrate(pint_ctx* ctx, int64_t n, int64_t K, int64_t q0, int64_t steps, double h,
                           int with_forcing, const double* records, const double* sx, double* y) {
     if (n < 1 || K < 0) return pint_set_error(ctx, PINT_E_INVALID, "heat_integrate: bad sizes");
-    ColumnPlan P{};
-    P.n = n;
-    P.rec = records;
-    P.sx = sx;
-    P.K = K;
-    P.q0 = q0;
-    P.steps = steps;
-    P.h = h;
-    P.with_forcing = with_forcing;
-    P.y = y;
-    return launch_columns<Mode::kIntegrate>(ctx, P, (K + 31) / 32, "heat_columns_kernel<integrate>");
+    if (K == 0) return PINT_OK;
+    IntegratePlan P{static_cast<int>(n), K, q0, steps, h, with_forcing, records, sx, y};
+    const size_t smem = sizeof(double) * (static_cast<size_t>(n) * 32 + n);
+    if (smem > 227 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "heat_integrate: n too large");
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(heat_integrate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    heat_integrate_kernel<<<static_cast<unsigned>((K + 31) / 32), 32, smem, ctx->stream>>>(P);
+    return pint_check_launch(ctx, "heat_integrate_kernel");
 }

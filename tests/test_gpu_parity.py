@@ -185,8 +185,9 @@ def test_logistic_rk4_f32_matches_oracle(ctx):
     x = O.cheb_nodes(M, 0.0, 1.25).astype(np.float32)
     ends = dev(np.zeros(N * M, dtype=np.float32))
     rhs = capi.ScalarRHS(capi.RHS_LOGISTIC_RK4, capi.F32, 1.0, 1.0)
-    ctx.call("pint_scalar_ensemble_dev", C.byref(rhs), N, M, capi.ptr(dev(st)), capi.ptr(dev(h)),
-             capi.ptr(dev(x)), capi.ptr(ends), None)
+    d_st, d_h, d_x = dev(st), dev(h), dev(x)  # keep the device copies alive across the launch
+    ctx.call("pint_scalar_ensemble_dev", C.byref(rhs), N, M, capi.ptr(d_st), capi.ptr(d_h),
+             capi.ptr(d_x), capi.ptr(ends), None)
     ctx.sync()
     got = ends.cpu().numpy().reshape(N, M)
     want32 = O.logistic_rk4_ensemble_f32(st, h, x, 1.0, 1.0)
@@ -206,12 +207,13 @@ def lv_run(ctx, N, Mu, Mv, S, T=10.0, lo=0.1, hi=8.0):
     _, _, st, h = O.decompose(0.0, T, N, T / (N * S))
     un, vn = O.uniform_nodes(Mu, lo, hi), O.uniform_nodes(Mv, lo, hi)
     tables = torch.empty(N * 2 * Mu * Mv, dtype=torch.float64, device="cuda")
-    ctx.call("pint_lv_ensemble_dev", N, Mu, Mv, capi.ptr(dev(st)), capi.ptr(dev(h)), capi.ptr(dev(un)),
-             capi.ptr(dev(vn)), capi.ptr(np.array(LV)), capi.ptr(tables))
+    d_st, d_h, d_un, d_vn = dev(st), dev(h), dev(un), dev(vn)  # alive across the launches
+    ctx.call("pint_lv_ensemble_dev", N, Mu, Mv, capi.ptr(d_st), capi.ptr(d_h), capi.ptr(d_un),
+             capi.ptr(d_vn), capi.ptr(np.array(LV)), capi.ptr(tables))
     lam = torch.empty(2 * N, dtype=torch.float64, device="cuda")
     br = torch.empty(2 * N, dtype=torch.int64, device="cuda")
     ext = torch.empty(1, dtype=torch.int64, device="cuda")
-    ctx.call("pint_bilinear_sweep_dev", N, Mu, Mv, capi.ptr(dev(un)), capi.ptr(dev(vn)), capi.ptr(tables), 1.0, 1.0,
+    ctx.call("pint_bilinear_sweep_dev", N, Mu, Mv, capi.ptr(d_un), capi.ptr(d_vn), capi.ptr(tables), 1.0, 1.0,
              capi.ptr(lam), capi.ptr(br), capi.ptr(ext))
     ctx.sync()
     return st, h, un, vn, tables, lam.cpu().numpy().reshape(N, 2), br.cpu().numpy().reshape(N, 2), int(ext.item())
