@@ -215,6 +215,8 @@ int pint_scalar_sweep(pint_ctx* ctx, int mode, int64_t N, int64_t M, const doubl
 
 /* ---- roofline probe: measured FMA throughput (TFLOP/s) of this GPU for PINT_F64 / PINT_F32 */
 int pint_probe_peak(pint_ctx* ctx, int precision, double* tflops);
+/* dependent-chain latency in SM cycles per op: {DFMA, DADD, DMUL, FFMA, LDS.64} */
+int pint_probe_latency(pint_ctx* ctx, double* cycles);
 
 #ifdef __cplusplus
 }

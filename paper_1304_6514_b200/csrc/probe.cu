@@ -20,7 +20,56 @@ __global__ void __launch_bounds__(256) fma_probe_kernel(int iters, R seed, R* si
     if (s == R(-1)) sink[threadIdx.x] = s;  // never true; keeps the chains alive
 }
 
+// Dependent-chain latency (cycles per op) of one warp: out = {DFMA, DADD, DMUL, FFMA, LDS.64}.
+__global__ void latency_probe_kernel(double seed, double* sink, double* out, const double* table) {
+    __shared__ double sh[64];
+    sh[threadIdx.x] = table[threadIdx.x];
+    sh[threadIdx.x + 32] = table[threadIdx.x + 32];
+    __syncwarp();
+    constexpr int kOps = 1024;
+    double a = seed + threadIdx.x;
+    long long t0 = clock64();
+#pragma unroll 64
+    for (int i = 0; i < kOps; ++i) a = __fma_rn(a, 0.999999, 1e-9);
+    long long t1 = clock64();
+#pragma unroll 64
+    for (int i = 0; i < kOps; ++i) a = __dadd_rn(a, 1e-9);
+    long long t2 = clock64();
+#pragma unroll 64
+    for (int i = 0; i < kOps; ++i) a = __dmul_rn(a, 0.999999);
+    long long t3 = clock64();
+    float fa = static_cast<float>(a);
+#pragma unroll 64
+    for (int i = 0; i < kOps; ++i) fa = __fmaf_rn(fa, 0.999f, 1e-6f);
+    long long t4 = clock64();
+    int idx = static_cast<int>(fa) & 1;
+#pragma unroll 64
+    for (int i = 0; i < kOps; ++i) idx = static_cast<int>(sh[idx]) & 31;
+    long long t5 = clock64();
+    if (threadIdx.x == 0) {
+        out[0] = double(t1 - t0) / kOps;
+        out[1] = double(t2 - t1) / kOps;
+        out[2] = double(t3 - t2) / kOps;
+        out[3] = double(t4 - t3) / kOps;
+        out[4] = double(t5 - t4) / kOps;
+    }
+    if (a == -1.0 || idx == 12345) sink[0] = a + fa;
+}
+
 }  // namespace
+
+extern "C" int pint_probe_latency(pint_ctx* ctx, double* cycles /* 5 */) {
+    if (!ctx || !cycles) return PINT_E_INVALID;
+    double* d = static_cast<double*>(pint_scratch(ctx, 3, 4096));
+    if (!d) return PINT_E_CUDA;
+    cudaMemsetAsync(d, 0, 4096, ctx->stream);  // table of zeros: the LDS chain reads sh[0]
+    latency_probe_kernel<<<1, 32, 0, ctx->stream>>>(1.0, d + 256, d + 128, d);
+    if (const int rc = pint_check_launch(ctx, "latency_probe_kernel")) return rc;
+    if (cudaMemcpyAsync(cycles, d + 128, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+        return pint_set_error(ctx, PINT_E_CUDA, "latency probe failed");
+    return PINT_OK;
+}
 
 extern "C" int pint_probe_peak(pint_ctx* ctx, int precision, double* tflops) {
     if (!ctx || !tflops) return PINT_E_INVALID;
