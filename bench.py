@@ -208,7 +208,7 @@ def main():
         if events:
             events[1].record(stream)
         ctx.call("pint_heat_build_dev", plan.n, plan.N, P(step_off), P(slice_dt), P(plan.factor), P(sx),
-                 P(plan.maps), None)
+                 P(plan.maps), None, plan.guarded)
         if events:
             events[2].record(stream)
         plan.compose_local(capi.COMPOSE_TREE)
@@ -222,6 +222,11 @@ def main():
     for _ in range(args.warmup):
         one_step()
     torch.cuda.synchronize()
+    if not plan.verify():  # a range check tripped: the plan switched to the guarded build
+        for _ in range(args.warmup):
+            one_step()
+        torch.cuda.synchronize()
+        plan.verify()
     if world > 1:
         dist.barrier()
 

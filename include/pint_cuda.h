@@ -34,6 +34,8 @@ enum {
     PINT_E_BAD_GRID = 3,            /* BadGrid             errors.hpp:20 */
     PINT_E_NON_INTEGER_STEPS = 4,   /* NonIntegerStepCount errors.hpp:25 */
     PINT_E_DUPLICATE_NODES = 5,     /* DuplicateNodes      errors.hpp:29 */
+    PINT_E_RANGE_RETRY = 6,         /* internal: a fast-division range check tripped; the
+                                       host-buffer entry points re-run with the guarded kernel */
     PINT_E_INVALID = 16,            /* bad argument to this ABI */
     PINT_E_CUDA = 17,               /* CUDA runtime failure (no CPU fallback exists) */
     PINT_E_NO_DEVICE = 18
@@ -152,10 +154,13 @@ int64_t pint_heat_record_stride(int64_t n);
 int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t total_steps, const double* r,
                          const double* fa, const double* fb, double* records);
 /* Build all N augmented maps into maps (N * n * ldm doubles). step_off/slice_dt/sx are device
- * copies of the host tables; per_slice_ns (may be NULL) accumulates per-slice device time. */
+ * copies of the host tables; per_slice_ns (may be NULL) accumulates per-slice device time.
+ * guarded = 0: fast exact division, forced lanes range-checked off the critical path; a tripped
+ * check latches PINT_E_RANGE_RETRY in the failure record and the caller re-runs with
+ * guarded = 1 (IEEE division on the chain outside [2^-960, 2^997]). Both are bit-exact. */
 int pint_heat_build_dev(pint_ctx* ctx, int64_t n, int64_t N, const int64_t* step_off,
                         const double* slice_dt, const double* records, const double* sx,
-                        double* maps, unsigned long long* per_slice_ns);
+                        double* maps, unsigned long long* per_slice_ns, int guarded);
 /* Integrate K state vectors y[k*n ...] in place through the steps [q0, q0+steps) of the
  * records (the integrate closure for one slice, or run_serial over one whole-interval slice). */
 int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t q0, int64_t steps,

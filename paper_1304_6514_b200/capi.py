@@ -19,6 +19,7 @@ PINT_E_SINGULAR = 2
 PINT_E_BAD_GRID = 3
 PINT_E_NON_INTEGER_STEPS = 4
 PINT_E_DUPLICATE_NODES = 5
+PINT_E_RANGE_RETRY = 6
 PINT_E_INVALID = 16
 PINT_E_CUDA = 17
 PINT_E_NO_DEVICE = 18
@@ -83,7 +84,7 @@ _SIGS = {
     "pint_heat_coefficients": (_int, [_d, C.POINTER(Slice), _i, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i)]),
     "pint_heat_record_stride": (_i, [_i]),
     "pint_heat_factor_dev": (_int, [_vp, _i, _i, _vp, _vp, _vp, _vp]),
-    "pint_heat_build_dev": (_int, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pint_heat_build_dev": (_int, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _int]),
     "pint_heat_integrate_dev": (_int, [_vp, _i, _i, _i, _i, _d, _int, _vp, _vp, _vp]),
     "pint_affine_compose_dev": (_int, [_vp, _int, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "pint_affine_pair_dev": (_int, [_vp, _i, _i, _vp, _vp, _vp]),

@@ -338,9 +338,9 @@ int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t total_steps, const do
 
 int pint_heat_build_dev(pint_ctx* ctx, int64_t n, int64_t N, const int64_t* step_off,
                         const double* slice_dt, const double* records, const double* sx,
-                        double* maps, unsigned long long* per_slice_ns) {
+                        double* maps, unsigned long long* per_slice_ns, int guarded) {
     if (!ctx) return PINT_E_INVALID;
-    return launch_heat_build(ctx, n, N, step_off, slice_dt, records, sx, maps, per_slice_ns);
+    return launch_heat_build(ctx, n, N, step_off, slice_dt, records, sx, maps, per_slice_ns, guarded);
 }
 
 int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t q0, int64_t steps,
@@ -612,6 +612,7 @@ int singular_check(pint_ctx* ctx) {
     pint_fail fr;
     if (const int rc = pint_fail_read(ctx, &fr)) return rc;
     if (fr.index >= 0) {
+        if (fr.code == PINT_E_RANGE_RETRY) return PINT_E_RANGE_RETRY;  // caller re-runs guarded
         char buf[96];
         std::snprintf(buf, sizeof buf, "thomas_solve: zero pivot at row %d", static_cast<int>(fr.value));
         return pint_set_error(ctx, PINT_E_SINGULAR, buf);
@@ -653,23 +654,28 @@ int pint_run_heat(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int 
         y0 = y0v.data();
     }
     cudaMemcpyAsync(d_y0, y0, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream);
-    if (per_slice_seconds) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
-    int rc = launch_heat_build(ctx, n, N, H.step_off, H.slice_dt, H.factor, H.sx, d_maps,
-                               per_slice_seconds ? d_ns : nullptr);
-    if (rc) return rc;
-    cudaEventRecord(ctx->evc, ctx->stream);
-    if (compose_mode == PINT_COMPOSE_TREE) rc = launch_affine_tree(ctx, n, N, d_maps, d_scr, d_y0, d_y, nullptr);
-    else rc = launch_affine_chain(ctx, n, N, d_maps, d_y0, d_y);
-    if (rc) return rc;
-    cudaEventRecord(ctx->ev1, ctx->stream);
-    cudaMemcpyAsync(y_out, d_y, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream);
     std::vector<unsigned long long> ns;
-    if (per_slice_seconds) {
-        ns.resize(static_cast<size_t>(N));
-        cudaMemcpyAsync(ns.data(), d_ns, sizeof(unsigned long long) * N, cudaMemcpyDeviceToHost, ctx->stream);
+    int rc = PINT_OK;
+    for (int guarded = 0; guarded < 2; ++guarded) {  // second pass only if a range check tripped
+        if (per_slice_seconds) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
+        rc = launch_heat_build(ctx, n, N, H.step_off, H.slice_dt, H.factor, H.sx, d_maps,
+                               per_slice_seconds ? d_ns : nullptr, guarded);
+        if (rc) return rc;
+        cudaEventRecord(ctx->evc, ctx->stream);
+        if (compose_mode == PINT_COMPOSE_TREE) rc = launch_affine_tree(ctx, n, N, d_maps, d_scr, d_y0, d_y, nullptr);
+        else rc = launch_affine_chain(ctx, n, N, d_maps, d_y0, d_y);
+        if (rc) return rc;
+        cudaEventRecord(ctx->ev1, ctx->stream);
+        cudaMemcpyAsync(y_out, d_y, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream);
+        if (per_slice_seconds) {
+            ns.resize(static_cast<size_t>(N));
+            cudaMemcpyAsync(ns.data(), d_ns, sizeof(unsigned long long) * N, cudaMemcpyDeviceToHost, ctx->stream);
+        }
+        if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "run_heat sync")) return PINT_E_CUDA;
+        rc = singular_check(ctx);
+        if (rc != PINT_E_RANGE_RETRY) break;
     }
-    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "run_heat sync")) return PINT_E_CUDA;
-    if ((rc = singular_check(ctx))) return rc;
+    if (rc) return rc;
     if (per_slice_seconds)
         for (int64_t j = 0; j < N; ++j) per_slice_seconds[j] = static_cast<double>(ns[j]) * 1e-9;
     if (report) {
@@ -701,12 +707,17 @@ int pint_heat_maps(pint_ctx* ctx, double dx, double dt, const pint_slice* slices
     const int64_t n = H.n, ldm = pint_affine_ldm(n);
     double* d_maps = static_cast<double*>(pint_scratch(ctx, 2, sizeof(double) * n * ldm * N));
     if (!d_maps) return PINT_E_CUDA;
-    int rc = launch_heat_build(ctx, n, N, H.step_off, H.slice_dt, H.factor, H.sx, d_maps, nullptr);
-    if (rc) return rc;
     std::vector<double> host(static_cast<size_t>(n * ldm * N));
-    cudaMemcpyAsync(host.data(), d_maps, sizeof(double) * host.size(), cudaMemcpyDeviceToHost, ctx->stream);
-    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "heat_maps sync")) return PINT_E_CUDA;
-    if ((rc = singular_check(ctx))) return rc;
+    int rc = PINT_OK;
+    for (int guarded = 0; guarded < 2; ++guarded) {
+        if ((rc = launch_heat_build(ctx, n, N, H.step_off, H.slice_dt, H.factor, H.sx, d_maps, nullptr, guarded)))
+            return rc;
+        cudaMemcpyAsync(host.data(), d_maps, sizeof(double) * host.size(), cudaMemcpyDeviceToHost, ctx->stream);
+        if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "heat_maps sync")) return PINT_E_CUDA;
+        rc = singular_check(ctx);
+        if (rc != PINT_E_RANGE_RETRY) break;
+    }
+    if (rc) return rc;
     for (int64_t j = 0; j < N; ++j)
         for (int64_t i = 0; i < n; ++i) {
             const double* row = host.data() + (j * n + i) * ldm;

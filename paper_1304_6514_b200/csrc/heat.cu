@@ -17,12 +17,15 @@
 //    from the subnormal range and run unguarded; the warp holding the forced column (and the
 //    integrate kernel, which sees caller data) checks the exponent of x and takes __ddiv_rn
 //    outside [2^-960, 2^997].
-//  * One warp per (slice, 32 columns), lane = trajectory: k < n starts at e_k, k == n is the
-//    forced run from 0 (c). The step record is staged into shared memory by cp.async one step
-//    ahead and read as broadcasts; the first kRegRows rows of every column live in registers,
-//    the rest lane-interleaved in shared memory (conflict-free), roughly doubling the resident
-//    warps per SM versus shared memory alone. Rows leave as coalesced 256 B stores into the
-//    row-major augmented map [G | c].
+//  * Lane = trajectory: column k < n starts at e_k, k == n is the forced run from 0 (c). A CTA
+//    holds all ceil((n+1)/32) warps of one slice (or one warp of it when n is large): the step
+//    record is staged once per CTA into shared memory by cp.async one step ahead and read as
+//    broadcasts; the first RR rows of every column live in registers, the rest lane-interleaved
+//    in shared memory (conflict-free). Rows leave as coalesced 256 B stores into the row-major
+//    augmented map [G | c].
+//  * The forced lane's quotients are range-checked OFF the dependent chain (a sticky flag);
+//    if it ever trips, the kernel reports PINT_E_RANGE_RETRY and the host re-runs the build
+//    with the guarded variant (exponent check on the chain, IEEE __ddiv_rn outside the range).
 //
 // Roofline: FP64 pipe. Algorithmic flops per slice-step: (n+1)(5n-4) + 5n (bench.py).
 #include "pint_internal.cuh"
@@ -31,7 +34,8 @@ namespace {
 
 using pint_dev::record_failure;
 
-constexpr int kRegRows = 64;  // rows of each column held in registers (n >= kRegRows + 2)
+constexpr int kRegRows = 56;  // rows of each column held in registers (n >= kRegRows + 2)
+constexpr int kMaxCtaThreads = 32 * 8;
 
 __host__ __device__ constexpr long long rec_stride(long long n) { return 4 + 3 * n + ((3 * n) & 1); }
 
@@ -89,7 +93,9 @@ __device__ __forceinline__ void stage_record(double* dst, const double* src, int
 struct BuildPlan {
     int n;
     int N;
-    int warps_per_slice;
+    int wps;            // warps per slice = ceil((n+1)/32)
+    int warps_per_cta;  // wps (one CTA per slice) or 1
+    int ctas_per_slice;
     const double* rec;
     const double* sx;
     const int64_t* step_off;
@@ -97,6 +103,7 @@ struct BuildPlan {
     double* maps;
     long long ldm;
     unsigned long long* per_slice_ns;
+    FailRec* fail;
 };
 
 // Forcing (pde_problems.cpp:91-94) folded into the row update: x + h*(fa s + fb s), where
@@ -105,87 +112,110 @@ __device__ __forceinline__ double forced(double x, double h, double fa, double f
     return __dadd_rn(x, __dmul_rn(h, __dadd_rn(__dmul_rn(fa, s), __dmul_rn(fb, s))));
 }
 
-// Warp (slice, g) owns columns k = 32 g + lane of the slice's n+1 trajectories (k > n idle).
-// Only the slice's last warp holds the forced column ("mixed"): f = 1 on that lane, 0 elsewhere,
-// so the other lanes add exactly +-0. Dynamic smem: rec[2][RS] | sx[n] (even) | state[(n-RR)*32].
-template <int RR, bool kMixed>
-__device__ __forceinline__ void slice_warp(const BuildPlan& P, int slice, int g) {
+__device__ __forceinline__ bool out_of_range(double x) {
+    const unsigned e = (static_cast<unsigned>(__double2hiint(x)) >> 20) & 0x7ffu;
+    return e - 63u > 1957u;
+}
+
+// One backward-Euler step of one column: forward elimination (linalg.cpp:84-90) with the forcing
+// folded in, then back substitution (linalg.cpp:91). Rows [0, RR) in reg[], the rest at st[32*(i-RR)].
+template <int RR, bool kMixed, bool kGuard>
+__device__ __forceinline__ void column_step(double (&reg)[RR > 0 ? RR : 1], double* st, const double* R, int n,
+                                            double h, double f, const double* sx, bool forced_lane,
+                                            bool& bad) {
+    const double negr = R[0];
+    const double ffa = kMixed ? __dmul_rn(f, R[1]) : 0.0;  // f in {0, 1}: exact
+    const double ffb = kMixed ? __dmul_rn(f, R[2]) : 0.0;
+    const double2* PR = reinterpret_cast<const double2*>(R + 4);
+    const double* CC = R + 4 + 2 * n;
+    double d = 0.0;
+#pragma unroll
+    for (int i = 0; i < RR; ++i) {
+        const double x = kMixed ? forced(reg[i], h, ffa, ffb, sx[i]) : reg[i];
+        const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
+        if (kMixed && !kGuard) bad |= forced_lane && out_of_range(num);
+        d = kGuard ? div_guarded(num, PR[i]) : div_fast(num, PR[i]);
+        reg[i] = d;
+    }
+    {
+        double* s = st;
+        const double2* pr = PR + RR;
+#pragma unroll 8
+        for (int i = RR; i < n; ++i, s += 32, ++pr) {
+            const double x = kMixed ? forced(*s, h, ffa, ffb, sx[i]) : *s;
+            const double num = (RR == 0 && i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
+            if (kMixed && !kGuard) bad |= forced_lane && out_of_range(num);
+            d = kGuard ? div_guarded(num, *pr) : div_fast(num, *pr);
+            *s = d;
+        }
+    }
+    {
+        double* s = st + (n - 2 - RR) * 32;
+        const double* c = CC + (n - 2);
+#pragma unroll 8
+        for (int i = n - 2; i >= RR; --i, s -= 32, --c) {
+            d = __dsub_rn(*s, __dmul_rn(*c, d));
+            *s = d;
+        }
+    }
+#pragma unroll
+    for (int i = RR - 1; i >= 0; --i) {
+        d = __dsub_rn(reg[i], __dmul_rn(CC[i], d));
+        reg[i] = d;
+    }
+}
+
+__device__ __forceinline__ void stage_record_cta(double* dst, const double* src, int chunks) {
+    for (int c = threadIdx.x; c < chunks; c += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst + 2 * c)), "l"(src + 2 * c));
+    asm volatile("cp.async.commit_group;\n" ::);
+}
+
+// CTA = warps [c*warps_per_cta, ...) of one slice. Dynamic smem:
+// rec[2][RS] | sx[n] (even) | state[warps_per_cta][(n - RR) * 32]
+template <int RR, bool kGuard>
+__global__ void __launch_bounds__(kMaxCtaThreads) heat_build_kernel(BuildPlan P) {
     extern __shared__ __align__(16) double smem[];
     const unsigned long long t_start = pint_dev::globaltimer();
     const int n = P.n;
-    const int lane = threadIdx.x;
+    const int lane = threadIdx.x & 31, wcta = threadIdx.x >> 5;
+    const int slice = blockIdx.x / P.ctas_per_slice;
+    const int g = (blockIdx.x - slice * P.ctas_per_slice) * P.warps_per_cta + wcta;  // warp in slice
     const long long RS = rec_stride(n);
     double* recbuf = smem;
     double* sx = smem + 2 * RS;
-    double* st = sx + ((n + 1) & ~1) + lane;  // row i >= RR lives at st[(i - RR) * 32]
+    double* st = sx + ((n + 1) & ~1) + static_cast<long long>(wcta) * (n - RR) * 32 + lane;
     const int k = g * 32 + lane;
     const bool active = k <= n;
-    const double f = (k == n) ? 1.0 : 0.0;
+    const bool forced_lane = (k == n);
+    const bool mixed = (g == P.wps - 1);
+    const double f = forced_lane ? 1.0 : 0.0;
     const long long q_begin = P.step_off[slice], q_end = P.step_off[slice + 1];
     const double h = P.slice_dt[slice];
     const int chunks = static_cast<int>(RS / 2);
     const double* rec = P.rec;
 
-    if (q_begin < q_end) stage_record(recbuf, rec + q_begin * RS, chunks, lane);
-    if (kMixed)
-        for (int i = lane; i < n; i += 32) sx[i] = P.sx[i];
+    if (q_begin < q_end) stage_record_cta(recbuf, rec + q_begin * RS, chunks);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sx[i] = P.sx[i];
     double reg[RR > 0 ? RR : 1];
 #pragma unroll
     for (int i = 0; i < RR; ++i) reg[i] = (i == k) ? 1.0 : 0.0;
     for (int i = RR; i < n; ++i) st[(i - RR) * 32] = (i == k) ? 1.0 : 0.0;
 
+    bool bad = false;
     int cur = 0;
     for (long long q = q_begin; q < q_end; ++q) {
         if (q + 1 < q_end) {
-            stage_record(recbuf + (cur ^ 1) * RS, rec + (q + 1) * RS, chunks, lane);
+            stage_record_cta(recbuf + (cur ^ 1) * RS, rec + (q + 1) * RS, chunks);
             asm volatile("cp.async.wait_group 1;\n" ::);
         } else {
             asm volatile("cp.async.wait_group 0;\n" ::);
         }
-        __syncwarp();
+        __syncthreads();  // record q (and sx) visible to every warp
         const double* R = recbuf + cur * RS;
-        const double negr = R[0];
-        const double ffa = kMixed ? __dmul_rn(f, R[1]) : 0.0;
-        const double ffb = kMixed ? __dmul_rn(f, R[2]) : 0.0;
-        const double2* PR = reinterpret_cast<const double2*>(R + 4);
-        const double* CC = R + 4 + 2 * n;
-
-        // forward elimination (linalg.cpp:84-90): d_i = (x_i - sub d_{i-1}) / p_i
-        double d = 0.0;
-#pragma unroll
-        for (int i = 0; i < RR; ++i) {
-            const double x = kMixed ? forced(reg[i], h, ffa, ffb, sx[i]) : reg[i];
-            const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
-            d = kMixed ? div_guarded(num, PR[i]) : div_fast(num, PR[i]);
-            reg[i] = d;
-        }
-        {
-            double* s = st;
-            const double2* pr = PR + RR;
-#pragma unroll 8
-            for (int i = RR; i < n; ++i, s += 32, ++pr) {
-                const double x = kMixed ? forced(*s, h, ffa, ffb, sx[i]) : *s;
-                const double num = (RR == 0 && i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
-                d = kMixed ? div_guarded(num, *pr) : div_fast(num, *pr);
-                *s = d;
-            }
-        }
-        // back substitution (linalg.cpp:91): d_i -= c_i * d_{i+1}
-        {
-            double* s = st + (n - 2 - RR) * 32;
-            const double* c = CC + (n - 2);
-#pragma unroll 8
-            for (int i = n - 2; i >= RR; --i, s -= 32, --c) {
-                d = __dsub_rn(*s, __dmul_rn(*c, d));
-                *s = d;
-            }
-        }
-#pragma unroll
-        for (int i = RR - 1; i >= 0; --i) {
-            d = __dsub_rn(reg[i], __dmul_rn(CC[i], d));
-            reg[i] = d;
-        }
-        __syncwarp();  // buffer `cur` is refilled next iteration
+        if (mixed) column_step<RR, true, kGuard>(reg, st, R, n, h, f, sx, forced_lane, bad);
+        else column_step<RR, false, kGuard>(reg, st, R, n, h, f, sx, forced_lane, bad);
+        __syncthreads();  // buffer `cur` is refilled next iteration
         cur ^= 1;
     }
     if (active) {
@@ -194,15 +224,8 @@ __device__ __forceinline__ void slice_warp(const BuildPlan& P, int slice, int g)
         for (int i = 0; i < RR; ++i) gp[i * P.ldm] = reg[i];
         for (int i = RR; i < n; ++i) gp[i * P.ldm] = st[(i - RR) * 32];
     }
-    if (P.per_slice_ns && lane == 0) atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
-}
-
-template <int RR>
-__global__ void __launch_bounds__(32) heat_build_kernel(BuildPlan P) {
-    const int slice = blockIdx.x / P.warps_per_slice;
-    const int g = blockIdx.x - slice * P.warps_per_slice;
-    if (g == P.warps_per_slice - 1) slice_warp<RR, true>(P, slice, g);
-    else slice_warp<RR, false>(P, slice, g);
+    if (bad) record_failure(P.fail, slice, PINT_E_RANGE_RETRY, static_cast<double>(k));
+    if (P.per_slice_ns && threadIdx.x == 0) atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
 }
 
 // ---- integrate: K caller columns of one slice, lane = column (guarded division) ---------------
@@ -251,14 +274,23 @@ __global__ void __launch_bounds__(32) heat_integrate_kernel(IntegratePlan P) {
         for (int i = 0; i < n; ++i) P.y[col * n + i] = st[i * 32];
 }
 
-template <int RR>
-int launch_build(pint_ctx* ctx, const BuildPlan& P) {
-    const size_t smem = sizeof(double) * (2 * rec_stride(P.n) + ((P.n + 1) & ~1) + static_cast<size_t>(P.n - RR) * 32);
+
+size_t build_smem(int n, int rr, int warps_per_cta) {
+    return sizeof(double) * (2 * rec_stride(n) + ((n + 1) & ~1) + static_cast<size_t>(n - rr) * 32 * warps_per_cta);
+}
+
+template <int RR, bool kGuard>
+int launch_build(pint_ctx* ctx, BuildPlan P) {
+    // one CTA per slice when two such CTAs fit an SM, else one CTA per warp
+    P.warps_per_cta = (P.wps <= kMaxCtaThreads / 32 && build_smem(P.n, RR, P.wps) <= 112 * 1024) ? P.wps : 1;
+    P.ctas_per_slice = P.wps / P.warps_per_cta;
+    const size_t smem = build_smem(P.n, RR, P.warps_per_cta);
     if (smem > 227 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: n too large for shared memory");
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(heat_build_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    const long long blocks = static_cast<long long>(P.N) * P.warps_per_slice;
-    heat_build_kernel<RR><<<static_cast<unsigned>(blocks), 32, smem, ctx->stream>>>(P);
+    auto kern = heat_build_kernel<RR, kGuard>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const long long blocks = static_cast<long long>(P.N) * P.ctas_per_slice;
+    kern<<<static_cast<unsigned>(blocks), 32 * P.warps_per_cta, smem, ctx->stream>>>(P);
     return pint_check_launch(ctx, "heat_build_kernel");
 }
 
@@ -276,14 +308,15 @@ int launch_heat_factor(pint_ctx* ctx, int64_t n, int64_t total_steps, const doub
 }
 
 int launch_heat_build(pint_ctx* ctx, int64_t n, int64_t N, const int64_t* step_off, const double* slice_dt,
-                      const double* records, const double* sx, double* maps, unsigned long long* per_slice_ns) {
+                      const double* records, const double* sx, double* maps, unsigned long long* per_slice_ns,
+                      int guarded) {
     if (n < 1 || N < 0) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: bad sizes");
     if (N == 0) return PINT_OK;
     if (n > (1 << 20) || N > (1 << 26)) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: sizes out of range");
     BuildPlan P{};
     P.n = static_cast<int>(n);
     P.N = static_cast<int>(N);
-    P.warps_per_slice = static_cast<int>((n + 1 + 31) / 32);
+    P.wps = static_cast<int>((n + 1 + 31) / 32);
     P.rec = records;
     P.sx = sx;
     P.step_off = step_off;
@@ -291,8 +324,10 @@ int launch_heat_build(pint_ctx* ctx, int64_t n, int64_t N, const int64_t* step_o
     P.maps = maps;
     P.ldm = pint_affine_ldm(n);
     P.per_slice_ns = per_slice_ns;
-    if (n >= kRegRows + 2) return launch_build<kRegRows>(ctx, P);
-    return launch_build<0>(ctx, P);
+    P.fail = ctx->d_fail;
+    if (n >= kRegRows + 2)
+        return guarded ? launch_build<kRegRows, true>(ctx, P) : launch_build<kRegRows, false>(ctx, P);
+    return guarded ? launch_build<0, true>(ctx, P) : launch_build<0, false>(ctx, P);
 }
 
 int launch_heat_integrate(pint_ctx* ctx, int64_t n, int64_t K, int64_t q0, int64_t steps, double h,

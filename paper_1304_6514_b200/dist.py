@@ -95,6 +95,7 @@ class HeatPlan:
         self.composed = torch.zeros(stride, dtype=torch.float64, device=dev)
         self.y0 = torch.as_tensor(pint.heat_initial(dx)).to(dev)
         self.y = torch.empty(self.n, dtype=torch.float64, device=dev)
+        self.guarded = 0
 
     @property
     def traj_steps(self) -> int:
@@ -111,7 +112,18 @@ class HeatPlan:
         step_off, slice_dt, r, fa, fb, sx = self.dev
         c.call("pint_heat_factor_dev", self.n, self.Q, P(r), P(fa), P(fb), P(self.factor))
         c.call("pint_heat_build_dev", self.n, self.N, P(step_off), P(slice_dt), P(self.factor), P(sx),
-               P(self.maps), None)
+               P(self.maps), None, self.guarded)
+
+    def verify(self) -> bool:
+        """Read the failure record after a step: a tripped range check switches this plan to the
+        guarded build (returns False: re-run the step); a singular pivot raises."""
+        f = self.ctx.fail()
+        if f.index < 0:
+            return True
+        if f.code == capi.PINT_E_RANGE_RETRY:
+            self.guarded = 1
+            return False
+        raise pint.SingularSystem(f"thomas_solve: zero pivot at row {int(f.value)}")
 
     def compose_local(self, mode: int = capi.COMPOSE_TREE):
         """Compose this block's maps; the composed augmented map lands in self.composed (TREE),
