@@ -34,7 +34,7 @@ namespace {
 
 using pint_dev::record_failure;
 
-constexpr int kRegRows = 56;  // rows of each column held in registers (n >= kRegRows + 2)
+constexpr int kRegRows = 64;  // rows of each column held in registers (n >= kRegRows + 2)
 constexpr int kMaxCtaThreads = 32 * 8;
 
 __host__ __device__ constexpr long long rec_stride(long long n) { return 4 + 3 * n + ((3 * n) & 1); }
@@ -93,9 +93,10 @@ __device__ __forceinline__ void stage_record(double* dst, const double* src, int
 struct BuildPlan {
     int n;
     int N;
-    int wps;            // warps per slice = ceil((n+1)/32)
-    int warps_per_cta;  // wps (one CTA per slice) or 1
+    int wb;             // basis warps per slice = ceil(n/32)
+    int warps_per_cta;  // wb (one CTA per slice) or 1
     int ctas_per_slice;
+    int forcing_ctas;   // CTAs holding the forced (c) runs, warps_per_cta * 32 slices each
     const double* rec;
     const double* sx;
     const int64_t* step_off;
@@ -107,7 +108,7 @@ struct BuildPlan {
 };
 
 // Forcing (pde_problems.cpp:91-94) folded into the row update: x + h*(fa s + fb s), where
-// heat_forcing is fa*s + fb*s (pde_problems.cpp:26-29). fa/fb arrive pre-multiplied by f in {0,1}.
+// heat_forcing(x_i, t) is fa*s + fb*s with fa = -sin t, fb = ((a pi) pi) cos t (pde_problems.cpp:26-29).
 __device__ __forceinline__ double forced(double x, double h, double fa, double fb, double s) {
     return __dadd_rn(x, __dmul_rn(h, __dadd_rn(__dmul_rn(fa, s), __dmul_rn(fb, s))));
 }
@@ -117,24 +118,19 @@ __device__ __forceinline__ bool out_of_range(double x) {
     return e - 63u > 1957u;
 }
 
-// One backward-Euler step of one column: forward elimination (linalg.cpp:84-90) with the forcing
-// folded in, then back substitution (linalg.cpp:91). Rows [0, RR) in reg[], the rest at st[32*(i-RR)].
-template <int RR, bool kMixed, bool kGuard>
-__device__ __forceinline__ void column_step(double (&reg)[RR > 0 ? RR : 1], double* st, const double* R, int n,
-                                            double h, double f, const double* sx, bool forced_lane,
-                                            bool& bad) {
+// One backward-Euler step of one basis column from a record in shared memory: forward
+// elimination (linalg.cpp:84-90), back substitution (linalg.cpp:91). Rows [0, RR) in reg[],
+// the rest at st[32*(i-RR)].
+template <int RR>
+__device__ __forceinline__ void basis_step(double (&reg)[RR > 0 ? RR : 1], double* st, const double* R, int n) {
     const double negr = R[0];
-    const double ffa = kMixed ? __dmul_rn(f, R[1]) : 0.0;  // f in {0, 1}: exact
-    const double ffb = kMixed ? __dmul_rn(f, R[2]) : 0.0;
     const double2* PR = reinterpret_cast<const double2*>(R + 4);
     const double* CC = R + 4 + 2 * n;
     double d = 0.0;
 #pragma unroll
     for (int i = 0; i < RR; ++i) {
-        const double x = kMixed ? forced(reg[i], h, ffa, ffb, sx[i]) : reg[i];
-        const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
-        if (kMixed && !kGuard) bad |= forced_lane && out_of_range(num);
-        d = kGuard ? div_guarded(num, PR[i]) : div_fast(num, PR[i]);
+        const double num = (i == 0) ? reg[i] : __dsub_rn(reg[i], __dmul_rn(negr, d));
+        d = div_fast(num, PR[i]);
         reg[i] = d;
     }
     {
@@ -142,10 +138,8 @@ __device__ __forceinline__ void column_step(double (&reg)[RR > 0 ? RR : 1], doub
         const double2* pr = PR + RR;
 #pragma unroll 8
         for (int i = RR; i < n; ++i, s += 32, ++pr) {
-            const double x = kMixed ? forced(*s, h, ffa, ffb, sx[i]) : *s;
-            const double num = (RR == 0 && i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
-            if (kMixed && !kGuard) bad |= forced_lane && out_of_range(num);
-            d = kGuard ? div_guarded(num, *pr) : div_fast(num, *pr);
+            const double num = (RR == 0 && i == 0) ? *s : __dsub_rn(*s, __dmul_rn(negr, d));
+            d = div_fast(num, *pr);
             *s = d;
         }
     }
@@ -165,44 +159,135 @@ __device__ __forceinline__ void column_step(double (&reg)[RR > 0 ? RR : 1], doub
     }
 }
 
+// One step of a forced (c) column whose record R is private to the lane (lanes are different
+// slices): pivots and multipliers stream from L2 kD rows ahead through a register ring.
+template <int RR, bool kGuard>
+__device__ __forceinline__ void forcing_step(double (&reg)[RR > 0 ? RR : 1], double* st, const double* R, int n,
+                                             double h, const double* sx, bool& bad) {
+    constexpr int kD = 8;
+    static_assert(RR % kD == 0, "register rows must be a multiple of the prefetch depth");
+    const double negr = __ldg(R), fa = __ldg(R + 1), fb = __ldg(R + 2);
+    const double2* PR = reinterpret_cast<const double2*>(R + 4);
+    const double* CC = R + 4 + 2 * n;
+    double2 pq[kD];
+    double cq[kD];
+#pragma unroll
+    for (int u = 0; u < kD; ++u) {
+        pq[u] = (u < n) ? __ldg(PR + u) : make_double2(1.0, 1.0);
+        cq[u] = (n - 2 - RR - u >= 0) ? __ldg(CC + (n - 2 - u)) : 0.0;
+    }
+    double d = 0.0;
+#pragma unroll
+    for (int i = 0; i < RR; ++i) {
+        const double2 pr = pq[i % kD];
+        if (i + kD < n) pq[i % kD] = __ldg(PR + i + kD);
+        const double x = forced(reg[i], h, fa, fb, sx[i]);
+        const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
+        if (!kGuard) bad |= out_of_range(num);
+        d = kGuard ? div_guarded(num, pr) : div_fast(num, pr);
+        reg[i] = d;
+    }
+    for (int i0 = RR; i0 < n; i0 += kD) {
+#pragma unroll
+        for (int u = 0; u < kD; ++u) {
+            const int i = i0 + u;
+            if (i < n) {
+                const double2 pr = pq[u];
+                if (i + kD < n) pq[u] = __ldg(PR + i + kD);
+                const double x = forced(st[(i - RR) * 32], h, fa, fb, sx[i]);
+                const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
+                if (!kGuard) bad |= out_of_range(num);
+                d = kGuard ? div_guarded(num, pr) : div_fast(num, pr);
+                st[(i - RR) * 32] = d;
+            }
+        }
+    }
+    // back substitution over the shared-memory rows in chunks of kD, c prefetched one chunk ahead
+    for (int t0 = 0; n - 2 - t0 >= RR; t0 += kD) {
+#pragma unroll
+        for (int u = 0; u < kD; ++u) {
+            const int i = n - 2 - t0 - u;
+            if (i >= RR) {
+                const double c = cq[u];
+                if (i - kD >= RR) cq[u] = __ldg(CC + i - kD);
+                d = __dsub_rn(st[(i - RR) * 32], __dmul_rn(c, d));
+                st[(i - RR) * 32] = d;
+            }
+        }
+    }
+#pragma unroll
+    for (int i = RR - 1; i >= 0; --i) {
+        if (i <= n - 2) {
+            d = __dsub_rn(reg[i], __dmul_rn(__ldg(CC + i), d));
+            reg[i] = d;
+        }
+    }
+}
+
 __device__ __forceinline__ void stage_record_cta(double* dst, const double* src, int chunks) {
     for (int c = threadIdx.x; c < chunks; c += blockDim.x)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst + 2 * c)), "l"(src + 2 * c));
     asm volatile("cp.async.commit_group;\n" ::);
 }
 
-// CTA = warps [c*warps_per_cta, ...) of one slice. Dynamic smem:
-// rec[2][RS] | sx[n] (even) | state[warps_per_cta][(n - RR) * 32]
+// Forcing CTA: warp w holds the c runs of 32 consecutive slices (lane = slice).
+// Dynamic smem: sx[n] (even) | state[warps_per_cta][(n - RR) * 32]
 template <int RR, bool kGuard>
-__global__ void __launch_bounds__(kMaxCtaThreads) heat_build_kernel(BuildPlan P) {
+__device__ void forcing_cta(const BuildPlan& P, int fcta) {
+    extern __shared__ __align__(16) double smem[];
+    const int n = P.n;
+    const int lane = threadIdx.x & 31, wcta = threadIdx.x >> 5;
+    double* sx = smem;
+    double* st = sx + ((n + 1) & ~1) + static_cast<long long>(wcta) * (n - RR) * 32 + lane;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sx[i] = P.sx[i];
+    __syncthreads();
+    const int slice = (fcta * P.warps_per_cta + wcta) * 32 + lane;
+    const bool active = slice < P.N;
+    const long long q0 = active ? P.step_off[slice] : 0;
+    const int steps = active ? static_cast<int>(P.step_off[slice + 1] - q0) : 0;
+    const double h = active ? P.slice_dt[slice] : 0.0;
+    const int max_steps = __reduce_max_sync(0xffffffffu, steps);
+    const long long RS = rec_stride(n);
+    double reg[RR > 0 ? RR : 1];
+#pragma unroll
+    for (int i = 0; i < RR; ++i) reg[i] = 0.0;  // c = the forced run from the zero state
+    for (int i = RR; i < n; ++i) st[(i - RR) * 32] = 0.0;
+    bool bad = false;
+    for (int s = 0; s < max_steps; ++s)
+        if (s < steps) forcing_step<RR, kGuard>(reg, st, P.rec + (q0 + s) * RS, n, h, sx, bad);
+    if (active) {
+        double* gp = P.maps + static_cast<long long>(slice) * n * P.ldm + n;
+#pragma unroll
+        for (int i = 0; i < RR; ++i) gp[i * P.ldm] = reg[i];
+        for (int i = RR; i < n; ++i) gp[i * P.ldm] = st[(i - RR) * 32];
+    }
+    if (bad) record_failure(P.fail, slice, PINT_E_RANGE_RETRY, static_cast<double>(n));
+}
+
+// Basis CTA = warps [c*warps_per_cta, ...) of one slice, lane = basis column e_k.
+// Dynamic smem: rec[2][RS] | state[warps_per_cta][(n - RR) * 32]
+template <int RR>
+__device__ void basis_cta(const BuildPlan& P, int b) {
     extern __shared__ __align__(16) double smem[];
     const unsigned long long t_start = pint_dev::globaltimer();
     const int n = P.n;
     const int lane = threadIdx.x & 31, wcta = threadIdx.x >> 5;
-    const int slice = blockIdx.x / P.ctas_per_slice;
-    const int g = (blockIdx.x - slice * P.ctas_per_slice) * P.warps_per_cta + wcta;  // warp in slice
+    const int slice = b / P.ctas_per_slice;
+    const int g = (b - slice * P.ctas_per_slice) * P.warps_per_cta + wcta;  // warp in slice
     const long long RS = rec_stride(n);
     double* recbuf = smem;
-    double* sx = smem + 2 * RS;
-    double* st = sx + ((n + 1) & ~1) + static_cast<long long>(wcta) * (n - RR) * 32 + lane;
+    double* st = smem + 2 * RS + static_cast<long long>(wcta) * (n - RR) * 32 + lane;
     const int k = g * 32 + lane;
-    const bool active = k <= n;
-    const bool forced_lane = (k == n);
-    const bool mixed = (g == P.wps - 1);
-    const double f = forced_lane ? 1.0 : 0.0;
     const long long q_begin = P.step_off[slice], q_end = P.step_off[slice + 1];
-    const double h = P.slice_dt[slice];
     const int chunks = static_cast<int>(RS / 2);
     const double* rec = P.rec;
 
     if (q_begin < q_end) stage_record_cta(recbuf, rec + q_begin * RS, chunks);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) sx[i] = P.sx[i];
     double reg[RR > 0 ? RR : 1];
 #pragma unroll
-    for (int i = 0; i < RR; ++i) reg[i] = (i == k) ? 1.0 : 0.0;
+    for (int i = 0; i < RR; ++i) reg[i] = (i == k) ? 1.0 : 0.0;  // e_k
     for (int i = RR; i < n; ++i) st[(i - RR) * 32] = (i == k) ? 1.0 : 0.0;
 
-    bool bad = false;
     int cur = 0;
     for (long long q = q_begin; q < q_end; ++q) {
         if (q + 1 < q_end) {
@@ -211,21 +296,31 @@ __global__ void __launch_bounds__(kMaxCtaThreads) heat_build_kernel(BuildPlan P)
         } else {
             asm volatile("cp.async.wait_group 0;\n" ::);
         }
-        __syncthreads();  // record q (and sx) visible to every warp
-        const double* R = recbuf + cur * RS;
-        if (mixed) column_step<RR, true, kGuard>(reg, st, R, n, h, f, sx, forced_lane, bad);
-        else column_step<RR, false, kGuard>(reg, st, R, n, h, f, sx, forced_lane, bad);
+        __syncthreads();  // record q visible to every warp
+        basis_step<RR>(reg, st, recbuf + cur * RS, n);
         __syncthreads();  // buffer `cur` is refilled next iteration
         cur ^= 1;
     }
-    if (active) {
+    if (k < n) {
         double* gp = P.maps + static_cast<long long>(slice) * n * P.ldm + k;
 #pragma unroll
         for (int i = 0; i < RR; ++i) gp[i * P.ldm] = reg[i];
         for (int i = RR; i < n; ++i) gp[i * P.ldm] = st[(i - RR) * 32];
     }
-    if (bad) record_failure(P.fail, slice, PINT_E_RANGE_RETRY, static_cast<double>(k));
     if (P.per_slice_ns && threadIdx.x == 0) atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
+}
+
+// Two kernels so each gets its own register allocation; the forcing kernel runs on the context's
+// side stream concurrently with the basis kernel. kGuard affects only the forced columns: basis
+// columns are positive and never need it.
+template <int RR>
+__global__ void __launch_bounds__(kMaxCtaThreads) heat_basis_kernel(BuildPlan P) {
+    basis_cta<RR>(P, blockIdx.x);
+}
+
+template <int RR, bool kGuard>
+__global__ void __launch_bounds__(32) heat_forcing_kernel(BuildPlan P) {
+    forcing_cta<RR, kGuard>(P, blockIdx.x);
 }
 
 // ---- integrate: K caller columns of one slice, lane = column (guarded division) ---------------
@@ -275,23 +370,41 @@ __global__ void __launch_bounds__(32) heat_integrate_kernel(IntegratePlan P) {
 }
 
 
-size_t build_smem(int n, int rr, int warps_per_cta) {
-    return sizeof(double) * (2 * rec_stride(n) + ((n + 1) & ~1) + static_cast<size_t>(n - rr) * 32 * warps_per_cta);
+
+
+template <class K>
+void smem_attrs(K kern, size_t smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
 }
 
 template <int RR, bool kGuard>
 int launch_build(pint_ctx* ctx, BuildPlan P) {
-    // one CTA per slice when two such CTAs fit an SM, else one CTA per warp
-    P.warps_per_cta = (P.wps <= kMaxCtaThreads / 32 && build_smem(P.n, RR, P.wps) <= 112 * 1024) ? P.wps : 1;
-    P.ctas_per_slice = P.wps / P.warps_per_cta;
-    const size_t smem = build_smem(P.n, RR, P.warps_per_cta);
-    if (smem > 227 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: n too large for shared memory");
-    auto kern = heat_build_kernel<RR, kGuard>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    const long long blocks = static_cast<long long>(P.N) * P.ctas_per_slice;
-    kern<<<static_cast<unsigned>(blocks), 32 * P.warps_per_cta, smem, ctx->stream>>>(P);
-    return pint_check_launch(ctx, "heat_build_kernel");
+    // basis: one CTA per slice when two such CTAs fit an SM, else one CTA per warp
+    const size_t state_cta = sizeof(double) * static_cast<size_t>(P.n - RR) * 32;
+    const size_t rec_bytes = sizeof(double) * 2 * rec_stride(P.n);
+    P.warps_per_cta = (P.wb <= kMaxCtaThreads / 32 && rec_bytes + state_cta * P.wb <= 112 * 1024) ? P.wb : 1;
+    P.ctas_per_slice = P.wb / P.warps_per_cta;
+    P.forcing_ctas = (P.N + 31) / 32;  // forcing kernel: one warp per CTA, 32 slices per warp
+    const size_t smem_b = rec_bytes + state_cta * P.warps_per_cta;
+    const size_t smem_f = sizeof(double) * ((P.n + 1) & ~1) + state_cta;
+    if (smem_b > 227 * 1024 || smem_f > 227 * 1024)
+        return pint_set_error(ctx, PINT_E_INVALID, "heat_build: n too large for shared memory");
+    auto kb = heat_basis_kernel<RR>;
+    auto kf = heat_forcing_kernel<RR, kGuard>;
+    smem_attrs(kb, smem_b);
+    smem_attrs(kf, smem_f);
+    // fork: forcing runs on the side stream, overlapping the basis kernel; join before returning
+    cudaEventRecord(ctx->ev_fork, ctx->stream);
+    cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
+    kf<<<static_cast<unsigned>(P.forcing_ctas), 32, smem_f, ctx->side>>>(P);
+    if (const int rc = pint_check_launch(ctx, "heat_forcing_kernel")) return rc;
+    kb<<<static_cast<unsigned>(static_cast<long long>(P.N) * P.ctas_per_slice), 32 * P.warps_per_cta, smem_b,
+         ctx->stream>>>(P);
+    if (const int rc = pint_check_launch(ctx, "heat_basis_kernel")) return rc;
+    cudaEventRecord(ctx->ev_join, ctx->side);
+    cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);
+    return PINT_OK;
 }
 
 }  // namespace
@@ -316,7 +429,7 @@ int launch_heat_build(pint_ctx* ctx, int64_t n, int64_t N, const int64_t* step_o
     BuildPlan P{};
     P.n = static_cast<int>(n);
     P.N = static_cast<int>(N);
-    P.wps = static_cast<int>((n + 1 + 31) / 32);
+    P.wb = static_cast<int>((n + 31) / 32);
     P.rec = records;
     P.sx = sx;
     P.step_off = step_off;
