@@ -159,107 +159,88 @@ __device__ __forceinline__ void basis_step(double (&reg)[RR > 0 ? RR : 1], doubl
     }
 }
 
-// One step of a forced (c) column whose record R is private to the lane (lanes are different
-// slices): pivots and multipliers stream from L2 kD rows ahead through a register ring.
-template <int RR, bool kGuard>
-__device__ __forceinline__ void forcing_step(double (&reg)[RR > 0 ? RR : 1], double* st, const double* R, int n,
-                                             double h, const double* sx, bool& bad) {
-    constexpr int kD = 8;
-    static_assert(RR % kD == 0, "register rows must be a multiple of the prefetch depth");
-    const double negr = __ldg(R), fa = __ldg(R + 1), fb = __ldg(R + 2);
-    const double2* PR = reinterpret_cast<const double2*>(R + 4);
-    const double* CC = R + 4 + 2 * n;
-    double2 pq[kD];
-    double cq[kD];
-#pragma unroll
-    for (int u = 0; u < kD; ++u) {
-        pq[u] = (u < n) ? __ldg(PR + u) : make_double2(1.0, 1.0);
-        cq[u] = (n - 2 - RR - u >= 0) ? __ldg(CC + (n - 2 - u)) : 0.0;
-    }
-    double d = 0.0;
-#pragma unroll
-    for (int i = 0; i < RR; ++i) {
-        const double2 pr = pq[i % kD];
-        if (i + kD < n) pq[i % kD] = __ldg(PR + i + kD);
-        const double x = forced(reg[i], h, fa, fb, sx[i]);
-        const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
-        if (!kGuard) bad |= out_of_range(num);
-        d = kGuard ? div_guarded(num, pr) : div_fast(num, pr);
-        reg[i] = d;
-    }
-    for (int i0 = RR; i0 < n; i0 += kD) {
-#pragma unroll
-        for (int u = 0; u < kD; ++u) {
-            const int i = i0 + u;
-            if (i < n) {
-                const double2 pr = pq[u];
-                if (i + kD < n) pq[u] = __ldg(PR + i + kD);
-                const double x = forced(st[(i - RR) * 32], h, fa, fb, sx[i]);
-                const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
-                if (!kGuard) bad |= out_of_range(num);
-                d = kGuard ? div_guarded(num, pr) : div_fast(num, pr);
-                st[(i - RR) * 32] = d;
-            }
-        }
-    }
-    // back substitution over the shared-memory rows in chunks of kD, c prefetched one chunk ahead
-    for (int t0 = 0; n - 2 - t0 >= RR; t0 += kD) {
-#pragma unroll
-        for (int u = 0; u < kD; ++u) {
-            const int i = n - 2 - t0 - u;
-            if (i >= RR) {
-                const double c = cq[u];
-                if (i - kD >= RR) cq[u] = __ldg(CC + i - kD);
-                d = __dsub_rn(st[(i - RR) * 32], __dmul_rn(c, d));
-                st[(i - RR) * 32] = d;
-            }
-        }
-    }
-#pragma unroll
-    for (int i = RR - 1; i >= 0; --i) {
-        if (i <= n - 2) {
-            d = __dsub_rn(reg[i], __dmul_rn(__ldg(CC + i), d));
-            reg[i] = d;
-        }
-    }
-}
-
 __device__ __forceinline__ void stage_record_cta(double* dst, const double* src, int chunks) {
     for (int c = threadIdx.x; c < chunks; c += blockDim.x)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst + 2 * c)), "l"(src + 2 * c));
     asm volatile("cp.async.commit_group;\n" ::);
 }
 
-// Forcing CTA: warp w holds the c runs of 32 consecutive slices (lane = slice).
-// Dynamic smem: sx[n] (even) | state[warps_per_cta][(n - RR) * 32]
-template <int RR, bool kGuard>
+// Forcing kernel: one warp per CTA holds the forced (c) runs of 32 consecutive slices, lane = slice.
+// Each lane's records are private (different slices), so pivots/reciprocals and multipliers stream
+// from L2 kD rows ahead through register rings; the next step's first rows are fetched during the
+// current back substitution. State lives in shared memory, lane-interleaved.
+// Dynamic smem: sx[n] (even) | state[n * 32]
+template <bool kGuard>
 __device__ void forcing_cta(const BuildPlan& P, int fcta) {
+    constexpr int kD = 32;
     extern __shared__ __align__(16) double smem[];
     const int n = P.n;
-    const int lane = threadIdx.x & 31, wcta = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     double* sx = smem;
-    double* st = sx + ((n + 1) & ~1) + static_cast<long long>(wcta) * (n - RR) * 32 + lane;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) sx[i] = P.sx[i];
-    __syncthreads();
-    const int slice = (fcta * P.warps_per_cta + wcta) * 32 + lane;
+    double* st = sx + ((n + 1) & ~1) + lane;
+    for (int i = lane; i < n; i += 32) sx[i] = P.sx[i];
+    const int slice = fcta * 32 + lane;
     const bool active = slice < P.N;
     const long long q0 = active ? P.step_off[slice] : 0;
     const int steps = active ? static_cast<int>(P.step_off[slice + 1] - q0) : 0;
     const double h = active ? P.slice_dt[slice] : 0.0;
     const int max_steps = __reduce_max_sync(0xffffffffu, steps);
     const long long RS = rec_stride(n);
-    double reg[RR > 0 ? RR : 1];
+    for (int i = 0; i < n; ++i) st[i * 32] = 0.0;  // c = the forced run from the zero state
+    __syncwarp();
+
+    double2 pq[kD];
+    double cq[kD];
+    auto load_head = [&](const double* R) {
+        const double2* PR = reinterpret_cast<const double2*>(R + 4);
 #pragma unroll
-    for (int i = 0; i < RR; ++i) reg[i] = 0.0;  // c = the forced run from the zero state
-    for (int i = RR; i < n; ++i) st[(i - RR) * 32] = 0.0;
+        for (int u = 0; u < kD; ++u) pq[u] = (u < n) ? __ldg(PR + u) : make_double2(1.0, 1.0);
+    };
+    if (steps > 0) load_head(P.rec + q0 * RS);
     bool bad = false;
-    for (int s = 0; s < max_steps; ++s)
-        if (s < steps) forcing_step<RR, kGuard>(reg, st, P.rec + (q0 + s) * RS, n, h, sx, bad);
+    for (int s = 0; s < max_steps; ++s) {
+        if (s >= steps) continue;
+        const double* R = P.rec + (q0 + s) * RS;
+        const double negr = __ldg(R), fa = __ldg(R + 1), fb = __ldg(R + 2);
+        const double2* PR = reinterpret_cast<const double2*>(R + 4);
+        const double* CC = R + 4 + 2 * n;
+#pragma unroll
+        for (int u = 0; u < kD; ++u) cq[u] = (n - 2 - u >= 0) ? __ldg(CC + (n - 2 - u)) : 0.0;
+        // forward elimination with the forcing folded in (linalg.cpp:84-90, pde_problems.cpp:91-94)
+        double d = 0.0;
+        for (int i0 = 0; i0 < n; i0 += kD) {
+#pragma unroll
+            for (int u = 0; u < kD; ++u) {
+                const int i = i0 + u;
+                if (i < n) {
+                    const double2 pr = pq[u];
+                    if (i + kD < n) pq[u] = __ldg(PR + i + kD);
+                    const double x = forced(st[i * 32], h, fa, fb, sx[i]);
+                    const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
+                    if (!kGuard) bad |= out_of_range(num);
+                    d = kGuard ? div_guarded(num, pr) : div_fast(num, pr);
+                    st[i * 32] = d;
+                }
+            }
+        }
+        if (s + 1 < steps) load_head(R + RS);  // next step's first rows, hidden behind the back sweep
+        // back substitution (linalg.cpp:91), multipliers kD rows ahead
+        for (int t0 = 0; n - 2 - t0 >= 0; t0 += kD) {
+#pragma unroll
+            for (int u = 0; u < kD; ++u) {
+                const int i = n - 2 - t0 - u;
+                if (i >= 0) {
+                    const double c = cq[u];
+                    if (i - kD >= 0) cq[u] = __ldg(CC + i - kD);
+                    d = __dsub_rn(st[i * 32], __dmul_rn(c, d));
+                    st[i * 32] = d;
+                }
+            }
+        }
+    }
     if (active) {
         double* gp = P.maps + static_cast<long long>(slice) * n * P.ldm + n;
-#pragma unroll
-        for (int i = 0; i < RR; ++i) gp[i * P.ldm] = reg[i];
-        for (int i = RR; i < n; ++i) gp[i * P.ldm] = st[(i - RR) * 32];
+        for (int i = 0; i < n; ++i) gp[i * P.ldm] = st[i * 32];
     }
     if (bad) record_failure(P.fail, slice, PINT_E_RANGE_RETRY, static_cast<double>(n));
 }
@@ -318,9 +299,9 @@ __global__ void __launch_bounds__(kMaxCtaThreads) heat_basis_kernel(BuildPlan P)
     basis_cta<RR>(P, blockIdx.x);
 }
 
-template <int RR, bool kGuard>
+template <bool kGuard>
 __global__ void __launch_bounds__(32) heat_forcing_kernel(BuildPlan P) {
-    forcing_cta<RR, kGuard>(P, blockIdx.x);
+    forcing_cta<kGuard>(P, blockIdx.x);
 }
 
 // ---- integrate: K caller columns of one slice, lane = column (guarded division) ---------------
@@ -387,11 +368,11 @@ int launch_build(pint_ctx* ctx, BuildPlan P) {
     P.ctas_per_slice = P.wb / P.warps_per_cta;
     P.forcing_ctas = (P.N + 31) / 32;  // forcing kernel: one warp per CTA, 32 slices per warp
     const size_t smem_b = rec_bytes + state_cta * P.warps_per_cta;
-    const size_t smem_f = sizeof(double) * ((P.n + 1) & ~1) + state_cta;
+    const size_t smem_f = sizeof(double) * (((P.n + 1) & ~1) + static_cast<size_t>(P.n) * 32);
     if (smem_b > 227 * 1024 || smem_f > 227 * 1024)
         return pint_set_error(ctx, PINT_E_INVALID, "heat_build: n too large for shared memory");
     auto kb = heat_basis_kernel<RR>;
-    auto kf = heat_forcing_kernel<RR, kGuard>;
+    auto kf = heat_forcing_kernel<kGuard>;
     smem_attrs(kb, smem_b);
     smem_attrs(kf, smem_f);
     // fork: forcing runs on the side stream, overlapping the basis kernel; join before returning
