@@ -146,26 +146,27 @@ int64_t pint_heat_total_steps(const pint_slice* slices, int64_t N);
  * fa[q] = -sin t, fb[q] = ((a(t) pi) pi) cos t; sx[i] = sin(pi (i+1) dx). n = interior points. */
 int pint_heat_coefficients(double dx, const pint_slice* slices, int64_t N, int64_t* step_off,
                            double* r, double* fa, double* fb, double* sx, int64_t* n_out);
-/* doubles per step record (see pint_heat_factor_dev) */
-int64_t pint_heat_record_stride(int64_t n);
-/* Shared tridiagonal factor per step — the Thomas forward pivots (linalg.cpp:77-93), computed
- * once per (slice, step) instead of once per trajectory. records[q * stride ...] =
- * {-r, fa, fb, 0, p[0..n), RN(1/p)[0..n), c[0..n)} for every step q < total_steps. */
-int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t total_steps, const double* r,
-                         const double* fa, const double* fb, double* records);
+/* doubles of the per-step records of N slices with at most S steps each (pint_heat_factor_dev) */
+int64_t pint_heat_records_size(int64_t n, int64_t N, int64_t S);
+/* Shared tridiagonal factor per (slice, step) — the Thomas forward pivots (linalg.cpp:77-93),
+ * computed once per step instead of once per trajectory, stored slice-minor:
+ * hdr[3][S][N] = {-r, fa, fb}, then (p_i, RN(1/p_i))[S][n][N], then c_i[S][n][N].
+ * step_off (device, N+1) and r/fa/fb (device, step_off[N]) come from pint_heat_coefficients. */
+int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
+                         const double* r, const double* fa, const double* fb, double* records);
 /* Build all N augmented maps into maps (N * n * ldm doubles). step_off/slice_dt/sx are device
  * copies of the host tables; per_slice_ns (may be NULL) accumulates per-slice device time.
  * guarded = 0: fast exact division, forced lanes range-checked off the critical path; a tripped
  * check latches PINT_E_RANGE_RETRY in the failure record and the caller re-runs with
  * guarded = 1 (IEEE division on the chain outside [2^-960, 2^997]). Both are bit-exact. */
-int pint_heat_build_dev(pint_ctx* ctx, int64_t n, int64_t N, const int64_t* step_off,
+int pint_heat_build_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
                         const double* slice_dt, const double* records, const double* sx,
                         double* maps, unsigned long long* per_slice_ns, int guarded);
-/* Integrate K state vectors y[k*n ...] in place through the steps [q0, q0+steps) of the
- * records (the integrate closure for one slice, or run_serial over one whole-interval slice). */
-int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t q0, int64_t steps,
-                            double h, int with_forcing, const double* records, const double* sx,
-                            double* y);
+/* Integrate K state vectors y[k*n ...] in place through steps [s0, s0+steps) of ONE slice's
+ * records (built with N = 1, S steps): the integrate closure, or run_serial over the interval. */
+int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t S, int64_t s0,
+                            int64_t steps, double h, int with_forcing, const double* records,
+                            const double* sx, double* y);
 
 /* ---- K4: affine composition (compose_sweep, nievergelt.cpp:90-110) ----
  * CHAIN: y <- G_j y + c_j in slice order, rows as sequential dots (bit-exact vs matvec,

@@ -82,10 +82,10 @@ _SIGS = {
     "pint_scalar_sweep_dev": (_int, [_vp, _int, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _i, _d, _vp, _vp, _vp]),
     "pint_heat_total_steps": (_i, [C.POINTER(Slice), _i]),
     "pint_heat_coefficients": (_int, [_d, C.POINTER(Slice), _i, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i)]),
-    "pint_heat_record_stride": (_i, [_i]),
-    "pint_heat_factor_dev": (_int, [_vp, _i, _i, _vp, _vp, _vp, _vp]),
-    "pint_heat_build_dev": (_int, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _int]),
-    "pint_heat_integrate_dev": (_int, [_vp, _i, _i, _i, _i, _d, _int, _vp, _vp, _vp]),
+    "pint_heat_records_size": (_i, [_i, _i, _i]),
+    "pint_heat_factor_dev": (_int, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "pint_heat_build_dev": (_int, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _int]),
+    "pint_heat_integrate_dev": (_int, [_vp, _i, _i, _i, _i, _i, _d, _int, _vp, _vp, _vp]),
     "pint_affine_compose_dev": (_int, [_vp, _int, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "pint_affine_pair_dev": (_int, [_vp, _i, _i, _vp, _vp, _vp]),
     "pint_lv_ensemble_dev": (_int, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -334,26 +334,26 @@ int pint_scalar_sweep_dev(pint_ctx* ctx, int mode, int64_t N, int64_t M, const d
                                y0, lambdas, y_out, extrapolations);
 }
 
-int64_t pint_heat_record_stride(int64_t n) { return heat_record_stride(n); }
+int64_t pint_heat_records_size(int64_t n, int64_t N, int64_t S) { return heat_records_doubles(n, N, S); }
 
-int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t total_steps, const double* r, const double* fa,
-                         const double* fb, double* records) {
+int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
+                         const double* r, const double* fa, const double* fb, double* records) {
     if (!ctx) return PINT_E_INVALID;
-    return launch_heat_factor(ctx, n, total_steps, r, fa, fb, records);
+    return launch_heat_factor(ctx, n, N, S, step_off, r, fa, fb, records);
 }
 
-int pint_heat_build_dev(pint_ctx* ctx, int64_t n, int64_t N, const int64_t* step_off,
+int pint_heat_build_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
                         const double* slice_dt, const double* records, const double* sx,
                         double* maps, unsigned long long* per_slice_ns, int guarded) {
     if (!ctx) return PINT_E_INVALID;
-    return launch_heat_build(ctx, n, N, step_off, slice_dt, records, sx, maps, per_slice_ns, guarded);
+    return launch_heat_build(ctx, n, N, S, step_off, slice_dt, records, sx, maps, per_slice_ns, guarded);
 }
 
-int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t q0, int64_t steps,
-                            double h, int with_forcing, const double* records, const double* sx,
-                            double* y) {
+int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t S, int64_t s0,
+                            int64_t steps, double h, int with_forcing, const double* records,
+                            const double* sx, double* y) {
     if (!ctx) return PINT_E_INVALID;
-    return launch_heat_integrate(ctx, n, K, q0, steps, h, with_forcing, records, sx, y);
+    return launch_heat_integrate(ctx, n, K, S, s0, steps, h, with_forcing, records, sx, y);
 }
 
 int pint_affine_compose_dev(pint_ctx* ctx, int mode, int64_t n, int64_t N, double* maps,
@@ -568,7 +568,7 @@ int pint_scalar_integrate(pint_ctx* ctx, const pint_scalar_rhs* rhs, const pint_
 // Device tables for a set of (closure-normalised) heat slices; returns device pointers.
 namespace {
 struct HeatDev {
-    int64_t n = 0, N = 0, Q = 0;
+    int64_t n = 0, N = 0, Q = 0, S = 0;
     int64_t* step_off = nullptr;
     double *slice_dt = nullptr, *r = nullptr, *fa = nullptr, *fb = nullptr, *sx = nullptr;
     double* factor = nullptr;
@@ -595,14 +595,17 @@ int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, Hea
     auto* h_sx = reinterpret_cast<double*>(h + b_off + b_dt + 3 * b_q);
     for (int64_t j = 0; j < N; ++j) h_dt[j] = sl[j].dt;
     pint_heat_coefficients(dx, sl.data(), N, h_off, h_r, h_fa, h_fb, h_sx, nullptr);
+    int64_t S = 0;
+    for (const auto& s : sl) S = std::max<int64_t>(S, s.steps);
     char* d = static_cast<char*>(pint_scratch(ctx, 0, in_bytes));
-    double* f = static_cast<double*>(pint_scratch(ctx, 1, sizeof(double) * heat_record_stride(n) * Q));
+    double* f = static_cast<double*>(pint_scratch(ctx, 1, sizeof(double) * heat_records_doubles(n, N, S)));
     if (!d || !f) return PINT_E_CUDA;
     if (!ok(ctx, cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D heat tables"))
         return PINT_E_CUDA;
     H.n = n;
     H.N = N;
     H.Q = Q;
+    H.S = S;
     H.step_off = reinterpret_cast<int64_t*>(d);
     H.slice_dt = reinterpret_cast<double*>(d + b_off);
     H.r = reinterpret_cast<double*>(d + b_off + b_dt);
@@ -611,7 +614,7 @@ int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, Hea
     H.sx = reinterpret_cast<double*>(d + b_off + b_dt + 3 * b_q);
     H.factor = f;
     H.h2d = in_bytes;
-    return launch_heat_factor(ctx, n, Q, H.r, H.fa, H.fb, H.factor);
+    return launch_heat_factor(ctx, n, N, S, H.step_off, H.r, H.fa, H.fb, H.factor);
 }
 
 int singular_check(pint_ctx* ctx) {
@@ -664,7 +667,7 @@ int pint_run_heat(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int 
     int rc = PINT_OK;
     for (int guarded = 0; guarded < 2; ++guarded) {  // second pass only if a range check tripped
         if (per_slice_seconds) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
-        rc = launch_heat_build(ctx, n, N, H.step_off, H.slice_dt, H.factor, H.sx, d_maps,
+        rc = launch_heat_build(ctx, n, N, H.S, H.step_off, H.slice_dt, H.factor, H.sx, d_maps,
                                per_slice_seconds ? d_ns : nullptr, guarded);
         if (rc) return rc;
         cudaEventRecord(ctx->evc, ctx->stream);
@@ -716,7 +719,7 @@ int pint_heat_maps(pint_ctx* ctx, double dx, double dt, const pint_slice* slices
     std::vector<double> host(static_cast<size_t>(n * ldm * N));
     int rc = PINT_OK;
     for (int guarded = 0; guarded < 2; ++guarded) {
-        if ((rc = launch_heat_build(ctx, n, N, H.step_off, H.slice_dt, H.factor, H.sx, d_maps, nullptr, guarded)))
+        if ((rc = launch_heat_build(ctx, n, N, H.S, H.step_off, H.slice_dt, H.factor, H.sx, d_maps, nullptr, guarded)))
             return rc;
         cudaMemcpyAsync(host.data(), d_maps, sizeof(double) * host.size(), cudaMemcpyDeviceToHost, ctx->stream);
         if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "heat_maps sync")) return PINT_E_CUDA;
@@ -745,7 +748,7 @@ int pint_heat_integrate(pint_ctx* ctx, double dx, const pint_slice* slice, doubl
     double* d_y = static_cast<double*>(pint_scratch(ctx, 2, sizeof(double) * n * K));
     if (!d_y) return PINT_E_CUDA;
     cudaMemcpyAsync(d_y, y, sizeof(double) * n * K, cudaMemcpyHostToDevice, ctx->stream);
-    int rc = launch_heat_integrate(ctx, n, K, 0, H.Q, sl[0].dt, with_forcing, H.factor, H.sx, d_y);
+    int rc = launch_heat_integrate(ctx, n, K, H.S, 0, H.Q, sl[0].dt, with_forcing, H.factor, H.sx, d_y);
     if (rc) return rc;
     cudaMemcpyAsync(y, d_y, sizeof(double) * n * K, cudaMemcpyDeviceToHost, ctx->stream);
     if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "heat_integrate sync")) return PINT_E_CUDA;

@@ -87,8 +87,9 @@ class HeatPlan:
         self.ldm = int(capi.load().pint_affine_ldm(self.n))
         dev = torch.device("cuda", ctx.device)
         self.dev = [t.to(dev) for t in self.host.tensors()]
-        stride_rec = int(capi.load().pint_heat_record_stride(self.n))
-        self.factor = torch.empty(self.Q * stride_rec, dtype=torch.float64, device=dev)
+        self.S = max(s.steps for s in self.slices)
+        rec_doubles = int(capi.load().pint_heat_records_size(self.n, self.N, self.S))
+        self.factor = torch.empty(rec_doubles, dtype=torch.float64, device=dev)
         stride = self.n * self.ldm
         self.maps = torch.zeros(self.N * stride, dtype=torch.float64, device=dev)
         self.scratch = torch.zeros(max(1, (self.N + 1) // 2) * stride, dtype=torch.float64, device=dev)
@@ -110,8 +111,8 @@ class HeatPlan:
     def factor_and_build(self):
         c, P = self.ctx, capi.ptr
         step_off, slice_dt, r, fa, fb, sx = self.dev
-        c.call("pint_heat_factor_dev", self.n, self.Q, P(r), P(fa), P(fb), P(self.factor))
-        c.call("pint_heat_build_dev", self.n, self.N, P(step_off), P(slice_dt), P(self.factor), P(sx),
+        c.call("pint_heat_factor_dev", self.n, self.N, self.S, P(step_off), P(r), P(fa), P(fb), P(self.factor))
+        c.call("pint_heat_build_dev", self.n, self.N, self.S, P(step_off), P(slice_dt), P(self.factor), P(sx),
                P(self.maps), None, self.guarded)
 
     def verify(self) -> bool:
