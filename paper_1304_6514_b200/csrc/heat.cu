@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kMaxCtaThreads) heat_basis_kernel(BuildPlan P)
 // Dynamic smem: sx[n] (even) | state[n * 32]
 template <bool kGuard>
 __global__ void __launch_bounds__(32) heat_forcing_kernel(BuildPlan P) {
-    constexpr int kD = 32;
+    constexpr int kD = 16;
     extern __shared__ __align__(16) double smem[];
     const int n = P.n;
     const int lane = threadIdx.x;
@@ -276,51 +276,71 @@ __global__ void __launch_bounds__(32) heat_forcing_kernel(BuildPlan P) {
     for (int i = 0; i < n; ++i) st[i * 32] = 0.0;  // c = the forced run from the zero state
     __syncwarp();
 
+    // Rings are refilled by UNCONDITIONAL loads from clamped rows: a predicated refill compiles to
+    // load-into-temp + MOV, and the MOV waits for the data, which defeats the prefetch.
+    const long long N = P.N;
     double2 pq[kD];
     double cq[kD];
+    double h_negr = 0.0, h_fa = 0.0, h_fb = 0.0;  // header of the step the ring was loaded for
     auto load_head = [&](long long s) {
+        const double2* base = V.pr + V.row(s, 0, js);
 #pragma unroll
-        for (int u = 0; u < kD; ++u) pq[u] = (u < n) ? __ldg(V.pr + V.row(s, u, js)) : make_double2(1.0, 1.0);
+        for (int u = 0; u < kD; ++u) pq[u] = __ldg(base + static_cast<long long>(u < n ? u : n - 1) * N);
+        h_negr = __ldg(V.negr + V.hdr(s, js));
+        h_fa = __ldg(V.fa + V.hdr(s, js));
+        h_fb = __ldg(V.fb + V.hdr(s, js));
     };
     if (steps > 0) load_head(0);
     bool bad = false;
     for (long long s = 0; s < max_steps; ++s) {
         if (s >= steps) continue;
-        const double negr = __ldg(V.negr + V.hdr(s, js));
-        const double fa = __ldg(V.fa + V.hdr(s, js)), fb = __ldg(V.fb + V.hdr(s, js));
+        const double negr = h_negr, fa = h_fa, fb = h_fb;
+        const double2* pbase = V.pr + V.row(s, 0, js);  // row i at pbase + i*N
+        const double* cbase = V.cc + V.row(s, 0, js);
 #pragma unroll
-        for (int u = 0; u < kD; ++u) cq[u] = (n - 2 - u >= 0) ? __ldg(V.cc + V.row(s, n - 2 - u, js)) : 0.0;
+        for (int u = 0; u < kD; ++u) cq[u] = __ldg(cbase + static_cast<long long>(n - 2 - u > 0 ? n - 2 - u : 0) * N);
         // forward elimination with the forcing folded in (linalg.cpp:84-90, pde_problems.cpp:91-94)
         double d = 0.0;
-        for (int i0 = 0; i0 < n; i0 += kD) {
+        auto fwd_row = [&](int i, double2 pr) {
+            const double x = forced(st[i * 32], h, fa, fb, sx[i]);
+            const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
+            if (!kGuard) bad |= out_of_range(num);
+            d = kGuard ? div_guarded(num, pr) : div_fast(num, pr);
+            st[i * 32] = d;
+        };
+        int i0 = 0;
+        for (; i0 + kD <= n; i0 += kD) {
+            const double2* nxt = pbase + static_cast<long long>(i0 + kD) * N;
 #pragma unroll
             for (int u = 0; u < kD; ++u) {
-                const int i = i0 + u;
-                if (i < n) {
-                    const double2 pr = pq[u];
-                    if (i + kD < n) pq[u] = __ldg(V.pr + V.row(s, i + kD, js));
-                    const double x = forced(st[i * 32], h, fa, fb, sx[i]);
-                    const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
-                    if (!kGuard) bad |= out_of_range(num);
-                    d = kGuard ? div_guarded(num, pr) : div_fast(num, pr);
-                    st[i * 32] = d;
-                }
+                const double2 pr = pq[u];
+                pq[u] = __ldg(i0 + kD + u < n ? nxt : pbase);
+                nxt += N;
+                fwd_row(i0 + u, pr);
             }
         }
+#pragma unroll
+        for (int u = 0; u < kD; ++u)
+            if (i0 + u < n) fwd_row(i0 + u, pq[u]);
         if (s + 1 < steps) load_head(s + 1);  // hidden behind the back sweep
         // back substitution (linalg.cpp:91), multipliers kD rows ahead
-        for (int t0 = 0; n - 2 - t0 >= 0; t0 += kD) {
+        auto back_row = [&](int i, double c) {
+            d = __dsub_rn(st[i * 32], __dmul_rn(c, d));
+            st[i * 32] = d;
+        };
+        int t0 = 0;
+        for (; n - 2 - t0 - (kD - 1) >= 0; t0 += kD) {
 #pragma unroll
             for (int u = 0; u < kD; ++u) {
                 const int i = n - 2 - t0 - u;
-                if (i >= 0) {
-                    const double c = cq[u];
-                    if (i - kD >= 0) cq[u] = __ldg(V.cc + V.row(s, i - kD, js));
-                    d = __dsub_rn(st[i * 32], __dmul_rn(c, d));
-                    st[i * 32] = d;
-                }
+                const double c = cq[u];
+                cq[u] = __ldg(cbase + static_cast<long long>(i - kD >= 0 ? i - kD : 0) * N);
+                back_row(i, c);
             }
         }
+#pragma unroll
+        for (int u = 0; u < kD; ++u)
+            if (n - 2 - t0 - u >= 0) back_row(n - 2 - t0 - u, cq[u]);
     }
     if (active) {
         double* gp = P.maps + static_cast<long long>(slice) * n * P.ldm + n;
