@@ -204,7 +204,8 @@ def main():
             events[0].record(stream)
         P = capi.ptr
         step_off, slice_dt, r, fa, fb, sx = plan.dev
-        ctx.call("pint_heat_factor_dev", plan.n, plan.N, plan.S, P(step_off), P(r), P(fa), P(fb), P(plan.factor))
+        ctx.call("pint_heat_factor_dev", plan.n, plan.N, plan.S, P(step_off), P(slice_dt), P(r), P(fa), P(fb), P(sx),
+                 P(plan.factor))
         if events:
             events[1].record(stream)
         ctx.call("pint_heat_build_dev", plan.n, plan.N, plan.S, P(step_off), P(slice_dt), P(plan.factor), P(sx),

@@ -149,11 +149,13 @@ int pint_heat_coefficients(double dx, const pint_slice* slices, int64_t N, int64
 /* doubles of the per-step records of N slices with at most S steps each (pint_heat_factor_dev) */
 int64_t pint_heat_records_size(int64_t n, int64_t N, int64_t S);
 /* Shared tridiagonal factor per (slice, step) — the Thomas forward pivots (linalg.cpp:77-93),
- * computed once per step instead of once per trajectory, stored slice-minor:
- * hdr[3][S][N] = {-r, fa, fb}, then (p_i, RN(1/p_i))[S][n][N], then c_i[S][n][N].
- * step_off (device, N+1) and r/fa/fb (device, step_off[N]) come from pint_heat_coefficients. */
+ * computed once per step instead of once per trajectory — plus the forcing increments, stored
+ * slice-minor: hdr[3][S][N] = {-r, fa, fb}, then (p_i, RN(1/p_i))[S][n][N], c_i[S][n][N] and
+ * h*b_i[S][n][N]. step_off/slice_dt/sx (device) and r/fa/fb (device, step_off[N] entries) come
+ * from pint_heat_coefficients. */
 int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
-                         const double* r, const double* fa, const double* fb, double* records);
+                         const double* slice_dt, const double* r, const double* fa,
+                         const double* fb, const double* sx, double* records);
 /* Build all N augmented maps into maps (N * n * ldm doubles). step_off/slice_dt/sx are device
  * copies of the host tables; per_slice_ns (may be NULL) accumulates per-slice device time.
  * guarded = 0: fast exact division, forced lanes range-checked off the critical path; a tripped

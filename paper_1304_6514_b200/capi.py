@@ -83,7 +83,7 @@ _SIGS = {
     "pint_heat_total_steps": (_i, [C.POINTER(Slice), _i]),
     "pint_heat_coefficients": (_int, [_d, C.POINTER(Slice), _i, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i)]),
     "pint_heat_records_size": (_i, [_i, _i, _i]),
-    "pint_heat_factor_dev": (_int, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "pint_heat_factor_dev": (_int, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pint_heat_build_dev": (_int, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _int]),
     "pint_heat_integrate_dev": (_int, [_vp, _i, _i, _i, _i, _i, _d, _int, _vp, _vp, _vp]),
     "pint_affine_compose_dev": (_int, [_vp, _int, _i, _i, _vp, _vp, _vp, _vp, _vp]),

@@ -337,9 +337,10 @@ int pint_scalar_sweep_dev(pint_ctx* ctx, int mode, int64_t N, int64_t M, const d
 int64_t pint_heat_records_size(int64_t n, int64_t N, int64_t S) { return heat_records_doubles(n, N, S); }
 
 int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
-                         const double* r, const double* fa, const double* fb, double* records) {
+                         const double* slice_dt, const double* r, const double* fa,
+                         const double* fb, const double* sx, double* records) {
     if (!ctx) return PINT_E_INVALID;
-    return launch_heat_factor(ctx, n, N, S, step_off, r, fa, fb, records);
+    return launch_heat_factor(ctx, n, N, S, step_off, slice_dt, r, fa, fb, sx, records);
 }
 
 int pint_heat_build_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
@@ -614,7 +615,7 @@ int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, Hea
     H.sx = reinterpret_cast<double*>(d + b_off + b_dt + 3 * b_q);
     H.factor = f;
     H.h2d = in_bytes;
-    return launch_heat_factor(ctx, n, N, S, H.step_off, H.r, H.fa, H.fb, H.factor);
+    return launch_heat_factor(ctx, n, N, S, H.step_off, H.slice_dt, H.r, H.fa, H.fb, H.sx, H.factor);
 }
 
 int singular_check(pint_ctx* ctx) {

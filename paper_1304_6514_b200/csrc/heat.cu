@@ -41,7 +41,7 @@ __host__ __device__ constexpr long long even(long long x) { return (x + 1) & ~1l
 
 // doubles needed for the records of N slices x S steps x n rows
 __host__ __device__ constexpr long long records_doubles(long long n, long long N, long long S) {
-    return even(3 * S * N) + 3 * S * n * N;
+    return even(3 * S * N) + 4 * S * n * N;
 }
 
 struct RecView {
@@ -50,6 +50,7 @@ struct RecView {
     const double* fb;
     const double2* pr;   // [S][n][N]
     const double* cc;    // [S][n][N]
+    const double* hb;    // [S][n][N]: the forcing increment h * heat_forcing(x_i, t)
     long long N;
     int n;
     __device__ __forceinline__ long long hdr(long long s, long long j) const { return s * N + j; }
@@ -63,16 +64,20 @@ __host__ __device__ inline RecView rec_view(const double* base, int n, long long
     v.fb = base + 2 * S * N;
     v.pr = reinterpret_cast<const double2*>(base + even(3 * S * N));
     v.cc = base + even(3 * S * N) + 2 * S * n * N;
+    v.hb = base + even(3 * S * N) + 3 * S * n * N;
     v.N = N;
     v.n = n;
     return v;
 }
 
 // Thread (s, j): step s of slice j — the Thomas forward pivots of tridiag(-r, 1+2r, -r)
-// (linalg.cpp:80-90, with sub = sup = -r, diag = 1 + 2r as solve_implicit builds them).
+// (linalg.cpp:80-90, with sub = sup = -r, diag = 1 + 2r as solve_implicit builds them), and the
+// forcing increment h * b_i with b_i = fa*s_i + fb*s_i = heat_forcing(x_i, t) (pde_problems.cpp:
+// 26-29, 91-94), rounded exactly as `state[i] += dt_step * b[i]` consumes it.
 __global__ void heat_record_kernel(int n, long long N, long long S, const int64_t* __restrict__ step_off,
-                                   const double* __restrict__ r_tab, const double* __restrict__ fa,
-                                   const double* __restrict__ fb, double* __restrict__ rec, FailRec* fail) {
+                                   const double* __restrict__ slice_dt, const double* __restrict__ r_tab,
+                                   const double* __restrict__ fa, const double* __restrict__ fb,
+                                   const double* __restrict__ sx, double* __restrict__ rec, FailRec* fail) {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= S * N) return;
     const long long s = t / N, j = t - s * N;
@@ -101,6 +106,12 @@ __global__ void heat_record_kernel(int n, long long N, long long S, const int64_
         c = (i < n - 1) ? __ddiv_rn(negr, p) : 0.0;
         pr_out[V.row(s, i, j)] = make_double2(p, __drcp_rn(p));
         cc_out[V.row(s, i, j)] = c;
+    }
+    double* hb_out = const_cast<double*>(V.hb);
+    const double h = slice_dt[j], fq = fa[q], gq = fb[q];
+    for (int i = 0; i < n; ++i) {
+        const double si = sx[i];
+        hb_out[V.row(s, i, j)] = __dmul_rn(h, __dadd_rn(__dmul_rn(fq, si), __dmul_rn(gq, si)));
     }
 }
 
@@ -256,21 +267,18 @@ __global__ void __launch_bounds__(kMaxCtaThreads) heat_basis_kernel(BuildPlan P)
 // One warp per CTA: the forced (c) runs of 32 consecutive slices, lane = slice. Row i of step s is
 // one coalesced 512 B load across the warp; rows stream kD ahead through register rings and the
 // next step's first rows are fetched during the current back substitution.
-// Dynamic smem: sx[n] (even) | state[n * 32]
+// Dynamic smem: state[n * 32]
 template <bool kGuard>
 __global__ void __launch_bounds__(32) heat_forcing_kernel(BuildPlan P) {
     constexpr int kD = 16;
     extern __shared__ __align__(16) double smem[];
     const int n = P.n;
     const int lane = threadIdx.x;
-    double* sx = smem;
-    double* st = sx + even(n) + lane;
-    for (int i = lane; i < n; i += 32) sx[i] = P.sx[i];
+    double* st = smem + lane;
     const int slice = blockIdx.x * 32 + lane;
     const bool active = slice < P.N;
     const int js = active ? slice : P.N - 1;  // clamp addresses of idle lanes
     const long long steps = active ? P.step_off[slice + 1] - P.step_off[slice] : 0;
-    const double h = active ? P.slice_dt[slice] : 0.0;
     const long long max_steps = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(steps));
     const RecView V = rec_view(P.rec, n, P.N, P.S);
     for (int i = 0; i < n; ++i) st[i * 32] = 0.0;  // c = the forced run from the zero state
@@ -280,29 +288,32 @@ __global__ void __launch_bounds__(32) heat_forcing_kernel(BuildPlan P) {
     // load-into-temp + MOV, and the MOV waits for the data, which defeats the prefetch.
     const long long N = P.N;
     double2 pq[kD];
+    double hq[kD];
     double cq[kD];
-    double h_negr = 0.0, h_fa = 0.0, h_fb = 0.0;  // header of the step the ring was loaded for
+    double h_negr = 0.0;  // header of the step the rings were loaded for
     auto load_head = [&](long long s) {
-        const double2* base = V.pr + V.row(s, 0, js);
+        const long long base = V.row(s, 0, js);
 #pragma unroll
-        for (int u = 0; u < kD; ++u) pq[u] = __ldg(base + static_cast<long long>(u < n ? u : n - 1) * N);
+        for (int u = 0; u < kD; ++u) {
+            const long long off = base + static_cast<long long>(u < n ? u : n - 1) * N;
+            pq[u] = __ldg(V.pr + off);
+            hq[u] = __ldg(V.hb + off);
+        }
         h_negr = __ldg(V.negr + V.hdr(s, js));
-        h_fa = __ldg(V.fa + V.hdr(s, js));
-        h_fb = __ldg(V.fb + V.hdr(s, js));
     };
     if (steps > 0) load_head(0);
     bool bad = false;
     for (long long s = 0; s < max_steps; ++s) {
         if (s >= steps) continue;
-        const double negr = h_negr, fa = h_fa, fb = h_fb;
-        const double2* pbase = V.pr + V.row(s, 0, js);  // row i at pbase + i*N
-        const double* cbase = V.cc + V.row(s, 0, js);
+        const double negr = h_negr;
+        const long long rbase = V.row(s, 0, js);  // row i at rbase + i*N
+        const double* cbase = V.cc + rbase;
 #pragma unroll
         for (int u = 0; u < kD; ++u) cq[u] = __ldg(cbase + static_cast<long long>(n - 2 - u > 0 ? n - 2 - u : 0) * N);
-        // forward elimination with the forcing folded in (linalg.cpp:84-90, pde_problems.cpp:91-94)
+        // forward elimination, forcing increment added first (pde_problems.cpp:91-94, linalg.cpp:84-90)
         double d = 0.0;
-        auto fwd_row = [&](int i, double2 pr) {
-            const double x = forced(st[i * 32], h, fa, fb, sx[i]);
+        auto fwd_row = [&](int i, double2 pr, double hbi) {
+            const double x = __dadd_rn(st[i * 32], hbi);
             const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
             if (!kGuard) bad |= out_of_range(num);
             d = kGuard ? div_guarded(num, pr) : div_fast(num, pr);
@@ -310,18 +321,21 @@ __global__ void __launch_bounds__(32) heat_forcing_kernel(BuildPlan P) {
         };
         int i0 = 0;
         for (; i0 + kD <= n; i0 += kD) {
-            const double2* nxt = pbase + static_cast<long long>(i0 + kD) * N;
+            long long nxt = rbase + static_cast<long long>(i0 + kD) * N;
 #pragma unroll
             for (int u = 0; u < kD; ++u) {
                 const double2 pr = pq[u];
-                pq[u] = __ldg(i0 + kD + u < n ? nxt : pbase);
+                const double hbi = hq[u];
+                const long long off = (i0 + kD + u < n) ? nxt : rbase;
+                pq[u] = __ldg(V.pr + off);
+                hq[u] = __ldg(V.hb + off);
                 nxt += N;
-                fwd_row(i0 + u, pr);
+                fwd_row(i0 + u, pr, hbi);
             }
         }
 #pragma unroll
         for (int u = 0; u < kD; ++u)
-            if (i0 + u < n) fwd_row(i0 + u, pq[u]);
+            if (i0 + u < n) fwd_row(i0 + u, pq[u], hq[u]);
         if (s + 1 < steps) load_head(s + 1);  // hidden behind the back sweep
         // back substitution (linalg.cpp:91), multipliers kD rows ahead
         auto back_row = [&](int i, double c) {
@@ -374,11 +388,11 @@ __global__ void __launch_bounds__(32) heat_integrate_kernel(IntegratePlan P) {
     const RecView V = rec_view(P.rec, n, 1, P.S);
     const bool forcing = P.with_forcing != 0;
     for (long long s = P.s0; s < P.s0 + P.steps; ++s) {
-        const double negr = __ldg(V.negr + s), fa = __ldg(V.fa + s), fb = __ldg(V.fb + s);
+        const double negr = __ldg(V.negr + s);
         double d = 0.0;
         for (int i = 0; i < n; ++i) {
             double x = st[i * 32];
-            if (forcing) x = forced(x, P.h, fa, fb, sx[i]);
+            if (forcing) x = __dadd_rn(x, __ldg(V.hb + V.row(s, i, 0)));  // state += h*b (pde_problems.cpp:93)
             const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
             d = div_guarded(num, __ldg(V.pr + V.row(s, i, 0)));
             st[i * 32] = d;
@@ -406,7 +420,7 @@ int launch_build(pint_ctx* ctx, BuildPlan P) {
     P.warps_per_cta = (P.wb <= kMaxCtaThreads / 32 && staged + state_warp * P.wb <= 112 * 1024) ? P.wb : 1;
     P.ctas_per_slice = P.wb / P.warps_per_cta;
     const size_t smem_b = staged + state_warp * P.warps_per_cta;
-    const size_t smem_f = sizeof(double) * (even(P.n) + static_cast<size_t>(P.n) * 32);
+    const size_t smem_f = sizeof(double) * static_cast<size_t>(P.n) * 32;
     if (smem_b > 227 * 1024 || smem_f > 227 * 1024)
         return pint_set_error(ctx, PINT_E_INVALID, "heat_build: n too large for shared memory");
     auto kb = heat_basis_kernel<RR>;
@@ -430,13 +444,14 @@ int launch_build(pint_ctx* ctx, BuildPlan P) {
 
 int64_t heat_records_doubles(int64_t n, int64_t N, int64_t S) { return records_doubles(n, N, S); }
 
-int launch_heat_factor(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off, const double* r,
-                       const double* fa, const double* fb, double* records) {
+int launch_heat_factor(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
+                       const double* slice_dt, const double* r, const double* fa, const double* fb,
+                       const double* sx, double* records) {
     if (n < 1 || N < 0 || S < 0) return pint_set_error(ctx, PINT_E_INVALID, "heat_factor: bad sizes");
     if (N == 0 || S == 0) return PINT_OK;
     const long long threads = N * S;
     heat_record_kernel<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, ctx->stream>>>(
-        static_cast<int>(n), N, S, step_off, r, fa, fb, records, ctx->d_fail);
+        static_cast<int>(n), N, S, step_off, slice_dt, r, fa, fb, sx, records, ctx->d_fail);
     return pint_check_launch(ctx, "heat_record_kernel");
 }
 

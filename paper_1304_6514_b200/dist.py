@@ -111,7 +111,8 @@ class HeatPlan:
     def factor_and_build(self):
         c, P = self.ctx, capi.ptr
         step_off, slice_dt, r, fa, fb, sx = self.dev
-        c.call("pint_heat_factor_dev", self.n, self.N, self.S, P(step_off), P(r), P(fa), P(fb), P(self.factor))
+        c.call("pint_heat_factor_dev", self.n, self.N, self.S, P(step_off), P(slice_dt), P(r), P(fa), P(fb), P(sx),
+               P(self.factor))
         c.call("pint_heat_build_dev", self.n, self.N, self.S, P(step_off), P(slice_dt), P(self.factor), P(sx),
                P(self.maps), None, self.guarded)
 
