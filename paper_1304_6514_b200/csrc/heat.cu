@@ -319,23 +319,35 @@ __global__ void __launch_bounds__(32) heat_forcing_kernel(BuildPlan P) {
             d = kGuard ? div_guarded(num, pr) : div_fast(num, pr);
             st[i * 32] = d;
         };
+        // Each slot is consumed BEFORE it is refilled, so the refill targets the same register
+        // (no temp + MOV at the back edge); the steady-state loop needs no address clamping.
         int i0 = 0;
-        for (; i0 + kD <= n; i0 += kD) {
-            long long nxt = rbase + static_cast<long long>(i0 + kD) * N;
+        {
+            const double2* pp = V.pr + rbase + static_cast<long long>(kD) * N;  // row i0 + kD
+            const double* hp = V.hb + rbase + static_cast<long long>(kD) * N;
+            for (; i0 + 2 * kD <= n; i0 += kD) {
 #pragma unroll
-            for (int u = 0; u < kD; ++u) {
-                const double2 pr = pq[u];
-                const double hbi = hq[u];
-                const long long off = (i0 + kD + u < n) ? nxt : rbase;
-                pq[u] = __ldg(V.pr + off);
-                hq[u] = __ldg(V.hb + off);
-                nxt += N;
-                fwd_row(i0 + u, pr, hbi);
+                for (int u = 0; u < kD; ++u) {
+                    fwd_row(i0 + u, pq[u], hq[u]);
+                    pq[u] = __ldg(pp);
+                    hq[u] = __ldg(hp);
+                    pp += N;
+                    hp += N;
+                }
             }
         }
+        for (; i0 < n; i0 += kD) {  // last one or two chunks: refills clamped to valid rows
 #pragma unroll
-        for (int u = 0; u < kD; ++u)
-            if (i0 + u < n) fwd_row(i0 + u, pq[u], hq[u]);
+            for (int u = 0; u < kD; ++u) {
+                const int i = i0 + u;
+                if (i < n) {
+                    fwd_row(i, pq[u], hq[u]);
+                    const long long off = rbase + static_cast<long long>(i + kD < n ? i + kD : i) * N;
+                    pq[u] = __ldg(V.pr + off);
+                    hq[u] = __ldg(V.hb + off);
+                }
+            }
+        }
         if (s + 1 < steps) load_head(s + 1);  // hidden behind the back sweep
         // back substitution (linalg.cpp:91), multipliers kD rows ahead
         auto back_row = [&](int i, double c) {
@@ -343,18 +355,27 @@ __global__ void __launch_bounds__(32) heat_forcing_kernel(BuildPlan P) {
             st[i * 32] = d;
         };
         int t0 = 0;
-        for (; n - 2 - t0 - (kD - 1) >= 0; t0 += kD) {
+        {
+            const double* cp = cbase + static_cast<long long>(n - 2 - kD) * N;  // row n-2-kD
+            for (; n - 2 - t0 - (2 * kD - 1) >= 0; t0 += kD) {
+#pragma unroll
+                for (int u = 0; u < kD; ++u) {
+                    back_row(n - 2 - t0 - u, cq[u]);
+                    cq[u] = __ldg(cp);
+                    cp -= N;
+                }
+            }
+        }
+        for (; n - 2 - t0 >= 0; t0 += kD) {
 #pragma unroll
             for (int u = 0; u < kD; ++u) {
                 const int i = n - 2 - t0 - u;
-                const double c = cq[u];
-                cq[u] = __ldg(cbase + static_cast<long long>(i - kD >= 0 ? i - kD : 0) * N);
-                back_row(i, c);
+                if (i >= 0) {
+                    back_row(i, cq[u]);
+                    cq[u] = __ldg(cbase + static_cast<long long>(i - kD >= 0 ? i - kD : 0) * N);
+                }
             }
         }
-#pragma unroll
-        for (int u = 0; u < kD; ++u)
-            if (n - 2 - t0 - u >= 0) back_row(n - 2 - t0 - u, cq[u]);
     }
     if (active) {
         double* gp = P.maps + static_cast<long long>(slice) * n * P.ldm + n;
