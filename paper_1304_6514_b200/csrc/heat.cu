@@ -36,6 +36,9 @@ using pint_dev::record_failure;
 
 constexpr int kRegRows = 64;  // rows of each basis column held in registers (n >= kRegRows + 2)
 constexpr int kMaxCtaThreads = 32 * 8;
+#ifndef PINT_FORCING_RING
+#define PINT_FORCING_RING 16  // rows the forcing warps keep in flight from L2 (register ring)
+#endif
 
 __host__ __device__ constexpr long long even(long long x) { return (x + 1) & ~1ll; }
 
@@ -139,6 +142,8 @@ __device__ __forceinline__ double forced(double x, double h, double fa, double f
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
+
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
 
 struct BuildPlan {
     int n;
@@ -270,7 +275,7 @@ __global__ void __launch_bounds__(kMaxCtaThreads) heat_basis_kernel(BuildPlan P)
 // Dynamic smem: state[n * 32]
 template <bool kGuard>
 __global__ void __launch_bounds__(32) heat_forcing_kernel(BuildPlan P) {
-    constexpr int kD = 16;
+    constexpr int kD = PINT_FORCING_RING;
     extern __shared__ __align__(16) double smem[];
     const int n = P.n;
     const int lane = threadIdx.x;
@@ -321,20 +326,26 @@ __global__ void __launch_bounds__(32) heat_forcing_kernel(BuildPlan P) {
         };
         // Each slot is consumed BEFORE it is refilled, so the refill targets the same register
         // (no temp + MOV at the back edge); the steady-state loop needs no address clamping.
+        // The records were written long before (HBM-resident): while sweeping forward, pull this
+        // step's multipliers into L2 for the back sweep (so the ring's loads hit L2).
         int i0 = 0;
         {
             const double2* pp = V.pr + rbase + static_cast<long long>(kD) * N;  // row i0 + kD
             const double* hp = V.hb + rbase + static_cast<long long>(kD) * N;
+            const double* cpf = cbase + static_cast<long long>(n - 1) * N;
             for (; i0 + 2 * kD <= n; i0 += kD) {
 #pragma unroll
                 for (int u = 0; u < kD; ++u) {
                     fwd_row(i0 + u, pq[u], hq[u]);
                     pq[u] = __ldg(pp);
                     hq[u] = __ldg(hp);
+                    prefetch_l2(cpf);
                     pp += N;
                     hp += N;
+                    cpf -= N;
                 }
             }
+            for (int i = i0; i < n; ++i, cpf -= N) prefetch_l2(cpf);
         }
         for (; i0 < n; i0 += kD) {  // last one or two chunks: refills clamped to valid rows
 #pragma unroll
@@ -356,13 +367,21 @@ __global__ void __launch_bounds__(32) heat_forcing_kernel(BuildPlan P) {
         };
         int t0 = 0;
         {
+            // meanwhile pull the next step's pivots/increments (rows kD..) into L2
+            const long long nb = V.row(s + 1 < steps ? s + 1 : s, kD < n ? kD : n - 1, js);
+            const double2* npp = V.pr + nb;
+            const double* nhp = V.hb + nb;
             const double* cp = cbase + static_cast<long long>(n - 2 - kD) * N;  // row n-2-kD
             for (; n - 2 - t0 - (2 * kD - 1) >= 0; t0 += kD) {
 #pragma unroll
                 for (int u = 0; u < kD; ++u) {
                     back_row(n - 2 - t0 - u, cq[u]);
                     cq[u] = __ldg(cp);
+                    prefetch_l2(npp);
+                    prefetch_l2(nhp);
                     cp -= N;
+                    npp += N;
+                    nhp += N;
                 }
             }
         }
