@@ -1,7 +1,7 @@
 /* pint_cuda.h — C ABI of the B200-native Nievergelt slice-map path (libpint_cuda.so).
  *
  * Plain pointers and sizes only; no C++ or torch types cross this boundary. The C++ drop-in
- * library (paper_1304_6514_b200/include/pint/*.hpp, libpint_b200.so) and the Python host
+ * library (paper_1304_6514_b200/include/pint/ headers, libpint_b200.so) and the Python host
  * (paper_1304_6514_b200/capi.py, ctypes) are both thin callers of these entry points.
  * Each entry point names the reference interface it replaces (file:line under
  * /root/reference/proj). Ctypes / C++ bindings a maintainer adds are shown in INTEGRATION.md.
@@ -220,6 +220,9 @@ int pint_scalar_sweep(pint_ctx* ctx, int mode, int64_t N, int64_t M, const doubl
                       int64_t node_stride, const double* weights, const double* values,
                       const double* a, const double* b, int64_t ab_stride, double y0,
                       double* lambdas, double* y_out, long long* extrapolations);
+
+/* Host-buffer barycentric weights (interp.cpp:43-55 / closed form); DuplicateNodes -> code 5. */
+int pint_bary_weights(pint_ctx* ctx, int kind, int64_t M, const double* nodes, double* w);
 
 /* ---- roofline probe: measured FMA throughput (TFLOP/s) of this GPU for PINT_F64 / PINT_F32 */
 int pint_probe_peak(pint_ctx* ctx, int precision, double* tflops);

@@ -826,4 +826,21 @@ int pint_scalar_sweep(pint_ctx* ctx, int mode, int64_t N, int64_t M, const doubl
     return PINT_OK;
 }
 
+int pint_bary_weights(pint_ctx* ctx, int kind, int64_t M, const double* nodes, double* w) {
+    if (!ctx || M < 1 || !nodes || !w) return PINT_E_INVALID;
+    char* d = static_cast<char*>(pint_scratch(ctx, 2, 2 * align256(sizeof(double) * M)));
+    if (!d) return PINT_E_CUDA;
+    Carve cv{d};
+    double* d_x = cv.take<double>(M);
+    double* d_w = cv.take<double>(M);
+    cudaMemcpyAsync(d_x, nodes, sizeof(double) * M, cudaMemcpyHostToDevice, ctx->stream);
+    if (const int rc = launch_bary_weights(ctx, kind, M, d_x, d_w)) return rc;
+    cudaMemcpyAsync(w, d_w, sizeof(double) * M, cudaMemcpyDeviceToHost, ctx->stream);
+    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "bary_weights sync")) return PINT_E_CUDA;
+    pint_fail fr;
+    if (const int rc = pint_fail_read(ctx, &fr)) return rc;
+    if (fr.index >= 0) return pint_set_error(ctx, PINT_E_DUPLICATE_NODES, "barycentric_weights: repeated node");
+    return PINT_OK;
+}
+
 }  // extern "C"
