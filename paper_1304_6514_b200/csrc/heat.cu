@@ -19,13 +19,14 @@
 //    unguarded. Forced columns are range-checked OFF the dependent chain (a sticky flag); if it
 //    ever trips, the kernel reports PINT_E_RANGE_RETRY and the host re-runs the build with the
 //    guarded variant (exponent check on the chain, IEEE __ddiv_rn outside [2^-960, 2^997]).
-//  * Basis kernel: a CTA holds the ceil(n/32) warps of one slice (or one warp when n is large),
-//    lane = trajectory e_k. The step's record is staged once per CTA into shared memory one step
-//    ahead and read as broadcasts; the first kRegRows rows of every column live in registers, the
-//    rest lane-interleaved in shared memory (conflict-free). Rows leave as coalesced 256 B stores
-//    into the row-major augmented map [G | c].
-//  * Forcing kernel (side stream, concurrent): one warp holds the c runs of 32 consecutive
-//    slices (lane = slice) and streams its rows kD = 32 ahead through register rings.
+//  * A CTA holds the ceil((n+1)/32) warps of one slice (or one warp when n is large), lane =
+//    trajectory: k < n runs from e_k, k == n is the forced run from 0 (c). The step's record is
+//    staged once per CTA into shared memory one step ahead (cp.async) and read as broadcasts;
+//    the first kRegRows rows of every column live in registers, the rest lane-interleaved in
+//    shared memory (conflict-free). The forcing increment h*b_i is precomputed in the record, so
+//    the forced lane costs one exact fma(f, hb_i, x) per row (f = 1 there, 0 on basis lanes) and
+//    the slice's warps stay balanced. Rows leave as coalesced 256 B stores into the row-major
+//    augmented map [G | c].
 //
 // Roofline: FP64 pipe. Algorithmic flops per slice-step: (n+1)(5n-4) + 5n (bench.py).
 #include "pint_internal.cuh"
@@ -149,61 +150,72 @@ struct BuildPlan {
     int n;
     int N;
     long long S;        // max steps per slice (record layout)
-    int wb;             // basis warps per slice = ceil(n/32)
-    int warps_per_cta;  // wb (one CTA per slice) or 1
+    int wps;            // warps per slice = ceil((n+1)/32): n basis columns + the forced column
+    int warps_per_cta;  // wps (one CTA per slice) or 1
     int ctas_per_slice;
     const double* rec;
-    const double* sx;
     const int64_t* step_off;
-    const double* slice_dt;
     double* maps;
     long long ldm;
     unsigned long long* per_slice_ns;
     FailRec* fail;
 };
 
-// ---- basis kernel -------------------------------------------------------------------------------
-// Staged record in shared memory: [negr, pad] | (p_i, rcp_i) x n | c_i x n
-__host__ __device__ constexpr long long staged_doubles(long long n) { return 2 + 3 * n + (n & 1); }
+// Staged record in shared memory: [negr, pad] | (p_i, rcp_i) x n | c_i x n | h b_i x n
+__host__ __device__ constexpr long long staged_doubles(long long n) { return 2 + 4 * n; }
 
-__device__ __forceinline__ void stage_step(double* dst, const RecView& V, long long s, long long j) {
+__device__ __forceinline__ void stage_step(double* dst, const RecView& V, long long s, long long j, bool with_hb) {
     const int n = V.n;
     double2* pr = reinterpret_cast<double2*>(dst + 2);
     double* cc = dst + 2 + 2 * n;
-    for (int c = threadIdx.x; c < 2 * n + 1; c += blockDim.x) {
+    double* hb = dst + 2 + 3 * n;
+    const int chunks = (with_hb ? 3 * n : 2 * n) + 1;
+    for (int c = threadIdx.x; c < chunks; c += blockDim.x) {
         if (c < n) {
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(pr + c)), "l"(V.pr + V.row(s, c, j)));
         } else if (c < 2 * n) {
             const int i = c - n;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(cc + i)), "l"(V.cc + V.row(s, i, j)));
-        } else {
+        } else if (c == chunks - 1) {
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(V.negr + V.hdr(s, j)));
+        } else {
+            const int i = c - 2 * n;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(hb + i)), "l"(V.hb + V.row(s, i, j)));
         }
     }
     asm volatile("cp.async.commit_group;\n" ::);
 }
 
-// One backward-Euler step of one basis column: forward elimination (linalg.cpp:84-90) and back
-// substitution (linalg.cpp:91). Rows [0, RR) in reg[], the rest at st[32*(i-RR)].
-template <int RR>
-__device__ __forceinline__ void basis_step(double (&reg)[RR > 0 ? RR : 1], double* st, const double* R, int n) {
+// One backward-Euler step of one column: forcing increment (mixed warp only), forward
+// elimination (linalg.cpp:84-90), back substitution (linalg.cpp:91). Rows [0, RR) in reg[], the
+// rest at st[32*(i-RR)]. f is 1 on the forced lane and 0 elsewhere: fma(f, hb, x) is exactly
+// x + h*b (pde_problems.cpp:93) there and exactly x on every basis lane.
+template <int RR, bool kMixed, bool kGuard>
+__device__ __forceinline__ void column_step(double (&reg)[RR > 0 ? RR : 1], double* st, const double* R, int n,
+                                            double f, bool forced_lane, bool& bad) {
     const double negr = R[0];
     const double2* PR = reinterpret_cast<const double2*>(R + 2);
     const double* CC = R + 2 + 2 * n;
+    const double* HB = R + 2 + 3 * n;
+    auto divide = [&](double num, double2 pr) {
+        if (kMixed && !kGuard) bad |= forced_lane && out_of_range(num);
+        return (kMixed && kGuard) ? div_guarded(num, pr) : div_fast(num, pr);
+    };
     double d = 0.0;
 #pragma unroll
     for (int i = 0; i < RR; ++i) {
-        const double num = (i == 0) ? reg[i] : __dsub_rn(reg[i], __dmul_rn(negr, d));
-        d = div_fast(num, PR[i]);
+        const double x = kMixed ? __fma_rn(f, HB[i], reg[i]) : reg[i];
+        d = divide((i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d)), PR[i]);
         reg[i] = d;
     }
     {
         double* s = st;
         const double2* pr = PR + RR;
+        const double* hb = HB + RR;
 #pragma unroll 8
-        for (int i = RR; i < n; ++i, s += 32, ++pr) {
-            const double num = (RR == 0 && i == 0) ? *s : __dsub_rn(*s, __dmul_rn(negr, d));
-            d = div_fast(num, *pr);
+        for (int i = RR; i < n; ++i, s += 32, ++pr, ++hb) {
+            const double x = kMixed ? __fma_rn(f, *hb, *s) : *s;
+            d = divide((RR == 0 && i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d)), *pr);
             *s = d;
         }
     }
@@ -223,184 +235,57 @@ __device__ __forceinline__ void basis_step(double (&reg)[RR > 0 ? RR : 1], doubl
     }
 }
 
-// CTA = warps [c*warps_per_cta, ...) of one slice, lane = basis column e_k.
-// Dynamic smem: staged[2][SD] | state[warps_per_cta][(n - RR) * 32]
-template <int RR>
-__global__ void __launch_bounds__(kMaxCtaThreads) heat_basis_kernel(BuildPlan P) {
+// CTA = warps [c*warps_per_cta, ...) of one slice; lane = trajectory k (k < n: basis e_k, k == n:
+// the forced run from 0, k > n: idle). Dynamic smem: staged[2][SD] | state[warps_per_cta][(n-RR)*32]
+template <int RR, bool kGuard>
+__global__ void __launch_bounds__(kMaxCtaThreads) heat_build_kernel(BuildPlan P) {
     extern __shared__ __align__(16) double smem[];
     const unsigned long long t_start = pint_dev::globaltimer();
     const int n = P.n;
     const int lane = threadIdx.x & 31, wcta = threadIdx.x >> 5;
     const int slice = blockIdx.x / P.ctas_per_slice;
-    const int g = (blockIdx.x - slice * P.ctas_per_slice) * P.warps_per_cta + wcta;  // warp in slice
+    const int cta = blockIdx.x - slice * P.ctas_per_slice;
+    const int g = cta * P.warps_per_cta + wcta;  // warp in slice
     const long long SD = staged_doubles(n);
     double* buf = smem;
     double* st = smem + 2 * SD + static_cast<long long>(wcta) * (n - RR) * 32 + lane;
     const int k = g * 32 + lane;
+    const bool forced_lane = (k == n);
+    const bool mixed = (g == n / 32);                         // the warp holding column n
+    const bool cta_has_forcing = (n / 32) / P.warps_per_cta == cta;  // stage h*b only if needed
+    const double f = forced_lane ? 1.0 : 0.0;
     const long long steps = P.step_off[slice + 1] - P.step_off[slice];
     const RecView V = rec_view(P.rec, n, P.N, P.S);
 
-    if (steps > 0) stage_step(buf, V, 0, slice);
+    if (steps > 0) stage_step(buf, V, 0, slice, cta_has_forcing);
     double reg[RR > 0 ? RR : 1];
 #pragma unroll
-    for (int i = 0; i < RR; ++i) reg[i] = (i == k) ? 1.0 : 0.0;  // e_k
+    for (int i = 0; i < RR; ++i) reg[i] = (i == k) ? 1.0 : 0.0;  // e_k (all zero for k >= n)
     for (int i = RR; i < n; ++i) st[(i - RR) * 32] = (i == k) ? 1.0 : 0.0;
 
+    bool bad = false;
     int cur = 0;
     for (long long s = 0; s < steps; ++s) {
         if (s + 1 < steps) {
-            stage_step(buf + (cur ^ 1) * SD, V, s + 1, slice);
+            stage_step(buf + (cur ^ 1) * SD, V, s + 1, slice, cta_has_forcing);
             asm volatile("cp.async.wait_group 1;\n" ::);
         } else {
             asm volatile("cp.async.wait_group 0;\n" ::);
         }
         __syncthreads();  // step s's record visible to every warp
-        basis_step<RR>(reg, st, buf + cur * SD, n);
+        if (mixed) column_step<RR, true, kGuard>(reg, st, buf + cur * SD, n, f, forced_lane, bad);
+        else column_step<RR, false, kGuard>(reg, st, buf + cur * SD, n, f, forced_lane, bad);
         __syncthreads();  // buffer `cur` is refilled next iteration
         cur ^= 1;
     }
-    if (k < n) {
+    if (k <= n) {
         double* gp = P.maps + static_cast<long long>(slice) * n * P.ldm + k;
 #pragma unroll
         for (int i = 0; i < RR; ++i) gp[i * P.ldm] = reg[i];
         for (int i = RR; i < n; ++i) gp[i * P.ldm] = st[(i - RR) * 32];
     }
-    if (P.per_slice_ns && threadIdx.x == 0) atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
-}
-
-// ---- forcing kernel -----------------------------------------------------------------------------
-// One warp per CTA: the forced (c) runs of 32 consecutive slices, lane = slice. Row i of step s is
-// one coalesced 512 B load across the warp; rows stream kD ahead through register rings and the
-// next step's first rows are fetched during the current back substitution.
-// Dynamic smem: state[n * 32]
-template <bool kGuard>
-__global__ void __launch_bounds__(32) heat_forcing_kernel(BuildPlan P) {
-    constexpr int kD = PINT_FORCING_RING;
-    extern __shared__ __align__(16) double smem[];
-    const int n = P.n;
-    const int lane = threadIdx.x;
-    double* st = smem + lane;
-    const int slice = blockIdx.x * 32 + lane;
-    const bool active = slice < P.N;
-    const int js = active ? slice : P.N - 1;  // clamp addresses of idle lanes
-    const long long steps = active ? P.step_off[slice + 1] - P.step_off[slice] : 0;
-    const long long max_steps = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(steps));
-    const RecView V = rec_view(P.rec, n, P.N, P.S);
-    for (int i = 0; i < n; ++i) st[i * 32] = 0.0;  // c = the forced run from the zero state
-    __syncwarp();
-
-    // Rings are refilled by UNCONDITIONAL loads from clamped rows: a predicated refill compiles to
-    // load-into-temp + MOV, and the MOV waits for the data, which defeats the prefetch.
-    const long long N = P.N;
-    double2 pq[kD];
-    double hq[kD];
-    double cq[kD];
-    double h_negr = 0.0;  // header of the step the rings were loaded for
-    auto load_head = [&](long long s) {
-        const long long base = V.row(s, 0, js);
-#pragma unroll
-        for (int u = 0; u < kD; ++u) {
-            const long long off = base + static_cast<long long>(u < n ? u : n - 1) * N;
-            pq[u] = __ldg(V.pr + off);
-            hq[u] = __ldg(V.hb + off);
-        }
-        h_negr = __ldg(V.negr + V.hdr(s, js));
-    };
-    if (steps > 0) load_head(0);
-    bool bad = false;
-    for (long long s = 0; s < max_steps; ++s) {
-        if (s >= steps) continue;
-        const double negr = h_negr;
-        const long long rbase = V.row(s, 0, js);  // row i at rbase + i*N
-        const double* cbase = V.cc + rbase;
-#pragma unroll
-        for (int u = 0; u < kD; ++u) cq[u] = __ldg(cbase + static_cast<long long>(n - 2 - u > 0 ? n - 2 - u : 0) * N);
-        // forward elimination, forcing increment added first (pde_problems.cpp:91-94, linalg.cpp:84-90)
-        double d = 0.0;
-        auto fwd_row = [&](int i, double2 pr, double hbi) {
-            const double x = __dadd_rn(st[i * 32], hbi);
-            const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
-            if (!kGuard) bad |= out_of_range(num);
-            d = kGuard ? div_guarded(num, pr) : div_fast(num, pr);
-            st[i * 32] = d;
-        };
-        // Each slot is consumed BEFORE it is refilled, so the refill targets the same register
-        // (no temp + MOV at the back edge); the steady-state loop needs no address clamping.
-        // The records were written long before (HBM-resident): while sweeping forward, pull this
-        // step's multipliers into L2 for the back sweep (so the ring's loads hit L2).
-        int i0 = 0;
-        {
-            const double2* pp = V.pr + rbase + static_cast<long long>(kD) * N;  // row i0 + kD
-            const double* hp = V.hb + rbase + static_cast<long long>(kD) * N;
-            const double* cpf = cbase + static_cast<long long>(n - 1) * N;
-            for (; i0 + 2 * kD <= n; i0 += kD) {
-#pragma unroll
-                for (int u = 0; u < kD; ++u) {
-                    fwd_row(i0 + u, pq[u], hq[u]);
-                    pq[u] = __ldg(pp);
-                    hq[u] = __ldg(hp);
-                    prefetch_l2(cpf);
-                    pp += N;
-                    hp += N;
-                    cpf -= N;
-                }
-            }
-            for (int i = i0; i < n; ++i, cpf -= N) prefetch_l2(cpf);
-        }
-        for (; i0 < n; i0 += kD) {  // last one or two chunks: refills clamped to valid rows
-#pragma unroll
-            for (int u = 0; u < kD; ++u) {
-                const int i = i0 + u;
-                if (i < n) {
-                    fwd_row(i, pq[u], hq[u]);
-                    const long long off = rbase + static_cast<long long>(i + kD < n ? i + kD : i) * N;
-                    pq[u] = __ldg(V.pr + off);
-                    hq[u] = __ldg(V.hb + off);
-                }
-            }
-        }
-        if (s + 1 < steps) load_head(s + 1);  // hidden behind the back sweep
-        // back substitution (linalg.cpp:91), multipliers kD rows ahead
-        auto back_row = [&](int i, double c) {
-            d = __dsub_rn(st[i * 32], __dmul_rn(c, d));
-            st[i * 32] = d;
-        };
-        int t0 = 0;
-        {
-            // meanwhile pull the next step's pivots/increments (rows kD..) into L2
-            const long long nb = V.row(s + 1 < steps ? s + 1 : s, kD < n ? kD : n - 1, js);
-            const double2* npp = V.pr + nb;
-            const double* nhp = V.hb + nb;
-            const double* cp = cbase + static_cast<long long>(n - 2 - kD) * N;  // row n-2-kD
-            for (; n - 2 - t0 - (2 * kD - 1) >= 0; t0 += kD) {
-#pragma unroll
-                for (int u = 0; u < kD; ++u) {
-                    back_row(n - 2 - t0 - u, cq[u]);
-                    cq[u] = __ldg(cp);
-                    prefetch_l2(npp);
-                    prefetch_l2(nhp);
-                    cp -= N;
-                    npp += N;
-                    nhp += N;
-                }
-            }
-        }
-        for (; n - 2 - t0 >= 0; t0 += kD) {
-#pragma unroll
-            for (int u = 0; u < kD; ++u) {
-                const int i = n - 2 - t0 - u;
-                if (i >= 0) {
-                    back_row(i, cq[u]);
-                    cq[u] = __ldg(cbase + static_cast<long long>(i - kD >= 0 ? i - kD : 0) * N);
-                }
-            }
-        }
-    }
-    if (active) {
-        double* gp = P.maps + static_cast<long long>(slice) * n * P.ldm + n;
-        for (int i = 0; i < n; ++i) gp[i * P.ldm] = st[i * 32];
-    }
     if (bad) record_failure(P.fail, slice, PINT_E_RANGE_RETRY, static_cast<double>(n));
+    if (P.per_slice_ns && threadIdx.x == 0) atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
 }
 
 // ---- integrate: K caller columns of one slice (records with N = 1), guarded division ----------
@@ -454,30 +339,18 @@ void smem_attrs(K kern, size_t smem) {
 
 template <int RR, bool kGuard>
 int launch_build(pint_ctx* ctx, BuildPlan P) {
-    // basis: one CTA per slice when two such CTAs fit an SM, else one CTA per warp
+    // one CTA per slice when two such CTAs fit an SM, else one CTA per warp
     const size_t state_warp = sizeof(double) * static_cast<size_t>(P.n - RR) * 32;
     const size_t staged = sizeof(double) * 2 * staged_doubles(P.n);
-    P.warps_per_cta = (P.wb <= kMaxCtaThreads / 32 && staged + state_warp * P.wb <= 112 * 1024) ? P.wb : 1;
-    P.ctas_per_slice = P.wb / P.warps_per_cta;
-    const size_t smem_b = staged + state_warp * P.warps_per_cta;
-    const size_t smem_f = sizeof(double) * static_cast<size_t>(P.n) * 32;
-    if (smem_b > 227 * 1024 || smem_f > 227 * 1024)
-        return pint_set_error(ctx, PINT_E_INVALID, "heat_build: n too large for shared memory");
-    auto kb = heat_basis_kernel<RR>;
-    auto kf = heat_forcing_kernel<kGuard>;
-    smem_attrs(kb, smem_b);
-    smem_attrs(kf, smem_f);
-    // fork: forcing runs on the side stream, overlapping the basis kernel; join before returning
-    cudaEventRecord(ctx->ev_fork, ctx->stream);
-    cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
-    kf<<<static_cast<unsigned>((P.N + 31) / 32), 32, smem_f, ctx->side>>>(P);
-    if (const int rc = pint_check_launch(ctx, "heat_forcing_kernel")) return rc;
-    kb<<<static_cast<unsigned>(static_cast<long long>(P.N) * P.ctas_per_slice), 32 * P.warps_per_cta, smem_b,
-         ctx->stream>>>(P);
-    if (const int rc = pint_check_launch(ctx, "heat_basis_kernel")) return rc;
-    cudaEventRecord(ctx->ev_join, ctx->side);
-    cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);
-    return PINT_OK;
+    P.warps_per_cta = (P.wps <= kMaxCtaThreads / 32 && staged + state_warp * P.wps <= 112 * 1024) ? P.wps : 1;
+    P.ctas_per_slice = P.wps / P.warps_per_cta;
+    const size_t smem = staged + state_warp * P.warps_per_cta;
+    if (smem > 227 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: n too large for shared memory");
+    auto kern = heat_build_kernel<RR, kGuard>;
+    smem_attrs(kern, smem);
+    kern<<<static_cast<unsigned>(static_cast<long long>(P.N) * P.ctas_per_slice), 32 * P.warps_per_cta, smem,
+           ctx->stream>>>(P);
+    return pint_check_launch(ctx, "heat_build_kernel");
 }
 
 }  // namespace
@@ -501,15 +374,15 @@ int launch_heat_build(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int6
     if (n < 1 || N < 0) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: bad sizes");
     if (N == 0) return PINT_OK;
     if (n > (1 << 20) || N > (1 << 26)) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: sizes out of range");
+    (void)slice_dt;  // the per-slice step lives in the records (h*b) and step_off
+    (void)sx;
     BuildPlan P{};
     P.n = static_cast<int>(n);
     P.N = static_cast<int>(N);
     P.S = S;
-    P.wb = static_cast<int>((n + 31) / 32);
+    P.wps = static_cast<int>((n + 1 + 31) / 32);
     P.rec = records;
-    P.sx = sx;
     P.step_off = step_off;
-    P.slice_dt = slice_dt;
     P.maps = maps;
     P.ldm = pint_affine_ldm(n);
     P.per_slice_ns = per_slice_ns;
