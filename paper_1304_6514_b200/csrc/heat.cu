@@ -10,8 +10,8 @@
 //    heat_record_kernel computes it once per (slice, step) with exactly thomas_solve's operations
 //    (every solve stays bit-identical). Records are stored slice-minor:
 //        hdr[3][S][N] = {-r, fa, fb},  pr[S][n][N] = (p_i, RN(1/p_i)),  cc[S][n][N] = c_i
-//    so the record kernel (thread = (step, slice)) and the forcing warps (lane = slice) are
-//    coalesced, and a basis CTA gathers its slice's column with 16-/8-byte cp.async chunks.
+//    (plus the forcing increments h*b_i[S][n][N]) so the record kernel (thread = (step, slice))
+//    writes coalesced, and a slice CTA gathers its column with 16-/8-byte cp.async chunks.
 //  * x / p_i is q0 = x*rcp, rem = fma(-p, q0, x), q = fma(rem, rcp, q0) with rcp = RN(1/p_i):
 //    Markstein's theorem makes q the correctly rounded quotient whenever no intermediate
 //    under/overflows. Basis columns are entrywise non-negative and bounded (each step matrix is an
@@ -29,6 +29,8 @@
 //    augmented map [G | c].
 //
 // Roofline: FP64 pipe. Algorithmic flops per slice-step: (n+1)(5n-4) + 5n (bench.py).
+#include <cstdlib>
+
 #include "pint_internal.cuh"
 
 namespace {
@@ -37,9 +39,6 @@ using pint_dev::record_failure;
 
 constexpr int kRegRows = 64;  // rows of each basis column held in registers (n >= kRegRows + 2)
 constexpr int kMaxCtaThreads = 32 * 8;
-#ifndef PINT_FORCING_RING
-#define PINT_FORCING_RING 16  // rows the forcing warps keep in flight from L2 (register ring)
-#endif
 
 __host__ __device__ constexpr long long even(long long x) { return (x + 1) & ~1ll; }
 
@@ -126,25 +125,20 @@ __device__ __forceinline__ double div_fast(double x, double2 pr) {
 }
 
 __device__ __forceinline__ bool out_of_range(double x) {
-    const unsigned e = (static_cast<unsigned>(__double2hiint(x)) >> 20) & 0x7ffu;
-    return e - 63u > 1957u;  // zero, subnormal, |x| < 2^-960, |x| >= 2^998, inf/nan
+    // |x| bits of the high word, window test on the biased exponent: true for zero, subnormal,
+    // |x| < 2^-960, |x| >= 2^998, inf and nan (LOP3 + IADD + ISETP)
+    const unsigned a = static_cast<unsigned>(__double2hiint(x)) & 0x7fffffffu;
+    return a - (63u << 20) > ((2021u - 63u) << 20) - 1u;
 }
 
 __device__ __forceinline__ double div_guarded(double x, double2 pr) {
     return out_of_range(x) ? __ddiv_rn(x, pr.x) : div_fast(x, pr);
 }
 
-// Forcing (pde_problems.cpp:91-94) folded into the row update: x + h*(fa s + fb s), where
-// heat_forcing(x_i, t) = fa*s + fb*s with fa = -sin t, fb = ((a pi) pi) cos t (pde_problems.cpp:26-29).
-__device__ __forceinline__ double forced(double x, double h, double fa, double fb, double s) {
-    return __dadd_rn(x, __dmul_rn(h, __dadd_rn(__dmul_rn(fa, s), __dmul_rn(fb, s))));
-}
-
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
 
 struct BuildPlan {
     int n;
@@ -159,6 +153,7 @@ struct BuildPlan {
     long long ldm;
     unsigned long long* per_slice_ns;
     FailRec* fail;
+    int debug_flags;  // PINT_HEAT_DEBUG (timing experiments only): 1 = no mixed warp
 };
 
 // Staged record in shared memory: [negr, pad] | (p_i, rcp_i) x n | c_i x n | h b_i x n
@@ -251,7 +246,7 @@ __global__ void __launch_bounds__(kMaxCtaThreads) heat_build_kernel(BuildPlan P)
     double* st = smem + 2 * SD + static_cast<long long>(wcta) * (n - RR) * 32 + lane;
     const int k = g * 32 + lane;
     const bool forced_lane = (k == n);
-    const bool mixed = (g == n / 32);                         // the warp holding column n
+    const bool mixed = (g == n / 32) && !(P.debug_flags & 1);  // the warp holding column n
     const bool cta_has_forcing = (n / 32) / P.warps_per_cta == cta;  // stage h*b only if needed
     const double f = forced_lane ? 1.0 : 0.0;
     const long long steps = P.step_off[slice + 1] - P.step_off[slice];
@@ -387,6 +382,7 @@ int launch_heat_build(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int6
     P.ldm = pint_affine_ldm(n);
     P.per_slice_ns = per_slice_ns;
     P.fail = ctx->d_fail;
+    if (const char* e = std::getenv("PINT_HEAT_DEBUG")) P.debug_flags = std::atoi(e);
     if (n >= kRegRows + 2)
         return guarded ? launch_build<kRegRows, true>(ctx, P) : launch_build<kRegRows, false>(ctx, P);
     return guarded ? launch_build<0, true>(ctx, P) : launch_build<0, false>(ctx, P);
