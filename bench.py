@@ -39,7 +39,7 @@ UNIT = "traj-steps/s"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--n", type=int, default=128, help="interior points (dx = 1/(n+1))")
@@ -83,7 +83,12 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 8:
-                self.rows.append(parts)
+                self.rows.append((time.time(), parts))
+
+    def wait_first_sample(self, timeout=5.0):
+        t0 = time.time()
+        while self.proc and not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.02)
 
     def stop(self):
         if self.proc:
@@ -95,15 +100,20 @@ class ClockSampler:
         if self.thread:
             self.thread.join(timeout=2)
 
-    def summary(self):
-        if not self.rows:
+    def summary(self, t0=None, t1=None):
+        """Median SM clock and active throttle reasons over samples inside [t0, t1] (the timed
+        region, padded by one sampling period so a short region still has a reading)."""
+        rows = [r for t, r in self.rows if t0 is None or (t0 - 0.15 <= t <= t1 + 0.15)]
+        if not rows:
+            rows = [r for _, r in self.rows[-1:]]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 def ref_tool():
@@ -143,7 +153,13 @@ def reference_arm(args, rank, world):
     N = args.slices_per_gpu * args.gpus
     for _ in range(args.warmup):
         pass  # the reference has no device state to warm; each rep is a cold full run
-    res = run_reference_cpu(args.n, N, args.S, args.T, max(1, args.steps))
+    # each timed step is one full reference solve; bound the whole arm to about a minute
+    res = run_reference_cpu(args.n, N, args.S, args.T, 1)
+    if res is not None and args.steps > 1:
+        per = max(res["runs"][0]["seconds"], 1e-3)
+        more = min(args.steps - 1, int(60.0 / per))
+        if more > 0:
+            res["runs"] += run_reference_cpu(args.n, N, args.S, args.T, more)["runs"]
     if res is None:
         rp = run_port_cpu(args.n, N, args.S, args.T)
         v = rp["traj_steps"] / rp["seconds"]
@@ -233,8 +249,10 @@ def main():
 
     clocks = ClockSampler(local)
     clocks.start()
+    clocks.wait_first_sample()
     tot = {"step": 0.0, "factor": 0.0, "build": 0.0, "compose": 0.0}
     launches0 = ctx.launches()
+    t_region0 = time.time()
     for _ in range(args.steps):
         flush.zero_()  # L2 flush between timed iterations (outside the events)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -251,6 +269,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot["step"] = float(t.item())
         dist.barrier()
+    t_region1 = time.time()
     clocks.stop()
 
     ms_per_step = tot["step"] / args.steps
@@ -334,13 +353,13 @@ def main():
                        "time_to_solution_ms": ms_per_step, "e2e_time_to_solution_ms": e2e_secs / args.steps * 1e3},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
-            "roofline": {"bound": "fp64", "kernel": "heat_columns_kernel<build>", "achieved": achieved,
+            "roofline": {"bound": "fp64", "kernel": "heat_build_kernel", "achieved": achieved,
                          "peak": peak64.value, "unit": "TFLOP/s", "frac": achieved / peak64.value,
                          "traffic": traffic, "peak_source": "measured DFMA probe (pint_probe_peak)",
                          "flops_per_launch": build_flops, "launch_ms": build_ms,
                          "share_of_step": build_ms / ms_per_step,
                          "factor_ms": tot["factor"] / args.steps, "compose_ms": tot["compose"] / args.steps},
-            "clocks": clocks.summary(),
+            "clocks": clocks.summary(t_region0, t_region1),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
