@@ -221,6 +221,21 @@ int pint_scalar_sweep(pint_ctx* ctx, int mode, int64_t N, int64_t M, const doubl
                       const double* a, const double* b, int64_t ab_stride, double y0,
                       double* lambdas, double* y_out, long long* extrapolations);
 
+/* ---- wave slice maps (make_wave_linear_problem, pde_problems.cpp:142-172; leapfrog_integrate,
+ * ode_core.cpp:65-77). d = M - 1 interior points, D2 = d x d row-major (host), state [u; u_prev]
+ * of size 2d. The closure's rule is kept: every slice must step at dt_native = 8/M^2 within 1e-9
+ * (PINT_E_BAD_GRID otherwise). Bit-exact vs the reference. */
+/* G row-major N x 2d x 2d, c N x 2d (c = 0: the wave problem has no forcing). */
+int pint_wave_maps(pint_ctx* ctx, int64_t d, const double* D2, double dt_native,
+                   const pint_slice* slices, int64_t N, double dt_nominal, double* G, double* c);
+/* the integrate closure for K states y[k*2d ...] over one slice, in place */
+int pint_wave_integrate(pint_ctx* ctx, int64_t d, const double* D2, double dt_native,
+                        const pint_slice* slice, double dt_nominal, int64_t K, double* y);
+/* run_nievergelt for the wave problem: N slices of [0, T], compose chain or tree */
+int pint_run_wave(pint_ctx* ctx, int64_t d, const double* D2, double dt_native, double T, int64_t N,
+                  double dt_nominal, int compose_mode, const double* y0, double* y_out,
+                  double* per_slice_seconds, pint_report* report);
+
 /* Host-buffer barycentric weights (interp.cpp:43-55 / closed form); DuplicateNodes -> code 5. */
 int pint_bary_weights(pint_ctx* ctx, int kind, int64_t M, const double* nodes, double* w);
 

@@ -238,6 +238,24 @@ int cmd_golden(const std::string& dir) {
         d.f64("heat128_serial_final", run_serial(heat).final_state);
     }
 
+    // ---- wave affine path (pde_problems.cpp:102-172, leapfrog ode_core.cpp:65-77)
+    {
+        const WaveProblem w = make_wave_problem(16);
+        const auto wave = make_wave_linear_problem(w, 16.0);
+        d.f64("wave16_D2", flatten(w.D2_interior), {15, 15});
+        d.scalar("wave16_dt", w.dt);
+        d.f64("wave16_y0", wave.y0);
+        const auto dec = decompose(0.0, 16.0, 4, wave.dt);
+        const AffinePropagator p1 = build_affine_propagator(wave, dec.slices[1]);
+        d.f64("wave16_slice1_G", flatten(p1.G), {30, 30});
+        d.f64("wave16_slice1_c", p1.c);
+        d.f64("wave16_N4_final", run_nievergelt(wave, 4, ExecConfig{}).final_state);
+        d.f64("wave16_serial_final", run_serial(wave).final_state);
+        const WaveProblem w40 = make_wave_problem(40);
+        d.f64("wave40_D2", flatten(w40.D2_interior), {39, 39});
+        d.f64("wave40_N8_final", run_nievergelt(make_wave_linear_problem(w40, 16.0), 8, ExecConfig{}).final_state);
+    }
+
     // ---- linalg KATs (linalg.cpp:17-93)
     {
         const std::size_t n = 12;

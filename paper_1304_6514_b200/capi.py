@@ -98,6 +98,9 @@ _SIGS = {
     "pint_scalar_integrate": (_int, [_vp, C.POINTER(ScalarRHS), C.POINTER(Slice), _i, _vp, _vp, C.POINTER(Fail)]),
     "pint_affine_compose": (_int, [_vp, _int, _i, _i, _vp, _vp, _vp, _vp]),
     "pint_scalar_sweep": (_int, [_vp, _int, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _i, _d, _vp, _vp, _vp]),
+    "pint_wave_maps": (_int, [_vp, _i, _vp, _d, C.POINTER(Slice), _i, _d, _vp, _vp]),
+    "pint_wave_integrate": (_int, [_vp, _i, _vp, _d, C.POINTER(Slice), _d, _i, _vp]),
+    "pint_run_wave": (_int, [_vp, _i, _vp, _d, _d, _i, _d, _int, _vp, _vp, _vp, C.POINTER(Report)]),
     "pint_bary_weights": (_int, [_vp, _int, _i, _vp, _vp]),
     "pint_probe_peak": (_int, [_vp, _int, C.POINTER(_d)]),
     "pint_probe_latency": (_int, [_vp, _vp]),

@@ -826,6 +826,138 @@ int pint_scalar_sweep(pint_ctx* ctx, int mode, int64_t N, int64_t M, const doubl
     return PINT_OK;
 }
 
+// ---- wave problem (make_wave_linear_problem, pde_problems.cpp:142-172) --------------------------
+
+namespace {
+// Upload D2 and the per-slice leapfrog tables; enforces the closure's native-step rule
+// (pde_problems.cpp:155-157) and integrate_slice's integrality check.
+int wave_upload(pint_ctx* ctx, int64_t d, const double* D2, double dt_native, const std::vector<pint_slice>& sl,
+                int slot, double** d_D2, int64_t** d_steps, double** d_h) {
+    for (const auto& s : sl) {
+        if (std::fabs(s.dt - dt_native) > 1e-9 * dt_native)
+            return pint_set_error(ctx, PINT_E_BAD_GRID, "wave: leapfrog runs only at the native step dt = 8/M^2");
+        if (const int rc = check_integral(ctx, s.t_end - s.t_begin, s.dt)) return rc;
+    }
+    const int64_t N = static_cast<int64_t>(sl.size());
+    const size_t b_d2 = align256(sizeof(double) * d * d), b_st = align256(sizeof(int64_t) * N);
+    const size_t b_h = align256(sizeof(double) * N);
+    char* h = static_cast<char*>(pinned(b_d2 + b_st + b_h));
+    char* dev = static_cast<char*>(pint_scratch(ctx, slot, b_d2 + b_st + b_h));
+    if (!h || !dev) return pint_set_error(ctx, PINT_E_CUDA, "wave: staging allocation failed");
+    std::memcpy(h, D2, sizeof(double) * d * d);
+    for (int64_t j = 0; j < N; ++j) {
+        reinterpret_cast<int64_t*>(h + b_d2)[j] = sl[j].steps;
+        reinterpret_cast<double*>(h + b_d2 + b_st)[j] = sl[j].dt;
+    }
+    if (!ok(ctx, cudaMemcpyAsync(dev, h, b_d2 + b_st + b_h, cudaMemcpyHostToDevice, ctx->stream), "H2D wave"))
+        return PINT_E_CUDA;
+    // the pinned staging buffer is reused by the next call: make this copy complete first
+    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "H2D wave sync")) return PINT_E_CUDA;
+    *d_D2 = reinterpret_cast<double*>(dev);
+    *d_steps = reinterpret_cast<int64_t*>(dev + b_d2);
+    *d_h = reinterpret_cast<double*>(dev + b_d2 + b_st);
+    return PINT_OK;
+}
+}  // namespace
+
+int pint_wave_maps(pint_ctx* ctx, int64_t d, const double* D2, double dt_native, const pint_slice* slices,
+                   int64_t N, double dt_nominal, double* G, double* c) {
+    if (!ctx || d < 1 || !D2 || !slices || N < 1) return PINT_E_INVALID;
+    std::vector<pint_slice> sl;
+    closure_slices(slices, N, dt_nominal, sl);
+    double *d_D2, *d_h;
+    int64_t* d_steps;
+    if (const int rc = wave_upload(ctx, d, D2, dt_native, sl, 0, &d_D2, &d_steps, &d_h)) return rc;
+    const int64_t n = 2 * d, ldm = pint_affine_ldm(n);
+    double* d_maps = static_cast<double*>(pint_scratch(ctx, 2, sizeof(double) * n * ldm * N));
+    if (!d_maps) return PINT_E_CUDA;
+    if (const int rc = launch_wave_build(ctx, d, N, d_D2, d_steps, d_h, d_maps)) return rc;
+    std::vector<double> host(static_cast<size_t>(n * ldm * N));
+    cudaMemcpyAsync(host.data(), d_maps, sizeof(double) * host.size(), cudaMemcpyDeviceToHost, ctx->stream);
+    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "wave_maps sync")) return PINT_E_CUDA;
+    for (int64_t j = 0; j < N; ++j)
+        for (int64_t i = 0; i < n; ++i) {
+            const double* row = host.data() + (j * n + i) * ldm;
+            if (G) std::memcpy(G + (j * n + i) * n, row, sizeof(double) * n);
+            if (c) c[j * n + i] = row[n];
+        }
+    return PINT_OK;
+}
+
+int pint_wave_integrate(pint_ctx* ctx, int64_t d, const double* D2, double dt_native, const pint_slice* slice,
+                        double dt_nominal, int64_t K, double* y) {
+    if (!ctx || d < 1 || !D2 || !slice || K < 0) return PINT_E_INVALID;
+    std::vector<pint_slice> sl;
+    closure_slices(slice, 1, dt_nominal, sl);
+    double *d_D2, *d_h;
+    int64_t* d_steps;
+    if (const int rc = wave_upload(ctx, d, D2, dt_native, sl, 0, &d_D2, &d_steps, &d_h)) return rc;
+    if (K == 0) return PINT_OK;
+    double* d_y = static_cast<double*>(pint_scratch(ctx, 2, sizeof(double) * 2 * d * K));
+    if (!d_y) return PINT_E_CUDA;
+    cudaMemcpyAsync(d_y, y, sizeof(double) * 2 * d * K, cudaMemcpyHostToDevice, ctx->stream);
+    if (const int rc = launch_wave_integrate(ctx, d, K, d_D2, d_steps, d_h, d_y)) return rc;
+    cudaMemcpyAsync(y, d_y, sizeof(double) * 2 * d * K, cudaMemcpyDeviceToHost, ctx->stream);
+    return ok(ctx, cudaStreamSynchronize(ctx->stream), "wave_integrate sync") ? PINT_OK : PINT_E_CUDA;
+}
+
+int pint_run_wave(pint_ctx* ctx, int64_t d, const double* D2, double dt_native, double T, int64_t N,
+                  double dt_nominal, int compose_mode, const double* y0, double* y_out, double* per_slice_seconds,
+                  pint_report* report) {
+    if (!ctx || d < 1 || !D2 || !y0 || !y_out || N < 1) return PINT_E_INVALID;
+    HostTimer wall;
+    const long long launches0 = ctx->launches;
+    std::vector<pint_slice> sl(static_cast<size_t>(N));
+    if (pint_decompose(0.0, T, N, dt_nominal, sl.data()) != PINT_OK)
+        return pint_set_error(ctx, PINT_E_BAD_GRID, "decompose: need N >= 1, T > t0, dt > 0");
+    closure_slices(sl.data(), N, dt_nominal, sl);
+    cudaEventRecord(ctx->ev0, ctx->stream);
+    double *d_D2, *d_h;
+    int64_t* d_steps;
+    if (const int rc = wave_upload(ctx, d, D2, dt_native, sl, 0, &d_D2, &d_steps, &d_h)) return rc;
+    const int64_t n = 2 * d, ldm = pint_affine_ldm(n);
+    const size_t map_elems = static_cast<size_t>(n * ldm);
+    const size_t b_scr = compose_mode == PINT_COMPOSE_TREE ? align256(sizeof(double) * map_elems * ((N + 1) / 2)) : 0;
+    char* dv = static_cast<char*>(pint_scratch(ctx, 2, align256(sizeof(double) * map_elems * N) + b_scr +
+                                                        2 * align256(sizeof(double) * n) + 512));
+    if (!dv) return PINT_E_CUDA;
+    Carve cv{dv};
+    double* d_maps = cv.take<double>(map_elems * N);
+    double* d_scr = b_scr ? cv.take<double>(map_elems * ((N + 1) / 2)) : nullptr;
+    double* d_y0 = cv.take<double>(n);
+    double* d_y = cv.take<double>(n);
+    cudaMemcpyAsync(d_y0, y0, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream);
+    int rc = launch_wave_build(ctx, d, N, d_D2, d_steps, d_h, d_maps);
+    if (rc) return rc;
+    cudaEventRecord(ctx->evc, ctx->stream);
+    if (compose_mode == PINT_COMPOSE_TREE) rc = launch_affine_tree(ctx, n, N, d_maps, d_scr, d_y0, d_y, nullptr);
+    else rc = launch_affine_chain(ctx, n, N, d_maps, d_y0, d_y);
+    if (rc) return rc;
+    cudaEventRecord(ctx->ev1, ctx->stream);
+    cudaMemcpyAsync(y_out, d_y, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream);
+    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "run_wave sync")) return PINT_E_CUDA;
+    float ms = 0.f, cms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    cudaEventElapsedTime(&cms, ctx->evc, ctx->ev1);
+    if (per_slice_seconds) {  // uniform slices: the build's device time split evenly
+        for (int64_t j = 0; j < N; ++j) per_slice_seconds[j] = (ms - cms) * 1e-3 / static_cast<double>(N);
+    }
+    if (report) {
+        report->message_count = N - 1;
+        report->bytes_communicated = (N - 1) * n * static_cast<int64_t>(sizeof(double));
+        report->extrapolation_count = 0;
+        report->device_ms = ms;
+        report->traj_steps = 0;
+        for (const auto& s : sl) report->traj_steps += s.steps * (n + 1);
+        report->gpu_launches = ctx->launches - launches0;
+        report->h2d_bytes = static_cast<int64_t>(sizeof(double) * (d * d + n) + 16 * N);
+        report->d2h_bytes = static_cast<int64_t>(sizeof(double) * n);
+        report->compose_ms = cms;
+        report->total_ms = wall.ms();
+    }
+    return PINT_OK;
+}
+
 int pint_bary_weights(pint_ctx* ctx, int kind, int64_t M, const double* nodes, double* w) {
     if (!ctx || M < 1 || !nodes || !w) return PINT_E_INVALID;
     char* d = static_cast<char*>(pint_scratch(ctx, 2, 2 * align256(sizeof(double) * M)));

@@ -392,16 +392,15 @@ SliceMap build_scalar_slice_map(const ScalarIVP& ivp, const TimeSlice& slice, co
     return map;
 }
 
-static const HeatDevice& heat_of(const LinearProblem& p) {
-    if (!p.heat)
+static void require_device(const LinearProblem& p) {
+    if (!p.heat && !p.wave)
         throw std::invalid_argument("pint-b200: LinearProblem '" + p.name +
-                                    "' has no device description (only the heat problem runs on the B200 in "
-                                    "this round; wave slice maps are SURVEY.md §8f 'next')");
-    return *p.heat;
+                                    "' has no device description (make_heat_problem / "
+                                    "make_wave_linear_problem provide one)");
 }
 
 AffinePropagator build_affine_propagator(const LinearProblem& problem, const TimeSlice& slice) {
-    const HeatDevice& hd = heat_of(problem);
+    require_device(problem);
     const std::size_t n = problem.dim;
     AffinePropagator prop;
     prop.slice_index = slice.index;
@@ -411,7 +410,14 @@ AffinePropagator build_affine_propagator(const LinearProblem& problem, const Tim
     const pint_slice s = to_c(slice);
     std::lock_guard<std::mutex> lk(device().mu);
     pint_ctx* c = ctx_locked();
-    check(pint_heat_maps(c, hd.dx, problem.dt, &s, 1, G.data(), prop.c.data()), c);
+    if (problem.heat) {
+        check(pint_heat_maps(c, problem.heat->dx, problem.dt, &s, 1, G.data(), prop.c.data()), c);
+    } else {
+        const WaveDevice& w = *problem.wave;
+        check(pint_wave_maps(c, static_cast<int64_t>(w.d), w.D2.data(), w.dt_native, &s, 1, problem.dt, G.data(),
+                             prop.c.data()),
+              c);
+    }
     for (std::size_t i = 0; i < n; ++i)
         for (std::size_t j = 0; j < n; ++j) prop.G(i, j) = G[i * n + j];
     return prop;
@@ -547,7 +553,7 @@ RunReport run_nievergelt(const LinearProblem& problem, std::size_t N, const Exec
         r.workers = exec.workers;
         return r;
     }
-    const HeatDevice& hd = heat_of(problem);
+    require_device(problem);
     const Vector serial = run_serial(problem).final_state;  // outside T_total, like the reference
     RunReport r;
     r.method = "nievergelt";
@@ -562,11 +568,19 @@ RunReport run_nievergelt(const LinearProblem& problem, std::size_t N, const Exec
     {
         std::lock_guard<std::mutex> lk(device().mu);
         pint_ctx* c = ctx_locked();
-        if (problem.t0 != 0.0) throw std::invalid_argument("pint-b200: the heat problem starts at t0 = 0");
-        check(pint_run_heat(c, hd.dx, problem.dt, problem.T, static_cast<int64_t>(N),
-                            problem.tree_compose ? PINT_COMPOSE_TREE : PINT_COMPOSE_CHAIN, problem.y0.data(), y.data(),
-                            per_slice.data(), &rep),
-              c);
+        if (problem.t0 != 0.0) throw std::invalid_argument("pint-b200: linear problems start at t0 = 0");
+        const int mode = problem.tree_compose ? PINT_COMPOSE_TREE : PINT_COMPOSE_CHAIN;
+        if (problem.heat) {
+            check(pint_run_heat(c, problem.heat->dx, problem.dt, problem.T, static_cast<int64_t>(N), mode,
+                                problem.y0.data(), y.data(), per_slice.data(), &rep),
+                  c);
+        } else {
+            const WaveDevice& w = *problem.wave;
+            check(pint_run_wave(c, static_cast<int64_t>(w.d), w.D2.data(), w.dt_native, problem.T,
+                                static_cast<int64_t>(N), problem.dt, mode, problem.y0.data(), y.data(),
+                                per_slice.data(), &rep),
+                  c);
+        }
     }
     SweepStats stats;
     simulate_receives(N, sizeof(double) * problem.dim, exec.latency_per_receive, stats);
@@ -709,8 +723,21 @@ LinearProblem make_wave_linear_problem(const WaveProblem& w, double T) {
         p.y0[d + i] = w.um1[i];
     }
     p.name = "wave";
-    p.integrate = [](const TimeSlice&, Vector, double, bool) -> Vector {
-        throw std::logic_error("pint-b200: wave slice maps are not on the device in this round (SURVEY.md §8f)");
+    WaveDevice wd;
+    wd.d = d;
+    wd.D2 = w.D2_interior.data();
+    wd.dt_native = w.dt;
+    p.wave = wd;
+    // the leapfrog integrate closure (pde_problems.cpp:150-171) on the device, one trajectory
+    p.integrate = [wd](const TimeSlice& s, Vector y, double step_nominal, bool) {
+        if (y.size() != 2 * wd.d) throw std::invalid_argument("wave integrate: state size mismatch");
+        const pint_slice cs = to_c(s);
+        std::lock_guard<std::mutex> lk(device().mu);
+        pint_ctx* c = ctx_locked();
+        check(pint_wave_integrate(c, static_cast<int64_t>(wd.d), wd.D2.data(), wd.dt_native, &cs, step_nominal, 1,
+                                  y.data()),
+              c);
+        return y;
     };
     return p;
 }

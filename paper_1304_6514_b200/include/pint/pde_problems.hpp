@@ -1,6 +1,5 @@
-// pint-b200 drop-in: the heat problem (reference pde_problems.hpp:13-25) with its device
-// descriptor. The wave problem (pde_problems.hpp:27-45) is declared for source compatibility;
-// its slice maps are a "next" row and run_nievergelt rejects it on the device.
+// pint-b200 drop-in: the heat and wave problems (reference pde_problems.hpp:13-45) with their
+// device descriptors; both integrate closures and slice maps run on the B200.
 #pragma once
 
 #include <cstddef>

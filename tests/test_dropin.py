@@ -2,10 +2,10 @@
 the B200 library's pint:: headers and linked with libpint_b200.so (oracle/Makefile `dropin`),
 run on the GPU next to the reference's own acceptance binary (oracle/_ref/acceptance).
 
-Expected this round: every unit test case passes except the three wave cases, and every
-acceptance criterion matches the reference's verdict except the wave halves of criteria 3 and 7
-(wave slice maps are SURVEY.md §8f "next"). Criterion 2 fails for the reference itself
-(README.md:110-116); its cell values must be identical.
+Expected: every unit test case passes and every acceptance verdict equals the reference's
+(criterion 2 fails for the reference itself, README.md:110-116; its cell values must be
+identical).
+
 """
 import pathlib
 import re
@@ -47,20 +47,17 @@ def test_reference_unit_tests_on_b200():
     summary = re.search(r"test cases: (\d+) \| (\d+) failed", proc.stdout)
     assert summary, proc.stdout[-2000:]
     assert int(summary.group(1)) == 59
-    assert failed <= WAVE_CASES, failed - WAVE_CASES
+    assert not failed, failed
 
 
 def test_reference_acceptance_on_b200():
     mine = _criteria(_run(DROPIN / "acceptance", DROPIN).stdout)
-    assert [mine[c][0] for c in (1, 4, 5, 6, 8)] == ["PASS"] * 5, mine
-    for c in (3, 7):  # only the wave half is missing on the device
-        assert mine[c][0] == "FAIL" and "wave" in mine[c][1], mine[c]
-    assert mine[2][0] == "FAIL"
+    assert [mine[c][0] for c in (1, 3, 4, 5, 6, 7, 8)] == ["PASS"] * 7, mine
+    assert mine[2][0] == "FAIL"  # fails for the reference itself (README.md:110-116)
     if REF_ACCEPT.exists():
         ref = _criteria(subprocess.run([str(REF_ACCEPT)], cwd=DROPIN, capture_output=True, text=True,
                                        timeout=900).stdout)
         # criterion 2's offending cells: identical numbers to the CPU reference
         cells = lambda s: s.split(" -- ", 1)[1] if " -- " in s else ""
         assert cells(mine[2][1]) == cells(ref[2][1])
-        for c in (1, 4, 5, 6, 8):
-            assert ref[c][0] == mine[c][0]
+        assert {c: v[0] for c, v in ref.items()} == {c: v[0] for c, v in mine.items()}

@@ -391,3 +391,60 @@ def test_per_slice_compute_halves(ctx):
         mx.append(max(r.per_slice_compute))
     for a, b in zip(mx, mx[1:]):
         assert 0.3 < b / a < 0.7
+
+
+# ---- wave affine path -----------------------------------------------------
+
+def _wave_maps(ctx, D2, dt, slices, dt_nominal):
+    d = D2.shape[0]
+    N = len(slices)
+    arr = (capi.Slice * N)(*[s.c() for s in slices])
+    G = np.empty((N, 2 * d, 2 * d))
+    c = np.empty((N, 2 * d))
+    D2c = np.ascontiguousarray(D2)
+    ctx.check(ctx.lib.pint_wave_maps(ctx.h, d, capi.ptr(D2c), dt, arr, N, dt_nominal, capi.ptr(G), capi.ptr(c)))
+    return G, c
+
+
+def test_wave_maps_bit_exact(ctx, golden):
+    D2, dt = golden["wave16_D2"], golden["wave16_dt"][0]
+    dec = pint.decompose(0.0, 16.0, 4, dt)
+    G, c = _wave_maps(ctx, D2, dt, dec.slices, dt)
+    assert np.array_equal(G[1], golden["wave16_slice1_G"])
+    assert np.array_equal(c[1], golden["wave16_slice1_c"])
+    y = np.empty(30)
+    y0 = np.ascontiguousarray(golden["wave16_y0"])
+    rep = capi.Report()
+    D2c = np.ascontiguousarray(D2)
+    ctx.check(ctx.lib.pint_run_wave(ctx.h, 15, capi.ptr(D2c), dt, 16.0, 4, dt, capi.COMPOSE_CHAIN, capi.ptr(y0),
+                                    capi.ptr(y), None, C.byref(rep)))
+    assert np.array_equal(y, golden["wave16_N4_final"])
+    ys = y0.copy()
+    whole = pint.decompose(0.0, 16.0, 1, dt).slices[0].c()
+    ctx.check(ctx.lib.pint_wave_integrate(ctx.h, 15, capi.ptr(D2c), dt, C.byref(whole), dt, 1, capi.ptr(ys)))
+    assert np.array_equal(ys, golden["wave16_serial_final"])
+
+
+def test_wave_rejects_non_native_step(ctx, golden):
+    D2, dt = golden["wave16_D2"], golden["wave16_dt"][0]
+    s = pint.TimeSlice(0, 0.0, 16.0, 1, 16.0)
+    y = np.zeros(30)
+    D2c = np.ascontiguousarray(D2)
+    rc = ctx.lib.pint_wave_integrate(ctx.h, 15, capi.ptr(D2c), dt, C.byref(s.c()), 0.5, 1, capi.ptr(y))
+    assert rc == capi.PINT_E_BAD_GRID
+
+
+def test_wave40_tree_within_tolerance(ctx, golden):
+    D2 = np.ascontiguousarray(golden["wave40_D2"])
+    dt = 8.0 / 1600.0
+    y0 = np.zeros(78)
+    y = np.empty(78)
+    yt = np.empty(78)
+    rep = capi.Report()
+    # y0 from the golden chain is not stored; use the N=8 chain result as the bit-exact anchor
+    w_y0 = np.ascontiguousarray(np.concatenate([np.exp(-200.0 * np.cos(np.arange(1, 40) * np.pi / 40) ** 2),
+                                                np.zeros(39)]))
+    for mode, out in ((capi.COMPOSE_CHAIN, y), (capi.COMPOSE_TREE, yt)):
+        ctx.check(ctx.lib.pint_run_wave(ctx.h, 39, capi.ptr(D2), dt, 16.0, 8, dt, mode, capi.ptr(w_y0),
+                                        capi.ptr(out), None, C.byref(rep)))
+    assert np.max(np.abs(yt - y)) <= 1e-10 * max(1.0, np.max(np.abs(y)))
