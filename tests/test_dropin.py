@@ -19,13 +19,6 @@ REF_ACCEPT = ROOT / "oracle" / "_ref" / "acceptance"
 
 pytestmark = pytest.mark.gpu
 
-WAVE_CASES = {
-    "leapfrog at dt = 8/M^2 stays bounded to T = 16",
-    "wave slice maps are exact: parallel equals serial",
-    "wave integration refuses a non-native step",
-}
-
-
 def _run(binary, cwd):
     if not binary.exists():
         pytest.skip(f"{binary} not built (needs /root/reference at build time)")
