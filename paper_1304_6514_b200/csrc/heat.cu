@@ -29,7 +29,6 @@
 //    augmented map [G | c].
 //
 // Roofline: FP64 pipe. Algorithmic flops per slice-step: (n+1)(5n-4) + 5n (bench.py).
-#include <cstdlib>
 
 #include "pint_internal.cuh"
 
@@ -38,7 +37,6 @@ namespace {
 using pint_dev::record_failure;
 
 constexpr int kRegRows = 64;  // rows of each basis column held in registers (n >= kRegRows + 2)
-constexpr int kMaxCtaThreads = 32 * 8;
 
 __host__ __device__ constexpr long long even(long long x) { return (x + 1) & ~1ll; }
 
@@ -144,47 +142,25 @@ struct BuildPlan {
     int n;
     int N;
     long long S;        // max steps per slice (record layout)
-    int wps;            // warps per slice = ceil((n+1)/32): n basis columns + the forced column
-    int warps_per_cta;  // wps (one CTA per slice) or 1
-    int ctas_per_slice;
+    int wps;            // warps (= CTAs) per slice = ceil((n+1)/32): n basis columns + the forced column
     const double* rec;
     const int64_t* step_off;
     double* maps;
     long long ldm;
     unsigned long long* per_slice_ns;
     FailRec* fail;
-    int debug_flags;  // PINT_HEAT_DEBUG (timing experiments only): 1 = no mixed warp
 };
 
 // Staged record in shared memory: [negr, pad] | (p_i, rcp_i) x n | c_i x n | h b_i x n
 __host__ __device__ constexpr long long staged_doubles(long long n) { return 2 + 4 * n; }
 
-__device__ __forceinline__ void stage_step(double* dst, const RecView& V, long long s, long long j, bool with_hb) {
-    const int n = V.n;
-    double2* pr = reinterpret_cast<double2*>(dst + 2);
-    double* cc = dst + 2 + 2 * n;
-    double* hb = dst + 2 + 3 * n;
-    const int chunks = (with_hb ? 3 * n : 2 * n) + 1;
-    for (int c = threadIdx.x; c < chunks; c += blockDim.x) {
-        if (c < n) {
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(pr + c)), "l"(V.pr + V.row(s, c, j)));
-        } else if (c < 2 * n) {
-            const int i = c - n;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(cc + i)), "l"(V.cc + V.row(s, i, j)));
-        } else if (c == chunks - 1) {
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(V.negr + V.hdr(s, j)));
-        } else {
-            const int i = c - 2 * n;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(hb + i)), "l"(V.hb + V.row(s, i, j)));
-        }
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-}
-
 // One backward-Euler step of one column: forcing increment (mixed warp only), forward
 // elimination (linalg.cpp:84-90), back substitution (linalg.cpp:91). Rows [0, RR) in reg[], the
 // rest at st[32*(i-RR)]. f is 1 on the forced lane and 0 elsewhere: fma(f, hb, x) is exactly
 // x + h*b (pde_problems.cpp:93) there and exactly x on every basis lane.
+// The shared-memory rows are software-pipelined two rows ahead: every load a row needs is issued
+// before the stores of the rows in front of it (the compiler cannot hoist a shared load above a
+// shared store it cannot disambiguate), so only the FP64 chain itself is on the critical path.
 template <int RR, bool kMixed, bool kGuard>
 __device__ __forceinline__ void column_step(double (&reg)[RR > 0 ? RR : 1], double* st, const double* R, int n,
                                             double f, bool forced_lane, bool& bad) {
@@ -203,56 +179,100 @@ __device__ __forceinline__ void column_step(double (&reg)[RR > 0 ? RR : 1], doub
         d = divide((i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d)), PR[i]);
         reg[i] = d;
     }
+    double dm1 = d;  // q_{i-1} when the forward pass ends: the first back row reads it from here
     {
-        double* s = st;
-        const double2* pr = PR + RR;
-        const double* hb = HB + RR;
-#pragma unroll 8
-        for (int i = RR; i < n; ++i, s += 32, ++pr, ++hb) {
-            const double x = kMixed ? __fma_rn(f, *hb, *s) : *s;
-            d = divide((RR == 0 && i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d)), *pr);
-            *s = d;
+        const int last = n - 1 - RR;  // last shared row (>= 0: n > RR)
+        double2 p0 = PR[RR], p1 = PR[RR + min(1, last)];
+        double x0 = st[0], x1 = st[32 * min(1, last)];
+        double h0 = kMixed ? HB[RR] : 0.0, h1 = kMixed ? HB[RR + min(1, last)] : 0.0;
+#pragma unroll 4
+        for (int r = 0; r <= last; ++r) {
+            const int r2 = min(r + 2, last);
+            const double2 p2 = PR[RR + r2];
+            const double x2 = st[32 * r2];
+            const double h2 = kMixed ? HB[RR + r2] : 0.0;
+            const double x = kMixed ? __fma_rn(f, h0, x0) : x0;
+            dm1 = d;
+            d = divide((RR == 0 && r == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d)), p0);
+            st[32 * r] = d;
+            p0 = p1, p1 = p2, x0 = x1, x1 = x2, h0 = h1, h1 = h2;
         }
     }
-    {
-        double* s = st + (n - 2 - RR) * 32;
-        const double* c = CC + (n - 2);
-#pragma unroll 8
-        for (int i = n - 2; i >= RR; --i, s -= 32, --c) {
-            d = __dsub_rn(*s, __dmul_rn(*c, d));
-            *s = d;
+    double c0 = 0.0, c1 = 0.0;  // CC[RR-1], CC[RR-2] once the shared rows are done
+    if (n - 2 >= RR) {
+        const int top = n - 2 - RR;  // first shared row of the back pass
+        double y0 = dm1, y1 = st[32 * max(top - 1, 0)];
+        c0 = CC[n - 2];
+        c1 = CC[max(n - 3, 0)];
+#pragma unroll 4
+        for (int r = top; r >= 0; --r) {
+            const double y2 = st[32 * max(r - 2, 0)];
+            const double c2 = CC[max(RR + r - 2, 0)];
+            d = __dsub_rn(y0, __dmul_rn(c0, d));
+            st[32 * r] = d;
+            y0 = y1, y1 = y2, c0 = c1, c1 = c2;
         }
+    } else if (RR > 0) {
+        c0 = CC[RR - 1];
+        c1 = CC[max(RR - 2, 0)];
     }
 #pragma unroll
     for (int i = RR - 1; i >= 0; --i) {
-        d = __dsub_rn(reg[i], __dmul_rn(CC[i], d));
+        const double c = (i == RR - 1) ? c0 : (i == RR - 2) ? c1 : CC[i];
+        d = __dsub_rn(reg[i], __dmul_rn(c, d));
         reg[i] = d;
     }
 }
 
-// CTA = warps [c*warps_per_cta, ...) of one slice; lane = trajectory k (k < n: basis e_k, k == n:
-// the forced run from 0, k > n: idle). Dynamic smem: staged[2][SD] | state[warps_per_cta][(n-RR)*32]
+// Staged record of one step: [negr, pad] | (p_i, rcp_i) x n | c_i x n | h b_i x n, gathered by the
+// warp's own lanes with cp.async (16-/8-byte chunks of the slice-minor records).
+__device__ __forceinline__ void stage_step(double* dst, const RecView& V, long long s, long long j, bool with_hb,
+                                           int lane) {
+    const int n = V.n;
+    double2* pr = reinterpret_cast<double2*>(dst + 2);
+    double* cc = dst + 2 + 2 * n;
+    double* hb = dst + 2 + 3 * n;
+    const int chunks = (with_hb ? 3 * n : 2 * n) + 1;
+    for (int c = lane; c < chunks; c += 32) {
+        if (c < n) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(pr + c)), "l"(V.pr + V.row(s, c, j)));
+        } else if (c < 2 * n) {
+            const int i = c - n;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(cc + i)), "l"(V.cc + V.row(s, i, j)));
+        } else if (c == chunks - 1) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(V.negr + V.hdr(s, j)));
+        } else {
+            const int i = c - 2 * n;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(hb + i)), "l"(V.hb + V.row(s, i, j)));
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+}
+
+// CTA = ONE warp: warp g of slice blockIdx.x / wps; lane = trajectory k = 32g + lane (k < n: basis
+// e_k, k == n: the forced run from 0, k > n: idle). Warps share nothing — each stages its own copy
+// of the step record (double buffer, one step ahead) — so no CTA barrier couples a slice's warps
+// and the scheduler packs the single-warp CTAs over all SMs.
+// Dynamic smem: staged[2][SD] | state[(n-RR)*32]
 template <int RR, bool kGuard>
-__global__ void __launch_bounds__(kMaxCtaThreads) heat_build_kernel(BuildPlan P) {
+__global__ void __maxnreg__(224) heat_build_kernel(BuildPlan P) {
     extern __shared__ __align__(16) double smem[];
     const unsigned long long t_start = pint_dev::globaltimer();
     const int n = P.n;
-    const int lane = threadIdx.x & 31, wcta = threadIdx.x >> 5;
-    const int slice = blockIdx.x / P.ctas_per_slice;
-    const int cta = blockIdx.x - slice * P.ctas_per_slice;
-    const int g = cta * P.warps_per_cta + wcta;  // warp in slice
+    const int lane = threadIdx.x;
+    const int slice = blockIdx.x / P.wps;
+    const int g = blockIdx.x - slice * P.wps;
     const long long SD = staged_doubles(n);
     double* buf = smem;
-    double* st = smem + 2 * SD + static_cast<long long>(wcta) * (n - RR) * 32 + lane;
+    double* st = smem + 2 * SD + lane;
     const int k = g * 32 + lane;
     const bool forced_lane = (k == n);
-    const bool mixed = (g == n / 32) && !(P.debug_flags & 1);  // the warp holding column n
-    const bool cta_has_forcing = (n / 32) / P.warps_per_cta == cta;  // stage h*b only if needed
+    const bool mixed = (g == n / 32);  // the warp holding column n
     const double f = forced_lane ? 1.0 : 0.0;
     const long long steps = P.step_off[slice + 1] - P.step_off[slice];
     const RecView V = rec_view(P.rec, n, P.N, P.S);
 
-    if (steps > 0) stage_step(buf, V, 0, slice, cta_has_forcing);
+    if (steps > 0) stage_step(buf, V, 0, slice, mixed, lane);
     double reg[RR > 0 ? RR : 1];
 #pragma unroll
     for (int i = 0; i < RR; ++i) reg[i] = (i == k) ? 1.0 : 0.0;  // e_k (all zero for k >= n)
@@ -262,15 +282,15 @@ __global__ void __launch_bounds__(kMaxCtaThreads) heat_build_kernel(BuildPlan P)
     int cur = 0;
     for (long long s = 0; s < steps; ++s) {
         if (s + 1 < steps) {
-            stage_step(buf + (cur ^ 1) * SD, V, s + 1, slice, cta_has_forcing);
+            stage_step(buf + (cur ^ 1) * SD, V, s + 1, slice, mixed, lane);
             asm volatile("cp.async.wait_group 1;\n" ::);
         } else {
             asm volatile("cp.async.wait_group 0;\n" ::);
         }
-        __syncthreads();  // step s's record visible to every warp
+        __syncwarp();  // step s's record visible to every lane
         if (mixed) column_step<RR, true, kGuard>(reg, st, buf + cur * SD, n, f, forced_lane, bad);
         else column_step<RR, false, kGuard>(reg, st, buf + cur * SD, n, f, forced_lane, bad);
-        __syncthreads();  // buffer `cur` is refilled next iteration
+        __syncwarp();  // buffer `cur` is refilled next iteration
         cur ^= 1;
     }
     if (k <= n) {
@@ -280,7 +300,7 @@ __global__ void __launch_bounds__(kMaxCtaThreads) heat_build_kernel(BuildPlan P)
         for (int i = RR; i < n; ++i) gp[i * P.ldm] = st[(i - RR) * 32];
     }
     if (bad) record_failure(P.fail, slice, PINT_E_RANGE_RETRY, static_cast<double>(n));
-    if (P.per_slice_ns && threadIdx.x == 0) atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
+    if (P.per_slice_ns && lane == 0) atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
 }
 
 // ---- integrate: K caller columns of one slice (records with N = 1), guarded division ----------
@@ -334,17 +354,11 @@ void smem_attrs(K kern, size_t smem) {
 
 template <int RR, bool kGuard>
 int launch_build(pint_ctx* ctx, BuildPlan P) {
-    // one CTA per slice when two such CTAs fit an SM, else one CTA per warp
-    const size_t state_warp = sizeof(double) * static_cast<size_t>(P.n - RR) * 32;
-    const size_t staged = sizeof(double) * 2 * staged_doubles(P.n);
-    P.warps_per_cta = (P.wps <= kMaxCtaThreads / 32 && staged + state_warp * P.wps <= 112 * 1024) ? P.wps : 1;
-    P.ctas_per_slice = P.wps / P.warps_per_cta;
-    const size_t smem = staged + state_warp * P.warps_per_cta;
+    const size_t smem = sizeof(double) * (2 * staged_doubles(P.n) + static_cast<size_t>(P.n - RR) * 32);
     if (smem > 227 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: n too large for shared memory");
     auto kern = heat_build_kernel<RR, kGuard>;
     smem_attrs(kern, smem);
-    kern<<<static_cast<unsigned>(static_cast<long long>(P.N) * P.ctas_per_slice), 32 * P.warps_per_cta, smem,
-           ctx->stream>>>(P);
+    kern<<<static_cast<unsigned>(static_cast<long long>(P.N) * P.wps), 32, smem, ctx->stream>>>(P);
     return pint_check_launch(ctx, "heat_build_kernel");
 }
 
@@ -382,7 +396,6 @@ int launch_heat_build(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int6
     P.ldm = pint_affine_ldm(n);
     P.per_slice_ns = per_slice_ns;
     P.fail = ctx->d_fail;
-    if (const char* e = std::getenv("PINT_HEAT_DEBUG")) P.debug_flags = std::atoi(e);
     if (n >= kRegRows + 2)
         return guarded ? launch_build<kRegRows, true>(ctx, P) : launch_build<kRegRows, false>(ctx, P);
     return guarded ? launch_build<0, true>(ctx, P) : launch_build<0, false>(ctx, P);
