@@ -149,17 +149,17 @@ int pint_heat_coefficients(double dx, const pint_slice* slices, int64_t N, int64
 /* doubles of the per-step records of N slices with at most S steps each (pint_heat_factor_dev) */
 int64_t pint_heat_records_size(int64_t n, int64_t N, int64_t S);
 /* Shared tridiagonal factor per (slice, step) — the Thomas forward pivots (linalg.cpp:77-93),
- * computed once per step instead of once per trajectory — plus the forcing increments, stored
- * slice-minor: hdr[3][S][N] = {-r, fa, fb}, then (p_i, RN(1/p_i))[S][n][N], c_i[S][n][N] and
- * h*b_i[S][n][N]. step_off/slice_dt/sx (device) and r/fa/fb (device, step_off[N] entries) come
- * from pint_heat_coefficients. */
+ * computed once per step instead of once per trajectory — plus the forcing increments. One
+ * contiguous record per (slice, step), slice-major [N][S]: {-r, 0} | (p_i, RN(1/p_i)) x n |
+ * h*b_i x even(n) | c_i x even(n). step_off/slice_dt/sx (device) and r/fa/fb (device,
+ * step_off[N] entries) come from pint_heat_coefficients. */
 int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
                          const double* slice_dt, const double* r, const double* fa,
                          const double* fb, const double* sx, double* records);
 /* Build all N augmented maps into maps (N * n * ldm doubles). step_off/slice_dt/sx are device
  * copies of the host tables; per_slice_ns (may be NULL) accumulates per-slice device time.
- * guarded = 0: fast exact division, forced lanes range-checked off the critical path; a tripped
- * check latches PINT_E_RANGE_RETRY in the failure record and the caller re-runs with
+ * guarded = 0: fast exact division, dividends range-checked off the critical path (forced lanes
+ * per row, basis lanes through a running minimum); a tripped check latches PINT_E_RANGE_RETRY in the failure record and the caller re-runs with
  * guarded = 1 (IEEE division on the chain outside [2^-960, 2^997]). Both are bit-exact. */
 int pint_heat_build_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
                         const double* slice_dt, const double* records, const double* sx,
@@ -241,7 +241,8 @@ int pint_bary_weights(pint_ctx* ctx, int kind, int64_t M, const double* nodes, d
 
 /* ---- roofline probe: measured FMA throughput (TFLOP/s) of this GPU for PINT_F64 / PINT_F32 */
 int pint_probe_peak(pint_ctx* ctx, int precision, double* tflops);
-/* dependent-chain latency in SM cycles per op: {DFMA, DADD, DMUL, FFMA, LDS.64} */
+/* dependent-chain latency in SM cycles per op: {DFMA, DADD, DMUL, FFMA, LDS.64}, then cycles per
+   heat forward row (5 dependent ops), per heat back row (2), per op of alternating DMUL/DADD */
 int pint_probe_latency(pint_ctx* ctx, double* cycles);
 
 #ifdef __cplusplus

@@ -8,112 +8,95 @@
 // B200 design:
 //  * The tridiagonal factor depends only on (slice, step), never on the right-hand side, so
 //    heat_record_kernel computes it once per (slice, step) with exactly thomas_solve's operations
-//    (every solve stays bit-identical). Records are stored slice-minor:
-//        hdr[3][S][N] = {-r, fa, fb},  pr[S][n][N] = (p_i, RN(1/p_i)),  cc[S][n][N] = c_i
-//    (plus the forcing increments h*b_i[S][n][N]) so the record kernel (thread = (step, slice))
-//    writes coalesced, and a slice CTA gathers its column with 16-/8-byte cp.async chunks.
+//    (every solve stays bit-identical), together with the forcing increments h*b_i. Each (slice,
+//    step) record is one contiguous block (slice-major), so a warp stages it with two bulk copies
+//    (cp.async.bulk + mbarrier) and pulls the record two steps ahead into L2.
 //  * x / p_i is q0 = x*rcp, rem = fma(-p, q0, x), q = fma(rem, rcp, q0) with rcp = RN(1/p_i):
 //    Markstein's theorem makes q the correctly rounded quotient whenever no intermediate
-//    under/overflows. Basis columns are entrywise non-negative and bounded (each step matrix is an
-//    M-matrix, p_i >= 1, |c_i| < 1), so their quotients stay far from the subnormal range and run
-//    unguarded. Forced columns are range-checked OFF the dependent chain (a sticky flag); if it
-//    ever trips, the kernel reports PINT_E_RANGE_RETRY and the host re-runs the build with the
-//    guarded variant (exponent check on the chain, IEEE __ddiv_rn outside [2^-960, 2^997]).
-//  * A CTA holds the ceil((n+1)/32) warps of one slice (or one warp when n is large), lane =
-//    trajectory: k < n runs from e_k, k == n is the forced run from 0 (c). The step's record is
-//    staged once per CTA into shared memory one step ahead (cp.async) and read as broadcasts;
-//    the first kRegRows rows of every column live in registers, the rest lane-interleaved in
-//    shared memory (conflict-free). The forcing increment h*b_i is precomputed in the record, so
-//    the forced lane costs one exact fma(f, hb_i, x) per row (f = 1 there, 0 on basis lanes) and
-//    the slice's warps stay balanced. Rows leave as coalesced 256 B stores into the row-major
-//    augmented map [G | c].
+//    under/overflows. The dividends are range-checked OFF the dependent chain (forced lane: a
+//    window test per row; basis lanes: a running minimum); if a check trips, the
+//    kernel reports PINT_E_RANGE_RETRY and the host re-runs the build with the guarded variant
+//    (exponent check on the chain, IEEE __ddiv_rn outside [2^-960, 2^997]).
+//  * CTA = ONE warp, lane = trajectory: warp g of a slice runs columns 32g..32g+31 (k < n: basis
+//    e_k, k == n: the forced run from 0, k > n: idle). The first kRegRows rows of every column
+//    live in registers, the rest lane-interleaved in shared memory (conflict-free), read through
+//    a software pipeline. Rows leave as coalesced 256 B stores into the row-major augmented map.
 //
-// Roofline: FP64 pipe. Algorithmic flops per slice-step: (n+1)(5n-4) + 5n (bench.py).
-
+// Roofline: the per-column recurrence (S x n dependent rows of 7 FP64 ops) — latency-bound;
+// algorithmic flops per slice-step: (n+1)(5n-4) + 5n (bench.py).
 #include "pint_internal.cuh"
 
 namespace {
 
 using pint_dev::record_failure;
 
-constexpr int kRegRows = 64;  // rows of each basis column held in registers (n >= kRegRows + 2)
+constexpr int kRegRows = 56;  // rows of each basis column held in registers (n >= kRegRows + 2)
 
 __host__ __device__ constexpr long long even(long long x) { return (x + 1) & ~1ll; }
 
-// doubles needed for the records of N slices x S steps x n rows
+// One (slice, step) record, doubles: [negr, pad] | (p_i, rcp_i) x n | h*b_i x even(n) | c_i x even(n).
+// The forward half (negr, p, rcp [, h*b]) and the back half (c) are each a 16-byte multiple.
+__host__ __device__ constexpr long long record_stride(long long n) { return 2 + 2 * n + 2 * even(n); }
+__host__ __device__ constexpr long long hb_offset(long long n) { return 2 + 2 * n; }
+__host__ __device__ constexpr long long cc_offset(long long n) { return 2 + 2 * n + even(n); }
+
+// doubles needed for the records of N slices x S steps x n rows: [N][S][record]
 __host__ __device__ constexpr long long records_doubles(long long n, long long N, long long S) {
-    return even(3 * S * N) + 4 * S * n * N;
+    return N * S * record_stride(n);
 }
 
 struct RecView {
-    const double* negr;  // [S][N]
-    const double* fa;
-    const double* fb;
-    const double2* pr;   // [S][n][N]
-    const double* cc;    // [S][n][N]
-    const double* hb;    // [S][n][N]: the forcing increment h * heat_forcing(x_i, t)
-    long long N;
+    const double* base;
+    long long S;
     int n;
-    __device__ __forceinline__ long long hdr(long long s, long long j) const { return s * N + j; }
-    __device__ __forceinline__ long long row(long long s, int i, long long j) const { return (s * n + i) * N + j; }
+    __device__ __forceinline__ const double* rec(long long j, long long s) const {
+        return base + (j * S + s) * record_stride(n);
+    }
 };
 
-__host__ __device__ inline RecView rec_view(const double* base, int n, long long N, long long S) {
-    RecView v;
-    v.negr = base;
-    v.fa = base + S * N;
-    v.fb = base + 2 * S * N;
-    v.pr = reinterpret_cast<const double2*>(base + even(3 * S * N));
-    v.cc = base + even(3 * S * N) + 2 * S * n * N;
-    v.hb = base + even(3 * S * N) + 3 * S * n * N;
-    v.N = N;
-    v.n = n;
-    return v;
-}
+__host__ __device__ inline RecView rec_view(const double* base, int n, long long S) { return RecView{base, S, n}; }
 
-// Thread (s, j): step s of slice j — the Thomas forward pivots of tridiag(-r, 1+2r, -r)
+// Thread (j, s): step s of slice j — the Thomas forward pivots of tridiag(-r, 1+2r, -r)
 // (linalg.cpp:80-90, with sub = sup = -r, diag = 1 + 2r as solve_implicit builds them), and the
 // forcing increment h * b_i with b_i = fa*s_i + fb*s_i = heat_forcing(x_i, t) (pde_problems.cpp:
-// 26-29, 91-94), rounded exactly as `state[i] += dt_step * b[i]` consumes it.
+// 26-29, 91-94), rounded exactly as `state[i] += dt_step * b[i]` consumes it. Consecutive threads
+// write consecutive records, so every 32-byte sector is filled by one thread's stores.
 __global__ void heat_record_kernel(int n, long long N, long long S, const int64_t* __restrict__ step_off,
                                    const double* __restrict__ slice_dt, const double* __restrict__ r_tab,
                                    const double* __restrict__ fa, const double* __restrict__ fb,
                                    const double* __restrict__ sx, double* __restrict__ rec, FailRec* fail) {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= S * N) return;
-    const long long s = t / N, j = t - s * N;
+    const long long j = t / S, s = t - j * S;
     const long long q = step_off[j] + s;
     if (q >= step_off[j + 1]) return;  // slice j has fewer steps
-    const RecView V = rec_view(rec, n, N, S);
-    double* negr_out = const_cast<double*>(V.negr);
-    double* fa_out = const_cast<double*>(V.fa);
-    double* fb_out = const_cast<double*>(V.fb);
-    double2* pr_out = const_cast<double2*>(V.pr);
-    double* cc_out = const_cast<double*>(V.cc);
+    double* R = rec + t * record_stride(n);
+    double2* pr_out = reinterpret_cast<double2*>(R + 2);
+    double* hb_out = R + hb_offset(n);
+    double* cc_out = R + cc_offset(n);
     const double r = r_tab[q];
     const double negr = -r;                                  // pde_problems.cpp:55
     const double diag = __dadd_rn(1.0, __dmul_rn(2.0, r));   // 1.0 + 2.0 * r
-    negr_out[V.hdr(s, j)] = negr;
-    fa_out[V.hdr(s, j)] = fa[q];
-    fb_out[V.hdr(s, j)] = fb[q];
+    R[0] = negr;
+    R[1] = 0.0;
     double p = diag;  // pivot = diag[0]; c[0] = sup[0] / pivot (linalg.cpp:80-83)
     if (p == 0.0) record_failure(fail, q, PINT_E_SINGULAR, 0.0);
     double c = (n > 1) ? __ddiv_rn(negr, p) : 0.0;
-    pr_out[V.row(s, 0, j)] = make_double2(p, __drcp_rn(p));
-    cc_out[V.row(s, 0, j)] = c;
+    pr_out[0] = make_double2(p, __drcp_rn(p));
+    cc_out[0] = c;
     for (int i = 1; i < n; ++i) {  // pivot = diag - sub*c[i-1]; c[i] = sup / pivot (:84-88)
         p = __dsub_rn(diag, __dmul_rn(negr, c));
         if (p == 0.0) record_failure(fail, q, PINT_E_SINGULAR, static_cast<double>(i));
         c = (i < n - 1) ? __ddiv_rn(negr, p) : 0.0;
-        pr_out[V.row(s, i, j)] = make_double2(p, __drcp_rn(p));
-        cc_out[V.row(s, i, j)] = c;
+        pr_out[i] = make_double2(p, __drcp_rn(p));
+        cc_out[i] = c;
     }
-    double* hb_out = const_cast<double*>(V.hb);
     const double h = slice_dt[j], fq = fa[q], gq = fb[q];
     for (int i = 0; i < n; ++i) {
         const double si = sx[i];
-        hb_out[V.row(s, i, j)] = __dmul_rn(h, __dadd_rn(__dmul_rn(fq, si), __dmul_rn(gq, si)));
+        hb_out[i] = __dmul_rn(h, __dadd_rn(__dmul_rn(fq, si), __dmul_rn(gq, si)));
     }
+    if (n & 1) hb_out[n] = 0.0, cc_out[n] = 0.0;
 }
 
 __device__ __forceinline__ double div_fast(double x, double2 pr) {
@@ -151,154 +134,260 @@ struct BuildPlan {
     FailRec* fail;
 };
 
-// Staged record in shared memory: [negr, pad] | (p_i, rcp_i) x n | c_i x n | h b_i x n
-__host__ __device__ constexpr long long staged_doubles(long long n) { return 2 + 4 * n; }
+// Per-warp shared memory (doubles): [front pad][staged record][state (n-RR)*32][tail pad][2
+// mbarriers]. The staged record mirrors one global record. The pads make the software pipeline's
+// look-ahead loads (up to kBackAhead rows before the state and kFwdAhead rows after it) land
+// inside the allocation; the values they read are never used.
+constexpr int kFwdAhead = 3;   // forward row: 5 dependent FP64 ops (~40 cycles) vs ~52-cycle LDS
+constexpr int kBackAhead = 8;  // back row: 2 dependent ops (~16 cycles)
+__host__ __device__ constexpr long long front_pad(long long n) {
+    return record_stride(n) >= 32 * kBackAhead ? 0 : even(32 * kBackAhead - record_stride(n));
+}
+__host__ __device__ constexpr long long warp_smem_doubles(long long n, int RR) {
+    return front_pad(n) + record_stride(n) + (n - RR) * 32 + 32 * kFwdAhead + 2;
+}
 
-// One backward-Euler step of one column: forcing increment (mixed warp only), forward
-// elimination (linalg.cpp:84-90), back substitution (linalg.cpp:91). Rows [0, RR) in reg[], the
-// rest at st[32*(i-RR)]. f is 1 on the forced lane and 0 elsewhere: fma(f, hb, x) is exactly
-// x + h*b (pde_problems.cpp:93) there and exactly x on every basis lane.
-// The shared-memory rows are software-pipelined two rows ahead: every load a row needs is issued
-// before the stores of the rows in front of it (the compiler cannot hoist a shared load above a
-// shared store it cannot disambiguate), so only the FP64 chain itself is on the critical path.
+__device__ __forceinline__ void mbar_init(unsigned bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    unsigned done;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+// One thread: arm `bar` for `bytes` and bulk-copy them global -> shared (completes on `bar`).
+__device__ __forceinline__ void bulk_load(unsigned dst, const double* src, unsigned bytes, unsigned bar) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(bar),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const double* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ unsigned hi_abs(double x) {
+    return static_cast<unsigned>(__double2hiint(x)) & 0x7fffffffu;
+}
+
+// Forward elimination of one step (linalg.cpp:84-90), with the forcing increment on the mixed
+// warp: fma(f, hb, x) is exactly x + h*b (pde_problems.cpp:93) on the forced lane (f = 1) and
+// exactly x on every basis lane (f = 0). Rows [0, RR) in reg[], the rest at st[32*(i-RR)],
+// software-pipelined kFwdAhead rows ahead (every load is issued before the stores in front of it:
+// the compiler cannot hoist a shared load above a shared store it cannot disambiguate). The
+// forced lane's dividends are range-checked off the chain: (|hi| - lo) > rng with lo/rng the
+// Markstein window on that lane and a never-true window elsewhere (LOP3 + IADD + ISETP.OR).
+// Returns q_{n-1}; dm1 = q_{n-2}.
 template <int RR, bool kMixed, bool kGuard>
-__device__ __forceinline__ void column_step(double (&reg)[RR > 0 ? RR : 1], double* st, const double* R, int n,
-                                            double f, bool forced_lane, bool& bad) {
+__device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1], double* st, const double* R,
+                                                 int n, double f, unsigned lo, unsigned rng, bool& bad,
+                                                 double& dm1) {
     const double negr = R[0];
     const double2* PR = reinterpret_cast<const double2*>(R + 2);
-    const double* CC = R + 2 + 2 * n;
-    const double* HB = R + 2 + 3 * n;
+    const double* HB = R + hb_offset(n);
     auto divide = [&](double num, double2 pr) {
-        if (kMixed && !kGuard) bad |= forced_lane && out_of_range(num);
-        return (kMixed && kGuard) ? div_guarded(num, pr) : div_fast(num, pr);
+        if (kMixed && !kGuard) bad = bad | ((hi_abs(num) - lo) > rng);
+        return kGuard ? div_guarded(num, pr) : div_fast(num, pr);
     };
-    double d = 0.0;
+    // RR == 0: row 0 goes through the generic x - negr*d with d = -0.0, where negr*d is +0 (negr
+    // <= 0) and x - (+0) == x bit-for-bit (even for x = -0), so the loop needs no row-0 select
+    double d = -0.0;
 #pragma unroll
     for (int i = 0; i < RR; ++i) {
         const double x = kMixed ? __fma_rn(f, HB[i], reg[i]) : reg[i];
         d = divide((i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d)), PR[i]);
         reg[i] = d;
     }
-    double dm1 = d;  // q_{i-1} when the forward pass ends: the first back row reads it from here
-    {
-        const int last = n - 1 - RR;  // last shared row (>= 0: n > RR)
-        double2 p0 = PR[RR], p1 = PR[RR + min(1, last)];
-        double x0 = st[0], x1 = st[32 * min(1, last)];
-        double h0 = kMixed ? HB[RR] : 0.0, h1 = kMixed ? HB[RR + min(1, last)] : 0.0;
-#pragma unroll 4
-        for (int r = 0; r <= last; ++r) {
-            const int r2 = min(r + 2, last);
-            const double2 p2 = PR[RR + r2];
-            const double x2 = st[32 * r2];
-            const double h2 = kMixed ? HB[RR + r2] : 0.0;
-            const double x = kMixed ? __fma_rn(f, h0, x0) : x0;
-            dm1 = d;
-            d = divide((RR == 0 && r == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d)), p0);
-            st[32 * r] = d;
-            p0 = p1, p1 = p2, x0 = x1, x1 = x2, h0 = h1, h1 = h2;
+    dm1 = d;
+    const int last = n - 1 - RR;  // last shared row (>= 0)
+    const double2* pr = PR + RR;
+    const double* hb = HB + RR;
+    double2 pv[kFwdAhead];
+    double xv[kFwdAhead], hv[kFwdAhead];
+#pragma unroll
+    for (int u = 0; u < kFwdAhead; ++u) {
+        pv[u] = pr[u];
+        xv[u] = st[32 * u];
+        hv[u] = kMixed ? hb[u] : 0.0;
+    }
+    // ring slot u holds row r + u; full blocks refill without predicates (a predicated refill
+    // would turn into conditional moves that wait on the load), the < kFwdAhead tail rows are
+    // already in the ring
+    auto row = [&](int rr, double2 p, double x0, double h) {
+        const double x = kMixed ? __fma_rn(f, h, x0) : x0;
+        dm1 = d;
+        d = divide(__dsub_rn(x, __dmul_rn(negr, d)), p);
+        st[32 * rr] = d;
+    };
+    int r = 0;
+#pragma unroll 1
+    for (; r + kFwdAhead - 1 <= last; r += kFwdAhead) {
+#pragma unroll
+        for (int u = 0; u < kFwdAhead; ++u) {  // consume, then refill the slot in place
+            row(r + u, pv[u], xv[u], hv[u]);
+            pv[u] = pr[r + u + kFwdAhead];
+            xv[u] = st[32 * (r + u + kFwdAhead)];
+            if (kMixed) hv[u] = hb[r + u + kFwdAhead];
         }
     }
-    double c0 = 0.0, c1 = 0.0;  // CC[RR-1], CC[RR-2] once the shared rows are done
-    if (n - 2 >= RR) {
-        const int top = n - 2 - RR;  // first shared row of the back pass
-        double y0 = dm1, y1 = st[32 * max(top - 1, 0)];
-        c0 = CC[n - 2];
-        c1 = CC[max(n - 3, 0)];
-#pragma unroll 4
-        for (int r = top; r >= 0; --r) {
-            const double y2 = st[32 * max(r - 2, 0)];
-            const double c2 = CC[max(RR + r - 2, 0)];
-            d = __dsub_rn(y0, __dmul_rn(c0, d));
-            st[32 * r] = d;
-            y0 = y1, y1 = y2, c0 = c1, c1 = c2;
+#pragma unroll
+    for (int u = 0; u < kFwdAhead - 1; ++u)
+        if (r + u <= last) row(r + u, pv[u], xv[u], hv[u]);
+    return d;
+}
+
+// Back substitution of one step (linalg.cpp:91): d_i = q_i - c_i d_{i+1}, shared rows pipelined
+// kBackAhead rows ahead, then the register rows. dmin tracks min |hi word| of every basis value:
+// all dividends of the next step are >= it, which is how basis lanes are
+// range-checked at one IMNMX per row.
+template <int RR>
+__device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], double* st, const double* R, int n,
+                                            double d, double dm1, unsigned& dmin) {
+    const double* CC = R + cc_offset(n);
+    const int top = n - 2 - RR;  // first shared row of the back pass
+    if (top >= 0) {
+        double yv[kBackAhead], cv[kBackAhead];
+        const double* cc = CC + RR;
+#pragma unroll
+        for (int u = 0; u < kBackAhead; ++u) {
+            yv[u] = (u == 0) ? dm1 : st[32 * (top - u)];
+            cv[u] = cc[top - u];
         }
-    } else if (RR > 0) {
-        c0 = CC[RR - 1];
-        c1 = CC[max(RR - 2, 0)];
+        // ring slot u holds row r - u (see column_forward)
+        auto row = [&](int rr, double y, double c) {
+            d = __dsub_rn(y, __dmul_rn(c, d));
+            st[32 * rr] = d;
+            dmin = min(dmin, hi_abs(d));
+        };
+        int r = top;
+#pragma unroll 1
+        for (; r >= kBackAhead - 1; r -= kBackAhead) {
+#pragma unroll
+            for (int u = 0; u < kBackAhead; ++u) {  // consume, then refill the slot in place
+                row(r - u, yv[u], cv[u]);
+                yv[u] = st[32 * (r - u - kBackAhead)];
+                cv[u] = cc[r - u - kBackAhead];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kBackAhead - 1; ++u)
+            if (r - u >= 0) row(r - u, yv[u], cv[u]);
     }
 #pragma unroll
     for (int i = RR - 1; i >= 0; --i) {
-        const double c = (i == RR - 1) ? c0 : (i == RR - 2) ? c1 : CC[i];
-        d = __dsub_rn(reg[i], __dmul_rn(c, d));
+        if (i > n - 2) continue;  // (RR > 0 implies n >= RR + 2: never taken)
+        d = __dsub_rn(reg[i], __dmul_rn(CC[i], d));
         reg[i] = d;
+        dmin = min(dmin, hi_abs(d));
     }
 }
 
-// Staged record of one step: [negr, pad] | (p_i, rcp_i) x n | c_i x n | h b_i x n, gathered by the
-// warp's own lanes with cp.async (16-/8-byte chunks of the slice-minor records).
-__device__ __forceinline__ void stage_step(double* dst, const RecView& V, long long s, long long j, bool with_hb,
-                                           int lane) {
-    const int n = V.n;
-    double2* pr = reinterpret_cast<double2*>(dst + 2);
-    double* cc = dst + 2 + 2 * n;
-    double* hb = dst + 2 + 3 * n;
-    const int chunks = (with_hb ? 3 * n : 2 * n) + 1;
-    for (int c = lane; c < chunks; c += 32) {
-        if (c < n) {
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(pr + c)), "l"(V.pr + V.row(s, c, j)));
-        } else if (c < 2 * n) {
-            const int i = c - n;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(cc + i)), "l"(V.cc + V.row(s, i, j)));
-        } else if (c == chunks - 1) {
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(V.negr + V.hdr(s, j)));
-        } else {
-            const int i = c - 2 * n;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(hb + i)), "l"(V.hb + V.row(s, i, j)));
-        }
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-}
+#ifdef PINT_HEAT_PROF  // section timing for tools/heat_micro.cu only (never in the library build)
+__device__ unsigned long long g_heat_prof[1 << 14][6];
+#define HEAT_PROF_MARK(k)                           \
+    do {                                            \
+        const long long t_ = clock64();             \
+        prof[k] += static_cast<unsigned long long>(t_ - t_prev); \
+        t_prev = t_;                                \
+    } while (0)
+#else
+#define HEAT_PROF_MARK(k) \
+    do {                  \
+    } while (0)
+#endif
 
 // CTA = ONE warp: warp g of slice blockIdx.x / wps; lane = trajectory k = 32g + lane (k < n: basis
 // e_k, k == n: the forced run from 0, k > n: idle). Warps share nothing — each stages its own copy
-// of the step record (double buffer, one step ahead) — so no CTA barrier couples a slice's warps
-// and the scheduler packs the single-warp CTAs over all SMs.
-// Dynamic smem: staged[2][SD] | state[(n-RR)*32]
+// of the step record — so no CTA barrier couples a slice's warps, and the single-warp CTAs pack
+// over every SM.
 template <int RR, bool kGuard>
-__global__ void __maxnreg__(224) heat_build_kernel(BuildPlan P) {
+__global__ void __maxnreg__(168) heat_build_kernel(BuildPlan P) {
     extern __shared__ __align__(16) double smem[];
     const unsigned long long t_start = pint_dev::globaltimer();
     const int n = P.n;
     const int lane = threadIdx.x;
     const int slice = blockIdx.x / P.wps;
     const int g = blockIdx.x - slice * P.wps;
-    const long long SD = staged_doubles(n);
-    double* buf = smem;
-    double* st = smem + 2 * SD + lane;
+    double* R = smem + front_pad(n);
+    double* st = R + record_stride(n) + lane;
+    const unsigned bar_f = smem_u32(R + record_stride(n) + (n - RR) * 32 + 32 * kFwdAhead);
+    const unsigned bar_b = bar_f + 8;
     const int k = g * 32 + lane;
     const bool forced_lane = (k == n);
     const bool mixed = (g == n / 32);  // the warp holding column n
     const double f = forced_lane ? 1.0 : 0.0;
+    const unsigned lo = forced_lane ? (63u << 20) : 0u;
+    const unsigned rng = forced_lane ? ((2021u - 63u) << 20) - 1u : 0xffffffffu;
     const long long steps = P.step_off[slice + 1] - P.step_off[slice];
-    const RecView V = rec_view(P.rec, n, P.N, P.S);
+    const RecView V = rec_view(P.rec, n, P.S);
+    const unsigned fwd_bytes = 8u * static_cast<unsigned>(mixed ? cc_offset(n) : hb_offset(n));
+    const unsigned back_bytes = 8u * static_cast<unsigned>(even(n));
+    const unsigned rec_bytes = 8u * static_cast<unsigned>(record_stride(n));
+    const unsigned dst_f = smem_u32(R), dst_b = smem_u32(R + cc_offset(n));
 
-    if (steps > 0) stage_step(buf, V, 0, slice, mixed, lane);
+    if (lane == 0) {
+        mbar_init(bar_f);
+        mbar_init(bar_b);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    if (lane == 0 && steps > 0) {
+        bulk_load(dst_f, V.rec(slice, 0), fwd_bytes, bar_f);
+        bulk_load(dst_b, V.rec(slice, 0) + cc_offset(n), back_bytes, bar_b);
+        if (steps > 1) prefetch_l2(V.rec(slice, 1), rec_bytes);
+    }
     double reg[RR > 0 ? RR : 1];
 #pragma unroll
     for (int i = 0; i < RR; ++i) reg[i] = (i == k) ? 1.0 : 0.0;  // e_k (all zero for k >= n)
     for (int i = RR; i < n; ++i) st[(i - RR) * 32] = (i == k) ? 1.0 : 0.0;
 
     bool bad = false;
-    int cur = 0;
+    unsigned dmin = 0x7fffffffu;
+#ifdef PINT_HEAT_PROF
+    unsigned long long prof[6] = {0, 0, 0, 0, 0, 0};
+    long long t_prev = clock64();
+#endif
     for (long long s = 0; s < steps; ++s) {
-        if (s + 1 < steps) {
-            stage_step(buf + (cur ^ 1) * SD, V, s + 1, slice, mixed, lane);
-            asm volatile("cp.async.wait_group 1;\n" ::);
-        } else {
-            asm volatile("cp.async.wait_group 0;\n" ::);
+        const unsigned parity = static_cast<unsigned>(s & 1);
+        mbar_wait(bar_f, parity);  // this step's forward half has landed
+        HEAT_PROF_MARK(0);
+        double dm1;
+        const double d = mixed ? column_forward<RR, true, kGuard>(reg, st, R, n, f, lo, rng, bad, dm1)
+                               : column_forward<RR, false, kGuard>(reg, st, R, n, f, lo, rng, bad, dm1);
+        dmin = min(dmin, hi_abs(d));  // row n-1 (the back pass starts at n-2)
+        HEAT_PROF_MARK(1);
+        __syncwarp();  // every lane is done with the forward half
+        if (lane == 0 && s + 1 < steps) bulk_load(dst_f, V.rec(slice, s + 1), fwd_bytes, bar_f);
+        mbar_wait(bar_b, parity);
+        HEAT_PROF_MARK(2);
+        column_back<RR>(reg, st, R, n, d, dm1, dmin);
+        HEAT_PROF_MARK(3);
+        __syncwarp();  // every lane is done with the back half
+        if (lane == 0 && s + 1 < steps) {
+            bulk_load(dst_b, V.rec(slice, s + 1) + cc_offset(n), back_bytes, bar_b);
+            if (s + 2 < steps) prefetch_l2(V.rec(slice, s + 2), rec_bytes);
         }
-        __syncwarp();  // step s's record visible to every lane
-        if (mixed) column_step<RR, true, kGuard>(reg, st, buf + cur * SD, n, f, forced_lane, bad);
-        else column_step<RR, false, kGuard>(reg, st, buf + cur * SD, n, f, forced_lane, bad);
-        __syncwarp();  // buffer `cur` is refilled next iteration
-        cur ^= 1;
+        HEAT_PROF_MARK(4);
     }
+#ifdef PINT_HEAT_PROF
+    if (lane == 0 && blockIdx.x < (1 << 14))
+        for (int q = 0; q < 5; ++q) g_heat_prof[blockIdx.x][q] = prof[q];
+#endif
     if (k <= n) {
         double* gp = P.maps + static_cast<long long>(slice) * n * P.ldm + k;
 #pragma unroll
         for (int i = 0; i < RR; ++i) gp[i * P.ldm] = reg[i];
         for (int i = RR; i < n; ++i) gp[i * P.ldm] = st[(i - RR) * 32];
     }
+    // basis lanes: every dividend was >= 2^(dmin exponent) — below 2^-960 means retry guarded
+    if (!kGuard && k < n && steps > 0 && dmin < (63u << 20)) bad = true;
     if (bad) record_failure(P.fail, slice, PINT_E_RANGE_RETRY, static_cast<double>(n));
     if (P.per_slice_ns && lane == 0) atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
 }
@@ -325,20 +414,24 @@ __global__ void __launch_bounds__(32) heat_integrate_kernel(IntegratePlan P) {
     for (int i = lane; i < n; i += 32) sx[i] = P.sx[i];
     for (int i = 0; i < n; ++i) st[i * 32] = active ? P.y[col * n + i] : 0.0;
     __syncwarp();
-    const RecView V = rec_view(P.rec, n, 1, P.S);
+    const RecView V = rec_view(P.rec, n, P.S);
     const bool forcing = P.with_forcing != 0;
     for (long long s = P.s0; s < P.s0 + P.steps; ++s) {
-        const double negr = __ldg(V.negr + s);
+        const double* R = V.rec(0, s);
+        const double2* PR = reinterpret_cast<const double2*>(R + 2);
+        const double* HB = R + hb_offset(n);
+        const double* CC = R + cc_offset(n);
+        const double negr = __ldg(R);
         double d = 0.0;
         for (int i = 0; i < n; ++i) {
             double x = st[i * 32];
-            if (forcing) x = __dadd_rn(x, __ldg(V.hb + V.row(s, i, 0)));  // state += h*b (pde_problems.cpp:93)
+            if (forcing) x = __dadd_rn(x, __ldg(HB + i));  // state += h*b (pde_problems.cpp:93)
             const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
-            d = div_guarded(num, __ldg(V.pr + V.row(s, i, 0)));
+            d = div_guarded(num, __ldg(PR + i));
             st[i * 32] = d;
         }
         for (int i = n - 2; i >= 0; --i) {
-            d = __dsub_rn(st[i * 32], __dmul_rn(__ldg(V.cc + V.row(s, i, 0)), d));
+            d = __dsub_rn(st[i * 32], __dmul_rn(__ldg(CC + i), d));
             st[i * 32] = d;
         }
     }
@@ -354,7 +447,7 @@ void smem_attrs(K kern, size_t smem) {
 
 template <int RR, bool kGuard>
 int launch_build(pint_ctx* ctx, BuildPlan P) {
-    const size_t smem = sizeof(double) * (2 * staged_doubles(P.n) + static_cast<size_t>(P.n - RR) * 32);
+    const size_t smem = sizeof(double) * warp_smem_doubles(P.n, RR);
     if (smem > 227 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: n too large for shared memory");
     auto kern = heat_build_kernel<RR, kGuard>;
     smem_attrs(kern, smem);

@@ -20,7 +20,10 @@ __global__ void __launch_bounds__(256) fma_probe_kernel(int iters, R seed, R* si
     if (s == R(-1)) sink[threadIdx.x] = s;  // never true; keeps the chains alive
 }
 
-// Dependent-chain latency (cycles per op) of one warp: out = {DFMA, DADD, DMUL, FFMA, LDS.64}.
+// Dependent-chain latency of one warp, cycles per op: out = {DFMA, DADD, DMUL, FFMA, LDS.64};
+// then cycles per ROW of the heat build's two recurrences: out[5] = forward row
+// (x - negr*d, then the Markstein division: 5 dependent ops), out[6] = back row (y - c*d: 2 ops),
+// out[7] = alternating DMUL/DADD, per op.
 __global__ void latency_probe_kernel(double seed, double* sink, double* out, const double* table) {
     __shared__ double sh[64];
     sh[threadIdx.x] = table[threadIdx.x];
@@ -46,7 +49,27 @@ __global__ void latency_probe_kernel(double seed, double* sink, double* out, con
 #pragma unroll 64
     for (int i = 0; i < kOps; ++i) idx = static_cast<int>(sh[idx]) & 31;
     long long t5 = clock64();
+    a = a + static_cast<double>(idx);
+    const double negr = -0.3, p = 1.7, rcp = 1.0 / 1.7, c = -0.2;
+    double x = a;
+#pragma unroll 64
+    for (int i = 0; i < kOps; ++i) {
+        const double num = __dsub_rn(x, __dmul_rn(negr, a));
+        const double q0 = __dmul_rn(num, rcp);
+        const double rem = __fma_rn(-p, q0, num);
+        a = __fma_rn(rem, rcp, q0);
+    }
+    long long t6 = clock64();
+#pragma unroll 64
+    for (int i = 0; i < kOps; ++i) a = __dsub_rn(x, __dmul_rn(c, a));
+    long long t7 = clock64();
+#pragma unroll 64
+    for (int i = 0; i < kOps; ++i) a = (i & 1) ? __dadd_rn(a, 1e-9) : __dmul_rn(a, 0.999999);
+    long long t8 = clock64();
     if (threadIdx.x == 0) {
+        out[5] = double(t6 - t5) / kOps;
+        out[6] = double(t7 - t6) / kOps;
+        out[7] = double(t8 - t7) / kOps;
         out[0] = double(t1 - t0) / kOps;
         out[1] = double(t2 - t1) / kOps;
         out[2] = double(t3 - t2) / kOps;
@@ -58,14 +81,14 @@ __global__ void latency_probe_kernel(double seed, double* sink, double* out, con
 
 }  // namespace
 
-extern "C" int pint_probe_latency(pint_ctx* ctx, double* cycles /* 5 */) {
+extern "C" int pint_probe_latency(pint_ctx* ctx, double* cycles /* 8 */) {
     if (!ctx || !cycles) return PINT_E_INVALID;
     double* d = static_cast<double*>(pint_scratch(ctx, 3, 4096));
     if (!d) return PINT_E_CUDA;
     cudaMemsetAsync(d, 0, 4096, ctx->stream);  // table of zeros: the LDS chain reads sh[0]
     latency_probe_kernel<<<1, 32, 0, ctx->stream>>>(1.0, d + 256, d + 128, d);
     if (const int rc = pint_check_launch(ctx, "latency_probe_kernel")) return rc;
-    if (cudaMemcpyAsync(cycles, d + 128, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+    if (cudaMemcpyAsync(cycles, d + 128, 8 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
         cudaStreamSynchronize(ctx->stream) != cudaSuccess)
         return pint_set_error(ctx, PINT_E_CUDA, "latency probe failed");
     return PINT_OK;

@@ -1,0 +1,73 @@
+// Section timing of heat_build_kernel (clock64 marks compiled in with -DPINT_HEAT_PROF): per warp,
+// cycles per step in {wait fwd half, forward, stage+wait back half, back, stage next}.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -DPINT_HEAT_PROF -std=c++17 \
+//        -Iinclude -Ipaper_1304_6514_b200/csrc tools/heat_micro.cu -o tools/_heat_micro
+//   tools/_heat_micro n N S
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_1304_6514_b200/csrc/heat.cu"
+
+int pint_set_error(pint_ctx*, int code, const std::string& msg) {
+    std::fprintf(stderr, "error %d: %s\n", code, msg.c_str());
+    return code;
+}
+int pint_check_launch(pint_ctx*, const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) std::fprintf(stderr, "%s: %s\n", what, cudaGetErrorString(e));
+    return e == cudaSuccess ? 0 : PINT_E_CUDA;
+}
+void* pint_scratch(pint_ctx*, int, size_t) { return nullptr; }
+extern "C" int64_t pint_affine_ldm(int64_t n) { return (n + 1 + 3) / 4 * 4; }
+
+int main(int argc, char** argv) {
+    const int n = argc > 1 ? std::atoi(argv[1]) : 128;
+    const int N = argc > 2 ? std::atoi(argv[2]) : 1;
+    const int S = argc > 3 ? std::atoi(argv[3]) : 256;
+    const long long Q = static_cast<long long>(N) * S;
+    std::vector<int64_t> off(N + 1);
+    for (int j = 0; j <= N; ++j) off[j] = static_cast<int64_t>(j) * S;
+    std::vector<double> dt(N, 1e-4), r(Q), fa(Q), fb(Q), sx(n);
+    for (long long q = 0; q < Q; ++q) r[q] = 2.5 + 0.001 * (q % 7), fa[q] = -0.3, fb[q] = 0.7;
+    for (int i = 0; i < n; ++i) sx[i] = std::sin(M_PI * (i + 1) / (n + 1));
+    int64_t* d_off;
+    double *d_dt, *d_r, *d_fa, *d_fb, *d_sx, *d_rec, *d_maps;
+    cudaMalloc(&d_off, sizeof(int64_t) * (N + 1));
+    cudaMalloc(&d_dt, 8 * N);
+    cudaMalloc(&d_r, 8 * Q);
+    cudaMalloc(&d_fa, 8 * Q);
+    cudaMalloc(&d_fb, 8 * Q);
+    cudaMalloc(&d_sx, 8 * n);
+    cudaMemcpy(d_off, off.data(), sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice);
+    cudaMemcpy(d_dt, dt.data(), 8 * N, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_r, r.data(), 8 * Q, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_fa, fa.data(), 8 * Q, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_fb, fb.data(), 8 * Q, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_sx, sx.data(), 8 * n, cudaMemcpyHostToDevice);
+    cudaMalloc(&d_rec, 8 * records_doubles(n, N, S));
+    const long long ldm = pint_affine_ldm(n);
+    cudaMalloc(&d_maps, 8 * ldm * n * N);
+    pint_ctx ctx;
+    cudaMalloc(&ctx.d_fail, sizeof(FailRec));
+    cudaMemset(ctx.d_fail, 0xff, sizeof(FailRec));
+    if (launch_heat_factor(&ctx, n, N, S, d_off, d_dt, d_r, d_fa, d_fb, d_sx, d_rec)) return 1;
+    for (int rep = 0; rep < 2; ++rep)
+        if (launch_heat_build(&ctx, n, N, S, d_off, d_dt, d_rec, d_sx, d_maps, nullptr, 0)) return 1;
+    cudaDeviceSynchronize();
+    const int wps = (n + 1 + 31) / 32;
+    std::vector<unsigned long long> prof(static_cast<size_t>(1 << 14) * 6);
+    cudaMemcpyFromSymbol(prof.data(), g_heat_prof, prof.size() * 8);
+    const char* names[5] = {"wait_fwd", "forward", "stage_wait_back", "back", "stage_next"};
+    for (int w = 0; w < wps && w < (1 << 14); ++w) {
+        std::printf("warp %d:", w);
+        unsigned long long tot = 0;
+        for (int q = 0; q < 5; ++q) {
+            std::printf(" %s=%.0f", names[q], double(prof[w * 6 + q]) / S);
+            tot += prof[w * 6 + q];
+        }
+        std::printf("  total/step=%.0f  per-row=%.1f\n", double(tot) / S, double(tot) / S / n);
+    }
+    return 0;
+}

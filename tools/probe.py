@@ -13,7 +13,7 @@ ctx = capi.Context(0)
 p64, p32 = C.c_double(), C.c_double()
 ctx.check(ctx.lib.pint_probe_peak(ctx.h, capi.F64, C.byref(p64)))
 ctx.check(ctx.lib.pint_probe_peak(ctx.h, capi.F32, C.byref(p32)))
-lat = np.zeros(5)
+lat = np.zeros(8)
 ctx.check(ctx.lib.pint_probe_latency(ctx.h, capi.ptr(lat)))
 print(json.dumps({"fp64_fma_tflops": p64.value, "fp32_fma_tflops": p32.value,
-                  "latency_cycles": dict(zip(["dfma", "dadd", "dmul", "ffma", "lds64"], lat.tolist()))}))
+                  "latency_cycles": dict(zip(["dfma", "dadd", "dmul", "ffma", "lds64", "heat_forward_row", "heat_back_row", "dmul_dadd_alt"], lat.tolist()))}))
