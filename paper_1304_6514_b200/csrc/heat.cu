@@ -30,7 +30,14 @@ namespace {
 
 using pint_dev::record_failure;
 
-constexpr int kRegRows = 56;  // rows of each basis column held in registers (n >= kRegRows + 2)
+constexpr int kRegRows = 56;
+// PINT_E_RANGE_RETRY is recorded at kRetryIndex + (slice or step): above every task index, so a
+// real failure (a zero pivot at step q) always wins the lowest-index race and is never masked.
+constexpr long long kRetryIndex = 1ll << 62;
+// The fast division is exact for dividends in [2^-960, 2^997]. Upper side: with r <= 2^40 and
+// |h*b| <= 2^900 (checked by heat_record_kernel) every state stays below 2^990 (each step map is
+// a max-norm contraction). Lower side: every quotient q is checked against 2^-950 (zero allowed).
+constexpr unsigned kQuotLo = (1023u - 950u) << 20;  // |hi word| of 2^-950  // rows of each basis column held in registers (n >= kRegRows + 2)
 
 __host__ __device__ constexpr long long even(long long x) { return (x + 1) & ~1ll; }
 
@@ -56,47 +63,75 @@ struct RecView {
 
 __host__ __device__ inline RecView rec_view(const double* base, int n, long long S) { return RecView{base, S, n}; }
 
-// Thread (j, s): step s of slice j — the Thomas forward pivots of tridiag(-r, 1+2r, -r)
+// Thread t = (j, s): step s of slice j — the Thomas forward pivots of tridiag(-r, 1+2r, -r)
 // (linalg.cpp:80-90, with sub = sup = -r, diag = 1 + 2r as solve_implicit builds them), and the
 // forcing increment h * b_i with b_i = fa*s_i + fb*s_i = heat_forcing(x_i, t) (pde_problems.cpp:
-// 26-29, 91-94), rounded exactly as `state[i] += dt_step * b[i]` consumes it. Consecutive threads
-// write consecutive records, so every 32-byte sector is filled by one thread's stores.
-__global__ void heat_record_kernel(int n, long long N, long long S, const int64_t* __restrict__ step_off,
-                                   const double* __restrict__ slice_dt, const double* __restrict__ r_tab,
-                                   const double* __restrict__ fa, const double* __restrict__ fb,
-                                   const double* __restrict__ sx, double* __restrict__ rec, FailRec* fail) {
+// 26-29, 91-94), rounded exactly as `state[i] += dt_step * b[i]` consumes it. The pivot
+// recurrence is sequential in i, so a thread owns a record; rows are produced in chunks of
+// kRecChunk into shared memory and leave as coalesced segments: per record and chunk, ONE warp
+// store writes the 16 (p, rcp) doubles, the 8 h*b and the 8 c doubles (three full sectors runs).
+constexpr int kRecChunk = 8;
+constexpr int kRecLane = 4 * kRecChunk + 1;  // padded per-lane stride (doubles)
+
+__global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, long long S,
+                                                          const int64_t* __restrict__ step_off,
+                                                          const double* __restrict__ slice_dt,
+                                                          const double* __restrict__ r_tab,
+                                                          const double* __restrict__ fa, const double* __restrict__ fb,
+                                                          const double* __restrict__ sx, double* __restrict__ rec,
+                                                          FailRec* fail) {
+    __shared__ double buf[4][32 * kRecLane];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= S * N) return;
+    const long long t0 = t - lane;  // the warp's first record
     const long long j = t / S, s = t - j * S;
-    const long long q = step_off[j] + s;
-    if (q >= step_off[j + 1]) return;  // slice j has fewer steps
-    double* R = rec + t * record_stride(n);
-    double2* pr_out = reinterpret_cast<double2*>(R + 2);
-    double* hb_out = R + hb_offset(n);
-    double* cc_out = R + cc_offset(n);
-    const double r = r_tab[q];
+    const bool live = t < S * N && step_off[j] + s < step_off[j + 1];  // slice j may have fewer steps
+    const long long q = live ? step_off[j] + s : 0;
+    const unsigned live_mask = __ballot_sync(0xffffffffu, live);
+    double* mine = buf[w] + lane * kRecLane;
+    const double r = live ? r_tab[q] : 0.0;
     const double negr = -r;                                  // pde_problems.cpp:55
     const double diag = __dadd_rn(1.0, __dmul_rn(2.0, r));   // 1.0 + 2.0 * r
-    R[0] = negr;
-    R[1] = 0.0;
-    double p = diag;  // pivot = diag[0]; c[0] = sup[0] / pivot (linalg.cpp:80-83)
-    if (p == 0.0) record_failure(fail, q, PINT_E_SINGULAR, 0.0);
-    double c = (n > 1) ? __ddiv_rn(negr, p) : 0.0;
-    pr_out[0] = make_double2(p, __drcp_rn(p));
-    cc_out[0] = c;
-    for (int i = 1; i < n; ++i) {  // pivot = diag - sub*c[i-1]; c[i] = sup / pivot (:84-88)
-        p = __dsub_rn(diag, __dmul_rn(negr, c));
-        if (p == 0.0) record_failure(fail, q, PINT_E_SINGULAR, static_cast<double>(i));
-        c = (i < n - 1) ? __ddiv_rn(negr, p) : 0.0;
-        pr_out[i] = make_double2(p, __drcp_rn(p));
-        cc_out[i] = c;
+    const double h = live ? slice_dt[j] : 0.0, fq = live ? fa[q] : 0.0, gq = live ? fb[q] : 0.0;
+    if (live && !(r >= 0.0 && r <= 0x1p40)) record_failure(fail, kRetryIndex + q, PINT_E_RANGE_RETRY, r);
+    unsigned hb_max = 0;
+    if (live) {
+        double* R = rec + t * record_stride(n);
+        R[0] = negr;
+        R[1] = 0.0;
+        if (n & 1) R[hb_offset(n) + n] = 0.0, R[cc_offset(n) + n] = 0.0;
     }
-    const double h = slice_dt[j], fq = fa[q], gq = fb[q];
-    for (int i = 0; i < n; ++i) {
-        const double si = sx[i];
-        hb_out[i] = __dmul_rn(h, __dadd_rn(__dmul_rn(fq, si), __dmul_rn(gq, si)));
+    double p = diag, c = 0.0;
+    for (int i0 = 0; i0 < n; i0 += kRecChunk) {
+        const int rows = min(kRecChunk, n - i0);
+        for (int u = 0; u < rows; ++u) {
+            const int i = i0 + u;
+            if (i > 0) p = __dsub_rn(diag, __dmul_rn(negr, c));  // pivot = diag - sub*c[i-1] (:84-88)
+            if (live && p == 0.0) record_failure(fail, q, PINT_E_SINGULAR, static_cast<double>(i));
+            c = (i < n - 1) ? __ddiv_rn(negr, p) : 0.0;           // c[i] = sup / pivot
+            const double si = sx[i];
+            mine[4 * u + 0] = p;
+            mine[4 * u + 1] = __drcp_rn(p);
+            const double hb = __dmul_rn(h, __dadd_rn(__dmul_rn(fq, si), __dmul_rn(gq, si)));
+            hb_max = max(hb_max, static_cast<unsigned>(__double2hiint(hb)) & 0x7fffffffu);
+            mine[4 * u + 2] = hb;
+            mine[4 * u + 3] = c;
+        }
+        __syncwarp();
+        // this lane's slot in every record of the chunk: (p, rcp) element `lane` (lanes 0-15), h*b
+        // row lane-16 (16-23) or c row lane-24 (24-31)
+        const int k = lane & 7, half = (lane >> 3) & 1;
+        const long long off = lane < 16 ? 2 + 2 * i0 + lane : (half ? cc_offset(n) : hb_offset(n)) + i0 + k;
+        const int soff = lane < 16 ? 4 * (lane >> 1) + (lane & 1) : 4 * k + 2 + half;
+        const bool valid = lane < 16 ? lane < 2 * rows : k < rows;
+        double* dst = rec + t0 * record_stride(n) + off;
+        const double* src = buf[w] + soff;
+#pragma unroll 4
+        for (int l = 0; l < 32; ++l, dst += record_stride(n), src += kRecLane)  // record t0 + l
+            if (valid && ((live_mask >> l) & 1u)) *dst = *src;
+        __syncwarp();
     }
-    if (n & 1) hb_out[n] = 0.0, cc_out[n] = 0.0;
+    if (live && hb_max >= ((1023u + 900u) << 20)) record_failure(fail, kRetryIndex + q, PINT_E_RANGE_RETRY, 0.0);
 }
 
 __device__ __forceinline__ double div_fast(double x, double2 pr) {
@@ -182,20 +217,14 @@ __device__ __forceinline__ unsigned hi_abs(double x) {
 // exactly x on every basis lane (f = 0). Rows [0, RR) in reg[], the rest at st[32*(i-RR)],
 // software-pipelined kFwdAhead rows ahead (every load is issued before the stores in front of it:
 // the compiler cannot hoist a shared load above a shared store it cannot disambiguate). The
-// forced lane's dividends are range-checked off the chain: (|hi| - lo) > rng with lo/rng the
-// Markstein window on that lane and a never-true window elsewhere (LOP3 + IADD + ISETP.OR).
-// Returns q_{n-1}; dm1 = q_{n-2}.
+// quotients are range-checked by column_back, off the chain. Returns q_{n-1}; dm1 = q_{n-2}.
 template <int RR, bool kMixed, bool kGuard>
 __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1], double* st, const double* R,
-                                                 int n, double f, unsigned lo, unsigned rng, bool& bad,
-                                                 double& dm1) {
+                                                 int n, double f, double& dm1) {
     const double negr = R[0];
     const double2* PR = reinterpret_cast<const double2*>(R + 2);
     const double* HB = R + hb_offset(n);
-    auto divide = [&](double num, double2 pr) {
-        if (kMixed && !kGuard) bad = bad | ((hi_abs(num) - lo) > rng);
-        return kGuard ? div_guarded(num, pr) : div_fast(num, pr);
-    };
+    auto divide = [&](double num, double2 pr) { return kGuard ? div_guarded(num, pr) : div_fast(num, pr); };
     // RR == 0: row 0 goes through the generic x - negr*d with d = -0.0, where negr*d is +0 (negr
     // <= 0) and x - (+0) == x bit-for-bit (even for x = -0), so the loop needs no row-0 select
     double d = -0.0;
@@ -244,12 +273,12 @@ __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1],
 }
 
 // Back substitution of one step (linalg.cpp:91): d_i = q_i - c_i d_{i+1}, shared rows pipelined
-// kBackAhead rows ahead, then the register rows. dmin tracks min |hi word| of every basis value:
-// all dividends of the next step are >= it, which is how basis lanes are
-// range-checked at one IMNMX per row.
+// kBackAhead rows ahead, then the register rows. qmin tracks min(|hi word of q_i| - 1) over the
+// forward quotients it reads anyway (zero wraps to the maximum, so exact zeros pass): a quotient
+// below 2^-950 means its dividend may have left Markstein's range (one VIADDMNMX per row).
 template <int RR>
 __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], double* st, const double* R, int n,
-                                            double d, double dm1, unsigned& dmin) {
+                                            double d, double dm1, unsigned& qmin) {
     const double* CC = R + cc_offset(n);
     const int top = n - 2 - RR;  // first shared row of the back pass
     if (top >= 0) {
@@ -262,9 +291,9 @@ __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], doub
         }
         // ring slot u holds row r - u (see column_forward)
         auto row = [&](int rr, double y, double c) {
+            qmin = min(qmin, hi_abs(y) - 1u);
             d = __dsub_rn(y, __dmul_rn(c, d));
             st[32 * rr] = d;
-            dmin = min(dmin, hi_abs(d));
         };
         int r = top;
 #pragma unroll 1
@@ -283,9 +312,9 @@ __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], doub
 #pragma unroll
     for (int i = RR - 1; i >= 0; --i) {
         if (i > n - 2) continue;  // (RR > 0 implies n >= RR + 2: never taken)
+        qmin = min(qmin, hi_abs(reg[i]) - 1u);
         d = __dsub_rn(reg[i], __dmul_rn(CC[i], d));
         reg[i] = d;
-        dmin = min(dmin, hi_abs(d));
     }
 }
 
@@ -323,8 +352,6 @@ __global__ void __maxnreg__(168) heat_build_kernel(BuildPlan P) {
     const bool forced_lane = (k == n);
     const bool mixed = (g == n / 32);  // the warp holding column n
     const double f = forced_lane ? 1.0 : 0.0;
-    const unsigned lo = forced_lane ? (63u << 20) : 0u;
-    const unsigned rng = forced_lane ? ((2021u - 63u) << 20) - 1u : 0xffffffffu;
     const long long steps = P.step_off[slice + 1] - P.step_off[slice];
     const RecView V = rec_view(P.rec, n, P.S);
     const unsigned fwd_bytes = 8u * static_cast<unsigned>(mixed ? cc_offset(n) : hb_offset(n));
@@ -348,8 +375,7 @@ __global__ void __maxnreg__(168) heat_build_kernel(BuildPlan P) {
     for (int i = 0; i < RR; ++i) reg[i] = (i == k) ? 1.0 : 0.0;  // e_k (all zero for k >= n)
     for (int i = RR; i < n; ++i) st[(i - RR) * 32] = (i == k) ? 1.0 : 0.0;
 
-    bool bad = false;
-    unsigned dmin = 0x7fffffffu;
+    unsigned qmin = 0xffffffffu;
 #ifdef PINT_HEAT_PROF
     unsigned long long prof[6] = {0, 0, 0, 0, 0, 0};
     long long t_prev = clock64();
@@ -359,15 +385,15 @@ __global__ void __maxnreg__(168) heat_build_kernel(BuildPlan P) {
         mbar_wait(bar_f, parity);  // this step's forward half has landed
         HEAT_PROF_MARK(0);
         double dm1;
-        const double d = mixed ? column_forward<RR, true, kGuard>(reg, st, R, n, f, lo, rng, bad, dm1)
-                               : column_forward<RR, false, kGuard>(reg, st, R, n, f, lo, rng, bad, dm1);
-        dmin = min(dmin, hi_abs(d));  // row n-1 (the back pass starts at n-2)
+        const double d = mixed ? column_forward<RR, true, kGuard>(reg, st, R, n, f, dm1)
+                               : column_forward<RR, false, kGuard>(reg, st, R, n, f, dm1);
+        qmin = min(qmin, hi_abs(d) - 1u);  // q_{n-1} (the back pass starts at row n-2)
         HEAT_PROF_MARK(1);
         __syncwarp();  // every lane is done with the forward half
         if (lane == 0 && s + 1 < steps) bulk_load(dst_f, V.rec(slice, s + 1), fwd_bytes, bar_f);
         mbar_wait(bar_b, parity);
         HEAT_PROF_MARK(2);
-        column_back<RR>(reg, st, R, n, d, dm1, dmin);
+        column_back<RR>(reg, st, R, n, d, dm1, qmin);
         HEAT_PROF_MARK(3);
         __syncwarp();  // every lane is done with the back half
         if (lane == 0 && s + 1 < steps) {
@@ -386,9 +412,7 @@ __global__ void __maxnreg__(168) heat_build_kernel(BuildPlan P) {
         for (int i = 0; i < RR; ++i) gp[i * P.ldm] = reg[i];
         for (int i = RR; i < n; ++i) gp[i * P.ldm] = st[(i - RR) * 32];
     }
-    // basis lanes: every dividend was >= 2^(dmin exponent) — below 2^-960 means retry guarded
-    if (!kGuard && k < n && steps > 0 && dmin < (63u << 20)) bad = true;
-    if (bad) record_failure(P.fail, slice, PINT_E_RANGE_RETRY, static_cast<double>(n));
+    if (!kGuard && qmin < kQuotLo - 1u) record_failure(P.fail, kRetryIndex + slice, PINT_E_RANGE_RETRY, 0.0);
     if (P.per_slice_ns && lane == 0) atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
 }
 

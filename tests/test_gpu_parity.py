@@ -311,6 +311,33 @@ def test_heat_config2_shape(ctx):
     assert r.traj_steps == N * S * 129
 
 
+def test_heat_underflow_retries_guarded(ctx):
+    """dt = 1e-9 at n = 128: r ~ 2e-5, so a basis column decays like r^|i-k| and runs through the
+    subnormal range inside the first step. The fast build must notice (range check off the chain
+    -> PINT_E_RANGE_RETRY) and the guarded build must then match the reference bit-for-bit."""
+    import torch
+
+    from paper_1304_6514_b200.dist import HeatPlan
+
+    dx, dt, T, N = 1.0 / 129.0, 1e-9, 6e-9, 2
+    plan = HeatPlan(ctx, dx, dt, T, N)
+    plan.upload()
+    plan.factor_and_build()
+    torch.cuda.synchronize()
+    assert plan.verify() is False and plan.guarded == 1  # the fast path flagged itself
+    plan.factor_and_build()
+    torch.cuda.synchronize()
+    assert plan.verify() is True
+    n, ldm = plan.n, plan.ldm
+    maps = plan.maps.view(N, n, ldm).cpu().numpy()
+    dec = pint.decompose(0.0, T, N, dt)
+    for j in range(N):
+        s = dec.slices[j]
+        Gw, cw = O.heat_build(dx, s.t_begin, s.t_end, dt)
+        assert np.count_nonzero((Gw != 0) & (np.abs(Gw) < 2.3e-308)) > 0  # subnormals really occur
+        assert np.array_equal(maps[j, :, :n], Gw) and np.array_equal(maps[j, :, n], cw)
+
+
 def test_affine_tree_random_maps(ctx):
     rng = np.random.default_rng(1304)
     for N, n in [(1, 5), (2, 9), (13, 9), (64, 128), (7, 200)]:
