@@ -41,11 +41,14 @@ constexpr unsigned kQuotLo = (1023u - 950u) << 20;  // |hi word| of 2^-950  // r
 
 __host__ __device__ constexpr long long even(long long x) { return (x + 1) & ~1ll; }
 
-// One (slice, step) record, doubles: [negr, pad] | (p_i, rcp_i) x n | h*b_i x even(n) | c_i x even(n).
-// The forward half (negr, p, rcp [, h*b]) and the back half (c) are each a 16-byte multiple.
-__host__ __device__ constexpr long long record_stride(long long n) { return 2 + 2 * n + 2 * even(n); }
-__host__ __device__ constexpr long long hb_offset(long long n) { return 2 + 2 * n; }
-__host__ __device__ constexpr long long cc_offset(long long n) { return 2 + 2 * n + even(n); }
+// One (slice, step) record, doubles, every block a whole number of 128-byte lines (so the record
+// kernel writes whole sectors and the bulk copies are aligned): [negr, 0 x 15] | (p_i, rcp_i) x n16 |
+// h*b_i x n16 | c_i x n16, n16 = n rounded up to 16. Forward half = header + (p, rcp) [+ h*b].
+__host__ __device__ constexpr long long n16(long long n) { return (n + 15) & ~15ll; }
+__host__ __device__ constexpr long long pr_offset() { return 16; }
+__host__ __device__ constexpr long long hb_offset(long long n) { return 16 + 2 * n16(n); }
+__host__ __device__ constexpr long long cc_offset(long long n) { return 16 + 3 * n16(n); }
+__host__ __device__ constexpr long long record_stride(long long n) { return 16 + 4 * n16(n); }
 
 // doubles needed for the records of N slices x S steps x n rows: [N][S][record]
 __host__ __device__ constexpr long long records_doubles(long long n, long long N, long long S) {
@@ -62,6 +65,19 @@ struct RecView {
 };
 
 __host__ __device__ inline RecView rec_view(const double* base, int n, long long S) { return RecView{base, S, n}; }
+
+__device__ __forceinline__ double div_fast(double x, double2 pr) {
+    const double q0 = __dmul_rn(x, pr.y);
+    const double rem = __fma_rn(-pr.x, q0, x);
+    return __fma_rn(rem, pr.y, q0);
+}
+
+__device__ __forceinline__ bool out_of_range(double x) {
+    // |x| bits of the high word, window test on the biased exponent: true for zero, subnormal,
+    // |x| < 2^-960, |x| >= 2^998, inf and nan (LOP3 + IADD + ISETP)
+    const unsigned a = static_cast<unsigned>(__double2hiint(x)) & 0x7fffffffu;
+    return a - (63u << 20) > ((2021u - 63u) << 20) - 1u;
+}
 
 // Thread t = (j, s): step s of slice j — the Thomas forward pivots of tridiag(-r, 1+2r, -r)
 // (linalg.cpp:80-90, with sub = sup = -r, diag = 1 + 2r as solve_implicit builds them), and the
@@ -95,11 +111,10 @@ __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, lo
     const double h = live ? slice_dt[j] : 0.0, fq = live ? fa[q] : 0.0, gq = live ? fb[q] : 0.0;
     if (live && !(r >= 0.0 && r <= 0x1p40)) record_failure(fail, kRetryIndex + q, PINT_E_RANGE_RETRY, r);
     unsigned hb_max = 0;
+    const bool fast_c = r >= 0x1p-960 && r <= 0x1p40;
     if (live) {
         double* R = rec + t * record_stride(n);
-        R[0] = negr;
-        R[1] = 0.0;
-        if (n & 1) R[hb_offset(n) + n] = 0.0, R[cc_offset(n) + n] = 0.0;
+        reinterpret_cast<double4*>(R)[0] = make_double4(negr, 0.0, 0.0, 0.0);
     }
     double p = diag, c = 0.0;
     for (int i0 = 0; i0 < n; i0 += kRecChunk) {
@@ -108,10 +123,13 @@ __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, lo
             const int i = i0 + u;
             if (i > 0) p = __dsub_rn(diag, __dmul_rn(negr, c));  // pivot = diag - sub*c[i-1] (:84-88)
             if (live && p == 0.0) record_failure(fail, q, PINT_E_SINGULAR, static_cast<double>(i));
-            c = (i < n - 1) ? __ddiv_rn(negr, p) : 0.0;           // c[i] = sup / pivot
+            const double rcp = __drcp_rn(p);
+            // c[i] = sup / pivot: the Markstein division with the reciprocal the record carries
+            // anyway when r in [2^-960, 2^40] (then p in [1 + r, 1 + 2r], |c| < 1: exact), IEEE otherwise
+            c = (i < n - 1) ? (fast_c ? div_fast(negr, make_double2(p, rcp)) : __ddiv_rn(negr, p)) : 0.0;
             const double si = sx[i];
             mine[4 * u + 0] = p;
-            mine[4 * u + 1] = __drcp_rn(p);
+            mine[4 * u + 1] = rcp;
             const double hb = __dmul_rn(h, __dadd_rn(__dmul_rn(fq, si), __dmul_rn(gq, si)));
             hb_max = max(hb_max, static_cast<unsigned>(__double2hiint(hb)) & 0x7fffffffu);
             mine[4 * u + 2] = hb;
@@ -121,30 +139,25 @@ __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, lo
         // this lane's slot in every record of the chunk: (p, rcp) element `lane` (lanes 0-15), h*b
         // row lane-16 (16-23) or c row lane-24 (24-31)
         const int k = lane & 7, half = (lane >> 3) & 1;
-        const long long off = lane < 16 ? 2 + 2 * i0 + lane : (half ? cc_offset(n) : hb_offset(n)) + i0 + k;
+        const long long off = lane < 16 ? pr_offset() + 2 * i0 + lane : (half ? cc_offset(n) : hb_offset(n)) + i0 + k;
         const int soff = lane < 16 ? 4 * (lane >> 1) + (lane & 1) : 4 * k + 2 + half;
         const bool valid = lane < 16 ? lane < 2 * rows : k < rows;
-        double* dst = rec + t0 * record_stride(n) + off;
-        const double* src = buf[w] + soff;
-#pragma unroll 4
-        for (int l = 0; l < 32; ++l, dst += record_stride(n), src += kRecLane)  // record t0 + l
-            if (valid && ((live_mask >> l) & 1u)) *dst = *src;
+        const unsigned mask = valid ? live_mask : 0u;
+        // 16 shared loads in flight, then 16 stores (a store holds its source register until the
+        // LSU drains it, so a load/store ping-pong on one register would serialise on that)
+#pragma unroll
+        for (int l0 = 0; l0 < 32; l0 += 16) {
+            double v[16];
+#pragma unroll
+            for (int l = 0; l < 16; ++l) v[l] = buf[w][soff + (l0 + l) * kRecLane];
+            double* dst = rec + (t0 + l0) * record_stride(n) + off;
+#pragma unroll
+            for (int l = 0; l < 16; ++l)
+                if ((mask >> (l0 + l)) & 1u) dst[l * record_stride(n)] = v[l];  // record t0 + l0 + l
+        }
         __syncwarp();
     }
     if (live && hb_max >= ((1023u + 900u) << 20)) record_failure(fail, kRetryIndex + q, PINT_E_RANGE_RETRY, 0.0);
-}
-
-__device__ __forceinline__ double div_fast(double x, double2 pr) {
-    const double q0 = __dmul_rn(x, pr.y);
-    const double rem = __fma_rn(-pr.x, q0, x);
-    return __fma_rn(rem, pr.y, q0);
-}
-
-__device__ __forceinline__ bool out_of_range(double x) {
-    // |x| bits of the high word, window test on the biased exponent: true for zero, subnormal,
-    // |x| < 2^-960, |x| >= 2^998, inf and nan (LOP3 + IADD + ISETP)
-    const unsigned a = static_cast<unsigned>(__double2hiint(x)) & 0x7fffffffu;
-    return a - (63u << 20) > ((2021u - 63u) << 20) - 1u;
 }
 
 __device__ __forceinline__ double div_guarded(double x, double2 pr) {
@@ -222,7 +235,7 @@ template <int RR, bool kMixed, bool kGuard>
 __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1], double* st, const double* R,
                                                  int n, double f, double& dm1) {
     const double negr = R[0];
-    const double2* PR = reinterpret_cast<const double2*>(R + 2);
+    const double2* PR = reinterpret_cast<const double2*>(R + pr_offset());
     const double* HB = R + hb_offset(n);
     auto divide = [&](double num, double2 pr) { return kGuard ? div_guarded(num, pr) : div_fast(num, pr); };
     // RR == 0: row 0 goes through the generic x - negr*d with d = -0.0, where negr*d is +0 (negr
@@ -442,7 +455,7 @@ __global__ void __launch_bounds__(32) heat_integrate_kernel(IntegratePlan P) {
     const bool forcing = P.with_forcing != 0;
     for (long long s = P.s0; s < P.s0 + P.steps; ++s) {
         const double* R = V.rec(0, s);
-        const double2* PR = reinterpret_cast<const double2*>(R + 2);
+        const double2* PR = reinterpret_cast<const double2*>(R + pr_offset());
         const double* HB = R + hb_offset(n);
         const double* CC = R + cc_offset(n);
         const double negr = __ldg(R);
