@@ -311,6 +311,28 @@ def test_heat_config2_shape(ctx):
     assert r.traj_steps == N * S * 129
 
 
+def test_heat_config4_shape_n512(ctx):
+    """Config 4's state size (n = 512, dx = 1/513, 2 MiB maps) at S = 4 on a few slices: maps
+    bit-exact against the oracle, chain bit-exact, tree within 1e-12 (the 8-GPU split itself is
+    covered by tests/test_dist_gloo.py)."""
+    N, S = 6, 4
+    dx, dt = 1.0 / 513.0, 10.0 / (4096 * S)
+    T = N * S * dt
+    prob = pint.make_heat_problem(dx, dt, T)
+    dec = pint.decompose(0.0, T, N, dt)
+    G, c = pint.build_affine_propagators(prob, dec)
+    assert G.shape == (N, 512, 512)
+    for j in (0, N - 1):
+        s = dec.slices[j]
+        Gw, cw = O.heat_build(dx, s.t_begin, s.t_end, dt)
+        assert np.array_equal(G[j], Gw) and np.array_equal(c[j], cw)
+    y_chain = O.affine_chain(G, c, prob.y0)
+    r = pint.run_nievergelt(prob, N, pint.ExecConfig())
+    assert np.array_equal(r.final_state, y_chain)
+    rt = pint.run_nievergelt(prob, N, pint.ExecConfig(), compose="tree")
+    assert np.max(np.abs(rt.final_state - y_chain)) / np.max(np.abs(y_chain)) <= REL_F64
+
+
 def test_heat_underflow_retries_guarded(ctx):
     """dt = 1e-9 at n = 128: r ~ 2e-5, so a basis column decays like r^|i-k| and runs through the
     subnormal range inside the first step. The fast build must notice (range check off the chain

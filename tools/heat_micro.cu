@@ -60,14 +60,26 @@ int main(int argc, char** argv) {
     std::vector<unsigned long long> prof(static_cast<size_t>(1 << 14) * 6);
     cudaMemcpyFromSymbol(prof.data(), g_heat_prof, prof.size() * 8);
     const char* names[5] = {"wait_fwd", "forward", "stage_wait_back", "back", "stage_next"};
-    for (int w = 0; w < wps && w < (1 << 14); ++w) {
-        std::printf("warp %d:", w);
-        unsigned long long tot = 0;
-        for (int q = 0; q < 5; ++q) {
-            std::printf(" %s=%.0f", names[q], double(prof[w * 6 + q]) / S);
-            tot += prof[w * 6 + q];
+    // mean over the warps of each role (g < wps-1: basis warps, g == wps-1: the forced column's)
+    for (int role = 0; role < 2; ++role) {
+        double acc[5] = {0, 0, 0, 0, 0}, worst = 0;
+        int cnt = 0;
+        for (int b = 0; b < N * wps && b < (1 << 14); ++b) {
+            const int g = b % wps;
+            if ((g == wps - 1) != (role == 1)) continue;
+            double tot = 0;
+            for (int q = 0; q < 5; ++q) acc[q] += prof[b * 6 + q], tot += prof[b * 6 + q];
+            worst = tot > worst ? tot : worst;
+            ++cnt;
         }
-        std::printf("  total/step=%.0f  per-row=%.1f\n", double(tot) / S, double(tot) / S / n);
+        if (!cnt) continue;
+        std::printf("%s warps (%d):", role ? "forced-column" : "basis", cnt);
+        double tot = 0;
+        for (int q = 0; q < 5; ++q) {
+            std::printf(" %s=%.0f", names[q], acc[q] / cnt / S);
+            tot += acc[q] / cnt;
+        }
+        std::printf("  per-row=%.1f (worst warp %.1f)\n", tot / S / n, worst / S / n);
     }
     return 0;
 }
