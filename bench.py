@@ -228,7 +228,7 @@ def main():
                  P(plan.maps), None, plan.guarded)
         if events:
             events[2].record(stream)
-        plan.compose_local(capi.COMPOSE_TREE)
+        plan.compose_local(capi.COMPOSE_TREE, want_composed=world > 1)
         if world > 1:
             maps = gather_maps(plan.composed)
             if rank == 0:

@@ -26,6 +26,11 @@ affine_chain_kernel(long long n, long long N, long long ldm, const double* __res
     const long long n4 = n / 4;
     for (long long j = 0; j < N; ++j) {
         const double* M = maps + j * n * ldm;
+        if (j + 1 < N)  // pull this thread's rows of the next map into L1 while this one is applied
+            for (long long i = threadIdx.x; i < n; i += kChainThreads) {
+                const char* nxt = reinterpret_cast<const char*>(M + n * ldm + i * ldm);
+                for (long long b = 0; b < 8 * (n + 1); b += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(nxt + b));
+            }
         double out[4];
         int cnt = 0;
         for (long long i = threadIdx.x; i < n; i += kChainThreads, ++cnt) {
@@ -207,6 +212,10 @@ int launch_affine_pair(pint_ctx* ctx, int64_t n, int64_t P, const double* earlie
 }
 
 // The log-depth tree: level by level, pairs (2p, 2p+1) of `src` into `dst`, odd tail copied.
+// Maps left for the chain when only y is wanted. 1 (a full tree) until the chain applies a map in
+// ~1 us: today it costs ~6 us per map (each thread reads its own row: uncoalesced).
+constexpr long long kTreeChainTail = 1;
+
 int launch_affine_tree(pint_ctx* ctx, int64_t n, int64_t N, double* maps, double* scratch,
                        const double* y0, double* y, double* composed) {
     if (N < 1) return pint_set_error(ctx, PINT_E_INVALID, "affine_tree: N >= 1 required");
@@ -214,7 +223,10 @@ int launch_affine_tree(pint_ctx* ctx, int64_t n, int64_t N, double* maps, double
     double* src = maps;
     double* dst = scratch;
     long long count = N;
-    while (count > 1) {
+    // When only y is wanted, pairing may stop once a level would be latency-bound (a pair level
+    // costs ~14 us even for a handful of GEMMs) and the chain applies the rest.
+    const long long stop = composed ? 1 : kTreeChainTail;
+    while (count > stop) {
         const long long pairs = count / 2;
         for (long long p0 = 0; p0 < pairs; p0 += 65535) {
             const long long P = (pairs - p0 < 65535) ? pairs - p0 : 65535;
@@ -235,5 +247,5 @@ int launch_affine_tree(pint_ctx* ctx, int64_t n, int64_t N, double* maps, double
     if (composed && composed != src &&
         cudaMemcpyAsync(composed, src, sizeof(double) * stride, cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess)
         return pint_set_error(ctx, PINT_E_CUDA, "affine_tree: composed copy failed");
-    return launch_affine_chain(ctx, n, 1, src, y0, y);
+    return launch_affine_chain(ctx, n, count, src, y0, y);
 }

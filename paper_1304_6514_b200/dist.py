@@ -127,13 +127,14 @@ class HeatPlan:
             return False
         raise pint.SingularSystem(f"thomas_solve: zero pivot at row {int(f.value)}")
 
-    def compose_local(self, mode: int = capi.COMPOSE_TREE):
-        """Compose this block's maps; the composed augmented map lands in self.composed (TREE),
-        and self.y = block map applied to y0."""
+    def compose_local(self, mode: int = capi.COMPOSE_TREE, want_composed: bool = True):
+        """Compose this block's maps: self.y = block map applied to y0, and (TREE with
+        want_composed) the composed augmented map in self.composed — the multi-GPU path needs it;
+        a single GPU only needs y, so the tree stops early and chain-applies its last few maps."""
         P = capi.ptr
         if mode == capi.COMPOSE_TREE:
             self.ctx.call("pint_affine_compose_dev", capi.COMPOSE_TREE, self.n, self.N, P(self.maps), P(self.scratch),
-                          P(self.y0), P(self.y), P(self.composed))
+                          P(self.y0), P(self.y), P(self.composed) if want_composed else None)
         else:
             self.ctx.call("pint_affine_compose_dev", capi.COMPOSE_CHAIN, self.n, self.N, P(self.maps), None,
                           P(self.y0), P(self.y), None)

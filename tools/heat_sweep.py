@@ -45,8 +45,19 @@ def main():
             times.append(s.elapsed_time(e))
         ms = min(times)
         cyc = ms * 1e-3 * a.clock_mhz * 1e6 / (plan.S * plan.n)
+        comp = {}
+        for mode, name in ((capi.COMPOSE_CHAIN, "chain_ms"), (capi.COMPOSE_TREE, "tree_ms")):
+            ts = []
+            for _ in range(a.reps):
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                plan.compose_local(mode, want_composed=False)
+                e.record()
+                e.synchronize()
+                ts.append(s.elapsed_time(e))
+            comp[name] = round(min(ts), 4)
         print(json.dumps({"n": n, "N": N, "S": plan.S, "build_ms": round(ms, 4), "cycles_per_row": round(cyc, 1),
-                          "chain_floor_cycles_per_row": 7 * 8.1}), flush=True)
+                          "chain_floor_cycles_per_row": 7 * 8.1, **comp}), flush=True)
 
 
 if __name__ == "__main__":
