@@ -1,8 +1,12 @@
 // K4 — composition of affine slice maps y -> G y + c.
 //
-//  * CHAIN (bit-exact): compose_sweep (nievergelt.cpp:90-110) as one CTA walking the slices in
-//    order; thread i owns row i and accumulates sum_k G(i,k) y_k sequentially in k exactly like
-//    matvec (linalg.cpp:17-26), then adds c_i. Rows are read as 32 B vectors.
+//  * CHAIN (bit-exact): compose_sweep (nievergelt.cpp:90-110) walking the slices in order; the
+//    owner of row i accumulates sum_k G(i,k) y_k sequentially in k exactly like matvec
+//    (linalg.cpp:17-26), then adds c_i. For n <= 256: a cluster of ceil(n/32) single-warp CTAs,
+//    CTA r owning rows 32r..32r+31 (lane = row); each CTA's 32-row block of the next two maps is
+//    bulk-copied into shared memory ahead of use (the block is contiguous in the row-major map),
+//    and the new y is exchanged through distributed shared memory with one cluster barrier per
+//    map. Larger n: one CTA, rows read from global.
 //  * TREE (EXTENSION, north_star subsystem 3): log-depth pairwise products
 //        (G2, c2) o (G1, c1) = (G2 G1, G2 c1 + c2)
 //    on FP64 tensor cores: mma.sync m8n8k4 f64 (SASS DMMA) with 64x64 CTA tiles staged through
@@ -10,9 +14,15 @@
 //
 // Maps are the row-major augmented blocks [G | c] with leading dimension ldm (pint_cuda.h).
 // Roofline: TREE is FP64 tensor (2 n^3 flops per pair); CHAIN is latency/L2 bound.
+#include <cooperative_groups.h>
+
 #include "pint_internal.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace {
+
+using namespace pint_async;
 
 constexpr int kChainThreads = 256;
 
@@ -54,6 +64,124 @@ affine_chain_kernel(long long n, long long N, long long ldm, const double* __res
         __syncthreads();
     }
     for (long long i = threadIdx.x; i < n; i += kChainThreads) y[i] = y_s[i];
+}
+
+// Cluster chain (n <= 256). Dynamic smem: rows[kRing][32][ldm] | y[2][ny] | pad | kRing map barriers
+// | 2 y barriers,
+// ny = n rounded up to 16 (16-byte aligned y pairs; the pipeline may read 16 doubles past n). A
+// CTA's 32 rows of a map are one contiguous block: one bulk copy per map.
+constexpr int kClusterMax = 8;
+constexpr int kChainAhead = 8;  // pairs of terms in flight per lane
+constexpr int kRing = 4;        // maps in flight (bulk-copy latency ~ 2 map applications)
+
+__global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long long N, int ldm,
+                                                                  const double* __restrict__ maps,
+                                                                  const double* __restrict__ y0,
+                                                                  double* __restrict__ y) {
+    extern __shared__ __align__(16) double sm[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const unsigned rank = cluster.block_rank();
+    const unsigned csize = cluster.num_blocks();
+    const int lane = threadIdx.x;
+    const int r0 = 32 * static_cast<int>(rank), rows = min(32, n - r0);
+    const int ny = (n + 15) & ~15;
+    double* blk = sm;                       // [kRing][32][ldm]
+    double* ys = sm + kRing * 32 * ldm;     // [2][ny] + look-ahead pad
+    const unsigned bar0 = smem_u32(ys + 2 * ny + 4 * kChainAhead);  // kRing map barriers
+    const unsigned ybar0 = bar0 + 8u * kRing;                         // 2 y barriers
+    const long long mstride = static_cast<long long>(n) * ldm;
+    const unsigned blk_bytes = 8u * static_cast<unsigned>(ldm) * static_cast<unsigned>(rows);
+    if (lane == 0) {
+        for (int b = 0; b < kRing + 2; ++b) mbar_init(bar0 + 8u * b);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    const bool mine = lane < rows;
+    auto fetch = [&](long long j, int b) {  // this CTA's rows of map j (contiguous) into block b
+        if (lane == 0)
+            bulk_load(smem_u32(blk + b * 32 * ldm), maps + j * mstride + static_cast<long long>(r0) * ldm, blk_bytes,
+                      bar0 + 8u * b);
+    };
+    for (long long j = 0; j < kRing && j < N; ++j) fetch(j, static_cast<int>(j));
+    for (int i = lane; i < 2 * ny + 4 * kChainAhead; i += 32) ys[i] = (i < n) ? y0[i] : 0.0;
+    cluster.sync();  // every CTA's barriers and y buffers are initialised before any remote write
+    const int pairs = n / 2;
+#ifdef PINT_CHAIN_PROF
+    long long tw = 0, tc = 0, tf = 0, ts = 0, t0 = clock64();
+#define CHAIN_MARK(v)                   \
+    do {                                \
+        const long long t1 = clock64(); \
+        v += t1 - t0;                   \
+        t0 = t1;                        \
+    } while (0)
+#else
+#define CHAIN_MARK(v) \
+    do {              \
+    } while (0)
+#endif
+    for (long long j = 0; j < N; ++j) {
+        const int b = static_cast<int>(j % kRing), yb = static_cast<int>(j & 1);
+        mbar_wait(bar0 + 8u * b, static_cast<unsigned>((j / kRing) & 1));
+        CHAIN_MARK(tw);
+        const double2* g2 = reinterpret_cast<const double2*>(blk + (b * 32 + lane) * ldm);
+        const double2* y2 = reinterpret_cast<const double2*>(ys + yb * ny);
+        double s = 0.0;
+        // sum_k G(i,k) y_k in k order (matvec), loads kChainAhead pairs ahead of the DADD chain
+        double2 gv[kChainAhead], yv[kChainAhead];
+#pragma unroll
+        for (int u = 0; u < kChainAhead; ++u) gv[u] = g2[u], yv[u] = y2[u];
+        int q = 0;
+#pragma unroll 1
+        for (; q + kChainAhead <= pairs; q += kChainAhead) {
+#pragma unroll
+            for (int u = 0; u < kChainAhead; ++u) {
+                s = __dadd_rn(s, __dmul_rn(gv[u].x, yv[u].x));
+                s = __dadd_rn(s, __dmul_rn(gv[u].y, yv[u].y));
+                gv[u] = g2[q + u + kChainAhead];
+                yv[u] = y2[q + u + kChainAhead];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kChainAhead - 1; ++u)
+            if (q + u < pairs) {
+                s = __dadd_rn(s, __dmul_rn(gv[u].x, yv[u].x));
+                s = __dadd_rn(s, __dmul_rn(gv[u].y, yv[u].y));
+            }
+        const double* g = blk + (b * 32 + lane) * ldm;
+        if (n & 1) s = __dadd_rn(s, __dmul_rn(g[n - 1], ys[yb * ny + n - 1]));
+        s = __dadd_rn(s, g[n]);  // + c_i
+        CHAIN_MARK(tc);
+        __syncwarp();  // block b fully read: refill it with map j + kRing
+        if (j + kRing < N) fetch(j + kRing, b);
+        // y_{j+1}: every CTA's rows land in every CTA's buffer yb^1 via st.async, each completing
+        // its bytes on that CTA's y barrier (n * 8 bytes expected per map)
+        const unsigned ybar = ybar0 + 8u * (yb ^ 1);
+        if (lane == 0)
+            asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(ybar),
+                         "r"(8u * static_cast<unsigned>(n))
+                         : "memory");
+        if (mine) {
+            const unsigned la = smem_u32(ys + (yb ^ 1) * ny + r0 + lane);
+            for (unsigned c = 0; c < csize; ++c) {
+                unsigned ra, rb;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(la), "r"(c));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(ybar), "r"(c));
+                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(ra),
+                             "d"(s), "r"(rb)
+                             : "memory");
+            }
+        }
+        CHAIN_MARK(tf);
+        mbar_wait(ybar, static_cast<unsigned>((j >> 1) & 1));  // y_{j+1} complete here
+        CHAIN_MARK(ts);
+    }
+#ifdef PINT_CHAIN_PROF
+    if (lane == 0)
+        printf("rank %u: per map wait %lld compute %lld fetch+store %lld sync %lld cycles\n", rank, tw / N, tc / N,
+               tf / N, ts / N);
+#endif
+    if (mine) y[r0 + lane] = ys[(N & 1) * ny + r0 + lane];
+    cluster.sync();  // no CTA leaves while a peer may still write into its shared memory
 }
 
 // ---- DMMA pair kernel ------------------------------------------------------------------------
@@ -199,6 +327,31 @@ int launch_pairs(pint_ctx* ctx, long long n, long long P, const double* earlier,
 int launch_affine_chain(pint_ctx* ctx, int64_t n, int64_t N, const double* maps, const double* y0,
                         double* y) {
     if (n < 1 || N < 0) return pint_set_error(ctx, PINT_E_INVALID, "affine_chain: bad sizes");
+    if (n <= 32 * kClusterMax && N > 0) {
+        const int ldm = static_cast<int>(pint_affine_ldm(n));
+        const size_t ny = static_cast<size_t>((n + 15) & ~15);
+        const size_t smem = sizeof(double) * (kRing * 32 * static_cast<size_t>(ldm) + 2 * ny + 4 * kChainAhead) +
+                            8 * (kRing + 2);
+        cudaFuncSetAttribute(affine_chain_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        const unsigned C = static_cast<unsigned>((n + 31) / 32);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(C, 1, 1);
+        cfg.blockDim = dim3(32, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, affine_chain_cluster_kernel, static_cast<int>(n), static_cast<long long>(N), ldm,
+                               maps, y0, y) != cudaSuccess)
+            return pint_check_launch(ctx, "affine_chain_cluster_kernel");
+        return pint_check_launch(ctx, "affine_chain_cluster_kernel");
+    }
     if (n > 4 * kChainThreads) return pint_set_error(ctx, PINT_E_INVALID, "affine_chain: n > 1024 unsupported");
     const size_t smem = sizeof(double) * static_cast<size_t>(n);
     affine_chain_kernel<<<1, kChainThreads, smem, ctx->stream>>>(n, N, pint_affine_ldm(n), maps, y0, y);
@@ -212,9 +365,9 @@ int launch_affine_pair(pint_ctx* ctx, int64_t n, int64_t P, const double* earlie
 }
 
 // The log-depth tree: level by level, pairs (2p, 2p+1) of `src` into `dst`, odd tail copied.
-// Maps left for the chain when only y is wanted. 1 (a full tree) until the chain applies a map in
-// ~1 us: today it costs ~6 us per map (each thread reads its own row: uncoalesced).
-constexpr long long kTreeChainTail = 1;
+// Maps left for the chain when only y is wanted: a pair level costs >= ~14 us even for a handful
+// of GEMMs, the cluster chain ~1.5 us per map (n = 128), so the last 4 levels become a chain.
+constexpr long long kTreeChainTail = 16;
 
 int launch_affine_tree(pint_ctx* ctx, int64_t n, int64_t N, double* maps, double* scratch,
                        const double* y0, double* y, double* composed) {

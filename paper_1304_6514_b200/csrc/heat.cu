@@ -29,6 +29,7 @@
 namespace {
 
 using pint_dev::record_failure;
+using namespace pint_async;
 
 constexpr int kRegRows = 56;
 // PINT_E_RANGE_RETRY is recorded at kRetryIndex + (slice or step): above every task index, so a
@@ -164,9 +165,6 @@ __device__ __forceinline__ double div_guarded(double x, double2 pr) {
     return out_of_range(x) ? __ddiv_rn(x, pr.x) : div_fast(x, pr);
 }
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
 
 
 struct BuildPlan {
@@ -195,31 +193,6 @@ __host__ __device__ constexpr long long warp_smem_doubles(long long n, int RR) {
     return front_pad(n) + record_stride(n) + (n - RR) * 32 + 32 * kFwdAhead + 2;
 }
 
-__device__ __forceinline__ void mbar_init(unsigned bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
-    unsigned done;
-    do {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-// One thread: arm `bar` for `bytes` and bulk-copy them global -> shared (completes on `bar`).
-__device__ __forceinline__ void bulk_load(unsigned dst, const double* src, unsigned bytes, unsigned bar) {
-    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(bar),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(bar)
-                 : "memory");
-}
-__device__ __forceinline__ void prefetch_l2(const double* src, unsigned bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
-}
 
 __device__ __forceinline__ unsigned hi_abs(double x) {
     return static_cast<unsigned>(__double2hiint(x)) & 0x7fffffffu;
