@@ -1,4 +1,4 @@
-"""Slice-block sharding of the heat (affine) path across GPUs — north_star subsystem (4).
+"""Slice-block sharding across GPUs — north_star subsystem (4), SURVEY.md §8e.
 
 One process per GPU (torch.distributed, NCCL over NVLink on the box, gloo in CPU tests). Rank g
 owns the contiguous slice block [floor(gN/W), floor((g+1)N/W)) of the reference decomposition
@@ -10,6 +10,16 @@ applies the W maps to y0 in rank order with the bit-exact chain.
 
 This replaces the reference's simulated wire (inject_latency + counters, nievergelt.cpp:95-101):
 message_count stays N-1 in the RunReport sense; the real exchange is W-1 map transfers.
+
+Nonlinear composition (scalar C1/C5, 2-D Lotka-Volterra C3) is sequential by nature — a
+composition of interpolants has no closed form — so the blocks build their slice tables in
+parallel (K1, no collective) and the sweep runs in one of the two ways §8e names:
+  * gather_rows: the endpoint tables of every block to rank 0 (C1/C5: 64 x 1024 doubles =
+    512 KiB), which sweeps all N slices (K2) — one collective;
+  * lambda_chain: the paper's hand-off of the running value (C3, whose tables
+    are 448 MiB): rank g receives the value leaving block g-1, sweeps its own block, sends the
+    result on — W-1 messages of 1-2 doubles.
+Both give results bit-identical to the single-GPU sweep (same slices, same order).
 """
 from __future__ import annotations
 
@@ -173,8 +183,170 @@ def sharded_heat_step(plan: HeatPlan, group=None) -> None:
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
         return
+    plan.ctx.sync()  # the maps are produced on the context's stream; the collective runs on torch's
     maps = gather_maps(plan.composed, group)
     if dist.get_rank(group) == 0:
         cat = torch.cat(maps)
         apply_chain(plan.ctx, plan.n, cat, plan.y0, plan.y)
 
+
+
+# ---- nonlinear composition across ranks ---------------------------------------
+
+def block_sizes(N: int, world: int) -> List[int]:
+    return [b - a for a, b in (slice_block(N, world, r) for r in range(world))]
+
+
+def gather_rows(local, N: int, group=None, root: int = 0):
+    """Gather every rank's contiguous block of per-slice rows (local: [rows, ...]) to `root` in
+    slice order. Blocks differ by at most one slice, so each rank pads to the largest block;
+    ONE gather; root trims and concatenates. Returns the [N, ...] tensor on root, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    sizes = block_sizes(N, world)
+    if local.shape[0] != sizes[rank]:
+        raise ValueError(f"rank {rank}: {local.shape[0]} rows, block holds {sizes[rank]}")
+    pad = torch.zeros((max(sizes),) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    bufs = [torch.empty_like(pad) for _ in range(world)] if rank == root else None
+    dist.gather(pad, bufs, dst=root, group=group)
+    if rank != root:
+        return None
+    return torch.cat([b[:n] for b, n in zip(bufs, sizes)])
+
+
+def lambda_chain(sweep_block, lam0, group=None):
+    """The paper's hand-off for nonlinear maps: rank g receives the value leaving block g-1
+    (rank 0 starts from lam0), applies its own block with sweep_block(lam) -> lam, sends the
+    result to g+1. The final value (leaving the last block) is broadcast to every rank."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    lam = lam0.clone()
+    if rank > 0:
+        dist.recv(lam, src=rank - 1, group=group)
+    out = sweep_block(lam).clone()
+    if rank < world - 1:
+        dist.send(out, dst=rank + 1, group=group)
+    dist.broadcast(out, src=world - 1, group=group)
+    return out
+
+
+class ScalarPlan:
+    """Device plan for the slice block [lo, hi) of a scalar Nievergelt run (C1/C5): the K1
+    ensemble of the block's N_local x M trajectories (pint_scalar_ensemble_dev), and — on the
+    rank that holds all N tables — the weights and the sweep (pint_bary_weights_dev,
+    pint_scalar_sweep_dev), exactly as pint_run_scalar sequences them (capi.cu)."""
+
+    def __init__(self, ctx: capi.Context, rhs: capi.ScalarRHS, t0: float, T: float, y0: float, N: int,
+                 dt: float, M: int, a: float, b: float, node_kind: int = capi.NODES_SECOND_KIND,
+                 weight_kind: int = capi.WEIGHTS_PRODUCT, sweep_mode: int = capi.SWEEP_EXACT,
+                 lo: int = 0, hi: Optional[int] = None):
+        import torch
+
+        hi = N if hi is None else hi
+        self.ctx, self.rhs, self.y0, self.N, self.M, self.a, self.b = ctx, rhs, y0, N, M, a, b
+        self.weight_kind, self.sweep_mode, self.lo, self.hi = weight_kind, sweep_mode, lo, hi
+        dec = pint.decompose(t0, T, N, dt)
+        steps, dts = pint.slice_table(dec)
+        dev = f"cuda:{ctx.device}"
+        self.steps = torch.as_tensor(steps[lo:hi]).to(dev)
+        self.dt = torch.as_tensor(dts[lo:hi]).to(dev)
+        kind = pint.FIRST_KIND if node_kind == capi.NODES_FIRST_KIND else pint.SECOND_KIND
+        self.nodes = torch.as_tensor(pint.sample_nodes(kind, M, a, b)).to(dev)
+        self.ab = torch.tensor([a, b], dtype=torch.float64, device=dev)
+        self.ends = torch.empty((hi - lo, M), dtype=torch.float64, device=dev)
+
+    def build(self):
+        """Launch the block's ensemble on the context's stream (asynchronous)."""
+        P = capi.ptr
+        self.ctx.call("pint_scalar_ensemble_dev", C.byref(self.rhs), self.hi - self.lo, self.M, P(self.steps),
+                      P(self.dt), P(self.nodes), P(self.ends), None)
+
+    def sweep(self, tables) -> Tuple[float, "object", int]:
+        """Sweep all N slice tables ([N, M] on this device) from y0: (y, lambdas[N], extrapolations)."""
+        import torch
+
+        P = capi.ptr
+        dev = tables.device
+        w = torch.empty(self.M, dtype=torch.float64, device=dev)
+        lam = torch.empty(self.N, dtype=torch.float64, device=dev)
+        y = torch.empty(1, dtype=torch.float64, device=dev)
+        ext = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.ctx.call("pint_bary_weights_dev", self.weight_kind, self.M, P(self.nodes), P(w))
+        self.ctx.call("pint_scalar_sweep_dev", self.sweep_mode, self.N, self.M, P(self.nodes), 0, P(w),
+                      P(tables), P(self.ab), P(self.ab[1:]), 0, self.y0, P(lam), P(y), P(ext))
+        self.ctx.sync()
+        return float(y.item()), lam, int(ext.item())
+
+
+def sharded_scalar_run(plan: ScalarPlan, group=None):
+    """C1/C5 on W GPUs: every rank builds its block's tables; the tables are gathered to rank 0,
+    which sweeps. Returns (y, lambdas, extrapolations) on rank 0, None elsewhere."""
+    import torch.distributed as dist
+
+    plan.build()
+    plan.ctx.sync()  # the tables are produced on the context's stream; the collective runs on torch's
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return plan.sweep(plan.ends)
+    tables = gather_rows(plan.ends, plan.N, group)
+    return plan.sweep(tables) if dist.get_rank(group) == 0 else None
+
+
+class LVPlan:
+    """Device plan for the slice block [lo, hi) of the 2-D Lotka-Volterra run (C3, EXTENSION):
+    the block's tensor-grid RK4 tables (pint_lv_ensemble_dev) and the block's bilinear sweep
+    (pint_bilinear_sweep_dev) from an incoming value."""
+
+    def __init__(self, ctx: capi.Context, params, T: float, N: int, S: int, un, vn, lo: int = 0,
+                 hi: Optional[int] = None):
+        import torch
+
+        hi = N if hi is None else hi
+        self.ctx, self.N, self.lo, self.hi = ctx, N, lo, hi
+        dec = pint.decompose(0.0, T, N, T / (N * S))
+        steps, dts = pint.slice_table(dec)
+        dev = f"cuda:{ctx.device}"
+        self.steps = torch.as_tensor(steps[lo:hi]).to(dev)
+        self.dt = torch.as_tensor(dts[lo:hi]).to(dev)
+        self.un = torch.as_tensor(np.ascontiguousarray(un, np.float64)).to(dev)
+        self.vn = torch.as_tensor(np.ascontiguousarray(vn, np.float64)).to(dev)
+        self.params = np.ascontiguousarray(params, np.float64)
+        self.tables = torch.empty((hi - lo) * 2 * len(un) * len(vn), dtype=torch.float64, device=dev)
+        self.lam = torch.empty(2 * (hi - lo), dtype=torch.float64, device=dev)
+        self.br = torch.empty(2 * (hi - lo), dtype=torch.int64, device=dev)
+        self.ext = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def build(self):
+        P = capi.ptr
+        self.ctx.call("pint_lv_ensemble_dev", self.hi - self.lo, len(self.un), len(self.vn), P(self.steps), P(self.dt),
+                      P(self.un), P(self.vn), P(self.params), P(self.tables))
+
+    def sweep_block(self, lam):
+        """Apply this block's bilinear maps in order from lam = (u, v); returns the value leaving it."""
+        P = capi.ptr
+        u0, v0 = (float(x) for x in lam.cpu())
+        self.ctx.call("pint_bilinear_sweep_dev", self.hi - self.lo, len(self.un), len(self.vn), P(self.un), P(self.vn),
+                      P(self.tables), u0, v0, P(self.lam), P(self.br), P(self.ext))
+        self.ctx.sync()
+        return self.lam.view(-1, 2)[-1].clone()
+
+
+def sharded_lv_run(plan: LVPlan, u0: float, v0: float, group=None):
+    """C3 on W GPUs: blocks build their tables in parallel; the running value crosses the ranks
+    once (lambda_chain). Returns the final (u, v) on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    plan.build()
+    plan.ctx.sync()
+    lam0 = torch.tensor([u0, v0], dtype=torch.float64, device=plan.lam.device)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return plan.sweep_block(lam0)
+    return lambda_chain(plan.sweep_block, lam0, group)

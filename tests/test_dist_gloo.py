@@ -79,3 +79,80 @@ def test_slice_blocks_partition(N_, W):
         assert b == c and a <= b
     sizes = [b - a for a, b in blocks]
     assert max(sizes) - min(sizes) <= 1
+
+
+# ---- nonlinear composition across ranks: the oracle stands in for K1/K2 --------
+
+def _scalar_worker(rank, world, port, out, N, M):
+    from paper_1304_6514_b200.dist import gather_rows
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _, _, steps, h = O.decompose(0.0, 0.5, N, 1e-4)
+        nodes = O.cheb_nodes(M, 0.0, 2.0)
+        lo, hi = slice_block(N, world, rank)
+        ends, fail, _ = O.riccati_ensemble(steps[lo:hi], h[lo:hi], nodes)
+        assert fail < 0
+        tables = gather_rows(torch.from_numpy(ends.copy()), N)
+        if rank == 0:
+            y, lam, ext = O.scalar_sweep(nodes, O.bary_weights(nodes), tables.numpy(), 0.0, 2.0, 1.0)
+            out["y"], out["lam"], out["ext"] = y, lam.tolist(), ext
+        else:
+            assert tables is None
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_scalar_tables_gather_then_sweep_is_bit_exact(world):
+    """C1/C5 across ranks: blocks of endpoint tables gathered to rank 0 (uneven blocks padded),
+    swept there: identical bits to the single-process pipeline."""
+    N, M = 7, 6
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_scalar_worker, args=(world, _free_port(), out, N, M), nprocs=world, join=True)
+    _, _, steps, h = O.decompose(0.0, 0.5, N, 1e-4)
+    nodes = O.cheb_nodes(M, 0.0, 2.0)
+    ends, _, _ = O.riccati_ensemble(steps, h, nodes)
+    y, lam, ext = O.scalar_sweep(nodes, O.bary_weights(nodes), ends, 0.0, 2.0, 1.0)
+    assert out["y"] == y and out["lam"] == lam.tolist() and out["ext"] == ext
+
+
+LV = (1.5, 1.0, 1.0, 3.0)
+
+
+def _lv_worker(rank, world, port, out, N, Mu, Mv, S):
+    from paper_1304_6514_b200.dist import lambda_chain
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _, _, steps, h = O.decompose(0.0, 10.0, N, 10.0 / (N * S))
+        un, vn = O.uniform_nodes(Mu, 0.1, 8.0), O.uniform_nodes(Mv, 0.1, 8.0)
+        lo, hi = slice_block(N, world, rank)
+        tables = O.lv_rk4_ensemble(steps[lo:hi], h[lo:hi], un, vn, LV)
+
+        def sweep_block(lam):
+            got, _, _ = O.bilinear_sweep(un, vn, tables, float(lam[0]), float(lam[1]))
+            return torch.from_numpy(got[-1].copy())
+
+        final = lambda_chain(sweep_block, torch.tensor([1.0, 1.0], dtype=torch.float64))
+        out[rank] = final.tolist()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_lv_lambda_chain_is_bit_exact(world):
+    """C3 across ranks: the running value crosses the ranks once (W-1 two-double messages);
+    every rank ends with the single-process sweep's final value, bit for bit."""
+    N, Mu, Mv, S = 8, 17, 13, 8
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_lv_worker, args=(world, _free_port(), out, N, Mu, Mv, S), nprocs=world, join=True)
+    _, _, steps, h = O.decompose(0.0, 10.0, N, 10.0 / (N * S))
+    un, vn = O.uniform_nodes(Mu, 0.1, 8.0), O.uniform_nodes(Mv, 0.1, 8.0)
+    lam, _, _ = O.bilinear_sweep(un, vn, O.lv_rk4_ensemble(steps, h, un, vn, LV), 1.0, 1.0)
+    for r in range(world):
+        assert out[r] == lam[-1].tolist()

@@ -497,3 +497,47 @@ def test_wave40_tree_within_tolerance(ctx, golden):
         ctx.check(ctx.lib.pint_run_wave(ctx.h, 39, capi.ptr(D2), dt, 16.0, 8, dt, mode, capi.ptr(w_y0),
                                         capi.ptr(out), None, C.byref(rep)))
     assert np.max(np.abs(yt - y)) <= 1e-10 * max(1.0, np.max(np.abs(y)))
+
+
+# ---- multi-GPU plans at world size 1 (the device half of dist.py; gloo tests cover the exchange)
+
+def test_scalar_plan_matches_run_scalar(ctx):
+    """dist.ScalarPlan + sharded_scalar_run (K1 on a block, K2 on the gathered tables) against
+    pint_run_scalar: same bits."""
+    from paper_1304_6514_b200.dist import ScalarPlan, sharded_scalar_run
+
+    N, M, dt = 64, 512, 0.5 / (64 * 79)
+    ivp = pint.make_model_problem()
+    rhs = ivp.device_rhs()
+    plan = ScalarPlan(ctx, rhs, ivp.t0, ivp.T, ivp.y0, N, dt, M, 0.0, 2.0)
+    y, lam, ext = sharded_scalar_run(plan)
+    r = pint.run_nievergelt(ivp, N, dt, pint.InitialValueSpace(M=M))
+    assert y == r.final_state
+    for lo, hi in ((0, 21), (21, 64)):  # two blocks of the same run: tables identical bits
+        part = ScalarPlan(ctx, rhs, ivp.t0, ivp.T, ivp.y0, N, dt, M, 0.0, 2.0, lo=lo, hi=hi)
+        part.build()
+        ctx.sync()
+        assert np.array_equal(part.ends.cpu().numpy(), plan.ends[lo:hi].cpu().numpy())
+
+
+def test_lv_plan_block_chain(ctx):
+    """dist.LVPlan: two blocks swept in turn (the lambda chain) == one sweep over all slices."""
+    import torch
+
+    from paper_1304_6514_b200.dist import LVPlan
+
+    N, Mu, Mv, S = 8, 17, 13, 8
+    un, vn = O.uniform_nodes(Mu, 0.1, 8.0), O.uniform_nodes(Mv, 0.1, 8.0)
+    full = LVPlan(ctx, LV, 10.0, N, S, un, vn)
+    full.build()
+    ctx.sync()
+    want = full.sweep_block(torch.tensor([1.0, 1.0], dtype=torch.float64)).cpu()
+    a, b = LVPlan(ctx, LV, 10.0, N, S, un, vn, 0, 3), LVPlan(ctx, LV, 10.0, N, S, un, vn, 3, N)
+    a.build()
+    b.build()
+    ctx.sync()
+    got = b.sweep_block(a.sweep_block(torch.tensor([1.0, 1.0], dtype=torch.float64))).cpu()
+    assert torch.equal(got, want)
+    _, _, st, h = O.decompose(0.0, 10.0, N, 10.0 / (N * S))
+    lam, _, _ = O.bilinear_sweep(un, vn, O.lv_rk4_ensemble(st, h, un, vn, LV), 1.0, 1.0)
+    assert want.tolist() == lam[-1].tolist()
