@@ -342,23 +342,23 @@ void or_affine_tree(double* G, double* c, int64_t N, int64_t n, const double* y0
 }
 
 /* ---- EXTENSION: RK4 logistic, y' = r y (1 - y/K). Op order:
- *   f(y) = (r*y) * fma(-iK, y, 1),  iK = 1/K
+ *   f(y) = y * fma(-rK, y, r),  rK = r/K  (one FMA + one multiply)
  *   k1 = f(y); k2 = f(fma(h/2, k1, y)); k3 = f(fma(h/2, k2, y)); k4 = f(fma(h, k3, y))
  *   y += h/6 * ((k1 + k4) + 2 (k2 + k3))  as fma(h6, fma(2, k2 + k3, k1 + k4), y) */
-static double logistic_f(double y, double r, double iK) { return (r * y) * fma(-iK, y, 1.0); }
+static double logistic_f(double y, double r, double rK) { return y * fma(-rK, y, r); }
 
 void or_logistic_rk4_ensemble(int64_t N, int64_t M, const int64_t* steps, const double* h,
                               const double* nodes, double r, double K, double* endpoints) {
-    const double iK = 1.0 / K;
+    const double rK = r / K;
     for (int64_t j = 0; j < N; ++j) {
         const double hh = h[j], h2 = 0.5 * hh, h6 = hh / 6.0;
         for (int64_t m = 0; m < M; ++m) {
             double y = nodes[m];
             for (int64_t s = 0; s < steps[j]; ++s) {
-                const double k1 = logistic_f(y, r, iK);
-                const double k2 = logistic_f(fma(h2, k1, y), r, iK);
-                const double k3 = logistic_f(fma(h2, k2, y), r, iK);
-                const double k4 = logistic_f(fma(hh, k3, y), r, iK);
+                const double k1 = logistic_f(y, r, rK);
+                const double k2 = logistic_f(fma(h2, k1, y), r, rK);
+                const double k3 = logistic_f(fma(h2, k2, y), r, rK);
+                const double k4 = logistic_f(fma(hh, k3, y), r, rK);
                 y = fma(h6, fma(2.0, k2 + k3, k1 + k4), y);
             }
             endpoints[j * M + m] = y;
@@ -366,20 +366,20 @@ void or_logistic_rk4_ensemble(int64_t N, int64_t M, const int64_t* steps, const 
     }
 }
 
-static float logistic_ff(float y, float r, float iK) { return (r * y) * fmaf(-iK, y, 1.0f); }
+static float logistic_ff(float y, float r, float rK) { return y * fmaf(-rK, y, r); }
 
 void or_logistic_rk4_ensemble_f32(int64_t N, int64_t M, const int64_t* steps, const double* h,
                                   const float* nodes, float r, float K, float* endpoints) {
-    const float iK = 1.0f / K;
+    const float rK = r / K;
     for (int64_t j = 0; j < N; ++j) {
         const float hh = (float)h[j], h2 = 0.5f * hh, h6 = hh / 6.0f;
         for (int64_t m = 0; m < M; ++m) {
             float y = nodes[m];
             for (int64_t s = 0; s < steps[j]; ++s) {
-                const float k1 = logistic_ff(y, r, iK);
-                const float k2 = logistic_ff(fmaf(h2, k1, y), r, iK);
-                const float k3 = logistic_ff(fmaf(h2, k2, y), r, iK);
-                const float k4 = logistic_ff(fmaf(hh, k3, y), r, iK);
+                const float k1 = logistic_ff(y, r, rK);
+                const float k2 = logistic_ff(fmaf(h2, k1, y), r, rK);
+                const float k3 = logistic_ff(fmaf(h2, k2, y), r, rK);
+                const float k4 = logistic_ff(fmaf(hh, k3, y), r, rK);
                 y = fmaf(h6, fmaf(2.0f, k2 + k3, k1 + k4), y);
             }
             endpoints[j * M + m] = y;

@@ -5,10 +5,14 @@
 // and per-step coefficients are bit-identical to what the reference computes inside its loops.
 // There is no CPU fallback anywhere: without a device every entry point returns an error.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -77,6 +81,79 @@ struct Pinned {
     size_t bytes = 0;
 };
 thread_local Pinned t_pinned;
+
+// Process-wide host worker pool for the per-step tables (glibc sin/cos must run on the host for
+// bit-parity): created once, so a run pays no thread start-up. parallel_for(n, fn) runs
+// fn(i0, i1) over [0, n) in up to `size` contiguous chunks and returns when all are done.
+class HostPool {
+  public:
+    static HostPool& get() {
+        static HostPool pool;
+        return pool;
+    }
+    unsigned size() const { return static_cast<unsigned>(workers_.size()) + 1; }
+    void parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& fn) {
+        const int64_t parts = std::min<int64_t>(n, size());
+        if (parts <= 1) {
+            fn(0, n);
+            return;
+        }
+        std::unique_lock<std::mutex> job_lock(job_mutex_);  // one parallel_for at a time
+        {
+            std::lock_guard<std::mutex> g(m_);
+            fn_ = &fn;
+            n_ = n;
+            parts_ = parts;
+            next_.store(1);
+            pending_ = parts - 1;
+            ++generation_;
+        }
+        cv_.notify_all();
+        fn(0, n / parts);  // the caller takes part 0
+        std::unique_lock<std::mutex> l(m_);
+        done_cv_.wait(l, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+
+  private:
+    HostPool() {
+        const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+        for (unsigned i = 1; i < hw; ++i) workers_.emplace_back([this] { run(); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+    void run() {
+        uint64_t seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> l(m_);
+            cv_.wait(l, [&] { return stop_ || generation_ != seen; });
+            if (stop_) return;
+            seen = generation_;
+            const auto* fn = fn_;
+            const int64_t n = n_, parts = parts_;
+            l.unlock();
+            for (int64_t k = next_.fetch_add(1); k < parts; k = next_.fetch_add(1)) {
+                (*fn)(n * k / parts, n * (k + 1) / parts);
+                std::lock_guard<std::mutex> g(m_);
+                if (--pending_ == 0) done_cv_.notify_one();
+            }
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex m_, job_mutex_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int64_t, int64_t)>* fn_ = nullptr;
+    int64_t n_ = 0, parts_ = 0, pending_ = 0;
+    std::atomic<int64_t> next_{0};
+    uint64_t generation_ = 0;
+    bool stop_ = false;
+};
 
 void* pinned(size_t bytes) {
     if (t_pinned.bytes < bytes) {
@@ -296,16 +373,8 @@ int pint_heat_coefficients(double dx, const pint_slice* slices, int64_t N, int64
             }
         }
     };
-    const int64_t total = step_off[N];
-    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-    if (total < 16384 || hw == 1 || N < 2) {
-        fill(0, N);
-    } else {
-        std::vector<std::thread> pool;
-        const int64_t per = (N + hw - 1) / hw;
-        for (int64_t j0 = 0; j0 < N; j0 += per) pool.emplace_back(fill, j0, std::min(N, j0 + per));
-        for (auto& t : pool) t.join();
-    }
+    if (step_off[N] < 4096 || N < 2) fill(0, N);
+    else HostPool::get().parallel_for(N, fill);
     if (sx)
         for (int64_t i = 0; i < n; ++i) sx[i] = std::sin(kPi * (static_cast<double>(i + 1) * dx));
     return PINT_OK;
