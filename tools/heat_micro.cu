@@ -3,6 +3,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -DPINT_HEAT_PROF -std=c++17 \
 //        -Iinclude -Ipaper_1304_6514_b200/csrc tools/heat_micro.cu -o tools/_heat_micro
 //   tools/_heat_micro n N S
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -50,23 +51,38 @@ int main(int argc, char** argv) {
     const long long ldm = pint_affine_ldm(n);
     cudaMalloc(&d_maps, 8 * ldm * n * N);
     pint_ctx ctx;
+    cudaStreamCreateWithFlags(&ctx.stream, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&ctx.side, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ctx.ev_fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx.ev_join, cudaEventDisableTiming);
     cudaMalloc(&ctx.d_fail, sizeof(FailRec));
     cudaMemset(ctx.d_fail, 0xff, sizeof(FailRec));
     if (launch_heat_factor(&ctx, n, N, S, d_off, d_dt, d_r, d_fa, d_fb, d_sx, d_rec)) return 1;
     for (int rep = 0; rep < 2; ++rep)
         if (launch_heat_build(&ctx, n, N, S, d_off, d_dt, d_rec, d_sx, d_maps, nullptr, 0)) return 1;
     cudaDeviceSynchronize();
-    const int wps = (n + 1 + 31) / 32;
+    const int wps = (n + 31) / 32;
+    {
+        std::vector<unsigned long long> span(2 * (1 << 14) * 2);
+        cudaMemcpyFromSymbol(span.data(), g_heat_span, span.size() * 8);
+        unsigned long long b0 = ~0ull, b1 = 0, f0 = ~0ull, f1 = 0;
+        for (int b = 0; b < N * wps && b < (1 << 14); ++b) b0 = std::min(b0, span[b * 2]), b1 = std::max(b1, span[b * 2 + 1]);
+        for (int b = 0; b < (N + 31) / 32; ++b) {
+            const size_t o = (size_t(1) << 15) + b * 2;
+            f0 = std::min(f0, span[o]), f1 = std::max(f1, span[o + 1]);
+        }
+        const unsigned long long t0 = std::min(b0, f0);
+        std::printf("basis CTAs: start %.3f end %.3f ms; forced CTAs: start %.3f end %.3f ms\n", (b0 - t0) * 1e-6,
+                    (b1 - t0) * 1e-6, (f0 - t0) * 1e-6, (f1 - t0) * 1e-6);
+    }
     std::vector<unsigned long long> prof(static_cast<size_t>(1 << 14) * 6);
     cudaMemcpyFromSymbol(prof.data(), g_heat_prof, prof.size() * 8);
     const char* names[5] = {"wait_fwd", "forward", "stage_wait_back", "back", "stage_next"};
-    // mean over the warps of each role (g < wps-1: basis warps, g == wps-1: the forced column's)
-    for (int role = 0; role < 2; ++role) {
+    for (int role = 0; role < 1; ++role) {  // basis warps
         double acc[5] = {0, 0, 0, 0, 0}, worst = 0;
         int cnt = 0;
         for (int b = 0; b < N * wps && b < (1 << 14); ++b) {
-            const int g = b % wps;
-            if ((g == wps - 1) != (role == 1)) continue;
+            (void)role;
             double tot = 0;
             for (int q = 0; q < 5; ++q) acc[q] += prof[b * 6 + q], tot += prof[b * 6 + q];
             worst = tot > worst ? tot : worst;
