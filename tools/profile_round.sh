@@ -12,7 +12,7 @@ python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_small.
       python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "launches rc=$?"
 python tools/prof_heat.py --n 128 --N 256 --S 256 --reps 1 > gpurun_out/prof_heat.log 2>&1 && \
   ncu --set full --import-source on --clock-control none \
-      -k regex:"heat_build_kernel|heat_record_kernel|affine_pair_kernel|affine_chain" -c 7 \
+      -k regex:"heat_build_kernel|heat_record_kernel|affine_pair_kernel|affine_chain" -c 8 \
       -o gpurun_out/full python tools/prof_heat.py --n 128 --N 256 --S 256 --reps 1 > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"
 tail -c 3000 gpurun_out/bench_full.log; tail -c 600 gpurun_out/bench_ref.log
