@@ -349,17 +349,14 @@ int64_t pint_heat_total_steps(const pint_slice* slices, int64_t N) {
     return t;
 }
 
-int pint_heat_coefficients(double dx, const pint_slice* slices, int64_t N, int64_t* step_off,
-                           double* r, double* fa, double* fb, double* sx, int64_t* n_out) {
-    int64_t n = 0;
-    if (const int rc = heat_dim(nullptr, dx, &n)) return rc;
-    if (n_out) *n_out = n;
-    step_off[0] = 0;
-    for (int64_t j = 0; j < N; ++j) step_off[j + 1] = step_off[j] + slices[j].steps;
+namespace {
+// Per-step tables of slices [j0, j1) (step_off already filled): heat_coefficient
+// (pde_problems.cpp:24), solve_implicit's r (:54), forcing (:26-29), on the host pool.
+void heat_fill_steps(double dx, const pint_slice* slices, int64_t j0, int64_t j1, const int64_t* step_off,
+                     double* r, double* fa, double* fb) {
     const double inv_dx2 = 1.0 / (dx * dx);  // pde_problems.cpp:33
-    // per step: heat_coefficient (pde_problems.cpp:24), solve_implicit's r (:54), forcing (:26-29)
-    auto fill = [&](int64_t j0, int64_t j1) {
-        for (int64_t j = j0; j < j1; ++j) {
+    auto fill = [&](int64_t a, int64_t b) {
+        for (int64_t j = j0 + a; j < j0 + b; ++j) {
             const double tb = slices[j].t_begin, h = slices[j].dt;
             const int64_t base = step_off[j];
             for (int64_t i = 1; i <= slices[j].steps; ++i) {
@@ -373,8 +370,19 @@ int pint_heat_coefficients(double dx, const pint_slice* slices, int64_t N, int64
             }
         }
     };
-    if (step_off[N] < 4096 || N < 2) fill(0, N);
-    else HostPool::get().parallel_for(N, fill);
+    if (step_off[j1] - step_off[j0] < 4096 || j1 - j0 < 2) fill(0, j1 - j0);
+    else HostPool::get().parallel_for(j1 - j0, fill);
+}
+}  // namespace
+
+int pint_heat_coefficients(double dx, const pint_slice* slices, int64_t N, int64_t* step_off,
+                           double* r, double* fa, double* fb, double* sx, int64_t* n_out) {
+    int64_t n = 0;
+    if (const int rc = heat_dim(nullptr, dx, &n)) return rc;
+    if (n_out) *n_out = n;
+    step_off[0] = 0;
+    for (int64_t j = 0; j < N; ++j) step_off[j + 1] = step_off[j] + slices[j].steps;
+    heat_fill_steps(dx, slices, 0, N, step_off, r, fa, fb);
     if (sx)
         for (int64_t i = 0; i < n; ++i) sx[i] = std::sin(kPi * (static_cast<double>(i + 1) * dx));
     return PINT_OK;
@@ -664,14 +672,14 @@ int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, Hea
     auto* h_fb = reinterpret_cast<double*>(h + b_off + b_dt + 2 * b_q);
     auto* h_sx = reinterpret_cast<double*>(h + b_off + b_dt + 3 * b_q);
     for (int64_t j = 0; j < N; ++j) h_dt[j] = sl[j].dt;
-    pint_heat_coefficients(dx, sl.data(), N, h_off, h_r, h_fa, h_fb, h_sx, nullptr);
+    h_off[0] = 0;
+    for (int64_t j = 0; j < N; ++j) h_off[j + 1] = h_off[j] + sl[j].steps;
+    for (int64_t i = 0; i < n; ++i) h_sx[i] = std::sin(kPi * (static_cast<double>(i + 1) * dx));
     int64_t S = 0;
     for (const auto& s : sl) S = std::max<int64_t>(S, s.steps);
     char* d = static_cast<char*>(pint_scratch(ctx, 0, in_bytes));
     double* f = static_cast<double*>(pint_scratch(ctx, 1, sizeof(double) * heat_records_doubles(n, N, S)));
     if (!d || !f) return PINT_E_CUDA;
-    if (!ok(ctx, cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D heat tables"))
-        return PINT_E_CUDA;
     H.n = n;
     H.N = N;
     H.Q = Q;
@@ -684,7 +692,27 @@ int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, Hea
     H.sx = reinterpret_cast<double*>(d + b_off + b_dt + 3 * b_q);
     H.factor = f;
     H.h2d = in_bytes;
-    return launch_heat_factor(ctx, n, N, S, H.step_off, H.slice_dt, H.r, H.fa, H.fb, H.sx, H.factor);
+    // slice table + sx first, then the per-step tables in chunks of slices (multiples of 32, the
+    // forced grid's slice groups): the host pool computes chunk c + 1 (glibc sin/cos) while the
+    // copy engine and the record kernel work on chunk c
+    auto h2d = [&](const void* src, void* dst, size_t bytes) {
+        return ok(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D heat tables");
+    };
+    if (!h2d(h_off, H.step_off, sizeof(int64_t) * (N + 1)) || !h2d(h_dt, H.slice_dt, sizeof(double) * N) ||
+        !h2d(h_sx, H.sx, sizeof(double) * n))
+        return PINT_E_CUDA;
+    const int64_t chunk = std::max<int64_t>(32, (N / 4 + 31) / 32 * 32);
+    for (int64_t j0 = 0; j0 < N; j0 += chunk) {
+        const int64_t j1 = std::min(N, j0 + chunk), q0 = h_off[j0], nq = h_off[j1] - q0;
+        heat_fill_steps(dx, sl.data(), j0, j1, h_off, h_r, h_fa, h_fb);
+        if (!h2d(h_r + q0, H.r + q0, sizeof(double) * nq) || !h2d(h_fa + q0, H.fa + q0, sizeof(double) * nq) ||
+            !h2d(h_fb + q0, H.fb + q0, sizeof(double) * nq))
+            return PINT_E_CUDA;
+        if (const int rc = launch_heat_factor_range(ctx, n, N, S, j0, j1 - j0, H.step_off, H.slice_dt, H.r, H.fa,
+                                                    H.fb, H.sx, H.factor))
+            return rc;
+    }
+    return PINT_OK;
 }
 
 int singular_check(pint_ctx* ctx) {

@@ -135,7 +135,7 @@ __device__ __forceinline__ bool out_of_range(double x) {
 constexpr int kRecChunk = 8;
 constexpr int kRecLane = 4 * kRecChunk + 1;  // padded per-lane stride (doubles)
 
-__global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, long long S,
+__global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, long long S, long long j0, long long Nc,
                                                           const int64_t* __restrict__ step_off,
                                                           const double* __restrict__ slice_dt,
                                                           const double* __restrict__ r_tab,
@@ -145,8 +145,8 @@ __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, lo
     __shared__ double buf[4][32 * kRecLane];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const long long s = t / N, j = t - s * N;
-    const bool live = t < S * N && step_off[j] + s < step_off[j + 1];  // slice j may have fewer steps
+    const long long s = t / Nc, j = j0 + (t - s * Nc);  // slices [j0, j0 + Nc) of the N laid out
+    const bool live = t < S * Nc && step_off[j] + s < step_off[j + 1];  // slice j may have fewer steps
     const long long q = live ? step_off[j] + s : 0;
     const unsigned live_mask = __ballot_sync(0xffffffffu, live);
     double* mine = buf[w] + lane * kRecLane;
@@ -586,15 +586,22 @@ int launch_build(pint_ctx* ctx, BuildPlan P) {
 
 int64_t heat_records_doubles(int64_t n, int64_t N, int64_t S) { return records_doubles(n, N, S); }
 
+int launch_heat_factor_range(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, int64_t j0, int64_t Nc,
+                             const int64_t* step_off, const double* slice_dt, const double* r, const double* fa,
+                             const double* fb, const double* sx, double* records) {
+    if (n < 1 || N < 0 || S < 0 || j0 < 0 || Nc < 0 || j0 + Nc > N)
+        return pint_set_error(ctx, PINT_E_INVALID, "heat_factor: bad sizes");
+    if (Nc == 0 || S == 0) return PINT_OK;
+    const long long threads = Nc * S;
+    heat_record_kernel<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, ctx->stream>>>(
+        static_cast<int>(n), N, S, j0, Nc, step_off, slice_dt, r, fa, fb, sx, records, ctx->d_fail);
+    return pint_check_launch(ctx, "heat_record_kernel");
+}
+
 int launch_heat_factor(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
                        const double* slice_dt, const double* r, const double* fa, const double* fb,
                        const double* sx, double* records) {
-    if (n < 1 || N < 0 || S < 0) return pint_set_error(ctx, PINT_E_INVALID, "heat_factor: bad sizes");
-    if (N == 0 || S == 0) return PINT_OK;
-    const long long threads = N * S;
-    heat_record_kernel<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, ctx->stream>>>(
-        static_cast<int>(n), N, S, step_off, slice_dt, r, fa, fb, sx, records, ctx->d_fail);
-    return pint_check_launch(ctx, "heat_record_kernel");
+    return launch_heat_factor_range(ctx, n, N, S, 0, N, step_off, slice_dt, r, fa, fb, sx, records);
 }
 
 int launch_heat_build(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
