@@ -149,9 +149,10 @@ int pint_heat_coefficients(double dx, const pint_slice* slices, int64_t N, int64
 /* doubles of the per-step records of N slices with at most S steps each (pint_heat_factor_dev) */
 int64_t pint_heat_records_size(int64_t n, int64_t N, int64_t S);
 /* Shared tridiagonal factor per (slice, step) — the Thomas forward pivots (linalg.cpp:77-93),
- * computed once per step instead of once per trajectory — plus the forcing increments. One
- * contiguous record per (slice, step), slice-major [N][S]: {-r, 0} | (p_i, RN(1/p_i)) x n |
- * h*b_i x even(n) | c_i x even(n). step_off/slice_dt/sx (device) and r/fa/fb (device,
+ * computed once per step instead of once per trajectory — plus the forcing increments. Layout
+ * (internal; size from pint_heat_records_size): for n up to ~200, slice-group blocks
+ * [S][N/32] of {(-r, 0), (p_i, RN(1/p_i))}[n+1][32] | h*b_i[n][32] | c_i[n][32]; for larger n,
+ * slice-major records [N][S] of {-r} | (p_i, RN(1/p_i)) | h*b_i | c_i. step_off/slice_dt/sx (device) and r/fa/fb (device,
  * step_off[N] entries) come from pint_heat_coefficients. */
 int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
                          const double* slice_dt, const double* r, const double* fa,

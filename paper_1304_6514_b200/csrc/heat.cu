@@ -24,6 +24,9 @@
 //
 // Roofline: the per-column recurrence (S x n dependent rows of 7 FP64 ops) — latency-bound;
 // algorithmic flops per slice-step: (n+1)(5n-4) + 5n (bench.py).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
 #include <cstring>
 
@@ -54,55 +57,58 @@ __host__ __device__ constexpr long long hb_offset(long long n) { return 16 + 2 *
 __host__ __device__ constexpr long long cc_offset(long long n) { return 16 + 3 * n16(n); }
 __host__ __device__ constexpr long long record_stride(long long n) { return 16 + 4 * n16(n); }
 
-// The forced columns of 32 slices run in one warp (lane = slice), so the record kernel also
-// writes a slice-group copy of the per-step data: block (s, G) for step s of slices 32G..32G+31,
-// lane-minor so a warp's loads are contiguous: [-r x 32] | (p_i, rcp_i)[n16][32] | h*b_i[n16][32]
-// | c_i[n16][32]. Forward half = -r, (p, rcp), h*b; back half = c.
-__host__ __device__ constexpr long long fblock_pr(long long) { return 32; }
-__host__ __device__ constexpr long long fblock_hb(long long n) { return 32 + 64 * n16(n); }
-__host__ __device__ constexpr long long fblock_cc(long long n) { return 32 + 96 * n16(n); }
-__host__ __device__ constexpr long long fblock_stride(long long n) { return 32 + 128 * n16(n); }
+// Slice-group block (s, G): the step-s data of slices 32G..32G+31, lane-minor, every part a whole
+// number of 128-byte lines: pr2[n16+1][32] of (x, y) pairs — row 0 = (-r, 0), row i+1 = (p_i,
+// rcp_i) — | h*b_i[n16][32] | c_i[n16][32]. The forced grid (lane = slice) bulk-copies a block's
+// halves (forward: pr2 + h*b; back: c); a basis warp fetches its slice's column of pr2 and of c
+// with a 2-D tile (TMA tensor copy), so one layout serves both grids.
+__host__ __device__ constexpr long long fblock_hb(long long n) { return 64 * (n16(n) + 1); }
+__host__ __device__ constexpr long long fblock_cc(long long n) { return 64 * (n16(n) + 1) + 32 * n16(n); }
+__host__ __device__ constexpr long long fblock_stride(long long n) { return 64 * (n16(n) + 1) + 64 * n16(n); }
 __host__ __device__ constexpr long long groups32(long long N) { return (N + 31) / 32; }
+__host__ __device__ constexpr long long round16(long long x) { return (x + 15) & ~15ll; }
 
-// Per-warp shared memory (doubles): [front pad][staged record][state (n-RR)*32][tail pad][2
-// mbarriers]. The staged record mirrors one global record. The pads make the software pipeline's
-// look-ahead loads (up to kBackAhead rows before the state and kFwdAhead rows after it) land
-// inside the allocation; the values they read are never used.
+// Per-warp shared memory (doubles): [front pad][staged step][state (n-RR)*32][tail pad][2
+// mbarriers]. The pads make the software pipeline's look-ahead loads (up to kBackAhead rows
+// before the state and kFwdAhead rows after it) land inside the allocation; the values they read
+// are never used.
 constexpr int kFwdAhead = 3;   // forward row: 5 dependent FP64 ops (~40 cycles) vs ~52-cycle LDS
 constexpr int kBackAhead = 8;  // back row: 2 dependent ops (~16 cycles)
-__host__ __device__ constexpr long long front_pad(long long n) {
-    return record_stride(n) >= 32 * kBackAhead ? 0 : even(32 * kBackAhead - record_stride(n));
-}
-// Warp roles: basis columns on the slice-major record; the forced columns of 32 slices per warp
-// on the slice-group block; or — when that block does not fit in shared memory (large n) — one
-// forced column per warp on the slice-major record.
-enum : int { kBasis = 0, kForcedGroup = 1, kForcedSingle = 2 };
+// Warp roles. With the slice-group layout (n small enough that a forced warp stages a whole block:
+// group_forced): basis columns on 2-D tiles of it (kBasisGroup) and 32 forced columns per warp on
+// its halves (kForcedGroup). Otherwise (large n) slice-major records: basis columns (kBasis) and
+// one forced column per warp (kForcedSingle).
+enum : int { kBasis = 0, kForcedGroup = 1, kForcedSingle = 2, kBasisGroup = 3 };
+// kBasisGroup staging: [-r, 0, (p, rcp) x n][pad] | c pairs [n][2] (the 2-lane tile of c)
+__host__ __device__ constexpr long long bg_fwd(long long n) { return round16(2 * (n + 1)); }
 __host__ __device__ constexpr long long staged_doubles(long long n, int mode) {
-    return mode == kForcedGroup ? fblock_stride(n) : record_stride(n);
+    return mode == kForcedGroup ? fblock_stride(n) : mode == kBasisGroup ? bg_fwd(n) + round16(2 * n) : record_stride(n);
+}
+__host__ __device__ constexpr long long front_pad(long long n, int mode) {  // (multiple of 128 bytes)
+    return staged_doubles(n, mode) >= 32 * kBackAhead ? 0 : round16(32 * kBackAhead - staged_doubles(n, mode));
 }
 __host__ __device__ constexpr int reg_rows(long long n) { return n >= kRegRows + 2 ? kRegRows : 0; }
 __host__ __device__ constexpr long long warp_smem_doubles(long long n, int mode) {
-    return (mode == kForcedGroup ? 0 : front_pad(n)) + staged_doubles(n, mode) + (n - reg_rows(n)) * 32 +
-           32 * kFwdAhead + 2;
+    return front_pad(n, mode) + staged_doubles(n, mode) + (n - reg_rows(n)) * 32 + 32 * kFwdAhead + 2;
 }
 __host__ __device__ constexpr bool group_forced(long long n) {
-    return 8 * warp_smem_doubles(n, kForcedGroup) <= 227 * 1024;
+    return 8 * warp_smem_doubles(n, kForcedGroup) <= 227 * 1024 && n + 1 <= 256;  // (tile rows <= 256)
 }
 
-// doubles needed for the records of N slices x S steps x n rows: [N][S][record] | [S][N/32][block]
+// doubles of the records: slice-major [N][S][record], or slice-group [S][N/32][block]
 __host__ __device__ constexpr long long records_doubles(long long n, long long N, long long S) {
-    return N * S * record_stride(n) + (group_forced(n) ? S * groups32(N) * fblock_stride(n) : 0);
+    return group_forced(n) ? S * groups32(N) * fblock_stride(n) : N * S * record_stride(n);
 }
 
 struct RecView {
     const double* base;
     long long S, N;
     int n;
-    __device__ __forceinline__ const double* rec(long long j, long long s) const {
+    __device__ __forceinline__ const double* rec(long long j, long long s) const {  // slice-major
         return base + (j * S + s) * record_stride(n);
     }
-    __device__ __forceinline__ const double* fblock(long long s, long long G) const {
-        return base + N * S * record_stride(n) + (s * groups32(N) + G) * fblock_stride(n);
+    __device__ __forceinline__ const double* fblock(long long s, long long G) const {  // slice-group
+        return base + (s * groups32(N) + G) * fblock_stride(n);
     }
 };
 
@@ -128,10 +134,10 @@ __device__ __forceinline__ bool out_of_range(double x) {
 // and the forcing increment h * b_i with b_i = fa*s_i + fb*s_i = heat_forcing(x_i, t)
 // (pde_problems.cpp:26-29, 91-94), rounded exactly as `state[i] += dt_step * b[i]` consumes it.
 // The pivot recurrence is sequential in i, so a thread owns a record; a warp holds 32 consecutive
-// slices of one step. Rows are produced in chunks of kRecChunk into shared memory and leave as
-// coalesced segments: per record and chunk, ONE warp store writes the 16 (p, rcp) doubles, the 8
-// h*b and the 8 c doubles of the slice-major record (whole sectors), and the slice-group copy is
-// written directly (32 consecutive lanes = 32 consecutive slices: contiguous).
+// slices of one step. Slice-group layout: each row goes straight out (32 consecutive lanes = 32
+// consecutive slices: contiguous, whole sectors). Slice-major layout (large n): rows are produced
+// in chunks of kRecChunk into shared memory and leave as ONE warp store per record and chunk (the
+// 16 (p, rcp), 8 h*b and 8 c doubles: whole sectors).
 constexpr int kRecChunk = 8;
 constexpr int kRecLane = 4 * kRecChunk + 1;  // padded per-lane stride (doubles)
 
@@ -157,13 +163,31 @@ __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, lo
     if (live && !(r >= 0.0 && r <= 0x1p40)) record_failure(fail, kRetryIndex + q, PINT_E_RANGE_RETRY, r);
     unsigned hb_max = 0;
     const bool fast_c = r >= 0x1p-960 && r <= 0x1p40;
-    double* const myrec = rec + (j * S + s) * record_stride(n);  // this lane's slice-major record
-    double* const fblk = rec + N * S * record_stride(n) + (s * groups32(N) + j / 32) * fblock_stride(n);
-    const int fl = static_cast<int>(j & 31);  // lane slot in the slice-group block
-    const bool grp = live && group_forced(n);  // the slice-group copy exists for this n
-    if (live) reinterpret_cast<double4*>(myrec)[0] = make_double4(negr, 0.0, 0.0, 0.0);
-    if (grp) fblk[fl] = negr;
+    const bool group = group_forced(n);
+    double* const myrec = rec + (j * S + s) * record_stride(n);  // slice-major: this lane's record
+    double* const fblk = rec + (s * groups32(N) + j / 32) * fblock_stride(n);  // slice-group block
+    double2* const pr2 = reinterpret_cast<double2*>(fblk) + (j & 31);
+    if (live && group) pr2[0] = make_double2(negr, 0.0);
+    if (live && !group) reinterpret_cast<double4*>(myrec)[0] = make_double4(negr, 0.0, 0.0, 0.0);
     double p = diag, c = 0.0;
+    if (group) {
+        for (int i = 0; i < n; ++i) {
+            if (i > 0) p = __dsub_rn(diag, __dmul_rn(negr, c));  // pivot = diag - sub*c[i-1] (:84-88)
+            if (live && p == 0.0) record_failure(fail, q, PINT_E_SINGULAR, static_cast<double>(i));
+            const double rcp = __drcp_rn(p);
+            c = (i < n - 1) ? (fast_c ? div_fast(negr, make_double2(p, rcp)) : __ddiv_rn(negr, p)) : 0.0;
+            const double si = sx[i];
+            const double hb = __dmul_rn(h, __dadd_rn(__dmul_rn(fq, si), __dmul_rn(gq, si)));
+            hb_max = max(hb_max, static_cast<unsigned>(__double2hiint(hb)) & 0x7fffffffu);
+            if (live) {
+                pr2[(i + 1) * 32] = make_double2(p, rcp);
+                fblk[fblock_hb(n) + i * 32 + (j & 31)] = hb;
+                fblk[fblock_cc(n) + i * 32 + (j & 31)] = c;
+            }
+        }
+        if (live && hb_max >= ((1023u + 900u) << 20)) record_failure(fail, kRetryIndex + q, PINT_E_RANGE_RETRY, 0.0);
+        return;
+    }
     for (int i0 = 0; i0 < n; i0 += kRecChunk) {
         const int rows = min(kRecChunk, n - i0);
         for (int u = 0; u < rows; ++u) {
@@ -181,11 +205,6 @@ __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, lo
             hb_max = max(hb_max, static_cast<unsigned>(__double2hiint(hb)) & 0x7fffffffu);
             mine[4 * u + 2] = hb;
             mine[4 * u + 3] = c;
-            if (grp) {
-                reinterpret_cast<double2*>(fblk + fblock_pr(n))[i * 32 + fl] = make_double2(p, rcp);
-                fblk[fblock_hb(n) + i * 32 + fl] = hb;
-                fblk[fblock_cc(n) + i * 32 + fl] = c;
-            }
         }
         __syncwarp();
         // this lane's slot in every record of the chunk: (p, rcp) element `lane` (lanes 0-15), h*b
@@ -219,7 +238,9 @@ __device__ __forceinline__ double div_guarded(double x, double2 pr) {
 
 
 
-struct BuildPlan {
+struct alignas(64) BuildPlan {
+    CUtensorMap tm_pr;  // kBasisGroup: pr2 of the slice-group blocks as [blocks][n16+1][64] doubles
+    CUtensorMap tm_cc;  // kBasisGroup: c of the slice-group blocks as [blocks][n16][32] doubles
     int n;
     int N;
     long long S;        // max steps per slice (record layout)
@@ -238,25 +259,32 @@ __device__ __forceinline__ unsigned hi_abs(double x) {
     return static_cast<unsigned>(__double2hiint(x)) & 0x7fffffffu;
 }
 
-// Record views of one warp's staged step. Basis and single-forced warps read the slice-major
-// record: one broadcast value per row. Group-forced warps (lane = slice) read the slice-group
-// block: row i of lane l at [i * 32 + l] (contiguous across lanes: conflict-free).
+// Record views of one warp's staged step. kBasis / kForcedSingle: the slice-major record, one
+// broadcast value per row. kBasisGroup: the slice's 2-D tiles — [-r, 0, (p, rcp) x n] and the c
+// pairs [n][2] of lanes (2m, 2m+1), this slice at parity (slice & 1). kForcedGroup (lane = slice):
+// the whole slice-group block, row i of lane l at [i * 32 + l] (contiguous: conflict-free).
 template <int kMode>
 struct StagedStep {
     const double* R;
-    int n, lane;
-    static constexpr bool kForced = kMode != kBasis;
-    static constexpr int kS = kMode == kForcedGroup ? 32 : 1;  // row stride of the per-row arrays
-    __device__ __forceinline__ double negr() const { return kMode == kForcedGroup ? R[lane] : R[0]; }
+    int n, lane, parity;
+    static constexpr bool kForced = kMode == kForcedGroup || kMode == kForcedSingle;
+    static constexpr int kS = kMode == kForcedGroup ? 32 : 1;                             // p, rcp, h*b
+    static constexpr int kSc = kMode == kForcedGroup ? 32 : kMode == kBasisGroup ? 2 : 1;  // c
+    __device__ __forceinline__ double negr() const {
+        return kMode == kForcedGroup ? R[2 * lane] : R[0];
+    }
     __device__ __forceinline__ const double2* pr() const {
-        return kMode == kForcedGroup ? reinterpret_cast<const double2*>(R + fblock_pr(n)) + lane
-                                     : reinterpret_cast<const double2*>(R + pr_offset());
+        return kMode == kForcedGroup ? reinterpret_cast<const double2*>(R) + 32 + lane
+               : kMode == kBasisGroup ? reinterpret_cast<const double2*>(R) + 1
+                                      : reinterpret_cast<const double2*>(R + pr_offset());
     }
     __device__ __forceinline__ const double* hb() const {  // forced modes only
         return kMode == kForcedGroup ? R + fblock_hb(n) + lane : R + hb_offset(n);
     }
     __device__ __forceinline__ const double* cc() const {
-        return kMode == kForcedGroup ? R + fblock_cc(n) + lane : R + cc_offset(n);
+        return kMode == kForcedGroup ? R + fblock_cc(n) + lane
+               : kMode == kBasisGroup ? R + bg_fwd(n) + parity
+                                      : R + cc_offset(n);
     }
 };
 
@@ -330,7 +358,7 @@ __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1],
 template <int RR, int kMode>
 __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], double* st, const StagedStep<kMode>& V,
                                             double d, double dm1, unsigned& qmin) {
-    constexpr int kS = StagedStep<kMode>::kS;
+    constexpr int kS = StagedStep<kMode>::kSc;
     const int n = V.n;
     const double* CC = V.cc();
     const int top = n - 2 - RR;  // first shared row of the back pass
@@ -386,23 +414,45 @@ __device__ unsigned long long g_heat_span[2][1 << 14][2];  // [forced][cta] = {s
     } while (0)
 #endif
 
-// CTA = ONE warp. Basis warps: warp g of slice blockIdx / wps, lane = basis column k = 32g + lane
-// (k < n: e_k; beyond: idle), the slice's slice-major record broadcast to all lanes. Group-forced
-// warps: lane = slice j = 32 blockIdx + lane, running that slice's forced trajectory c from 0 on
-// the slice-group block. Single-forced warps (large n): slice blockIdx, lane 0 runs c. Warps share nothing — each stages its own
-// copy of the step data in two halves with cp.async.bulk + mbarriers (forward half refilled during
-// the back pass, back half during the forward pass) and pulls the step after next into L2 — so no
-// CTA barrier couples a slice's warps and the single-warp CTAs pack over every SM. The forced
-// columns run as their own grid on a side stream: no warp carries 31 idle lanes, and the basis
-// grid stays at <= 2 warps per SM sub-partition at C2.
+// 2-D/3-D tile copies (TMA tensor) of a slice's columns out of the slice-group blocks.
+__device__ __forceinline__ void tile_load(unsigned dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                          unsigned bytes, unsigned bar) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(bar),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(dst),
+        "l"(reinterpret_cast<unsigned long long>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tile_prefetch(const CUtensorMap* tm, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(
+                     reinterpret_cast<unsigned long long>(tm)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+
+// CTA = ONE warp. Basis warps (kBasis / kBasisGroup): warp g of slice blockIdx / wps, lane = basis
+// column k = 32g + lane (k < n: e_k; beyond: idle), reading the slice's step data as broadcasts.
+// Group-forced warps: lane = slice j = 32 blockIdx + lane, running that slice's forced trajectory
+// c from 0 on the slice-group block. Single-forced warps (large n): slice blockIdx, lane 0 runs c.
+// Warps share nothing — each stages its own copy of the step data in two halves (cp.async.bulk, or
+// TMA tiles for kBasisGroup, completing on mbarriers; the forward half refilled during the back
+// pass, the back half during the forward pass) and pulls the step after next into L2 — so no CTA
+// barrier couples a slice's warps and the single-warp CTAs pack over every SM. The forced columns
+// are their own grid, launched first: no warp carries 31 idle lanes, and the basis grid stays at
+// <= 2 warps per SM sub-partition at C2.
 template <int RR, int kMode, bool kGuard>
-__global__ void __maxnreg__(168) heat_build_kernel(BuildPlan P) {
-    constexpr bool kForced = kMode != kBasis, kGroup = kMode == kForcedGroup;
-    extern __shared__ __align__(16) double smem[];
+__global__ void __maxnreg__(168) heat_build_kernel(const __grid_constant__ BuildPlan P) {
+    constexpr bool kForced = kMode == kForcedGroup || kMode == kForcedSingle;
+    constexpr bool kGroup = kMode == kForcedGroup;   // lane = slice
+    constexpr bool kTiles = kMode == kBasisGroup;    // TMA tiles of the slice-group blocks
+    extern __shared__ __align__(128) double smem[];
     const unsigned long long t_start = pint_dev::globaltimer();
     // forced grid: let the basis grid (launched after it with programmatic stream serialization)
-    // start now that this CTA is resident — its 8 large CTAs are placed before the basis CTAs
-    // fill the SMs
+    // start now that this CTA is resident — its large CTAs are placed before the basis CTAs fill
+    // the SMs
     if (kForced) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const int n = P.n;
     const int lane = threadIdx.x;
@@ -410,7 +460,7 @@ __global__ void __maxnreg__(168) heat_build_kernel(BuildPlan P) {
     const long long g0 = kGroup ? blockIdx.x : slice;  // the block's slice group / slice
     const int k = kForced ? (kGroup || lane == 0 ? n : n + 1) : static_cast<int>(blockIdx.x - g0 * P.wps) * 32 + lane;
     const bool live = kGroup ? slice < P.N : k < n + (kForced ? 1 : 0);
-    double* R = smem + (kGroup ? 0 : front_pad(n));
+    double* R = smem + front_pad(n, kMode);
     double* st = R + staged_doubles(n, kMode) + lane;
     const unsigned bar_f = smem_u32(R + staged_doubles(n, kMode) + (n - RR) * 32 + 32 * kFwdAhead);
     const unsigned bar_b = bar_f + 8;
@@ -419,14 +469,32 @@ __global__ void __maxnreg__(168) heat_build_kernel(BuildPlan P) {
     const RecView V = rec_view(P.rec, n, P.N, P.S);
     auto src = [&](long long s) { return kGroup ? V.fblock(s, g0) : V.rec(g0, s); };
     // forward half: header + (p, rcp) [+ h*b for the forced modes]; back half: c
-    const long long fwd_doubles = kGroup ? fblock_cc(n) : kForced ? cc_offset(n) : hb_offset(n);
-    const long long back_doubles = kGroup ? 32 * n16(n) : even(n);
-    const long long back_off = kGroup ? fblock_cc(n) : cc_offset(n);
+    const long long fwd_doubles = kGroup ? fblock_cc(n) : kTiles ? 2 * (n + 1) : kForced ? cc_offset(n) : hb_offset(n);
+    const long long back_doubles = kGroup ? 32 * n16(n) : kTiles ? 2 * n : even(n);
+    const long long back_off = kGroup ? fblock_cc(n) : kTiles ? bg_fwd(n) : cc_offset(n);
     const unsigned fwd_bytes = 8u * static_cast<unsigned>(fwd_doubles);
     const unsigned back_bytes = 8u * static_cast<unsigned>(back_doubles);
     const unsigned all_bytes = 8u * static_cast<unsigned>(staged_doubles(n, kMode));
     const unsigned dst_f = smem_u32(R), dst_b = smem_u32(R + back_off);
-    const StagedStep<kMode> SV{R, n, lane};
+    const StagedStep<kMode> SV{R, n, lane, static_cast<int>(slice & 1)};
+    // kTiles coordinates: column 2*(slice % 32) of pr2 / lanes (slice % 32) & ~1 of c; block s*N32 + G
+    const int tx = static_cast<int>(slice & 31), tg = static_cast<int>(slice >> 5), ng = static_cast<int>(groups32(P.N));
+    auto load_fwd = [&](long long s) {
+        if (kTiles) tile_load(dst_f, &P.tm_pr, 2 * tx, 0, static_cast<int>(s) * ng + tg, fwd_bytes, bar_f);
+        else bulk_load(dst_f, src(s), fwd_bytes, bar_f);
+    };
+    auto load_back = [&](long long s) {
+        if (kTiles) tile_load(dst_b, &P.tm_cc, tx & ~1, 0, static_cast<int>(s) * ng + tg, back_bytes, bar_b);
+        else bulk_load(dst_b, src(s) + back_off, back_bytes, bar_b);
+    };
+    auto prefetch = [&](long long s) {
+        if (kTiles) {
+            tile_prefetch(&P.tm_pr, 2 * tx, 0, static_cast<int>(s) * ng + tg);
+            tile_prefetch(&P.tm_cc, tx & ~1, 0, static_cast<int>(s) * ng + tg);
+        } else {
+            prefetch_l2(src(s), all_bytes);
+        }
+    };
 
     if (lane == 0) {
         mbar_init(bar_f);
@@ -435,9 +503,9 @@ __global__ void __maxnreg__(168) heat_build_kernel(BuildPlan P) {
     }
     __syncwarp();
     if (lane == 0 && steps > 0) {
-        bulk_load(dst_f, src(0), fwd_bytes, bar_f);
-        bulk_load(dst_b, src(0) + back_off, back_bytes, bar_b);
-        if (steps > 1) prefetch_l2(src(1), all_bytes);
+        load_fwd(0);
+        load_back(0);
+        if (steps > 1) prefetch(1);
     }
     double reg[RR > 0 ? RR : 1];
 #pragma unroll
@@ -461,15 +529,15 @@ __global__ void __maxnreg__(168) heat_build_kernel(BuildPlan P) {
         }
         HEAT_PROF_MARK(1);
         __syncwarp();  // every lane is done with the forward half
-        if (lane == 0 && s + 1 < steps) bulk_load(dst_f, src(s + 1), fwd_bytes, bar_f);
+        if (lane == 0 && s + 1 < steps) load_fwd(s + 1);
         mbar_wait(bar_b, parity);
         HEAT_PROF_MARK(2);
         if (active) column_back<RR, kMode>(reg, st, SV, d, dm1, qmin);
         HEAT_PROF_MARK(3);
         __syncwarp();  // every lane is done with the back half
         if (lane == 0 && s + 1 < steps) {
-            bulk_load(dst_b, src(s + 1) + back_off, back_bytes, bar_b);
-            if (s + 2 < steps) prefetch_l2(src(s + 2), all_bytes);
+            load_back(s + 1);
+            if (s + 2 < steps) prefetch(s + 2);
         }
         HEAT_PROF_MARK(4);
     }
@@ -506,7 +574,7 @@ struct IntegratePlan {
 };
 
 __global__ void __launch_bounds__(32) heat_integrate_kernel(IntegratePlan P) {
-    extern __shared__ __align__(16) double smem[];
+    extern __shared__ __align__(128) double smem[];
     const int n = P.n;
     const int lane = threadIdx.x;
     const long long col = static_cast<long long>(blockIdx.x) * 32 + lane;
@@ -518,22 +586,24 @@ __global__ void __launch_bounds__(32) heat_integrate_kernel(IntegratePlan P) {
     __syncwarp();
     const RecView V = rec_view(P.rec, n, 1, P.S);
     const bool forcing = P.with_forcing != 0;
+    const bool group = group_forced(n);  // records of ONE slice: slice-group block, lane 0
     for (long long s = P.s0; s < P.s0 + P.steps; ++s) {
-        const double* R = V.rec(0, s);
-        const double2* PR = reinterpret_cast<const double2*>(R + pr_offset());
-        const double* HB = R + hb_offset(n);
-        const double* CC = R + cc_offset(n);
-        const double negr = __ldg(R);
+        const double* B = group ? V.fblock(s, 0) : V.rec(0, s);
+        const double2* PR = group ? reinterpret_cast<const double2*>(B) + 32 : reinterpret_cast<const double2*>(B + pr_offset());
+        const double* HB = group ? B + fblock_hb(n) : B + hb_offset(n);
+        const double* CC = group ? B + fblock_cc(n) : B + cc_offset(n);
+        const int ks = group ? 32 : 1;
+        const double negr = __ldg(B);
         double d = 0.0;
         for (int i = 0; i < n; ++i) {
             double x = st[i * 32];
-            if (forcing) x = __dadd_rn(x, __ldg(HB + i));  // state += h*b (pde_problems.cpp:93)
+            if (forcing) x = __dadd_rn(x, __ldg(HB + i * ks));  // state += h*b (pde_problems.cpp:93)
             const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
-            d = div_guarded(num, __ldg(PR + i));
+            d = div_guarded(num, __ldg(PR + i * ks));
             st[i * 32] = d;
         }
         for (int i = n - 2; i >= 0; --i) {
-            d = __dsub_rn(st[i * 32], __dmul_rn(__ldg(CC + i), d));
+            d = __dsub_rn(st[i * 32], __dmul_rn(__ldg(CC + i * ks), d));
             st[i * 32] = d;
         }
     }
@@ -547,14 +617,58 @@ void smem_attrs(K kern, size_t smem) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// The kBasisGroup tiles: pr2 as [blocks][n16+1][64] doubles (box 2 x (n+1) x 1: one slice's
+// (-r, 0), (p, rcp) column) and c as [blocks][n16][32] doubles (box 2 x n x 1: two slices' c).
+int make_tile_maps(pint_ctx* ctx, BuildPlan& P) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return pint_set_error(ctx, PINT_E_CUDA, "heat_build: cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t blocks = static_cast<cuuint64_t>(P.S * groups32(P.N));
+    const cuuint64_t bstride = static_cast<cuuint64_t>(8 * fblock_stride(P.n));
+    const cuuint32_t estr[3] = {1, 1, 1};
+    {
+        const cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(n16(P.n) + 1), blocks};
+        const cuuint64_t strides[2] = {64 * 8, bstride};
+        const cuuint32_t box[3] = {2, static_cast<cuuint32_t>(P.n + 1), 1};
+        if (enc(&P.tm_pr, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(P.rec), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return pint_set_error(ctx, PINT_E_CUDA, "heat_build: tensor map (p, rcp) failed");
+    }
+    {
+        const cuuint64_t dims[3] = {32, static_cast<cuuint64_t>(n16(P.n)), blocks};
+        const cuuint64_t strides[2] = {32 * 8, bstride};
+        const cuuint32_t box[3] = {2, static_cast<cuuint32_t>(P.n), 1};
+        if (enc(&P.tm_cc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(P.rec + fblock_cc(P.n)), dims,
+                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return pint_set_error(ctx, PINT_E_CUDA, "heat_build: tensor map (c) failed");
+    }
+    return PINT_OK;
+}
+
 template <int RR, bool kGuard>
 int launch_build(pint_ctx* ctx, BuildPlan P) {
     const bool grp = group_forced(P.n);
-    const size_t smem = sizeof(double) * warp_smem_doubles(P.n, kBasis);
+    const size_t smem = sizeof(double) * warp_smem_doubles(P.n, grp ? kBasisGroup : kBasis);
     const size_t fsmem = sizeof(double) * warp_smem_doubles(P.n, grp ? kForcedGroup : kForcedSingle);
     if (smem > 227 * 1024 || fsmem > 227 * 1024)
         return pint_set_error(ctx, PINT_E_INVALID, "heat_build: n too large for shared memory");
-    auto kern = heat_build_kernel<RR, kBasis, kGuard>;
+    if (grp)
+        if (const int rc = make_tile_maps(ctx, P)) return rc;
+    auto kern = grp ? heat_build_kernel<RR, kBasisGroup, kGuard> : heat_build_kernel<RR, kBasis, kGuard>;
     auto fkern = grp ? heat_build_kernel<RR, kForcedGroup, kGuard> : heat_build_kernel<RR, kForcedSingle, kGuard>;
     smem_attrs(kern, smem);
     smem_attrs(fkern, fsmem);
