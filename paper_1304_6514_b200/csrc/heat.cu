@@ -37,7 +37,7 @@ namespace {
 using pint_dev::record_failure;
 using namespace pint_async;
 
-constexpr int kRegRows = 56;  // rows of each column held in registers (n >= kRegRows + 2)
+constexpr int kRegRows = 96;  // rows of each column held in registers (n >= kRegRows + 2)
 // PINT_E_RANGE_RETRY is recorded at kRetryIndex + (slice or step): above every task index, so a
 // real failure (a zero pivot at step q) always wins the lowest-index race and is never masked.
 constexpr long long kRetryIndex = 1ll << 62;
@@ -292,11 +292,11 @@ struct StagedStep {
 // increment, x + h*b (pde_problems.cpp:93, __dadd_rn as the reference's `state[i] += dt*b[i]`).
 // Rows [0, RR) in reg[], the rest at st[32*(i-RR)], software-pipelined kFwdAhead rows ahead
 // (every load is issued before the stores in front of it: the compiler cannot hoist a shared load
-// above a shared store it cannot disambiguate). The quotients are range-checked by column_back,
-// off the chain. Returns q_{n-1}; dm1 = q_{n-2}.
+// above a shared store it cannot disambiguate). Quotients are range-checked off the chain: the
+// register rows here, the shared rows in column_back. Returns q_{n-1}; dm1 = q_{n-2}.
 template <int RR, int kMode, bool kGuard>
 __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1], double* st,
-                                                 const StagedStep<kMode>& V, double& dm1) {
+                                                 const StagedStep<kMode>& V, double& dm1, unsigned& qmin) {
     constexpr int kS = StagedStep<kMode>::kS;
     constexpr bool kForced = StagedStep<kMode>::kForced;
     const int n = V.n;
@@ -312,6 +312,7 @@ __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1],
         const double x = kForced ? __dadd_rn(reg[i], HB[i * kS]) : reg[i];
         d = divide((i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d)), PR[i * kS]);
         reg[i] = d;
+        qmin = min(qmin, hi_abs(d) - 1u);  // ~40 cycles of chain per row: room for the check here
     }
     dm1 = d;
     const int last = n - 1 - RR;  // last shared row (>= 0)
@@ -353,8 +354,9 @@ __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1],
 
 // Back substitution of one step (linalg.cpp:91): d_i = q_i - c_i d_{i+1}, shared rows pipelined
 // kBackAhead rows ahead, then the register rows. qmin tracks min(|hi word of q_i| - 1) over the
-// forward quotients it reads anyway (zero wraps to the maximum, so exact zeros pass): a quotient
-// below 2^-950 means its dividend may have left Markstein's range (one VIADDMNMX per row).
+// forward quotients (zero wraps to the maximum, so exact zeros pass): a quotient below 2^-950
+// means its dividend may have left Markstein's range (one VIADDMNMX per row) — for the shared
+// rows here, as they are read back anyway; for the register rows in column_forward.
 template <int RR, int kMode>
 __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], double* st, const StagedStep<kMode>& V,
                                             double d, double dm1, unsigned& qmin) {
@@ -391,16 +393,15 @@ __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], doub
             if (r - u >= 0) row(r - u, yv[u], cv[u]);
     }
 #pragma unroll
-    for (int i = RR - 1; i >= 0; --i) {
-        if (i > n - 2) continue;  // (RR > 0 implies n >= RR + 2: never taken)
-        qmin = min(qmin, hi_abs(reg[i]) - 1u);
-        d = __dsub_rn(reg[i], __dmul_rn(CC[i * kS], d));
-        reg[i] = d;
+    for (int i = RR - 1; i >= 0; --i) {  // (RR > 0 only for n >= RR + 2: every register row is a back row)
+        d = __dsub_rn(reg[i], __dmul_rn(CC[i * kS], d));  // (the register rows' quotients were checked
+        reg[i] = d;                                         //  by column_forward, where they are made)
     }
 }
 
 #ifdef PINT_HEAT_PROF  // section timing for tools/heat_micro.cu only (never in the library build)
 __device__ unsigned long long g_heat_prof[1 << 14][6];
+__device__ unsigned long long g_heat_prof_f[1 << 10][6];  // forced grid
 __device__ unsigned long long g_heat_span[2][1 << 14][2];  // [forced][cta] = {start, end} globaltimer
 #define HEAT_PROF_MARK(k)                           \
     do {                                            \
@@ -444,7 +445,7 @@ __device__ __forceinline__ void tile_prefetch(const CUtensorMap* tm, int c0, int
 // are their own grid, launched first: no warp carries 31 idle lanes, and the basis grid stays at
 // <= 2 warps per SM sub-partition at C2.
 template <int RR, int kMode, bool kGuard>
-__global__ void __maxnreg__(168) heat_build_kernel(const __grid_constant__ BuildPlan P) {
+__global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ BuildPlan P) {
     constexpr bool kForced = kMode == kForcedGroup || kMode == kForcedSingle;
     constexpr bool kGroup = kMode == kForcedGroup;   // lane = slice
     constexpr bool kTiles = kMode == kBasisGroup;    // TMA tiles of the slice-group blocks
@@ -524,7 +525,7 @@ __global__ void __maxnreg__(168) heat_build_kernel(const __grid_constant__ Build
         HEAT_PROF_MARK(0);
         double d = 0.0, dm1 = 0.0;
         if (active) {
-            d = column_forward<RR, kMode, kGuard>(reg, st, SV, dm1);
+            d = column_forward<RR, kMode, kGuard>(reg, st, SV, dm1, qmin);
             qmin = min(qmin, hi_abs(d) - 1u);  // q_{n-1} (the back pass starts at row n-2)
         }
         HEAT_PROF_MARK(1);
@@ -543,8 +544,7 @@ __global__ void __maxnreg__(168) heat_build_kernel(const __grid_constant__ Build
     }
 #ifdef PINT_HEAT_PROF
     if (lane == 0 && blockIdx.x < (1 << 14)) {
-        if (!kForced)
-            for (int q = 0; q < 5; ++q) g_heat_prof[blockIdx.x][q] = prof[q];
+        for (int q = 0; q < 5; ++q) (kForced ? g_heat_prof_f[blockIdx.x & 1023] : g_heat_prof[blockIdx.x])[q] = prof[q];
         g_heat_span[kForced ? 1 : 0][blockIdx.x][0] = t_start;
         g_heat_span[kForced ? 1 : 0][blockIdx.x][1] = pint_dev::globaltimer();
     }

@@ -78,6 +78,18 @@ int main(int argc, char** argv) {
     std::vector<unsigned long long> prof(static_cast<size_t>(1 << 14) * 6);
     cudaMemcpyFromSymbol(prof.data(), g_heat_prof, prof.size() * 8);
     const char* names[5] = {"wait_fwd", "forward", "stage_wait_back", "back", "stage_next"};
+    {
+        std::vector<unsigned long long> pf(size_t(1024) * 6);
+        cudaMemcpyFromSymbol(pf.data(), g_heat_prof_f, pf.size() * 8);
+        const int nf = (N + 31) / 32;
+        double acc[5] = {0, 0, 0, 0, 0};
+        for (int b = 0; b < nf && b < 1024; ++b)
+            for (int q = 0; q < 5; ++q) acc[q] += pf[b * 6 + q];
+        std::printf("forced warps (%d):", nf);
+        double tot = 0;
+        for (int q = 0; q < 5; ++q) std::printf(" %.0f", acc[q] / nf / S), tot += acc[q] / nf;
+        std::printf("  per-row=%.1f\n", tot / S / n);
+    }
     for (int role = 0; role < 1; ++role) {  // basis warps
         double acc[5] = {0, 0, 0, 0, 0}, worst = 0;
         int cnt = 0;
