@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -663,7 +664,10 @@ template <int RR, bool kGuard>
 int launch_build(pint_ctx* ctx, BuildPlan P) {
     const bool grp = group_forced(P.n);
     const size_t smem = sizeof(double) * warp_smem_doubles(P.n, grp ? kBasisGroup : kBasis);
-    const size_t fsmem = sizeof(double) * warp_smem_doubles(P.n, grp ? kForcedGroup : kForcedSingle);
+    size_t fsmem = sizeof(double) * warp_smem_doubles(P.n, grp ? kForcedGroup : kForcedSingle);
+    // a group-forced warp is the longest chain of the launch: reserve enough shared memory that at
+    // most 3 basis CTAs share its SM (one warp per sub-partition); the basis grid still fits
+    if (grp) fsmem = std::max(fsmem, std::min<size_t>(227 * 1024, 228 * 1024 - 4 * (smem + 1024)) & ~size_t(127));
     if (smem > 227 * 1024 || fsmem > 227 * 1024)
         return pint_set_error(ctx, PINT_E_INVALID, "heat_build: n too large for shared memory");
     if (grp)
