@@ -185,9 +185,10 @@ __global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long lo
 }
 
 // ---- DMMA pair kernel ------------------------------------------------------------------------
-constexpr int BM = 64, BN = 64, BK = 16;
-constexpr int AS = BK + 4;   // padded strides: conflict-free fragment loads
-constexpr int BS = BN + 4;
+constexpr int BM = 64, BN = 64, BK = 16, kStages = 4;
+constexpr int AS = BK + 4;       // padded strides: conflict-free fragment loads
+constexpr int BW = BN + 8;       // B tile width: 64 columns + one 8-column fragment for column n
+constexpr int BS = BW + 4;
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -195,8 +196,11 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-// out_p = later_p o earlier_p for pair p = blockIdx.z. Blocks with blockIdx.x == tilesN
-// compute the translation column c_out = G_later c_earlier + c_later for their 64 rows.
+// out_p = later_p o earlier_p for pair p = blockIdx.z, as ONE product of augmented matrices:
+// [G2 | c2] [[G1, c1], [0, 1]] = [G2 G1 | G2 c1 + c2] — the B tiles span E's n+1 columns (c1 is
+// column n) and the epilogue adds c2 to column n. Column tiles cover n columns; when n is a
+// multiple of 64 the column n would open a 64-wide tile of its own, so the last tile's right-hand
+// warps carry one extra 8-column fragment instead.
 __global__ void __launch_bounds__(128)
 affine_pair_kernel(long long n, long long ldm, const double* __restrict__ earlier,
                    long long e_stride, const double* __restrict__ later, long long l_stride,
@@ -207,103 +211,99 @@ affine_pair_kernel(long long n, long long ldm, const double* __restrict__ earlie
     double* O = out + p * o_stride;
     const long long row0 = static_cast<long long>(blockIdx.y) * BM;
     const int tid = threadIdx.x;
+    const long long nc = n + 1;  // output / B columns
+    (void)tilesN;
 
-    if (static_cast<int>(blockIdx.x) == tilesN) {  // translation column (GEMV)
-        if (tid < BM && row0 + tid < n) {
-            const long long i = row0 + tid;
-            const double* lr = L + i * ldm;
-            double s = 0.0;
-            for (long long k = 0; k < n; ++k) s = fma(lr[k], E[k * ldm + n], s);
-            O[i * ldm + n] = s + lr[n];
-        }
-        return;
-    }
-
-    __shared__ __align__(16) double As[2][BM * AS];
-    __shared__ __align__(16) double Bs[2][BK * BS];
+    // kStages-deep cp.async pipeline of 64x16 (A) and 16x64 (B) tiles; out-of-range elements are
+    // zero-filled by the copy itself (src-size 0 or 8 of 16)
+    extern __shared__ __align__(16) double pair_smem[];
+    double* As = pair_smem;                        // [kStages][BM * AS]
+    double* Bs = pair_smem + kStages * BM * AS;    // [kStages][BK * BS]
     const long long col0 = static_cast<long long>(blockIdx.x) * BN;
     const int lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 1, wn = warp & 1;
     const int g = lane >> 2, t4 = lane & 3;
 
-    double acc[4][4][2];
+    double acc[4][5][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+        for (int b = 0; b < 5; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    const bool extra = wn == 1 && col0 + BN == n;  // this warp also owns columns n .. n+7
 
-    // register staging: A tile 64x16 and B tile 16x64 as 4 double2 per thread each
-    double2 ra[4], rb[4];
-    auto load_tiles = [&](long long k0) {
+    auto cp16 = [](double* dst, const double* src, long long bytes) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+                     "r"(static_cast<unsigned>(bytes))
+                     : "memory");
+    };
+    auto issue = [&](int stage, long long k0) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int idx = tid + u * 128;           // 0..511
+            const int idx = tid + u * 128;  // 0..511: 16-byte chunks of each tile
             const int ar = idx >> 3, ac = (idx & 7) * 2;
             const long long gr = row0 + ar, gc = k0 + ac;
-            double2 v = make_double2(0.0, 0.0);
-            if (gr < n) {
-                const double* src = L + gr * ldm + gc;
-                if (gc + 1 < n) v = *reinterpret_cast<const double2*>(src);
-                else if (gc < n) v.x = src[0];
-            }
-            ra[u] = v;
+            const long long abytes = gr < n ? 8 * max(0ll, min(2ll, n - gc)) : 0;
+            cp16(As + stage * BM * AS + ar * AS + ac, abytes ? L + gr * ldm + gc : L, abytes);
             const int br = idx >> 5, bc = (idx & 31) * 2;
             const long long gk = k0 + br, gn = col0 + bc;
-            double2 w = make_double2(0.0, 0.0);
-            if (gk < n) {
-                const double* src = E + gk * ldm + gn;
-                if (gn + 1 < n) w = *reinterpret_cast<const double2*>(src);
-                else if (gn < n) w.x = src[0];
-            }
-            rb[u] = w;
+            const long long bbytes = gk < n ? 8 * max(0ll, min(2ll, nc - gn)) : 0;
+            cp16(Bs + stage * BK * BS + br * BS + bc, bbytes ? E + gk * ldm + gn : E, bbytes);
         }
-    };
-    auto store_tiles = [&](int buf) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int idx = tid + u * 128;
-            const int ar = idx >> 3, ac = (idx & 7) * 2;
-            As[buf][ar * AS + ac] = ra[u].x;
-            As[buf][ar * AS + ac + 1] = ra[u].y;
-            const int br = idx >> 5, bc = (idx & 31) * 2;
-            Bs[buf][br * BS + bc] = rb[u].x;
-            Bs[buf][br * BS + bc + 1] = rb[u].y;
+        if (tid < 64) {  // B columns 64..71 of the tile (16 rows x 4 chunks)
+            const int br = tid >> 2, bc = BN + (tid & 3) * 2;
+            const long long gk = k0 + br, gn = col0 + bc;
+            const long long bbytes = gk < n ? 8 * max(0ll, min(2ll, nc - gn)) : 0;
+            cp16(Bs + stage * BK * BS + br * BS + bc, bbytes ? E + gk * ldm + gn : E, bbytes);
         }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
 
     const long long kTiles = (n + BK - 1) / BK;
-    load_tiles(0);
-    store_tiles(0);
-    __syncthreads();
+#pragma unroll
+    for (int st = 0; st < kStages - 1; ++st) {
+        if (st < kTiles) issue(st, st * BK);
+        else asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
     for (long long kt = 0; kt < kTiles; ++kt) {
-        const int buf = static_cast<int>(kt & 1);
-        if (kt + 1 < kTiles) load_tiles((kt + 1) * BK);
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kStages - 2) : "memory");  // tile kt has landed
+        __syncthreads();  // ... for every thread; and stage (kt-1) % kStages is free again
+        if (kt + kStages - 1 < kTiles) issue(static_cast<int>((kt + kStages - 1) % kStages), (kt + kStages - 1) * BK);
+        else asm volatile("cp.async.commit_group;\n" ::: "memory");
+        const double* A = As + (kt % kStages) * BM * AS;
+        const double* B = Bs + (kt % kStages) * BK * BS;
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
             double af[4], bf[4];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi) af[mi] = As[buf][(wm * 32 + mi * 8 + g) * AS + kk + t4];
+            for (int mi = 0; mi < 4; ++mi) af[mi] = A[(wm * 32 + mi * 8 + g) * AS + kk + t4];
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) bf[ni] = Bs[buf][(kk + t4) * BS + wn * 32 + ni * 8 + g];
+            for (int ni = 0; ni < 4; ++ni) bf[ni] = B[(kk + t4) * BS + wn * 32 + ni * 8 + g];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
                 for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+            if (extra) {
+                const double bx = B[(kk + t4) * BS + BN + g];
+#pragma unroll
+                for (int mi = 0; mi < 4; ++mi) dmma(acc[mi][4][0], acc[mi][4][1], af[mi], bx);
+            }
         }
-        if (kt + 1 < kTiles) store_tiles(buf ^ 1);
-        __syncthreads();
     }
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi) {
         const long long r = row0 + wm * 32 + mi * 8 + g;
         if (r >= n) continue;
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-            const long long c = col0 + wn * 32 + ni * 8 + t4 * 2;
-            if (c + 1 < n) {
-                *reinterpret_cast<double2*>(O + r * ldm + c) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
-            } else if (c < n) {
-                O[r * ldm + c] = acc[mi][ni][0];
+        for (int ni = 0; ni < 5; ++ni) {
+            if (ni == 4 && !extra) continue;
+            const long long c = ni == 4 ? col0 + BN + t4 * 2 : col0 + wn * 32 + ni * 8 + t4 * 2;
+            double v0 = acc[mi][ni][0], v1 = acc[mi][ni][1];
+            if (c == n) v0 += L[r * ldm + n];          // + c2
+            else if (c + 1 == n) v1 += L[r * ldm + n];
+            if (c + 1 < nc) {
+                *reinterpret_cast<double2*>(O + r * ldm + c) = make_double2(v0, v1);
+            } else if (c < nc) {
+                O[r * ldm + c] = v0;
             }
         }
     }
@@ -313,11 +313,17 @@ int launch_pairs(pint_ctx* ctx, long long n, long long P, const double* earlier,
                  const double* later, long long l_stride, double* out, long long o_stride) {
     if (P <= 0) return PINT_OK;
     const long long ldm = pint_affine_ldm(n);
-    const int tilesN = static_cast<int>((n + BN - 1) / BN);
+    const int tilesN = static_cast<int>((n + BN - 1) / BN);  // (column n: see affine_pair_kernel)
     const unsigned tilesM = static_cast<unsigned>((n + BM - 1) / BM);
     if (P > 65535) return pint_set_error(ctx, PINT_E_INVALID, "affine_pair: too many pairs per launch");
-    dim3 grid(static_cast<unsigned>(tilesN + 1), tilesM, static_cast<unsigned>(P));
-    affine_pair_kernel<<<grid, 128, 0, ctx->stream>>>(n, ldm, earlier, e_stride, later, l_stride, out,
+    dim3 grid(static_cast<unsigned>(tilesN), tilesM, static_cast<unsigned>(P));
+    constexpr size_t smem = sizeof(double) * kStages * (BM * AS + BK * BS);
+    static bool attr = [] {
+        return cudaFuncSetAttribute(affine_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)) == cudaSuccess;
+    }();
+    (void)attr;
+    affine_pair_kernel<<<grid, 128, smem, ctx->stream>>>(n, ldm, earlier, e_stride, later, l_stride, out,
                                                       o_stride, tilesN);
     return pint_check_launch(ctx, "affine_pair_kernel");
 }
