@@ -16,6 +16,8 @@
 // Roofline: TREE is FP64 tensor (2 n^3 flops per pair); CHAIN is latency/L2 bound.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include "pint_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -66,15 +68,16 @@ affine_chain_kernel(long long n, long long N, long long ldm, const double* __res
     for (long long i = threadIdx.x; i < n; i += kChainThreads) y[i] = y_s[i];
 }
 
-// Cluster chain (n <= 256). Dynamic smem: rows[kRing][32][ldm] | y[2][ny] | pad | kRing map barriers
+// Cluster chain (n <= 256). Dynamic smem: rows[ring][32][ldm] | y[2][ny] | pad | ring map barriers
 // | 2 y barriers,
 // ny = n rounded up to 16 (16-byte aligned y pairs; the pipeline may read 16 doubles past n). A
 // CTA's 32 rows of a map are one contiguous block: one bulk copy per map.
 constexpr int kClusterMax = 8;
 constexpr int kChainAhead = 8;  // pairs of terms in flight per lane
-constexpr int kRing = 4;        // maps in flight (bulk-copy latency ~ 2 map applications)
+constexpr int kRing = 4;        // maps in flight (bulk-copy latency ~ 2 map applications); fewer
+                                // when 4 blocks of 32 rows do not fit (n > ~220)
 
-__global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long long N, int ldm,
+__global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long long N, int ldm, int ring,
                                                                   const double* __restrict__ maps,
                                                                   const double* __restrict__ y0,
                                                                   double* __restrict__ y) {
@@ -85,14 +88,14 @@ __global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long lo
     const int lane = threadIdx.x;
     const int r0 = 32 * static_cast<int>(rank), rows = min(32, n - r0);
     const int ny = (n + 15) & ~15;
-    double* blk = sm;                       // [kRing][32][ldm]
-    double* ys = sm + kRing * 32 * ldm;     // [2][ny] + look-ahead pad
-    const unsigned bar0 = smem_u32(ys + 2 * ny + 4 * kChainAhead);  // kRing map barriers
-    const unsigned ybar0 = bar0 + 8u * kRing;                         // 2 y barriers
+    double* blk = sm;                       // [ring][32][ldm]
+    double* ys = sm + ring * 32 * ldm;        // [2][ny] + look-ahead pad
+    const unsigned bar0 = smem_u32(ys + 2 * ny + 4 * kChainAhead);  // ring map barriers
+    const unsigned ybar0 = bar0 + 8u * ring;                           // 2 y barriers
     const long long mstride = static_cast<long long>(n) * ldm;
     const unsigned blk_bytes = 8u * static_cast<unsigned>(ldm) * static_cast<unsigned>(rows);
     if (lane == 0) {
-        for (int b = 0; b < kRing + 2; ++b) mbar_init(bar0 + 8u * b);
+        for (int b = 0; b < ring + 2; ++b) mbar_init(bar0 + 8u * b);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncwarp();
@@ -102,7 +105,7 @@ __global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long lo
             bulk_load(smem_u32(blk + b * 32 * ldm), maps + j * mstride + static_cast<long long>(r0) * ldm, blk_bytes,
                       bar0 + 8u * b);
     };
-    for (long long j = 0; j < kRing && j < N; ++j) fetch(j, static_cast<int>(j));
+    for (long long j = 0; j < ring && j < N; ++j) fetch(j, static_cast<int>(j));
     for (int i = lane; i < 2 * ny + 4 * kChainAhead; i += 32) ys[i] = (i < n) ? y0[i] : 0.0;
     cluster.sync();  // every CTA's barriers and y buffers are initialised before any remote write
     const int pairs = n / 2;
@@ -120,8 +123,8 @@ __global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long lo
     } while (0)
 #endif
     for (long long j = 0; j < N; ++j) {
-        const int b = static_cast<int>(j % kRing), yb = static_cast<int>(j & 1);
-        mbar_wait(bar0 + 8u * b, static_cast<unsigned>((j / kRing) & 1));
+        const int b = static_cast<int>(j % ring), yb = static_cast<int>(j & 1);
+        mbar_wait(bar0 + 8u * b, static_cast<unsigned>((j / ring) & 1));
         CHAIN_MARK(tw);
         const double2* g2 = reinterpret_cast<const double2*>(blk + (b * 32 + lane) * ldm);
         const double2* y2 = reinterpret_cast<const double2*>(ys + yb * ny);
@@ -151,8 +154,8 @@ __global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long lo
         if (n & 1) s = __dadd_rn(s, __dmul_rn(g[n - 1], ys[yb * ny + n - 1]));
         s = __dadd_rn(s, g[n]);  // + c_i
         CHAIN_MARK(tc);
-        __syncwarp();  // block b fully read: refill it with map j + kRing
-        if (j + kRing < N) fetch(j + kRing, b);
+        __syncwarp();  // block b fully read: refill it with map j + ring
+        if (j + ring < N) fetch(j + ring, b);
         // y_{j+1}: every CTA's rows land in every CTA's buffer yb^1 via st.async, each completing
         // its bytes on that CTA's y barrier (n * 8 bytes expected per map)
         const unsigned ybar = ybar0 + 8u * (yb ^ 1);
@@ -336,8 +339,10 @@ int launch_affine_chain(pint_ctx* ctx, int64_t n, int64_t N, const double* maps,
     if (n <= 32 * kClusterMax && N > 0) {
         const int ldm = static_cast<int>(pint_affine_ldm(n));
         const size_t ny = static_cast<size_t>((n + 15) & ~15);
-        const size_t smem = sizeof(double) * (kRing * 32 * static_cast<size_t>(ldm) + 2 * ny + 4 * kChainAhead) +
-                            8 * (kRing + 2);
+        const size_t blk = sizeof(double) * 32 * static_cast<size_t>(ldm);
+        const size_t rest = sizeof(double) * (2 * ny + 4 * kChainAhead) + 8 * (kRing + 2);
+        const int ring = static_cast<int>(std::min<size_t>(kRing, (227 * 1024 - rest) / blk));
+        const size_t smem = ring * blk + rest;
         cudaFuncSetAttribute(affine_chain_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
         const unsigned C = static_cast<unsigned>((n + 31) / 32);
@@ -354,7 +359,7 @@ int launch_affine_chain(pint_ctx* ctx, int64_t n, int64_t N, const double* maps,
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         if (cudaLaunchKernelEx(&cfg, affine_chain_cluster_kernel, static_cast<int>(n), static_cast<long long>(N), ldm,
-                               maps, y0, y) != cudaSuccess)
+                               ring, maps, y0, y) != cudaSuccess)
             return pint_check_launch(ctx, "affine_chain_cluster_kernel");
         return pint_check_launch(ctx, "affine_chain_cluster_kernel");
     }

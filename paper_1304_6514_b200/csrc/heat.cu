@@ -89,11 +89,50 @@ __host__ __device__ constexpr long long front_pad(long long n, int mode) {  // (
     return staged_doubles(n, mode) >= 32 * kBackAhead ? 0 : round16(32 * kBackAhead - staged_doubles(n, mode));
 }
 __host__ __device__ constexpr int reg_rows(long long n) { return n >= kRegRows + 2 ? kRegRows : 0; }
+// Shared state rows are lane-interleaved (row i of lane l at 32 i + l), except for a single-forced
+// warp: its 32 lanes all run the one forced column in lockstep, so they share ONE copy (stride 1,
+// every lane stores the same value).
+__host__ __device__ constexpr int lane_stride(int mode) { return mode == kForcedSingle ? 1 : 32; }
 __host__ __device__ constexpr long long warp_smem_doubles(long long n, int mode) {
-    return front_pad(n, mode) + staged_doubles(n, mode) + (n - reg_rows(n)) * 32 + 32 * kFwdAhead + 2;
+    return front_pad(n, mode) + staged_doubles(n, mode) + (n - reg_rows(n)) * lane_stride(mode) +
+           lane_stride(mode) * kFwdAhead + 2;
 }
 __host__ __device__ constexpr bool group_forced(long long n) {
     return 8 * warp_smem_doubles(n, kForcedGroup) <= 227 * 1024 && n + 1 <= 256;  // (tile rows <= 256)
+}
+
+// Rows per TMEM loop body: 2 chunks of 8 (the two register buffers alternate) and a multiple of
+// both look-ahead rings (kTmAhead and kBackAhead), so every ring slot is a compile-time index.
+constexpr int kTmBody = 16;
+constexpr int kTmAhead = 4;  // forward (p, rcp) look-ahead over the TMEM rows
+
+// ---- large n: heat_build_tmem_kernel --------------------------------------------------------
+// When a warp's state no longer fits 4 times into shared memory (n >~ 280 with the one-warp-CTA
+// build above: 134 KB per warp at n = 512, ONE warp per SM), a CTA of 5 warps runs ONE slice:
+// warps 0-3 four basis column groups whose rows are split three ways — kTmRegRows in registers,
+// tm_rows(n) in tensor memory (each warp owns a 32-lane quarter of the SM's 256 KB TMEM: up to 256
+// doubles per thread), the rest lane-interleaved in shared memory — and warp 4 the slice's forced
+// column (compact, see lane_stride) in the CTA that holds groups 0-3. The five warps share one
+// staged copy of the step's record; whichever warp finishes a half last refills it.
+constexpr int kTmRegRows = 64;
+__host__ __device__ constexpr int tm_rows(long long n) {  // (256 doubles per thread at most)
+    return n - kTmRegRows - 2 < kTmBody ? 0
+           : (n - kTmRegRows - 2) / kTmBody >= 256 / kTmBody
+               ? 256
+               : static_cast<int>((n - kTmRegRows - 2) / kTmBody) * kTmBody;
+}
+__host__ __device__ constexpr long long tm_shared_rows(long long n) { return n - kTmRegRows - tm_rows(n); }
+// shared memory (doubles): record | 4 x basis state [tm_shared_rows][32] | tail pad | forced state
+// [n - kTmRegRows] | pad | bar_f, bar_b, counters, TMEM address
+__host__ __device__ constexpr long long tm_forced_off(long long n) {
+    return record_stride(n) + 4 * tm_shared_rows(n) * 32 + 32 * kFwdAhead;
+}
+__host__ __device__ constexpr long long tm_smem_doubles(long long n) {
+    return tm_forced_off(n) + even(n - kTmRegRows + kFwdAhead) + 4;
+}
+__host__ __device__ constexpr bool use_tmem(long long n) {
+    return !group_forced(n) && tm_rows(n) >= kTmBody && 8 * tm_smem_doubles(n) <= 227 * 1024 &&
+           4 * (8 * warp_smem_doubles(n, kBasis) + 1024) > 228 * 1024;
 }
 
 // doubles of the records: slice-major [N][S][record], or slice-group [S][N/32][block]
@@ -289,15 +328,126 @@ struct StagedStep {
     }
 };
 
+// ---- TMEM rows (large n, heat_build_tmem_kernel) --------------------------------------------
+// tcgen05.ld / st, shape 32x32b: thread i of warp w <-> TMEM lane 32 (w % 4) + i; x16 = 16 32-bit
+// columns = 8 doubles of that thread's own column (row r of the TMEM part at columns 2r, 2r + 1).
+struct Tm8 {
+    unsigned u[16];
+    __device__ __forceinline__ double get(int i) const { return __hiloint2double(u[2 * i + 1], u[2 * i]); }
+    __device__ __forceinline__ void put(int i, double v) {
+        u[2 * i] = static_cast<unsigned>(__double2loint(v));
+        u[2 * i + 1] = static_cast<unsigned>(__double2hiint(v));
+    }
+};
+__device__ __forceinline__ void tm_ld(unsigned addr, Tm8& t) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];\n"
+        : "=r"(t.u[0]), "=r"(t.u[1]), "=r"(t.u[2]), "=r"(t.u[3]), "=r"(t.u[4]), "=r"(t.u[5]), "=r"(t.u[6]),
+          "=r"(t.u[7]), "=r"(t.u[8]), "=r"(t.u[9]), "=r"(t.u[10]), "=r"(t.u[11]), "=r"(t.u[12]), "=r"(t.u[13]),
+          "=r"(t.u[14]), "=r"(t.u[15])
+        : "r"(addr));
+}
+// the loaded registers are operands of the wait, so no use of them can be scheduled above it
+__device__ __forceinline__ void tm_wait_ld(Tm8& t) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+                 : "+r"(t.u[0]), "+r"(t.u[1]), "+r"(t.u[2]), "+r"(t.u[3]), "+r"(t.u[4]), "+r"(t.u[5]), "+r"(t.u[6]),
+                   "+r"(t.u[7]), "+r"(t.u[8]), "+r"(t.u[9]), "+r"(t.u[10]), "+r"(t.u[11]), "+r"(t.u[12]),
+                   "+r"(t.u[13]), "+r"(t.u[14]), "+r"(t.u[15])
+                 :
+                 : "memory");
+}
+__device__ __forceinline__ void tm_st(unsigned addr, const Tm8& t) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};\n" ::"r"(addr),
+        "r"(t.u[0]), "r"(t.u[1]), "r"(t.u[2]), "r"(t.u[3]), "r"(t.u[4]), "r"(t.u[5]), "r"(t.u[6]), "r"(t.u[7]),
+        "r"(t.u[8]), "r"(t.u[9]), "r"(t.u[10]), "r"(t.u[11]), "r"(t.u[12]), "r"(t.u[13]), "r"(t.u[14]), "r"(t.u[15])
+        : "memory");  // (also keeps the look-ahead loads from being hoisted across chunks)
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// Forward rows [RR, RR + 16 nb) from TMEM (base row RR at column 0): chunk c + 1 is loaded while
+// chunk c is eliminated, (p, rcp) read kTmAhead rows ahead. Quotients are range-checked here.
+template <bool kGuard>
+__device__ __forceinline__ void tmem_forward(unsigned tm, int nb, const double2* pr, double negr, double& d,
+                                             unsigned& qmin) {
+    auto divide = [&](double num, double2 p) { return kGuard ? div_guarded(num, p) : div_fast(num, p); };
+    static_assert(kTmBody % kTmAhead == 0 && kTmBody % 16 == 0, "ring slots");
+    double2 pv[kTmAhead];
+#pragma unroll
+    for (int u = 0; u < kTmAhead; ++u) pv[u] = pr[u];
+    Tm8 A, B;
+    tm_wait_st();  // the back pass's stores
+    tm_ld(tm, A);
+    tm_wait_ld(A);
+#pragma unroll 1
+    for (int b = 0; b < nb; ++b) {
+#pragma unroll
+        for (int c = 0; c < kTmBody / 8; ++c) {
+            Tm8& cur = (c & 1) ? B : A;
+            Tm8& nxt = (c & 1) ? A : B;
+            const int ch = (kTmBody / 8) * b + c;
+            const bool more = c + 1 < kTmBody / 8 || b + 1 < nb;
+            if (more) tm_ld(tm + 16u * (ch + 1), nxt);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int rr = 8 * c + u;
+                d = divide(__dsub_rn(cur.get(u), __dmul_rn(negr, d)), pv[rr % kTmAhead]);
+                pv[rr % kTmAhead] = pr[kTmBody * b + rr + kTmAhead];
+                cur.put(u, d);
+                qmin = min(qmin, hi_abs(d) - 1u);
+            }
+            tm_st(tm + 16u * ch, cur);
+            if (more) tm_wait_ld(nxt);
+        }
+    }
+}
+
+// Back substitution over the TMEM rows, last chunk first; cc = c of row RR; c read kBackAhead rows
+// ahead.
+__device__ __forceinline__ void tmem_back(unsigned tm, int nb, const double* cc, double& d) {
+    static_assert(kTmBody % kBackAhead == 0 && kBackAhead == 8, "ring slots");
+    const int nch = nb * (kTmBody / 8);
+    double cv[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) cv[v] = cc[8 * nch - 1 - v];
+    Tm8 A, B;
+    tm_wait_st();  // the forward pass's stores
+    tm_ld(tm + 16u * (nch - 1), A);
+    tm_wait_ld(A);
+#pragma unroll 1
+    for (int b = 0; b < nb; ++b) {
+#pragma unroll
+        for (int c = 0; c < kTmBody / 8; ++c) {
+            Tm8& cur = (c & 1) ? B : A;
+            Tm8& nxt = (c & 1) ? A : B;
+            const int ch = nch - 1 - ((kTmBody / 8) * b + c);
+            const bool more = c + 1 < kTmBody / 8 || b + 1 < nb;
+            if (more) tm_ld(tm + 16u * (ch - 1), nxt);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+                const int u = 7 - v;
+                d = __dsub_rn(cur.get(u), __dmul_rn(cv[v], d));
+                cv[v] = cc[8 * ch + u - 8];
+                cur.put(u, d);
+            }
+            tm_st(tm + 16u * ch, cur);
+            if (more) tm_wait_ld(nxt);
+        }
+    }
+}
+
 // Forward elimination of one step (linalg.cpp:84-90). Forced warps first add the forcing
 // increment, x + h*b (pde_problems.cpp:93, __dadd_rn as the reference's `state[i] += dt*b[i]`).
 // Rows [0, RR) in reg[], the rest at st[32*(i-RR)], software-pipelined kFwdAhead rows ahead
 // (every load is issued before the stores in front of it: the compiler cannot hoist a shared load
 // above a shared store it cannot disambiguate). Quotients are range-checked off the chain: the
 // register rows here, the shared rows in column_back. Returns q_{n-1}; dm1 = q_{n-2}.
-template <int RR, int kMode, bool kGuard>
+template <int RR, int kMode, bool kGuard, int kLS = lane_stride(kMode), bool kTm = false>
 __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1], double* st,
-                                                 const StagedStep<kMode>& V, double& dm1, unsigned& qmin) {
+                                                 const StagedStep<kMode>& V, double& dm1, unsigned& qmin,
+                                                 unsigned tm = 0, int tm_bodies = 0) {
     constexpr int kS = StagedStep<kMode>::kS;
     constexpr bool kForced = StagedStep<kMode>::kForced;
     const int n = V.n;
@@ -316,15 +466,17 @@ __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1],
         qmin = min(qmin, hi_abs(d) - 1u);  // ~40 cycles of chain per row: room for the check here
     }
     dm1 = d;
-    const int last = n - 1 - RR;  // last shared row (>= 0)
-    const double2* pr = PR + RR * kS;
-    const double* hb = HB + RR * kS;
+    const int B = RR + (kTm ? kTmBody * tm_bodies : 0);  // first shared row
+    if (kTm) tmem_forward<kGuard>(tm, tm_bodies, PR + RR, negr, d, qmin);
+    const int last = n - 1 - B;  // last shared row (>= 0)
+    const double2* pr = PR + B * kS;
+    const double* hb = HB + B * kS;
     double2 pv[kFwdAhead];
     double xv[kFwdAhead], hv[kFwdAhead];
 #pragma unroll
     for (int u = 0; u < kFwdAhead; ++u) {
         pv[u] = pr[u * kS];
-        xv[u] = st[32 * u];
+        xv[u] = st[kLS * u];
         hv[u] = kForced ? hb[u * kS] : 0.0;
     }
     // ring slot u holds row r + u; full blocks refill without predicates (a predicated refill
@@ -334,7 +486,7 @@ __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1],
         const double x = kForced ? __dadd_rn(x0, h) : x0;
         dm1 = d;
         d = divide(__dsub_rn(x, __dmul_rn(negr, d)), p);
-        st[32 * rr] = d;
+        st[kLS * rr] = d;
     };
     int r = 0;
 #pragma unroll 1
@@ -343,7 +495,7 @@ __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1],
         for (int u = 0; u < kFwdAhead; ++u) {  // consume, then refill the slot in place
             row(r + u, pv[u], xv[u], hv[u]);
             pv[u] = pr[(r + u + kFwdAhead) * kS];
-            xv[u] = st[32 * (r + u + kFwdAhead)];
+            xv[u] = st[kLS * (r + u + kFwdAhead)];
             if (kForced) hv[u] = hb[(r + u + kFwdAhead) * kS];
         }
     }
@@ -358,26 +510,28 @@ __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1],
 // forward quotients (zero wraps to the maximum, so exact zeros pass): a quotient below 2^-950
 // means its dividend may have left Markstein's range (one VIADDMNMX per row) — for the shared
 // rows here, as they are read back anyway; for the register rows in column_forward.
-template <int RR, int kMode>
+template <int RR, int kMode, int kLS = lane_stride(kMode), bool kTm = false>
 __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], double* st, const StagedStep<kMode>& V,
-                                            double d, double dm1, unsigned& qmin) {
+                                            double d, double dm1, unsigned& qmin, unsigned tm = 0,
+                                            int tm_bodies = 0) {
     constexpr int kS = StagedStep<kMode>::kSc;
     const int n = V.n;
     const double* CC = V.cc();
-    const int top = n - 2 - RR;  // first shared row of the back pass
+    const int B = RR + (kTm ? kTmBody * tm_bodies : 0);  // first shared row
+    const int top = n - 2 - B;                           // first shared row of the back pass
     if (top >= 0) {
         double yv[kBackAhead], cv[kBackAhead];
-        const double* cc = CC + RR * kS;
+        const double* cc = CC + B * kS;
 #pragma unroll
         for (int u = 0; u < kBackAhead; ++u) {
-            yv[u] = (u == 0) ? dm1 : st[32 * (top - u)];
+            yv[u] = (u == 0) ? dm1 : st[kLS * (top - u)];
             cv[u] = cc[(top - u) * kS];
         }
         // ring slot u holds row r - u (see column_forward)
         auto row = [&](int rr, double y, double c) {
             qmin = min(qmin, hi_abs(y) - 1u);
             d = __dsub_rn(y, __dmul_rn(c, d));
-            st[32 * rr] = d;
+            st[kLS * rr] = d;
         };
         int r = top;
 #pragma unroll 1
@@ -385,7 +539,7 @@ __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], doub
 #pragma unroll
             for (int u = 0; u < kBackAhead; ++u) {  // consume, then refill the slot in place
                 row(r - u, yv[u], cv[u]);
-                yv[u] = st[32 * (r - u - kBackAhead)];
+                yv[u] = st[kLS * (r - u - kBackAhead)];
                 cv[u] = cc[(r - u - kBackAhead) * kS];
             }
         }
@@ -393,6 +547,7 @@ __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], doub
         for (int u = 0; u < kBackAhead - 1; ++u)
             if (r - u >= 0) row(r - u, yv[u], cv[u]);
     }
+    if (kTm) tmem_back(tm, tm_bodies, CC + RR, d);
 #pragma unroll
     for (int i = RR - 1; i >= 0; --i) {  // (RR > 0 only for n >= RR + 2: every register row is a back row)
         d = __dsub_rn(reg[i], __dmul_rn(CC[i * kS], d));  // (the register rows' quotients were checked
@@ -460,11 +615,14 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
     const int lane = threadIdx.x;
     const long long slice = kGroup ? 32ll * blockIdx.x + lane : kForced ? blockIdx.x : blockIdx.x / P.wps;
     const long long g0 = kGroup ? blockIdx.x : slice;  // the block's slice group / slice
-    const int k = kForced ? (kGroup || lane == 0 ? n : n + 1) : static_cast<int>(blockIdx.x - g0 * P.wps) * 32 + lane;
-    const bool live = kGroup ? slice < P.N : k < n + (kForced ? 1 : 0);
+    // (single-forced: all 32 lanes run the forced column on one shared copy of the state; lane 0
+    // writes it out)
+    constexpr int kLS = lane_stride(kMode);
+    const int k = kForced ? n : static_cast<int>(blockIdx.x - g0 * P.wps) * 32 + lane;
+    const bool live = kGroup ? slice < P.N : kForced ? lane == 0 : k < n;
     double* R = smem + front_pad(n, kMode);
-    double* st = R + staged_doubles(n, kMode) + lane;
-    const unsigned bar_f = smem_u32(R + staged_doubles(n, kMode) + (n - RR) * 32 + 32 * kFwdAhead);
+    double* st = R + staged_doubles(n, kMode) + (kLS == 32 ? lane : 0);
+    const unsigned bar_f = smem_u32(R + staged_doubles(n, kMode) + (n - RR) * kLS + kLS * kFwdAhead);
     const unsigned bar_b = bar_f + 8;
     const long long my_steps = (kGroup && !live) ? 0 : P.step_off[slice + 1] - P.step_off[slice];
     const long long steps = kGroup ? __reduce_max_sync(0xffffffffu, static_cast<unsigned>(my_steps)) : my_steps;
@@ -512,7 +670,7 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
     double reg[RR > 0 ? RR : 1];
 #pragma unroll
     for (int i = 0; i < RR; ++i) reg[i] = (i == k) ? 1.0 : 0.0;  // e_k; the forced run starts at 0
-    for (int i = RR; i < n; ++i) st[(i - RR) * 32] = (i == k) ? 1.0 : 0.0;
+    for (int i = RR; i < n; ++i) st[(i - RR) * kLS] = (i == k) ? 1.0 : 0.0;
 
     unsigned qmin = 0xffffffffu;
 #ifdef PINT_HEAT_PROF
@@ -554,13 +712,141 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
         double* gp = P.maps + slice * n * P.ldm + k;
 #pragma unroll
         for (int i = 0; i < RR; ++i) gp[i * P.ldm] = reg[i];
-        for (int i = RR; i < n; ++i) gp[i * P.ldm] = st[(i - RR) * 32];
+        for (int i = RR; i < n; ++i) gp[i * P.ldm] = st[(i - RR) * kLS];
         if (!kGuard && qmin < kQuotLo - 1u) record_failure(P.fail, kRetryIndex + slice, PINT_E_RANGE_RETRY, 0.0);
     }
     if (P.per_slice_ns && (kGroup ? live : lane == 0)) atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
     // basis grid: complete only after the forced grid (so the stream order after this launch
     // holds for both); it overlapped this whole kernel, so the wait costs nothing
     if (!kForced) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
+template <bool kGuard>
+__global__ void __launch_bounds__(160, 1) heat_build_tmem_kernel(const __grid_constant__ BuildPlan P) {
+    constexpr int RR = kTmRegRows;
+    extern __shared__ __align__(128) double smem[];
+    const unsigned long long t_start = pint_dev::globaltimer();
+    const int n = P.n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cps = (P.wps + 3) / 4;  // CTAs per slice
+    const long long slice = blockIdx.x / cps;
+    const int cta = static_cast<int>(blockIdx.x - slice * cps);
+    const bool forced = warp == 4;
+    const int g = 4 * cta + warp;
+    const bool wlive = forced ? cta == 0 : g < P.wps;  // this warp has columns
+    const int k = forced ? n : 32 * g + lane;
+    const int nlive = min(4, P.wps - 4 * cta) + (cta == 0 ? 1 : 0);
+    const int nb = tm_rows(n) / kTmBody;
+    const long long M = tm_shared_rows(n);
+    double* R = smem;
+    double* st = forced ? R + tm_forced_off(n) : R + record_stride(n) + warp * M * 32 + lane;
+    double* tail = R + tm_smem_doubles(n) - 4;
+    const unsigned bar_f = smem_u32(tail), bar_b = bar_f + 8;
+    unsigned* cnt = reinterpret_cast<unsigned*>(tail + 2);
+    unsigned* tslot = reinterpret_cast<unsigned*>(tail + 3);
+    const long long steps = P.step_off[slice + 1] - P.step_off[slice];
+    const RecView V = rec_view(P.rec, n, P.N, P.S);
+    const unsigned fwd_bytes = 8u * static_cast<unsigned>(cc_offset(n));  // header, (p, rcp), h*b
+    const unsigned back_bytes = 8u * static_cast<unsigned>(even(n));
+    auto load_fwd = [&](long long s) { bulk_load(smem_u32(R), V.rec(slice, s), fwd_bytes, bar_f); };
+    auto load_back = [&](long long s) {
+        bulk_load(smem_u32(R + cc_offset(n)), V.rec(slice, s) + cc_offset(n), back_bytes, bar_b);
+    };
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tslot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(bar_f);
+        mbar_init(bar_b);
+        cnt[0] = cnt[1] = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const unsigned tm = *tslot + ((32u * static_cast<unsigned>(warp & 3)) << 16);
+    if (threadIdx.x == 0 && steps > 0) {
+        load_fwd(0);
+        load_back(0);
+        if (steps > 1) prefetch_l2(V.rec(slice, 1), 8u * static_cast<unsigned>(record_stride(n)));
+    }
+    double reg[RR];
+#pragma unroll
+    for (int i = 0; i < RR; ++i) reg[i] = (i == k) ? 1.0 : 0.0;  // e_k; the forced run starts at 0
+    if (!forced) {
+        for (int ch = 0; ch < nb * (kTmBody / 8); ++ch) {
+            Tm8 t;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t.put(u, (RR + 8 * ch + u == k) ? 1.0 : 0.0);
+            tm_st(tm + 16u * ch, t);
+        }
+    }
+    const int kls = forced ? 1 : 32;
+    for (long long i = RR + (forced ? 0 : nb * kTmBody); i < n; ++i)
+        st[(i - RR - (forced ? 0 : nb * kTmBody)) * kls] = (i == k) ? 1.0 : 0.0;
+
+    unsigned qmin = 0xffffffffu;
+    const StagedStep<kBasis> SB{R, n, lane, 0};
+    const StagedStep<kForcedSingle> SF{R, n, lane, 0};
+    if (wlive) {
+        for (long long s = 0; s < steps; ++s) {
+            const unsigned parity = static_cast<unsigned>(s & 1);
+            mbar_wait(bar_f, parity);
+            double d, dm1 = 0.0;
+            if (forced) d = column_forward<RR, kForcedSingle, kGuard>(reg, st, SF, dm1, qmin);
+            else d = column_forward<RR, kBasis, kGuard, 32, true>(reg, st, SB, dm1, qmin, tm, nb);
+            qmin = min(qmin, hi_abs(d) - 1u);
+            __syncwarp();
+            if (lane == 0) {  // the last of the CTA's live warps to finish the forward half refills it
+                __threadfence_block();
+                if (atomicAdd(cnt, 1u) % nlive == static_cast<unsigned>(nlive - 1) && s + 1 < steps) load_fwd(s + 1);
+            }
+            mbar_wait(bar_b, parity);
+            if (forced) column_back<RR, kForcedSingle>(reg, st, SF, d, dm1, qmin);
+            else column_back<RR, kBasis, 32, true>(reg, st, SB, d, dm1, qmin, tm, nb);
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                if (atomicAdd(cnt + 1, 1u) % nlive == static_cast<unsigned>(nlive - 1) && s + 1 < steps) {
+                    load_back(s + 1);
+                    if (s + 2 < steps) prefetch_l2(V.rec(slice, s + 2), 8u * static_cast<unsigned>(record_stride(n)));
+                }
+            }
+        }
+        const bool live = forced ? lane == 0 : k < n;
+        double* gp = P.maps + slice * n * P.ldm + k;
+        if (live) {
+#pragma unroll
+            for (int i = 0; i < RR; ++i) gp[i * P.ldm] = reg[i];
+        }
+        long long i0 = RR;
+        if (!forced) {
+            tm_wait_st();
+            for (int ch = 0; ch < nb * (kTmBody / 8); ++ch) {
+                Tm8 t;
+                tm_ld(tm + 16u * ch, t);
+                tm_wait_ld(t);
+                if (live) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) gp[(RR + 8 * ch + u) * P.ldm] = t.get(u);
+                }
+            }
+            i0 += nb * kTmBody;
+        }
+        if (live) {
+            for (long long i = i0; i < n; ++i) gp[i * P.ldm] = st[(i - i0) * kls];
+            if (!kGuard && qmin < kQuotLo - 1u) record_failure(P.fail, kRetryIndex + slice, PINT_E_RANGE_RETRY, 0.0);
+        }
+        if (P.per_slice_ns && lane == 0) atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
+    }
+    tm_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(*tslot) : "memory");
 }
 
 // ---- integrate: K caller columns of one slice (records with N = 1), guarded division ----------
@@ -741,6 +1027,14 @@ int launch_heat_build(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int6
     P.ldm = pint_affine_ldm(n);
     P.per_slice_ns = per_slice_ns;
     P.fail = ctx->d_fail;
+    if (use_tmem(n)) {
+        const size_t smem = sizeof(double) * tm_smem_doubles(n);
+        auto kern = guarded ? heat_build_tmem_kernel<true> : heat_build_tmem_kernel<false>;
+        smem_attrs(kern, smem);
+        const long long ctas = N * ((P.wps + 3) / 4);
+        kern<<<static_cast<unsigned>(ctas), 160, smem, ctx->stream>>>(P);
+        return pint_check_launch(ctx, "heat_build_tmem_kernel");
+    }
     static_assert(reg_rows(kRegRows + 2) == kRegRows, "reg_rows");
     if (reg_rows(n) == kRegRows)
         return guarded ? launch_build<kRegRows, true>(ctx, P) : launch_build<kRegRows, false>(ctx, P);

@@ -333,15 +333,34 @@ def test_heat_config4_shape_n512(ctx):
     assert np.max(np.abs(rt.final_state - y_chain)) / np.max(np.abs(y_chain)) <= REL_F64
 
 
-def test_heat_underflow_retries_guarded(ctx):
-    """dt = 1e-9 at n = 128: r ~ 2e-5, so a basis column decays like r^|i-k| and runs through the
+@pytest.mark.parametrize("n", [270, 300, 384, 520])
+def test_heat_large_n_build_paths(ctx, n):
+    """The large-n builds, bit-exact against the oracle: n = 270 the one-warp-CTA build with the
+    compact single-forced warp; n = 300 / 384 / 520 the TMEM build (rows split registers / tensor
+    memory / shared; 300: idle warps in a slice's last CTA, 520: the largest n it takes)."""
+    N, S = 3, 3
+    dx, dt = 1.0 / (n + 1), 1e-3
+    T = N * S * dt
+    prob = pint.make_heat_problem(dx, dt, T)
+    dec = pint.decompose(0.0, T, N, dt)
+    G, c = pint.build_affine_propagators(prob, dec)
+    for j in range(N):
+        s = dec.slices[j]
+        Gw, cw = O.heat_build(dx, s.t_begin, s.t_end, dt)
+        assert np.array_equal(G[j], Gw) and np.array_equal(c[j], cw)
+
+
+@pytest.mark.parametrize("n", [128, 300])
+def test_heat_underflow_retries_guarded(ctx, n):
+    """dt = 1e-9: r ~ 2e-5 (n = 128), so a basis column decays like r^|i-k| and runs through the
     subnormal range inside the first step. The fast build must notice (range check off the chain
-    -> PINT_E_RANGE_RETRY) and the guarded build must then match the reference bit-for-bit."""
+    -> PINT_E_RANGE_RETRY) and the guarded build must then match the reference bit-for-bit
+    (n = 300: the TMEM build's guarded variant)."""
     import torch
 
     from paper_1304_6514_b200.dist import HeatPlan
 
-    dx, dt, T, N = 1.0 / 129.0, 1e-9, 6e-9, 2
+    dx, dt, T, N = 1.0 / (n + 1), 1e-9, 6e-9, 2
     plan = HeatPlan(ctx, dx, dt, T, N)
     plan.upload()
     plan.factor_and_build()
@@ -362,7 +381,8 @@ def test_heat_underflow_retries_guarded(ctx):
 
 def test_affine_tree_random_maps(ctx):
     rng = np.random.default_rng(1304)
-    for N, n in [(1, 5), (2, 9), (13, 9), (64, 128), (7, 200)]:
+    # n = 240 / 256: the cluster chain with a 3-deep ring; n = 300: the single-CTA chain
+    for N, n in [(1, 5), (2, 9), (13, 9), (64, 128), (7, 200), (9, 240), (6, 256), (5, 300)]:
         G = rng.uniform(-1, 1, (N, n, n)) / np.sqrt(n)
         c = rng.uniform(-1, 1, (N, n))
         y0 = rng.uniform(-1, 1, n)

@@ -40,5 +40,31 @@ def main():
                       "compose_ms": w[:, 3].mean(), "host_tables_ms(py, incl. pinned alloc)": tables_ms}))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def host_tables_ms(reps: int = 20) -> float:
+    """Host-only time of pint_heat_coefficients for the bench's slices (the glibc sin/cos tables)."""
+    from paper_1304_6514_b200 import capi, pint
+    from paper_1304_6514_b200.dist import closure_slices
+
+    n, N, S, T = 128, 256, 256, 10.0
+    dx, dt = 1.0 / (n + 1), T / (N * S)
+    sl = closure_slices(pint.decompose(0.0, T, N, dt), dt)
+    arr = (capi.Slice * N)(*sl)
+    Q = sum(s.steps for s in sl)
+    off, r, fa, fb, sx = np.empty(N + 1, np.int64), np.empty(Q), np.empty(Q), np.empty(Q), np.empty(n)
+    nn = C.c_int64()
+    lib = capi.load()
+    best = 1e9
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        lib.pint_heat_coefficients(dx, arr, N, capi.ptr(off), capi.ptr(r), capi.ptr(fa), capi.ptr(fb),
+                                   capi.ptr(sx), C.byref(nn))
+        best = min(best, time.perf_counter() - t0)
+    return best * 1e3
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "--host":
+    print(json.dumps({"host_tables_ms": host_tables_ms()}))
