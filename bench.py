@@ -32,7 +32,15 @@ import time
 ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "ODE trajectory-steps/s (heat n=128 affine slice maps + tree compose)"
+METRIC = "ODE trajectory-steps/s (heat affine slice maps + tree compose)"
+
+
+def workload_name(n: int, slices_per_gpu: int, S: int) -> str:
+    """BASELINE.json config the flags select: configs[1] (default) or configs[3]'s per-GPU share."""
+    if n == 512:
+        return f"heat n=512 affine slice maps + tree compose (BASELINE.json configs[3]: {slices_per_gpu} " \
+               f"slices per GPU of 4096 at S={S})"
+    return f"heat n={n} affine slice maps + tree compose (BASELINE.json configs[1])"
 UNIT = "traj-steps/s"
 
 
@@ -173,7 +181,7 @@ def reference_arm(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "heat n=128 affine slice maps (BASELINE.json configs[1])", "n": args.n,
+        "config": {"workload": workload_name(args.n, args.slices_per_gpu, args.S), "n": args.n,
                    "slices": N, "steps_per_slice": args.S, "T": args.T, "compose": "chain (reference)"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -321,7 +329,10 @@ def main():
     prof = ROOT / "profiles" / "r01_build_traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            tr = json.loads(prof.read_text())
+            # (only when the capture is of this very configuration)
+            if tuple(tr.get("config", (128, 256, 256))) == (n, args.slices_per_gpu, args.S):
+                traffic = tr.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -346,14 +357,15 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "heat n=128 affine slice maps + tree compose (BASELINE.json configs[1])",
+            "config": {"workload": workload_name(n, args.slices_per_gpu, args.S),
                        "n": n, "slices": N, "slices_per_gpu": args.slices_per_gpu, "steps_per_slice": S, "T": T,
                        "dt": dt, "compose": "tree (DMMA)" + (" + NCCL gather" if world > 1 else ""),
                        "parallelism": f"slice blocks x{world}", "l2": "flushed (256 MB write) between steps",
                        "time_to_solution_ms": ms_per_step, "e2e_time_to_solution_ms": e2e_secs / args.steps * 1e3},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
-            "roofline": {"bound": "fp64", "kernel": "heat_build_kernel", "achieved": achieved,
+            "roofline": {"bound": "fp64", "kernel": "heat_build_tmem_kernel" if 282 <= n <= 520 else "heat_build_kernel",  # (heat.cu use_tmem)
+                         "achieved": achieved,
                          "peak": peak64.value, "unit": "TFLOP/s", "frac": achieved / peak64.value,
                          "traffic": traffic, "peak_source": "measured DFMA probe (pint_probe_peak)",
                          "flops_per_launch": build_flops, "launch_ms": build_ms,

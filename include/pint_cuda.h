@@ -240,7 +240,9 @@ int pint_run_wave(pint_ctx* ctx, int64_t d, const double* D2, double dt_native, 
 /* Host-buffer barycentric weights (interp.cpp:43-55 / closed form); DuplicateNodes -> code 5. */
 int pint_bary_weights(pint_ctx* ctx, int kind, int64_t M, const double* nodes, double* w);
 
-/* ---- roofline probe: measured FMA throughput (TFLOP/s) of this GPU for PINT_F64 / PINT_F32 */
+/* ---- roofline probe: measured FMA throughput (TFLOP/s) of this GPU for PINT_F64 / PINT_F32, or
+   the FP64 tensor-core (DMMA m8n8k4) throughput for PINT_PROBE_DMMA — the tree compose's roof */
+enum { PINT_PROBE_DMMA = 2 };
 int pint_probe_peak(pint_ctx* ctx, int precision, double* tflops);
 /* dependent-chain latency in SM cycles per op: {DFMA, DADD, DMUL, FFMA, LDS.64}, then cycles per
    heat forward row (5 dependent ops), per heat back row (2), per op of alternating DMUL/DADD */

@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "pint_internal.cuh"
 
@@ -188,10 +189,13 @@ __global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long lo
 }
 
 // ---- DMMA pair kernel ------------------------------------------------------------------------
-constexpr int BM = 64, BN = 64, BK = 16, kStages = 4;
+// CTA = 2 x 2 warps, warp tile (8 MI) x 32: BM = 16 MI rows, BN = 64 columns (+ the extra fragment).
+constexpr int BN = 64, BK = 16, kStages = 3;
 constexpr int AS = BK + 4;       // padded strides: conflict-free fragment loads
 constexpr int BW = BN + 8;       // B tile width: 64 columns + one 8-column fragment for column n
 constexpr int BS = BW + 4;
+template <int MI>
+constexpr size_t pair_smem_bytes() { return sizeof(double) * kStages * (16 * MI * AS + BK * BS); }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -204,10 +208,12 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // column n) and the epilogue adds c2 to column n. Column tiles cover n columns; when n is a
 // multiple of 64 the column n would open a 64-wide tile of its own, so the last tile's right-hand
 // warps carry one extra 8-column fragment instead.
+template <int MI>
 __global__ void __launch_bounds__(128)
 affine_pair_kernel(long long n, long long ldm, const double* __restrict__ earlier,
                    long long e_stride, const double* __restrict__ later, long long l_stride,
-                   double* __restrict__ out, long long o_stride, int tilesN) {
+                   double* __restrict__ out, long long o_stride) {
+    constexpr int BM = 16 * MI;
     const long long p = blockIdx.z;
     const double* E = earlier + p * e_stride;
     const double* L = later + p * l_stride;
@@ -215,9 +221,8 @@ affine_pair_kernel(long long n, long long ldm, const double* __restrict__ earlie
     const long long row0 = static_cast<long long>(blockIdx.y) * BM;
     const int tid = threadIdx.x;
     const long long nc = n + 1;  // output / B columns
-    (void)tilesN;
 
-    // kStages-deep cp.async pipeline of 64x16 (A) and 16x64 (B) tiles; out-of-range elements are
+    // kStages-deep cp.async pipeline of BMx16 (A) and 16x72 (B) tiles; out-of-range elements are
     // zero-filled by the copy itself (src-size 0 or 8 of 16)
     extern __shared__ __align__(16) double pair_smem[];
     double* As = pair_smem;                        // [kStages][BM * AS]
@@ -227,9 +232,9 @@ affine_pair_kernel(long long n, long long ldm, const double* __restrict__ earlie
     const int wm = warp >> 1, wn = warp & 1;
     const int g = lane >> 2, t4 = lane & 3;
 
-    double acc[4][5][2];
+    double acc[MI][5][2];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < MI; ++a)
 #pragma unroll
         for (int b = 0; b < 5; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
     const bool extra = wn == 1 && col0 + BN == n;  // this warp also owns columns n .. n+7
@@ -241,12 +246,16 @@ affine_pair_kernel(long long n, long long ldm, const double* __restrict__ earlie
     };
     auto issue = [&](int stage, long long k0) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int idx = tid + u * 128;  // 0..511: 16-byte chunks of each tile
+        for (int u = 0; u < MI; ++u) {  // A: BM x 16 = 8 MI x 128 16-byte chunks
+            const int idx = tid + u * 128;
             const int ar = idx >> 3, ac = (idx & 7) * 2;
             const long long gr = row0 + ar, gc = k0 + ac;
             const long long abytes = gr < n ? 8 * max(0ll, min(2ll, n - gc)) : 0;
             cp16(As + stage * BM * AS + ar * AS + ac, abytes ? L + gr * ldm + gc : L, abytes);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // B: 16 x 64
+            const int idx = tid + u * 128;
             const int br = idx >> 5, bc = (idx & 31) * 2;
             const long long gk = k0 + br, gn = col0 + bc;
             const long long bbytes = gk < n ? 8 * max(0ll, min(2ll, nc - gn)) : 0;
@@ -276,25 +285,25 @@ affine_pair_kernel(long long n, long long ldm, const double* __restrict__ earlie
         const double* B = Bs + (kt % kStages) * BK * BS;
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
-            double af[4], bf[4];
+            double af[MI], bf[4];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi) af[mi] = A[(wm * 32 + mi * 8 + g) * AS + kk + t4];
+            for (int mi = 0; mi < MI; ++mi) af[mi] = A[(wm * 8 * MI + mi * 8 + g) * AS + kk + t4];
 #pragma unroll
             for (int ni = 0; ni < 4; ++ni) bf[ni] = B[(kk + t4) * BS + wn * 32 + ni * 8 + g];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
+            for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
                 for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
             if (extra) {
                 const double bx = B[(kk + t4) * BS + BN + g];
 #pragma unroll
-                for (int mi = 0; mi < 4; ++mi) dmma(acc[mi][4][0], acc[mi][4][1], af[mi], bx);
+                for (int mi = 0; mi < MI; ++mi) dmma(acc[mi][4][0], acc[mi][4][1], af[mi], bx);
             }
         }
     }
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi) {
-        const long long r = row0 + wm * 32 + mi * 8 + g;
+    for (int mi = 0; mi < MI; ++mi) {
+        const long long r = row0 + wm * 8 * MI + mi * 8 + g;
         if (r >= n) continue;
 #pragma unroll
         for (int ni = 0; ni < 5; ++ni) {
@@ -312,23 +321,39 @@ affine_pair_kernel(long long n, long long ldm, const double* __restrict__ earlie
     }
 }
 
-int launch_pairs(pint_ctx* ctx, long long n, long long P, const double* earlier, long long e_stride,
-                 const double* later, long long l_stride, double* out, long long o_stride) {
-    if (P <= 0) return PINT_OK;
+template <int MI>
+int launch_pairs_mi(pint_ctx* ctx, long long n, long long P, const double* earlier, long long e_stride,
+                    const double* later, long long l_stride, double* out, long long o_stride) {
     const long long ldm = pint_affine_ldm(n);
-    const int tilesN = static_cast<int>((n + BN - 1) / BN);  // (column n: see affine_pair_kernel)
-    const unsigned tilesM = static_cast<unsigned>((n + BM - 1) / BM);
-    if (P > 65535) return pint_set_error(ctx, PINT_E_INVALID, "affine_pair: too many pairs per launch");
-    dim3 grid(static_cast<unsigned>(tilesN), tilesM, static_cast<unsigned>(P));
-    constexpr size_t smem = sizeof(double) * kStages * (BM * AS + BK * BS);
+    const unsigned tilesN = static_cast<unsigned>((n + BN - 1) / BN);  // (column n: see affine_pair_kernel)
+    const unsigned tilesM = static_cast<unsigned>((n + 16 * MI - 1) / (16 * MI));
+    dim3 grid(tilesN, tilesM, static_cast<unsigned>(P));
+    constexpr size_t smem = pair_smem_bytes<MI>();
     static bool attr = [] {
-        return cudaFuncSetAttribute(affine_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        return cudaFuncSetAttribute(affine_pair_kernel<MI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)) == cudaSuccess;
     }();
     (void)attr;
-    affine_pair_kernel<<<grid, 128, smem, ctx->stream>>>(n, ldm, earlier, e_stride, later, l_stride, out,
-                                                      o_stride, tilesN);
+    affine_pair_kernel<MI><<<grid, 128, smem, ctx->stream>>>(n, ldm, earlier, e_stride, later, l_stride, out,
+                                                             o_stride);
     return pint_check_launch(ctx, "affine_pair_kernel");
+}
+
+int launch_pairs(pint_ctx* ctx, long long n, long long P, const double* earlier, long long e_stride,
+                 const double* later, long long l_stride, double* out, long long o_stride) {
+    if (P <= 0) return PINT_OK;
+    if (P > 65535) return pint_set_error(ctx, PINT_E_INVALID, "affine_pair: too many pairs per launch");
+    // PINT_PAIR_MI: tile-shape experiments only
+    static const int mi_env = [] {
+        const char* e = std::getenv("PINT_PAIR_MI");
+        return e ? std::atoi(e) : 0;
+    }();
+    // 128-row tiles (warp tile 64 x 32: half the B-fragment loads per DMMA) pay once the grid is
+    // large enough to fill the SMs anyway (n = 512: tree -9%); at n = 128 the 64-row tiles win
+    const int mi = mi_env ? mi_env : n >= 384 ? 8 : 4;
+    if (mi == 8) return launch_pairs_mi<8>(ctx, n, P, earlier, e_stride, later, l_stride, out, o_stride);
+    if (mi == 6) return launch_pairs_mi<6>(ctx, n, P, earlier, e_stride, later, l_stride, out, o_stride);
+    return launch_pairs_mi<4>(ctx, n, P, earlier, e_stride, later, l_stride, out, o_stride);
 }
 
 }  // namespace

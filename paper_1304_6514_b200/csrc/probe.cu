@@ -20,6 +20,25 @@ __global__ void __launch_bounds__(256) fma_probe_kernel(int iters, R seed, R* si
     if (s == R(-1)) sink[threadIdx.x] = s;  // never true; keeps the chains alive
 }
 
+// FP64 tensor-core throughput: 8 independent m8n8k4 accumulators per warp.
+__global__ void __launch_bounds__(256) dmma_probe_kernel(int iters, double seed, double* sink) {
+    double acc[8][2];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k][0] = acc[k][1] = seed * k;
+    const double a = seed + threadIdx.x, b = 0.5 + 1e-3 * threadIdx.x;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(acc[k][0]), "+d"(acc[k][1])
+                         : "d"(a), "d"(b));
+    }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += acc[k][0] + acc[k][1];
+    if (s == -1.0) sink[threadIdx.x] = s;
+}
+
 // Dependent-chain latency of one warp, cycles per op: out = {DFMA, DADD, DMUL, FFMA, LDS.64};
 // then cycles per ROW of the heat build's two recurrences: out[5] = forward row
 // (x - negr*d, then the Markstein division: 5 dependent ops), out[6] = back row (y - c*d: 2 ops),
@@ -103,7 +122,9 @@ extern "C" int pint_probe_peak(pint_ctx* ctx, int precision, double* tflops) {
     float best = 1e30f;
     for (int rep = 0; rep < 4; ++rep) {
         cudaEventRecord(ctx->ev0, ctx->stream);
-        if (precision == PINT_F32)
+        if (precision == PINT_PROBE_DMMA)
+            dmma_probe_kernel<<<blocks, 256, 0, ctx->stream>>>(iters / 8, 1.0, static_cast<double*>(sink));
+        else if (precision == PINT_F32)
             fma_probe_kernel<float><<<blocks, 256, 0, ctx->stream>>>(iters, 1.0f, static_cast<float*>(sink));
         else
             fma_probe_kernel<double><<<blocks, 256, 0, ctx->stream>>>(iters, 1.0, static_cast<double*>(sink));
@@ -114,7 +135,9 @@ extern "C" int pint_probe_peak(pint_ctx* ctx, int precision, double* tflops) {
         cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
         if (rep > 0 && ms < best) best = ms;
     }
-    const double flops = 2.0 * 8.0 * iters * 256.0 * blocks;
+    // DMMA: 8 m8n8k4 (512 flops each) per warp per iteration
+    const double flops = precision == PINT_PROBE_DMMA ? 512.0 * 8.0 * (iters / 8) * 8.0 * blocks
+                                                      : 2.0 * 8.0 * iters * 256.0 * blocks;
     *tflops = flops / (best * 1e-3) / 1e12;
     return PINT_OK;
 }

@@ -36,6 +36,8 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("report")
     p.add_argument("--round", default="r01")
+    p.add_argument("--name", default="", help="summary of another capture: profiles/<round>_<name>_ncu_summary.json")
+    p.add_argument("--config", default="128,256,256", help="n,N,S of the capture (build traffic file)")
     a = p.parse_args()
     raw = list(csv.reader(io.StringIO(ncu("-i", a.report, "--page", "raw", "--csv"))))
     hdr, units, rows = raw[0], raw[1], raw[2:]
@@ -52,6 +54,11 @@ def main():
         d["top_stalls_pct"] = {k: round(100 * v / tot, 1) for k, v in sorted(st.items(), key=lambda x: -x[1])[:6]}
         out[key] = d
     prof = ROOT / "profiles"
+    if a.name:
+        (prof / f"{a.round}_{a.name}_ncu_summary.json").write_text(json.dumps(out, indent=1) + "\n")
+        print(json.dumps({k: {m: v.get(m) for m in ("gpu__time_duration.sum", "dram__bytes_read.sum")}
+                          for k, v in out.items()}, indent=1))
+        return
     (prof / f"{a.round}_ncu_summary.json").write_text(json.dumps(out, indent=1) + "\n")
     # the dominant launch: the basis grid (mode 0), else any build kernel
     import re
@@ -69,6 +76,7 @@ def main():
         traffic = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
         (prof / f"{a.round}_build_traffic.json").write_text(json.dumps({
             "kernel": "heat_build_kernel (basis grid)", "dram_bytes_per_launch": int(traffic),
+            "config": [int(v) for v in a.config.split(",")],
             "source": f"profiles/{a.round}_ncu_summary.json (ncu --set full, one launch, n=128 N=256 S=256)"},
             indent=1) + "\n")
     print(json.dumps({k: {m: v.get(m) for m in ("gpu__time_duration.sum", "dram__bytes_read.sum")}
