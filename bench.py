@@ -29,10 +29,26 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "ODE trajectory-steps/s (heat affine slice maps + tree compose)"
+
+
+def chain_floor(n: int, slices: int, S: int, lat, build_ms: float, sm_mhz: float) -> dict:
+    """The build's real bound: every column is a chain of S*n dependent rows (forward + back row
+    latencies measured live by pint_probe_latency), run in `waves` rounds of resident columns."""
+    row = float(lat[5] + lat[6])
+    sms = 148
+    if 282 <= n <= 520:  # heat_build_tmem_kernel: one 5-warp CTA per SM per slice quarter
+        waves = -(-slices * -(-(-(-n // 32)) // 4) // sms)
+    else:  # one-warp CTAs; at C2 every warp is resident at once
+        waves = 1
+    floor_ms = waves * S * n * row / (sm_mhz * 1e3)
+    return {"chain_floor_ms": floor_ms, "frac_of_chain_floor": floor_ms / build_ms, "chain_row_cycles": row,
+            "chain_waves": waves}
 
 
 def workload_name(n: int, slices_per_gpu: int, S: int) -> str:
@@ -222,6 +238,8 @@ def main():
 
     peak64 = C.c_double()
     ctx.check(ctx.lib.pint_probe_peak(ctx.h, capi.F64, C.byref(peak64)))
+    lat = np.zeros(8)
+    ctx.check(ctx.lib.pint_probe_latency(ctx.h, capi.ptr(lat)))  # [5] forward row, [6] back row
 
     def one_step(events=None):
         if events:
@@ -353,6 +371,7 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
     if rank == 0:
+        csum = clocks.summary(t_region0, t_region1)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -370,8 +389,9 @@ def main():
                          "traffic": traffic, "peak_source": "measured DFMA probe (pint_probe_peak)",
                          "flops_per_launch": build_flops, "launch_ms": build_ms,
                          "share_of_step": build_ms / ms_per_step,
-                         "factor_ms": tot["factor"] / args.steps, "compose_ms": tot["compose"] / args.steps},
-            "clocks": clocks.summary(t_region0, t_region1),
+                         "factor_ms": tot["factor"] / args.steps, "compose_ms": tot["compose"] / args.steps,
+                         **chain_floor(n, hi - lo, S, lat, build_ms, csum.get("sm_mhz") or 1965.0)},
+            "clocks": csum,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -251,7 +251,7 @@ void pint_ctx_destroy(pint_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 5; ++i)
         if (ctx->scratch[i]) cudaFree(ctx->scratch[i]);
     if (ctx->d_fail) cudaFree(ctx->d_fail);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -533,8 +533,20 @@ int pint_run_scalar(pint_ctx* ctx, const pint_scalar_rhs* rhs, double t0, double
     if (!ok(ctx, cudaMemcpyAsync(d_in, h_in, in_bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D inputs"))
         return PINT_E_CUDA;
     if (per_slice_seconds) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
-    int rc = launch_scalar_ensemble(ctx, rhs, N, Mn, d_steps, d_dt, d_nodes, d_ends,
-                                    per_slice_seconds ? d_ns : nullptr);
+    int rc = PINT_OK;
+    const bool sweep = !serial && !f32;
+    if (sweep) {
+        // the weights depend on the nodes only: side stream, overlapping the ensemble
+        cudaEventRecord(ctx->ev_fork, ctx->stream);
+        cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
+        cudaStream_t main_stream = ctx->stream;
+        ctx->stream = ctx->side;
+        rc = launch_bary_weights(ctx, weight_kind, M, reinterpret_cast<const double*>(d_nodes), d_w);
+        ctx->stream = main_stream;
+        if (rc) return rc;
+        cudaEventRecord(ctx->ev_join, ctx->side);
+    }
+    rc = launch_scalar_ensemble(ctx, rhs, N, Mn, d_steps, d_dt, d_nodes, d_ends, per_slice_seconds ? d_ns : nullptr);
     if (rc) return rc;
     long long ext = 0;
     double y = 0.0;
@@ -543,7 +555,7 @@ int pint_run_scalar(pint_ctx* ctx, const pint_scalar_rhs* rhs, double t0, double
             return PINT_E_CUDA;
     } else {
         if (f32) return pint_set_error(ctx, PINT_E_INVALID, "FP32 runs support the ensemble only; sweep in FP64");
-        if ((rc = launch_bary_weights(ctx, weight_kind, M, reinterpret_cast<const double*>(d_nodes), d_w))) return rc;
+        cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);  // (the weights, from the side stream)
         cudaEventRecord(ctx->evc, ctx->stream);
         rc = launch_scalar_sweep(ctx, sweep_mode, N, M, reinterpret_cast<const double*>(d_nodes), 0, d_w,
                                  static_cast<const double*>(d_ends), d_ab, d_ab + 1, 0, y0, d_lam, d_y, d_ext);

@@ -14,21 +14,87 @@ namespace {
 
 using pint_dev::record_failure;
 
-__global__ void bary_product_kernel(long long M, const double* __restrict__ x, double* __restrict__ w,
-                                    FailRec* fail) {
+// w_j = 1 / prod_{k != j} (x_j - x_k) as the reference's running quotient acc /= (x_j - x_k), k in
+// order (interp.cpp:43-55). Each quotient must be the IEEE one; the chain runs M - 1 of them, so
+// the divide is Markstein's exact sequence — q0 = acc * rcp, rem = fma(-d, q0, acc), q = fma(rem,
+// rcp, q0) with rcp = RN(1/d) computed OFF the chain (it depends on the nodes only, bary_rcp_kernel):
+// 3 dependent ops instead of a full division. Exact (the correctly rounded quotient) when nothing under- or
+// overflows: |d| in [2^-60, 2^60] and |acc| in [2^-900, 2^900]; outside that window the step
+// takes __ddiv_rn (acc grows like the product of the inverse spacings, so large M gets there).
+__device__ __forceinline__ bool in_window(double v, unsigned lo_exp, unsigned hi_exp) {
+    const unsigned a = static_cast<unsigned>(__double2hiint(v)) & 0x7fffffffu;
+    return a - (lo_exp << 20) < ((hi_exp - lo_exp) << 20);
+}
+
+// The reciprocals depend on the nodes only: one massively parallel pass writes RN(1/(x_j - x_k))
+// for every pair, k-major (so the chain kernel's loads, lanes = consecutive j, are coalesced).
+__global__ void bary_rcp_kernel(long long M, const double* __restrict__ x, double* __restrict__ rcp) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= M * M) return;
+    const long long k = t / M, j = t - k * M;
+    rcp[t] = __drcp_rn(__dsub_rn(x[j], x[k]));
+}
+
+constexpr int kBaryChunk = 8;
+
+__global__ void __launch_bounds__(32) bary_product_kernel(long long M, const double* __restrict__ x,
+                                                          const double* __restrict__ rcp, double* __restrict__ w,
+                                                          FailRec* fail) {
+    extern __shared__ double xs[];  // the nodes, staged once per CTA
+    for (long long k = threadIdx.x; k < M; k += blockDim.x) xs[k] = x[k];
+    __syncwarp();
     const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= M) return;
-    const double xj = x[j];
+    const double xj = xs[j];
     double acc = 1.0;
     bool dup = false;
-    for (long long k = 0; k < M; ++k) {
-        if (k == j) continue;
-        const double diff = __dsub_rn(xj, x[k]);
-        if (diff == 0.0) {
-            dup = true;
-            break;
+    // reciprocals three chunks ahead through three fixed register sets (a rotation by moves would
+    // make every chunk wait for the loads it just issued)
+    auto fetch = [&](long long k0, double (&r)[kBaryChunk]) {
+#pragma unroll
+        for (int u = 0; u < kBaryChunk; ++u) r[u] = __ldg(rcp + (k0 + u < M ? k0 + u : 0) * M + j);
+    };
+    // A chunk runs the exact fast sequence unconditionally (a skipped k — k == j or past M — divides
+    // by d = 1 with r = 1: exact, acc unchanged) while tracking the windows; if any step left them,
+    // the chunk is redone from its starting value with IEEE divisions. No branch on the chain.
+    auto chunk = [&](long long k0, const double (&r)[kBaryChunk]) {
+        double d[kBaryChunk], rr[kBaryChunk];
+        bool use[kBaryChunk];
+#pragma unroll
+        for (int u = 0; u < kBaryChunk; ++u) {
+            const long long k = k0 + u < M ? k0 + u : 0;
+            use[u] = k0 + u < M && k != j;
+            const double dk = __dsub_rn(xj, xs[k]);
+            dup |= use[u] && dk == 0.0;
+            d[u] = use[u] ? dk : 1.0;
+            rr[u] = use[u] ? r[u] : 1.0;
         }
-        acc = __ddiv_rn(acc, diff);
+        const double acc0 = acc;
+        bool ok = true;
+#pragma unroll
+        for (int u = 0; u < kBaryChunk; ++u) {
+            ok &= in_window(d[u], 1023u - 60u, 1023u + 60u) & in_window(acc, 1023u - 900u, 1023u + 900u);
+            const double q0 = __dmul_rn(acc, rr[u]);
+            acc = __fma_rn(rr[u], __fma_rn(-d[u], q0, acc), q0);
+        }
+        if (!ok) {
+            acc = acc0;
+#pragma unroll 1
+            for (int u = 0; u < kBaryChunk; ++u)
+                if (use[u]) acc = __ddiv_rn(acc, d[u]);
+        }
+    };
+    double ra[kBaryChunk], rb[kBaryChunk], rc[kBaryChunk];
+    fetch(0, ra);
+    fetch(kBaryChunk, rb);
+    fetch(2 * kBaryChunk, rc);
+    for (long long k0 = 0; k0 < M; k0 += 3 * kBaryChunk) {
+        chunk(k0, ra);
+        fetch(k0 + 3 * kBaryChunk, ra);
+        chunk(k0 + kBaryChunk, rb);
+        fetch(k0 + 4 * kBaryChunk, rb);
+        chunk(k0 + 2 * kBaryChunk, rc);
+        fetch(k0 + 5 * kBaryChunk, rc);
     }
     if (dup) record_failure(fail, j, PINT_E_DUPLICATE_NODES, xj);
     w[j] = acc;
@@ -49,19 +115,16 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// One CTA walks the N slices in order. Dynamic smem: r[M], rv[M] (EXACT mode).
-template <bool kExact>
+// TREE mode (EXTENSION): one CTA walks the N slices in order; per slice the snap test, then
+// num/den by warp-tree reduction.
 __global__ void __launch_bounds__(kSweepThreads)
-scalar_sweep_kernel(long long N, long long M, const double* __restrict__ nodes, long long node_stride,
-                    const double* __restrict__ weights, const double* __restrict__ values,
-                    const double* __restrict__ a_arr, const double* __restrict__ b_arr,
-                    long long ab_stride, double y0, double* lambdas, double* y_out,
-                    long long* extrapolations) {
-    extern __shared__ double smem[];
-    double* r_s = smem;
-    double* rv_s = smem + M;
+scalar_sweep_tree_kernel(long long N, long long M, const double* __restrict__ nodes, long long node_stride,
+                         const double* __restrict__ weights, const double* __restrict__ values,
+                         const double* __restrict__ a_arr, const double* __restrict__ b_arr,
+                         long long ab_stride, double y0, double* lambdas, double* y_out,
+                         long long* extrapolations) {
     __shared__ double y_s;
-    __shared__ long long hit_s;
+    __shared__ unsigned long long hit_s;
     __shared__ double red_num[kSweepThreads / 32], red_den[kSweepThreads / 32];
     const int tid = threadIdx.x;
     double y = y0;
@@ -72,45 +135,20 @@ scalar_sweep_kernel(long long N, long long M, const double* __restrict__ nodes, 
         const double* v = values + j * M;
         const double a = a_arr[j * ab_stride], b = b_arr[j * ab_stride];
         if (y < a || y > b) ++ext;  // nievergelt.cpp:83
-        if (tid == 0) hit_s = M;
+        if (tid == 0) hit_s = static_cast<unsigned long long>(M);
         __syncthreads();
         // node snap: the lowest node within 1e-14 (relative) returns its value (interp.cpp:70-72)
         for (long long k = tid; k < M; k += kSweepThreads) {
             const double xk = x[k];
             if (fabs(__dsub_rn(y, xk)) <= __dmul_rn(1e-14, fmax(1.0, fabs(xk)))) {
-                atomicMin(reinterpret_cast<unsigned long long*>(&hit_s), static_cast<unsigned long long>(k));
+                atomicMin(&hit_s, static_cast<unsigned long long>(k));
                 break;
             }
         }
         __syncthreads();
-        const long long hit = hit_s;
+        const long long hit = static_cast<long long>(hit_s);
         if (hit < M) {
             y = v[hit];
-        } else if (kExact) {
-            for (long long k = tid; k < M; k += kSweepThreads) {
-                const double r = __ddiv_rn(w[k], __dsub_rn(y, x[k]));
-                r_s[k] = r;
-                rv_s[k] = __dmul_rn(r, v[k]);
-            }
-            __syncthreads();
-            if (tid == 0) {
-                // the reference's order: num += r*v, den += r for j = 0..M-1 (interp.cpp:74-78)
-                double num = 0.0, den = 0.0;
-                long long k = 0;
-                for (; k + 4 <= M; k += 4) {
-                    const double n0 = rv_s[k], n1 = rv_s[k + 1], n2 = rv_s[k + 2], n3 = rv_s[k + 3];
-                    const double d0 = r_s[k], d1 = r_s[k + 1], d2 = r_s[k + 2], d3 = r_s[k + 3];
-                    num = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(num, n0), n1), n2), n3);
-                    den = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(den, d0), d1), d2), d3);
-                }
-                for (; k < M; ++k) {
-                    num = __dadd_rn(num, rv_s[k]);
-                    den = __dadd_rn(den, r_s[k]);
-                }
-                y_s = __ddiv_rn(num, den);
-            }
-            __syncthreads();
-            y = y_s;
         } else {
             double num = 0.0, den = 0.0;
             for (long long k = tid; k < M; k += kSweepThreads) {
@@ -137,8 +175,132 @@ scalar_sweep_kernel(long long N, long long M, const double* __restrict__ nodes, 
             y = y_s;
         }
         if (tid == 0 && lambdas) lambdas[j] = y;
-        __syncthreads();
     }
+    if (tid == 0) {
+        if (y_out) *y_out = y;
+        if (extrapolations) *extrapolations = ext;
+    }
+}
+
+// EXACT mode (bit-exact): one CTA of 512 threads walks the N slices in order. Per slice:
+// (A) thread k (and k + 512, ...) takes node k — the snap test (interp.cpp:70-72, lowest hit by
+// atomicMin) and the term (r v, r), r = w / (y - x), into shared memory; (B) thread 0 adds the
+// terms in the reference's order (interp.cpp:74-78). B's two dependent DADD chains are the
+// slice's critical path (M x 8 cycles), so the terms are read kSumAhead ahead through a register
+// ring, and A is one node per thread with every operand already in shared memory: the nodes and
+// weights staged once (or per slice when node_stride != 0), the slice's values copied in by the
+// other warps while thread 0 sums the previous slice. Dynamic smem: x[M] | w[M] | v[2][M] |
+// (r v, r)[M + kSumAhead].
+constexpr int kSumAhead = 16;
+constexpr int kExactThreads = 512;
+#ifdef PINT_SWEEP_PROF  // tools/sweep_micro.cu only: thread 0's cycles in {terms + sync, sum, next sync}
+__device__ unsigned long long g_sweep_prof[3];
+#endif
+
+__global__ void __launch_bounds__(kExactThreads)
+scalar_sweep_exact_kernel(long long N, long long M, const double* __restrict__ nodes, long long node_stride,
+                          const double* __restrict__ weights, const double* __restrict__ values,
+                          const double* __restrict__ a_arr, const double* __restrict__ b_arr,
+                          long long ab_stride, double y0, double* lambdas, double* y_out,
+                          long long* extrapolations) {
+    extern __shared__ double2 sw_smem[];
+    double* x_s = reinterpret_cast<double*>(sw_smem);
+    double* w_s = x_s + M;
+    double* v_s = w_s + M;  // [2][M]
+    double2* terms = reinterpret_cast<double2*>(v_s + 2 * M);
+    __shared__ double y_s;
+    __shared__ unsigned long long hit_s;
+    const int tid = threadIdx.x;
+    // stage slice j's operands (the nodes/weights only when they differ per slice, or at j = 0)
+    auto stage = [&](long long j, int t0, int nt) {
+        const double* v = values + j * M;
+        double* vd = v_s + (j & 1) * M;
+        for (long long k = tid - t0; k < M; k += nt) vd[k] = v[k];
+        if (node_stride || j == 0)
+            for (long long k = tid - t0; k < M; k += nt) {
+                x_s[k] = nodes[j * node_stride + k];
+                w_s[k] = weights[j * node_stride + k];
+            }
+    };
+    double y = y0;
+    long long ext = 0;
+    if (tid == 0) hit_s = static_cast<unsigned long long>(M);
+    for (long long k = M + tid; k < M + kSumAhead; k += kExactThreads) terms[k] = make_double2(0.0, 0.0);
+    if (N > 0) stage(0, 0, kExactThreads);
+    __syncthreads();
+#ifdef PINT_SWEEP_PROF
+    unsigned long long pa = 0, pb = 0, pc = 0;
+#endif
+    for (long long j = 0; j < N; ++j) {
+#ifdef PINT_SWEEP_PROF
+        const long long c0 = clock64();
+#endif
+        const double* v = v_s + (j & 1) * M;
+        const double a = a_arr[j * ab_stride], b = b_arr[j * ab_stride];
+        if (y < a || y > b) ++ext;  // nievergelt.cpp:83
+        for (long long k = tid; k < M; k += kExactThreads) {
+            const double xk = x_s[k], diff = __dsub_rn(y, xk);
+            if (fabs(diff) <= __dmul_rn(1e-14, fmax(1.0, fabs(xk))))  // node snap (interp.cpp:70-72)
+                atomicMin(&hit_s, static_cast<unsigned long long>(k));
+            const double r = __ddiv_rn(w_s[k], diff);
+            terms[k] = make_double2(__dmul_rn(r, v[k]), r);
+        }
+        __syncthreads();
+#ifdef PINT_SWEEP_PROF
+        const long long c1 = clock64();
+#endif
+        if (tid == 0) {
+            const long long hit = static_cast<long long>(hit_s);
+            if (hit < M) {
+                y = v[hit];
+            } else {
+                double num = 0.0, den = 0.0;  // num += r*v, den += r for j = 0..M-1, in order
+                double2 ring[kSumAhead];
+#pragma unroll
+                for (int u = 0; u < kSumAhead; ++u) ring[u] = terms[u];
+                long long k = 0;
+                // (volatile asm keeps "consume slot u, then refill it" in order; ptxas still parks
+                // one accumulator in slot 0's register for the body, so that slot's refill is late
+                // once per 16 terms: measured 10.3 cycles per term against the 8-cycle DADD chain)
+                unsigned addr = static_cast<unsigned>(__cvta_generic_to_shared(terms + kSumAhead));
+#pragma unroll 1
+                for (; k + kSumAhead <= M; k += kSumAhead, addr += 16u * kSumAhead) {
+#pragma unroll
+                    for (int u = 0; u < kSumAhead; ++u) {
+                        asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(num) : "d"(ring[u].x));
+                        asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(den) : "d"(ring[u].y));
+                        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                                     : "=d"(ring[u].x), "=d"(ring[u].y)
+                                     : "r"(addr + 16u * u));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kSumAhead - 1; ++u)
+                    if (k + u < M) {
+                        num = __dadd_rn(num, ring[u].x);
+                        den = __dadd_rn(den, ring[u].y);
+                    }
+                y = __ddiv_rn(num, den);
+            }
+            y_s = y;
+            hit_s = static_cast<unsigned long long>(M);
+            if (lambdas) lambdas[j] = y;
+        } else if (tid >= 32 && j + 1 < N) {
+            stage(j + 1, 32, kExactThreads - 32);  // (warp 0 stays out of thread 0's way)
+        }
+#ifdef PINT_SWEEP_PROF
+        const long long c2 = clock64();
+#endif
+        __syncthreads();
+        y = y_s;
+#ifdef PINT_SWEEP_PROF
+        const long long c3 = clock64();
+        pa += c1 - c0, pb += c2 - c1, pc += c3 - c2;
+#endif
+    }
+#ifdef PINT_SWEEP_PROF
+    if (tid == 0) g_sweep_prof[0] = pa, g_sweep_prof[1] = pb, g_sweep_prof[2] = pc;
+#endif
     if (tid == 0) {
         if (y_out) *y_out = y;
         if (extrapolations) *extrapolations = ext;
@@ -211,7 +373,18 @@ int launch_bary_weights(pint_ctx* ctx, int kind, int64_t M, const double* nodes,
     if (kind == PINT_WEIGHTS_CLOSED2) {
         bary_closed2_kernel<<<blocks, 128, 0, ctx->stream>>>(M, w);
     } else if (kind == PINT_WEIGHTS_PRODUCT) {
-        bary_product_kernel<<<blocks, 128, 0, ctx->stream>>>(M, nodes, w, ctx->d_fail);
+        // the M^2 reciprocals in parallel, then one warp per CTA: every weight is a chain of M - 1
+        // dependent quotients, so spread the chains over as many SM sub-partitions as there are warps
+        const size_t smem = sizeof(double) * static_cast<size_t>(M);
+        if (smem > 220 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "barycentric_weights: M too large");
+        auto* rcp = static_cast<double*>(pint_scratch(ctx, 4, sizeof(double) * static_cast<size_t>(M) * M));
+        if (!rcp) return PINT_E_CUDA;
+        bary_rcp_kernel<<<static_cast<unsigned>((M * M + 255) / 256), 256, 0, ctx->stream>>>(M, nodes, rcp);
+        if (const int rc = pint_check_launch(ctx, "bary_rcp_kernel")) return rc;
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(bary_product_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        bary_product_kernel<<<static_cast<unsigned>((M + 31) / 32), 32, smem, ctx->stream>>>(M, nodes, rcp, w,
+                                                                                             ctx->d_fail);
     } else {
         return pint_set_error(ctx, PINT_E_INVALID, "barycentric_weights: unknown kind");
     }
@@ -224,15 +397,15 @@ int launch_scalar_sweep(pint_ctx* ctx, int mode, int64_t N, int64_t M, const dou
                         double* lambdas, double* y_out, long long* extrapolations) {
     if (M < 1 || N < 0) return pint_set_error(ctx, PINT_E_INVALID, "scalar_sweep: bad sizes");
     if (mode == PINT_SWEEP_EXACT) {
-        const size_t smem = sizeof(double) * 2 * static_cast<size_t>(M);
+        const size_t smem = sizeof(double) * 4 * static_cast<size_t>(M) + sizeof(double2) * (M + kSumAhead);
         if (smem > 220 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "scalar_sweep: M too large for EXACT mode");
         if (smem > 48 * 1024)
-            cudaFuncSetAttribute(scalar_sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(scalar_sweep_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem));
-        scalar_sweep_kernel<true><<<1, kSweepThreads, smem, ctx->stream>>>(
+        scalar_sweep_exact_kernel<<<1, kExactThreads, smem, ctx->stream>>>(
             N, M, nodes, node_stride, weights, values, a, b, ab_stride, y0, lambdas, y_out, extrapolations);
     } else if (mode == PINT_SWEEP_TREE) {
-        scalar_sweep_kernel<false><<<1, kSweepThreads, 0, ctx->stream>>>(
+        scalar_sweep_tree_kernel<<<1, kSweepThreads, 0, ctx->stream>>>(
             N, M, nodes, node_stride, weights, values, a, b, ab_stride, y0, lambdas, y_out, extrapolations);
     } else {
         return pint_set_error(ctx, PINT_E_INVALID, "scalar_sweep: unknown mode");

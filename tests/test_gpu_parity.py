@@ -128,6 +128,20 @@ def test_weights_bit_exact(ctx, golden, M):
     assert np.array_equal(pint.barycentric_weights(golden[f"nodes2_{M}"], "closed2"), O.bary_weights_closed2(M))
 
 
+@pytest.mark.parametrize("M,a,b,kind", [(1024, 0.0, 2.0, 2), (777, -3.0, 5.0, 1), (300, -1e3, 1e3, 2),
+                                         (200, 0.0, 1e-4, 1), (1500, 0.0, 2.0, 1)])
+def test_weights_product_form_vs_oracle(ctx, M, a, b, kind):
+    """The product-form weights' fast exact division and its IEEE fallback (wide / tiny spacings,
+    and M >= 1024 where the running quotient overflows to inf as in the reference): bit-exact
+    against the oracle's plain sequential divides."""
+    x = O.cheb_nodes(M, a, b, kind)
+    got = pint.barycentric_weights(x)
+    want = O.bary_weights(x)
+    assert np.array_equal(got, want, equal_nan=True)
+    if M >= 1024:
+        assert not np.all(np.isfinite(want))  # the overflow really happens
+
+
 def test_duplicate_nodes(ctx):
     with pytest.raises(pint.DuplicateNodes):
         pint.barycentric_weights([0.0, 1.0, 1.0])
