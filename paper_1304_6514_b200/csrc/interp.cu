@@ -329,40 +329,148 @@ __device__ __forceinline__ double lerp(double a, double b, double t) {
 }
 
 // EXTENSION: chain of bilinear maps over tables (N, 2, Mu, Mv). Nodes staged in smem.
-__global__ void bilinear_sweep_kernel(long long N, long long Mu, long long Mv,
-                                      const double* __restrict__ un, const double* __restrict__ vn,
-                                      const double* __restrict__ tables, double u, double v,
-                                      double* lambdas, long long* brackets, long long* extrapolations) {
+// The sweep is one dependent chain: slice j's brackets need the value leaving slice j-1, then
+// its corner values come from a 1 MiB table (HBM). Warp 0 runs the chain — all 32 lanes carry the
+// same values, lane 0 stores — so that:
+//  * the bracket is found by the warp at once: lane l tests the cell g - 15 + l around the
+//    linearly extrapolated guess g (x[c] <= xi < x[c+1] is, for sorted nodes, exactly
+//    upper_bound(xi) - 1); a ballot picks it, and only a miss of all 32 runs the binary search;
+//  * t = (xi - x[i]) / (x[i+1] - x[i]) is Markstein's exact sequence on the cell's reciprocal
+//    (staged once), the IEEE division only outside the exactness window (see bary_product_kernel);
+//  * warps 1..kLvAhead pull the rows around the extrapolated brackets of slices j+1..j+kLvAhead into
+//    L2 as soon as lane 0 publishes slice j's brackets.
+constexpr int kLvAhead = 3;
+constexpr int kLvRows = 16;  // rows either side of the guess pulled into L2
+
+#ifdef PINT_SWEEP_PROF
+__device__ unsigned long long g_bracket_miss;
+#endif
+__device__ __forceinline__ long long bracket_warp(const double* x, long long M, double xi, long long g, int lane) {
+    g = g < 15 ? 15 : (g > M - 18 ? M - 18 : g);
+    const long long c = g - 15 + lane;
+    const bool in = c >= 0 && c + 1 < M && x[c] <= xi && xi < x[c + 1];
+    const unsigned m = __ballot_sync(0xffffffffu, in);
+#ifdef PINT_SWEEP_PROF
+    if (!m && lane == 0) atomicAdd(&g_bracket_miss, 1ull);
+#endif
+    return m ? g - 15 + (__ffs(m) - 1) : bracket(x, M, xi);
+}
+
+__device__ __forceinline__ double cell_frac(double num, double den, double rcp) {
+    // (num / den, correctly rounded: Markstein with rcp = RN(1 / den) inside the window)
+    if (in_window(num, 1023u - 900u, 1023u + 900u) && in_window(den, 1023u - 60u, 1023u + 60u)) {
+        const double q0 = __dmul_rn(num, rcp);
+        return __fma_rn(rcp, __fma_rn(-den, q0, num), q0);
+    }
+    return __ddiv_rn(num, den);
+}
+
+__global__ void __launch_bounds__(32 * (kLvAhead + 1)) bilinear_sweep_kernel(
+    long long N, long long Mu, long long Mv, const double* __restrict__ un, const double* __restrict__ vn,
+    const double* __restrict__ tables, double u, double v, double* lambdas, long long* brackets,
+    long long* extrapolations) {
     extern __shared__ double nodes_s[];
-    double* us = nodes_s;
-    double* vs = nodes_s + Mu;
+    double* us = nodes_s;                    // [Mu]
+    double* vs = us + Mu;                    // [Mv]
+    double* ru = vs + Mv;                    // [Mu - 1] RN(1 / (us[i+1] - us[i]))
+    double* rv = ru + Mu;                    // [Mv - 1]
+    // published by lane 0 of warp 0: {j, iu, iv, diu, div} (j = -1: not yet; j = N: done)
+    __shared__ volatile long long pub[5];
     for (long long i = threadIdx.x; i < Mu; i += blockDim.x) us[i] = un[i];
     for (long long i = threadIdx.x; i < Mv; i += blockDim.x) vs[i] = vn[i];
+    for (long long i = threadIdx.x; i + 1 < Mu; i += blockDim.x) ru[i] = __drcp_rn(__dsub_rn(un[i + 1], un[i]));
+    for (long long i = threadIdx.x; i + 1 < Mv; i += blockDim.x) rv[i] = __drcp_rn(__dsub_rn(vn[i + 1], vn[i]));
+    if (threadIdx.x == 0) pub[0] = -1;
     __syncthreads();
-    if (threadIdx.x != 0) return;
     const long long P = Mu * Mv;
-    long long ext = 0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp > 0) {  // L2 prefetchers: warp w covers slice j + w
+        long long seen = -1;
+        while (true) {
+            const long long j = pub[0];
+            if (j == seen) {
+                __nanosleep(64);  // (a tight spin would compete with warp 0's shared loads)
+                continue;
+            }
+            if (j >= N) break;
+            const long long iu = pub[1], iv = pub[2], du = pub[3], dv = pub[4];
+            if (pub[0] != j) continue;  // (republished meanwhile: take the newer one)
+            seen = j;
+            const long long t = j + warp;
+            if (t >= N) continue;
+            const long long gu = iu + warp * du, gv = iv + warp * dv;
+            // rows gu - kLvRows .. gu + kLvRows + 1, the 3 lines around column gv, both components
+            for (int e = lane; e < 2 * (2 * kLvRows + 2) * 3; e += 32) {
+                const int comp = e & 1, line = (e >> 1) % 3, row = (e >> 1) / 3;
+                const long long r = gu - kLvRows + row;
+                long long c = gv - 16 + 16 * line;
+                if (r < 0 || r >= Mu) continue;
+                c = c < 0 ? 0 : (c >= Mv ? Mv - 1 : c);
+                asm volatile("prefetch.global.L2 [%0];\n" ::"l"(tables + (t * 2 + comp) * P + r * Mv + c));
+            }
+        }
+        return;
+    }
+    long long ext = 0, piu = 0, piv = 0, du = 0, dv = 0;
+#ifdef PINT_SWEEP_PROF  // (tools/prof_lv_sweep.sh) lane 0's cycles per slice by section
+    long long pa = 0, pb = 0, pc = 0, t0 = clock64();
+#define LV_MARK(v)                      \
+    do {                                \
+        const long long t1 = clock64(); \
+        v += t1 - t0;                   \
+        t0 = t1;                        \
+    } while (0)
+#else
+#define LV_MARK(v) \
+    do {           \
+    } while (0)
+#endif
     for (long long j = 0; j < N; ++j) {
         if (u < us[0] || u > us[Mu - 1] || v < vs[0] || v > vs[Mv - 1]) ++ext;
-        const long long iu = bracket(us, Mu, u), iv = bracket(vs, Mv, v);
-        const double tu = __ddiv_rn(__dsub_rn(u, us[iu]), __dsub_rn(us[iu + 1], us[iu]));
-        const double tv = __ddiv_rn(__dsub_rn(v, vs[iv]), __dsub_rn(vs[iv + 1], vs[iv]));
+        const long long iu = j ? bracket_warp(us, Mu, u, piu + du, lane) : bracket(us, Mu, u);
+        const long long iv = j ? bracket_warp(vs, Mv, v, piv + dv, lane) : bracket(vs, Mv, v);
+        if (j) du = iu - piu, dv = iv - piv;
+        piu = iu, piv = iv;
+        if (lane == 0) {  // (no fence: a torn read only misdirects a prefetch)
+            pub[1] = iu, pub[2] = iv, pub[3] = du, pub[4] = dv;
+            pub[0] = j;
+        }
+        LV_MARK(pa);
         const double* Tu = tables + (j * 2) * P + iu * Mv + iv;
         const double* Tv = Tu + P;
-        const double u00 = Tu[0], u01 = Tu[1], u10 = Tu[Mv], u11 = Tu[Mv + 1];
-        const double v00 = Tv[0], v01 = Tv[1], v10 = Tv[Mv], v11 = Tv[Mv + 1];
-        u = lerp(lerp(u00, u10, tu), lerp(u01, u11, tu), tv);
-        v = lerp(lerp(v00, v10, tu), lerp(v01, v11, tu), tv);
-        if (lambdas) {
-            lambdas[2 * j] = u;
-            lambdas[2 * j + 1] = v;
+        double c[8];
+        c[0] = Tu[0], c[1] = Tu[1], c[2] = Tu[Mv], c[3] = Tu[Mv + 1];
+        c[4] = Tv[0], c[5] = Tv[1], c[6] = Tv[Mv], c[7] = Tv[Mv + 1];
+        const double tu = cell_frac(__dsub_rn(u, us[iu]), __dsub_rn(us[iu + 1], us[iu]), ru[iu]);
+        const double tv = cell_frac(__dsub_rn(v, vs[iv]), __dsub_rn(vs[iv + 1], vs[iv]), rv[iv]);
+        u = lerp(lerp(c[0], c[2], tu), lerp(c[1], c[3], tu), tv);
+        v = lerp(lerp(c[4], c[6], tu), lerp(c[5], c[7], tu), tv);
+#ifdef PINT_SWEEP_PROF
+        if (u == -1.2345) printf("x");  // (forces u, v before the mark)
+#endif
+        LV_MARK(pb);
+        if (lane == 0) {
+            if (lambdas) {
+                lambdas[2 * j] = u;
+                lambdas[2 * j + 1] = v;
+            }
+            if (brackets) {
+                brackets[2 * j] = iu;
+                brackets[2 * j + 1] = iv;
+            }
         }
-        if (brackets) {
-            brackets[2 * j] = iu;
-            brackets[2 * j + 1] = iv;
-        }
+        LV_MARK(pc);
     }
-    if (extrapolations) *extrapolations = ext;
+#ifdef PINT_SWEEP_PROF
+    if (lane == 0)
+        printf("bilinear sweep per slice: bracket+publish %lld, loads+fractions+lerp %lld, stores %lld cycles; "
+               "bracket misses %llu (cumulative)\n",
+               pa / (N ? N : 1), pb / (N ? N : 1), pc / (N ? N : 1), g_bracket_miss);
+#endif
+    if (lane == 0) {
+        pub[0] = N;  // release the prefetchers
+        if (extrapolations) *extrapolations = ext;
+    }
 }
 
 }  // namespace
@@ -417,12 +525,12 @@ int launch_bilinear_sweep(pint_ctx* ctx, int64_t N, int64_t Mu, int64_t Mv, cons
                           const double* vn, const double* tables, double u0, double v0,
                           double* lambdas, long long* brackets, long long* extrapolations) {
     if (Mu < 2 || Mv < 2 || N < 0) return pint_set_error(ctx, PINT_E_BAD_GRID, "bilinear_sweep: need >= 2 nodes per axis");
-    const size_t smem = sizeof(double) * static_cast<size_t>(Mu + Mv);
+    const size_t smem = sizeof(double) * 2 * static_cast<size_t>(Mu + Mv);
     if (smem > 220 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "bilinear_sweep: grid too large");
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(bilinear_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-    bilinear_sweep_kernel<<<1, 128, smem, ctx->stream>>>(N, Mu, Mv, un, vn, tables, u0, v0, lambdas,
-                                                         brackets, extrapolations);
+    bilinear_sweep_kernel<<<1, 32 * (kLvAhead + 1), smem, ctx->stream>>>(N, Mu, Mv, un, vn, tables, u0, v0,
+                                                                       lambdas, brackets, extrapolations);
     return pint_check_launch(ctx, "bilinear_sweep_kernel");
 }
