@@ -20,6 +20,8 @@ int pint_check_launch(pint_ctx*, const char* what) {
     return e == cudaSuccess ? 0 : PINT_E_CUDA;
 }
 
+void* pint_scratch(pint_ctx*, int, size_t) { return nullptr; }
+
 int main(int argc, char** argv) {
     const int N = argc > 1 ? std::atoi(argv[1]) : 64;
     const int M = argc > 2 ? std::atoi(argv[2]) : 1024;
