@@ -5,6 +5,8 @@
 //   ref_tool golden <outdir>      dump golden vectors from the reference's own functions
 //   ref_tool bench-heat  ...      time pint::run_nievergelt(make_heat_problem(...)) (CPU baseline)
 //   ref_tool bench-scalar ...     time pint::run_nievergelt(make_model_problem(), ...)
+//   ref_tool bench-serial --dt h  time pint::run_serial(make_model_problem(), h) (one core)
+//   ref_tool fit <fixture>        pint::fit_params(load_observations(fixture), 0.5) as JSON
 //
 // Every vector below is produced by calling the reference API exactly as its own tests do
 // (tests/test_nievergelt.cpp, tests/test_ode_core.cpp, tests/acceptance.cpp).
@@ -20,6 +22,7 @@
 #include <thread>
 #include <vector>
 
+#include "pint/cost_model.hpp"
 #include "pint/exec_harness.hpp"
 #include "pint/interp.hpp"
 #include "pint/linalg.hpp"
@@ -360,6 +363,34 @@ int cmd_bench_scalar(std::map<std::string, std::string> a) {
     return 0;
 }
 
+// The reference's serial scalar run (the CPU side of the cost model's ratio column).
+int cmd_bench_serial(std::map<std::string, std::string> a) {
+    const double dt = arg_d(a, "--dt", 6.103515625e-05);
+    const int reps = static_cast<int>(arg_d(a, "--reps", 3));
+    double best = 1e30, y = 0.0;
+    for (int rep = 0; rep < reps; ++rep) {
+        const auto t0 = std::chrono::steady_clock::now();
+        const RunReport r = run_serial(make_model_problem(), dt);
+        best = std::min(best, std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+        y = r.final_state[0];
+    }
+    std::printf("{\"seconds\": %.9g, \"final\": %.17g}\n", best, y);
+    return 0;
+}
+
+// The reference's least-squares fit of (tau_F, tau_N, tau_K, tau_F_cpu) on a 5-column fixture.
+int cmd_fit(const std::string& path) {
+    const auto obs = load_observations(path);
+    const FitResult f = fit_params(obs, 0.5);
+    std::printf("{\"tau_F\": %.9g, \"tau_N\": %.9g, \"tau_K\": %.9g, \"tau_F_cpu\": %.9g, \"predicted\": [",
+                f.params.tau_F, f.params.tau_N, f.params.tau_K, f.params.tau_F_cpu);
+    for (std::size_t i = 0; i < f.predicted.size(); ++i) std::printf("%s%.9g", i ? ", " : "", f.predicted[i]);
+    std::printf("], \"observed\": [");
+    for (std::size_t i = 0; i < obs.size(); ++i) std::printf("%s%.9g", i ? ", " : "", obs[i].total_us);
+    std::printf("]}\n");
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -374,6 +405,8 @@ int main(int argc, char** argv) {
         if (cmd == "golden" && argc >= 3) return cmd_golden(argv[2]);
         if (cmd == "bench-heat") return cmd_bench_heat(args);
         if (cmd == "bench-scalar") return cmd_bench_scalar(args);
+        if (cmd == "bench-serial") return cmd_bench_serial(args);
+        if (cmd == "fit" && argc >= 3) return cmd_fit(argv[2]);
     } catch (const std::exception& e) {
         std::fprintf(stderr, "ref_tool: %s\n", e.what());
         return 1;
