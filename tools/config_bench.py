@@ -89,11 +89,10 @@ def port_logistic(N, M, S, sample=4):
 def run_lv(ctx, N, Mg, S, reps):
     import torch
 
-    import oracle as O
     from paper_1304_6514_b200.dist import LVPlan
 
     LV = [1.5, 1.0, 1.0, 3.0]
-    un = O.uniform_nodes(Mg, 0.1, 8.0)
+    un = 0.1 + ((8.0 - 0.1) * np.arange(Mg, dtype=np.float64)) / (Mg - 1)  # uniform grid on [0.1, 8]
     plan = LVPlan(ctx, LV, 10.0, N, S, un, un)
     lam0 = torch.tensor([1.0, 1.0], dtype=torch.float64)
     stream = torch.cuda.current_stream()
