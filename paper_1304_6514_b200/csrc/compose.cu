@@ -413,8 +413,10 @@ int launch_affine_tree(pint_ctx* ctx, int64_t n, int64_t N, double* maps, double
     double* dst = scratch;
     long long count = N;
     // When only y is wanted, pairing may stop once a level would be latency-bound (a pair level
-    // costs ~14 us even for a handful of GEMMs) and the chain applies the rest.
-    const long long stop = composed ? 1 : kTreeChainTail;
+    // costs ~14 us even for a handful of GEMMs) and the chain applies the rest — where the chain is
+    // the cluster kernel (n <= 256). Beyond that the one-CTA chain costs ~84 us per map at n = 512,
+    // more than finishing the tree (~30 us a level there).
+    const long long stop = (composed || n > 32 * kClusterMax) ? 1 : kTreeChainTail;
     while (count > stop) {
         const long long pairs = count / 2;
         for (long long p0 = 0; p0 < pairs; p0 += 65535) {
