@@ -1,4 +1,6 @@
 #include <cstdio>
+#define PINT_ENSEMBLE_STANDALONE
+
 __global__ void k(double seed, double* out, long long* cyc) {
     double a = seed + threadIdx.x * 1e-3;
     long long t0 = clock64();
