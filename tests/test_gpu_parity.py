@@ -347,6 +347,25 @@ def test_heat_config4_shape_n512(ctx):
     assert np.max(np.abs(rt.final_state - y_chain)) / np.max(np.abs(y_chain)) <= REL_F64
 
 
+@pytest.mark.parametrize("n,N", [(97, 3), (98, 3), (129, 33), (200, 5), (255, 3), (256, 3), (281, 2), (282, 2),
+                                 (521, 1)])
+def test_heat_build_layout_boundaries(ctx, n, N):
+    """Every switch point of the build, bit-exact against the oracle: register rows start at
+    n = 98; the slice-group records / group-forced grid end where a forced warp's block stops
+    fitting (n ~ 220-256); the TMEM build covers n in [282, 520]; N = 33 leaves a partial slice
+    group (lanes past N idle in the forced grid)."""
+    S = 2
+    dx, dt = 1.0 / (n + 1), 1e-3
+    T = N * S * dt
+    prob = pint.make_heat_problem(dx, dt, T)
+    dec = pint.decompose(0.0, T, N, dt)
+    G, c = pint.build_affine_propagators(prob, dec)
+    for j in sorted({0, N - 1}):
+        s = dec.slices[j]
+        Gw, cw = O.heat_build(dx, s.t_begin, s.t_end, dt)
+        assert np.array_equal(G[j], Gw) and np.array_equal(c[j], cw), (n, N, j)
+
+
 @pytest.mark.parametrize("n", [270, 300, 384, 520])
 def test_heat_large_n_build_paths(ctx, n):
     """The large-n builds, bit-exact against the oracle: n = 270 the one-warp-CTA build with the
