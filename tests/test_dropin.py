@@ -54,3 +54,40 @@ def test_reference_acceptance_on_b200():
         cells = lambda s: s.split(" -- ", 1)[1] if " -- " in s else ""
         assert cells(mine[2][1]) == cells(ref[2][1])
         assert {c: v[0] for c, v in ref.items()} == {c: v[0] for c, v in mine.items()}
+
+
+REF_BENCH = ROOT / "oracle" / "_ref" / "pint_bench"
+TIMING_COLUMNS = {"T_total", "T_comm", "modeled_time"}
+
+
+def _table(binary, args):
+    if not binary.exists():
+        pytest.skip(f"{binary} not built (needs /root/reference at build time)")
+    proc = subprocess.run([str(binary), *args], cwd=DROPIN, capture_output=True, text=True, timeout=900)
+    assert proc.returncode == 0, proc.stderr
+    rows = [line.split(",") for line in proc.stdout.strip().splitlines()]
+    out, header = [], None
+    for r in rows:  # tables separated by blank lines; every table starts with its header
+        if r == [""]:
+            header = None
+            continue
+        if header is None:
+            header = r
+            continue
+        out.append({h: v for h, v in zip(header, r) if h not in TIMING_COLUMNS})
+    return out
+
+
+@pytest.mark.parametrize("args", [
+    ["scalar-table", "--dt", "0.01,0.001", "--cheb-points", "3,5,7", "--slices", "4"],
+    ["compare", "--slices", "1,4,16", "--iterations", "2,3"],
+    ["heat", "--slices", "1,2,4,8,16"],
+    ["wave", "--wave-points", "16", "--final-time", "4", "--slices", "1,2,4"],
+    ["costmodel"],
+])
+def test_reference_pint_bench_on_b200(args):
+    """The reference's own CLI (tools/pint_bench.cpp, unmodified, CLI11 stand-in) built against
+    the drop-in: every table cell except the wall-clock columns equals the CPU reference's."""
+    mine = _table(DROPIN / "pint_bench", args)
+    ref = _table(REF_BENCH, args)
+    assert mine and mine == ref
