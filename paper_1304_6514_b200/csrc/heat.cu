@@ -613,18 +613,22 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
     if (kForced) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const int n = P.n;
     const int lane = threadIdx.x;
-    const long long slice = kGroup ? 32ll * blockIdx.x + lane : kForced ? blockIdx.x : blockIdx.x / P.wps;
-    const long long g0 = kGroup ? blockIdx.x : slice;  // the block's slice group / slice
+    // group-forced: two CTAs per slice group, each running 16 of its slices on lanes 0-15 (lanes
+    // 16-31 shadow them — same addresses, broadcast — and store nothing): half the shared-memory
+    // wavefronts per row of a full 32-slice warp
+    const int el = kGroup ? 16 * static_cast<int>(blockIdx.x & 1) + (lane & 15) : lane;
+    const long long slice = kGroup ? 32ll * (blockIdx.x >> 1) + el : kForced ? blockIdx.x : blockIdx.x / P.wps;
+    const long long g0 = kGroup ? (blockIdx.x >> 1) : slice;  // the block's slice group / slice
     // (single-forced: all 32 lanes run the forced column on one shared copy of the state; lane 0
     // writes it out)
     constexpr int kLS = lane_stride(kMode);
     const int k = kForced ? n : static_cast<int>(blockIdx.x - g0 * P.wps) * 32 + lane;
-    const bool live = kGroup ? slice < P.N : kForced ? lane == 0 : k < n;
+    const bool live = kGroup ? (lane < 16 && slice < P.N) : kForced ? lane == 0 : k < n;
     double* R = smem + front_pad(n, kMode);
     double* st = R + staged_doubles(n, kMode) + (kLS == 32 ? lane : 0);
     const unsigned bar_f = smem_u32(R + staged_doubles(n, kMode) + (n - RR) * kLS + kLS * kFwdAhead);
     const unsigned bar_b = bar_f + 8;
-    const long long my_steps = (kGroup && !live) ? 0 : P.step_off[slice + 1] - P.step_off[slice];
+    const long long my_steps = (kGroup && slice >= P.N) ? 0 : P.step_off[slice + 1] - P.step_off[slice];
     const long long steps = kGroup ? __reduce_max_sync(0xffffffffu, static_cast<unsigned>(my_steps)) : my_steps;
     const RecView V = rec_view(P.rec, n, P.N, P.S);
     auto src = [&](long long s) { return kGroup ? V.fblock(s, g0) : V.rec(g0, s); };
@@ -636,7 +640,7 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
     const unsigned back_bytes = 8u * static_cast<unsigned>(back_doubles);
     const unsigned all_bytes = 8u * static_cast<unsigned>(staged_doubles(n, kMode));
     const unsigned dst_f = smem_u32(R), dst_b = smem_u32(R + back_off);
-    const StagedStep<kMode> SV{R, n, lane, static_cast<int>(slice & 1)};
+    const StagedStep<kMode> SV{R, n, el, static_cast<int>(slice & 1)};
     // kTiles coordinates: column 2*(slice % 32) of pr2 / lanes (slice % 32) & ~1 of c; block s*N32 + G
     const int tx = static_cast<int>(slice & 31), tg = static_cast<int>(slice >> 5), ng = static_cast<int>(groups32(P.N));
     auto load_fwd = [&](long long s) {
@@ -967,7 +971,7 @@ int launch_build(pint_ctx* ctx, BuildPlan P) {
     // PINT_HEAT_ONLY=basis|forced: timing experiments only (the other part of the maps is not built)
     const char* only = std::getenv("PINT_HEAT_ONLY");
     const bool run_f = !only || std::strcmp(only, "basis") != 0, run_b = !only || std::strcmp(only, "forced") != 0;
-    if (run_f) fkern<<<static_cast<unsigned>(grp ? groups32(P.N) : P.N), 32, fsmem, ctx->stream>>>(P);
+    if (run_f) fkern<<<static_cast<unsigned>(grp ? 2 * groups32(P.N) : P.N), 32, fsmem, ctx->stream>>>(P);
     if (const int rc = pint_check_launch(ctx, "heat_build_kernel (forced)")) return rc;
     if (run_b) {
         cudaLaunchConfig_t cfg = {};
