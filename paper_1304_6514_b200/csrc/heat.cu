@@ -93,9 +93,12 @@ __host__ __device__ constexpr int reg_rows(long long n) { return n >= kRegRows +
 // warp: its 32 lanes all run the one forced column in lockstep, so they share ONE copy (stride 1,
 // every lane stores the same value).
 __host__ __device__ constexpr int lane_stride(int mode) { return mode == kForcedSingle ? 1 : 32; }
+// staged copies of the step data: the TMA-tiled basis warps double-buffer theirs (step s + 2 is
+// fetched while step s + 1 waits in the other buffer), so no refill waits at a pass boundary
+__host__ __device__ constexpr int stage_bufs(int mode) { return mode == kBasisGroup ? 2 : 1; }
 __host__ __device__ constexpr long long warp_smem_doubles(long long n, int mode) {
-    return front_pad(n, mode) + staged_doubles(n, mode) + (n - reg_rows(n)) * lane_stride(mode) +
-           lane_stride(mode) * kFwdAhead + 2;
+    return front_pad(n, mode) + stage_bufs(mode) * staged_doubles(n, mode) + (n - reg_rows(n)) * lane_stride(mode) +
+           lane_stride(mode) * kFwdAhead + 2 * stage_bufs(mode);
 }
 __host__ __device__ constexpr bool group_forced(long long n) {
     return 8 * warp_smem_doubles(n, kForcedGroup) <= 227 * 1024 && n + 1 <= 256;  // (tile rows <= 256)
@@ -624,10 +627,11 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
     constexpr int kLS = lane_stride(kMode);
     const int k = kForced ? n : static_cast<int>(blockIdx.x - g0 * P.wps) * 32 + lane;
     const bool live = kGroup ? (lane < 16 && slice < P.N) : kForced ? lane == 0 : k < n;
-    double* R = smem + front_pad(n, kMode);
-    double* st = R + staged_doubles(n, kMode) + (kLS == 32 ? lane : 0);
-    const unsigned bar_f = smem_u32(R + staged_doubles(n, kMode) + (n - RR) * kLS + kLS * kFwdAhead);
-    const unsigned bar_b = bar_f + 8;
+    constexpr int kBufs = stage_bufs(kMode);
+    double* R0 = smem + front_pad(n, kMode);  // kBufs staged copies of the step data
+    double* st = R0 + kBufs * staged_doubles(n, kMode) + (kLS == 32 ? lane : 0);
+    // mbarriers of buffer b: forward half at bar0 + 16 b, back half at bar0 + 16 b + 8
+    const unsigned bar0 = smem_u32(R0 + kBufs * staged_doubles(n, kMode) + (n - RR) * kLS + kLS * kFwdAhead);
     const long long my_steps = (kGroup && slice >= P.N) ? 0 : P.step_off[slice + 1] - P.step_off[slice];
     const long long steps = kGroup ? __reduce_max_sync(0xffffffffu, static_cast<unsigned>(my_steps)) : my_steps;
     const RecView V = rec_view(P.rec, n, P.N, P.S);
@@ -639,17 +643,18 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
     const unsigned fwd_bytes = 8u * static_cast<unsigned>(fwd_doubles);
     const unsigned back_bytes = 8u * static_cast<unsigned>(back_doubles);
     const unsigned all_bytes = 8u * static_cast<unsigned>(staged_doubles(n, kMode));
-    const unsigned dst_f = smem_u32(R), dst_b = smem_u32(R + back_off);
-    const StagedStep<kMode> SV{R, n, el, static_cast<int>(slice & 1)};
+    auto buf = [&](int b) { return R0 + b * staged_doubles(n, kMode); };
     // kTiles coordinates: column 2*(slice % 32) of pr2 / lanes (slice % 32) & ~1 of c; block s*N32 + G
     const int tx = static_cast<int>(slice & 31), tg = static_cast<int>(slice >> 5), ng = static_cast<int>(groups32(P.N));
-    auto load_fwd = [&](long long s) {
-        if (kTiles) tile_load(dst_f, &P.tm_pr, 2 * tx, 0, static_cast<int>(s) * ng + tg, fwd_bytes, bar_f);
-        else bulk_load(dst_f, src(s), fwd_bytes, bar_f);
+    auto load_fwd = [&](long long s, int b) {
+        const unsigned dst = smem_u32(buf(b)), bar = bar0 + 16u * b;
+        if (kTiles) tile_load(dst, &P.tm_pr, 2 * tx, 0, static_cast<int>(s) * ng + tg, fwd_bytes, bar);
+        else bulk_load(dst, src(s), fwd_bytes, bar);
     };
-    auto load_back = [&](long long s) {
-        if (kTiles) tile_load(dst_b, &P.tm_cc, tx & ~1, 0, static_cast<int>(s) * ng + tg, back_bytes, bar_b);
-        else bulk_load(dst_b, src(s) + back_off, back_bytes, bar_b);
+    auto load_back = [&](long long s, int b) {
+        const unsigned dst = smem_u32(buf(b) + back_off), bar = bar0 + 16u * b + 8u;
+        if (kTiles) tile_load(dst, &P.tm_cc, tx & ~1, 0, static_cast<int>(s) * ng + tg, back_bytes, bar);
+        else bulk_load(dst, src(s) + back_off, back_bytes, bar);
     };
     auto prefetch = [&](long long s) {
         if (kTiles) {
@@ -661,15 +666,16 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
     };
 
     if (lane == 0) {
-        mbar_init(bar_f);
-        mbar_init(bar_b);
+        for (int b = 0; b < 2 * kBufs; ++b) mbar_init(bar0 + 8u * b);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncwarp();
     if (lane == 0 && steps > 0) {
-        load_fwd(0);
-        load_back(0);
-        if (steps > 1) prefetch(1);
+        for (int b = 0; b < kBufs && b < steps; ++b) {
+            load_fwd(b, b);
+            load_back(b, b);
+        }
+        if (steps > kBufs) prefetch(kBufs);
     }
     double reg[RR > 0 ? RR : 1];
 #pragma unroll
@@ -682,9 +688,11 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
     long long t_prev = clock64();
 #endif
     for (long long s = 0; s < steps; ++s) {
-        const unsigned parity = static_cast<unsigned>(s & 1);
+        const int b = kBufs == 2 ? static_cast<int>(s & 1) : 0;
+        const unsigned parity = static_cast<unsigned>((kBufs == 2 ? s >> 1 : s) & 1);
         const bool active = s < my_steps;  // forced lanes of shorter slices idle at the tail
-        mbar_wait(bar_f, parity);  // this step's forward half has landed
+        const StagedStep<kMode> SV{buf(b), n, el, static_cast<int>(slice & 1)};
+        mbar_wait(bar0 + 16u * b, parity);  // this step's forward half has landed
         HEAT_PROF_MARK(0);
         double d = 0.0, dm1 = 0.0;
         if (active) {
@@ -692,16 +700,19 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
             qmin = min(qmin, hi_abs(d) - 1u);  // q_{n-1} (the back pass starts at row n-2)
         }
         HEAT_PROF_MARK(1);
-        __syncwarp();  // every lane is done with the forward half
-        if (lane == 0 && s + 1 < steps) load_fwd(s + 1);
-        mbar_wait(bar_b, parity);
+        if (kBufs == 1) {
+            __syncwarp();  // every lane is done with the forward half
+            if (lane == 0 && s + 1 < steps) load_fwd(s + 1, 0);
+        }
+        mbar_wait(bar0 + 16u * b + 8u, parity);
         HEAT_PROF_MARK(2);
         if (active) column_back<RR, kMode>(reg, st, SV, d, dm1, qmin);
         HEAT_PROF_MARK(3);
-        __syncwarp();  // every lane is done with the back half
-        if (lane == 0 && s + 1 < steps) {
-            load_back(s + 1);
-            if (s + 2 < steps) prefetch(s + 2);
+        __syncwarp();  // every lane is done with this step's buffer
+        if (lane == 0 && s + kBufs < steps) {
+            if (kBufs == 2) load_fwd(s + 2, b);
+            load_back(s + kBufs, b);
+            if (s + kBufs + 1 < steps) prefetch(s + kBufs + 1);
         }
         HEAT_PROF_MARK(4);
     }
