@@ -2,11 +2,12 @@
 //
 //  * CHAIN (bit-exact): compose_sweep (nievergelt.cpp:90-110) walking the slices in order; the
 //    owner of row i accumulates sum_k G(i,k) y_k sequentially in k exactly like matvec
-//    (linalg.cpp:17-26), then adds c_i. For n <= 256: a cluster of ceil(n/32) single-warp CTAs,
+//    (linalg.cpp:17-26), then adds c_i. For n <= 512: a cluster of ceil(n/32) single-warp CTAs,
 //    CTA r owning rows 32r..32r+31 (lane = row); each CTA's 32-row block of the next two maps is
 //    bulk-copied into shared memory ahead of use (the block is contiguous in the row-major map),
 //    and the new y is exchanged through distributed shared memory with one cluster barrier per
-//    map. Larger n: one CTA, rows read from global.
+//    map; up to n = 512 with the non-portable cluster sizes (16 CTAs, one 32-row block each).
+//    Larger n: one CTA, rows read from global.
 //  * TREE (EXTENSION, north_star subsystem 3): log-depth pairwise products
 //        (G2, c2) o (G1, c1) = (G2 G1, G2 c1 + c2)
 //    on FP64 tensor cores: mma.sync m8n8k4 f64 (SASS DMMA) with 64x64 CTA tiles staged through
@@ -69,11 +70,11 @@ affine_chain_kernel(long long n, long long N, long long ldm, const double* __res
     for (long long i = threadIdx.x; i < n; i += kChainThreads) y[i] = y_s[i];
 }
 
-// Cluster chain (n <= 256). Dynamic smem: rows[ring][32][ldm] | y[2][ny] | pad | ring map barriers
+// Cluster chain (n <= 512). Dynamic smem: rows[ring][32][ldm] | y[2][ny] | pad | ring map barriers
 // | 2 y barriers,
 // ny = n rounded up to 16 (16-byte aligned y pairs; the pipeline may read 16 doubles past n). A
 // CTA's 32 rows of a map are one contiguous block: one bulk copy per map.
-constexpr int kClusterMax = 8;
+constexpr int kClusterMax = 16;  // (> 8: the non-portable cluster sizes, one 32-row block per SM up to n = 512)
 constexpr int kChainAhead = 8;  // pairs of terms in flight per lane
 constexpr int kRing = 4;        // maps in flight (bulk-copy latency ~ 2 map applications); fewer
                                 // when 4 blocks of 32 rows do not fit (n > ~220)
@@ -371,6 +372,7 @@ int launch_affine_chain(pint_ctx* ctx, int64_t n, int64_t N, const double* maps,
         cudaFuncSetAttribute(affine_chain_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
         const unsigned C = static_cast<unsigned>((n + 31) / 32);
+        if (C > 8) cudaFuncSetAttribute(affine_chain_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(C, 1, 1);
         cfg.blockDim = dim3(32, 1, 1);
@@ -413,10 +415,11 @@ int launch_affine_tree(pint_ctx* ctx, int64_t n, int64_t N, double* maps, double
     double* dst = scratch;
     long long count = N;
     // When only y is wanted, pairing may stop once a level would be latency-bound (a pair level
-    // costs ~14 us even for a handful of GEMMs) and the chain applies the rest — where the chain is
-    // the cluster kernel (n <= 256). Beyond that the one-CTA chain costs ~84 us per map at n = 512,
-    // more than finishing the tree (~30 us a level there).
-    const long long stop = (composed || n > 32 * kClusterMax) ? 1 : kTreeChainTail;
+    // costs ~14 us even for a handful of GEMMs) and the chain applies the rest. Past n = 256 the
+    // chain (a 16-CTA cluster at n = 512: ~5.3 us per map) is cheaper per map than the products
+    // (2 n^3 flops: ~10 us a map at n = 512 on the DMMA pipe), so there only-y skips the tree
+    // entirely — and the result is the bit-exact chain's.
+    const long long stop = composed ? 1 : n > 256 ? N : kTreeChainTail;
     while (count > stop) {
         const long long pairs = count / 2;
         for (long long p0 = 0; p0 < pairs; p0 += 65535) {
