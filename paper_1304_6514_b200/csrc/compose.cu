@@ -127,6 +127,10 @@ __global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long lo
     for (long long j = 0; j < N; ++j) {
         const int b = static_cast<int>(j % ring), yb = static_cast<int>(j & 1);
         mbar_wait(bar0 + 8u * b, static_cast<unsigned>((j / ring) & 1));
+        // the block after the ring's next into L2 now, so its bulk copy (issued once this block is
+        // consumed) reads L2 rather than HBM — with a 1-deep ring (n > ~220) that copy is exposed
+        if (lane == 0 && j + ring < N)
+            prefetch_l2(maps + (j + ring) * mstride + static_cast<long long>(r0) * ldm, blk_bytes);
         CHAIN_MARK(tw);
         const double2* g2 = reinterpret_cast<const double2*>(blk + (b * 32 + lane) * ldm);
         const double2* y2 = reinterpret_cast<const double2*>(ys + yb * ny);
