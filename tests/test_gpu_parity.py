@@ -245,6 +245,20 @@ def test_lv_small_bit_exact(ctx):
     assert np.array_equal(lam, wl) and ext == wext
 
 
+@pytest.mark.parametrize("Mu,Mv,N", [(5, 300, 3), (300, 3, 2), (2, 2, 5), (129, 129, 2)])
+def test_lv_grid_shapes(ctx, Mu, Mv, N):
+    """The tensor-grid kernel's 3-D launch (x: iv over 128-thread blocks, y: iu, z: slice) on
+    ragged shapes — several x-blocks, one-node-wide sides, a partial last block — bit-exact, and
+    the warp-tested brackets of the sweep (including a 2-node axis) equal the oracle's."""
+    S = -(-240 // N)  # dt = 10 / (N S) <= 1/24: RK4 stays bounded on the grid's corners
+    st, h, un, vn, tables, lam, br, ext = lv_run(ctx, N, Mu, Mv, S)
+    want = O.lv_rk4_ensemble(st, h, un, vn, LV)
+    assert np.array_equal(tables.cpu().numpy().reshape(N, 2, Mu, Mv), want)
+    assert np.all(np.isfinite(want))
+    wl, wb, wext = O.bilinear_sweep(un, vn, want, 1.0, 1.0)
+    assert np.array_equal(br, wb) and np.array_equal(lam, wl, equal_nan=True) and ext == wext
+
+
 def test_lv_config3_shape(ctx):
     """Config 3: 512 slices x 256x256 tensor grid, RK4 S=8; spot-check slices + full sweep."""
     N, Mu, Mv, S = 512, 256, 256, 8
