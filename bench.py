@@ -19,6 +19,7 @@ e2e:   the same metric through the host-buffer C-ABI call pint_run_heat (N=1) / 
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import pathlib
@@ -71,6 +72,12 @@ def parse():
     p.add_argument("--S", type=int, default=256, help="backward-Euler steps per slice")
     p.add_argument("--T", type=float, default=10.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--configs", nargs="*", default=None,
+                   help="measure BASELINE configs 1/3/5 instead (cases: c1ref c1rk4 c5 c3; default all)")
+    p.add_argument("--config-reps", type=int, default=5)
+    p.add_argument("--cost-model", action="store_true", help="refit the paper's cost model on B200 timings")
+    p.add_argument("--cost-model-reps", type=int, default=7)
+    p.add_argument("--cost-model-out", default="profiles")
     return p.parse_args()
 
 
@@ -206,6 +213,239 @@ def reference_arm(args, rank, world):
     return 0
 
 
+
+# ---- configs 1, 3, 5 and the cost-model refit (`--configs`, `--cost-model`) --------------------
+# Measurement modes next to the headline line: the other BASELINE.json configs end to end with
+# their CPU baselines (the unmodified reference through oracle/_ref/ref_tool where it implements
+# the path, the oracle port on one core for the extensions), and the paper's GPU cost model
+# refitted on B200 timings with the reference's own fit_params. These are bench.py's CPU-baseline
+# legs; the GPU side goes through the C ABI like every other measurement here.
+#
+#   python bench.py --configs [c1ref c1rk4 c5 c3]      -> one JSON line per case (profiles/r01_configs.*)
+#   python bench.py --cost-model [--cost-model-out DIR] -> r01_b200_timings*.txt, r01_cost_model.json
+#
+# c1ref  config 1 on the reference path: y' = y^2 (make_model_problem), backward-Euler Riccati,
+#        N = 64, M = 512, S in {79, 782}, vs the reference (ref_tool bench-scalar, all host cores).
+# c1rk4  config 1 as BASELINE.json names it: logistic y' = y (1 - y), RK4, y0 = 0.1 on [0, 10],
+#        nodes second kind on [0, 1.25], N = 64, M = 1024 (closed-form weights), S = 977.
+# c5     config 5: the c1rk4 and c1ref problems at M*S ~ 1e5, 1e6, 1e7 trajectory-steps per slice.
+# c3     config 3: Lotka-Volterra (1.5, 1, 1, 3) from (1, 1) on [0, 10], 256 x 256 uniform grid on
+#        [0.1, 8]^2 per slice, N = 512, S in {8, 64}: tables + the bilinear chain.
+def run_scalar(ctx, capi, kind, N, M, S, reps, closed_weights=False):
+    if kind == "riccati":
+        rhs = capi.ScalarRHS(capi.RHS_RICCATI_BE, capi.F64, 0.0, 0.0)
+        t0, T, y0, a, b, wk = 0.0, 0.5, 1.0, 0.0, 2.0, capi.WEIGHTS_PRODUCT
+    else:
+        rhs = capi.ScalarRHS(capi.RHS_LOGISTIC_RK4, capi.F64, 1.0, 1.0)
+        t0, T, y0, a, b, wk = 0.0, 10.0, 0.1, 0.0, 1.25, capi.WEIGHTS_CLOSED2
+    if closed_weights:
+        wk = capi.WEIGHTS_CLOSED2
+    dt = (T - t0) / (N * S)
+    y = C.c_double()
+    rep, fail = capi.Report(), capi.Fail()
+    walls, dev = [], []
+    for i in range(reps + 2):
+        t = time.perf_counter()
+        ctx.check(ctx.lib.pint_run_scalar(ctx.h, C.byref(rhs), t0, T, y0, N, dt, capi.NODES_SECOND_KIND, M, a, b,
+                                          wk, capi.SWEEP_EXACT, C.byref(y), None, None, None, C.byref(rep),
+                                          C.byref(fail)))
+        w = time.perf_counter() - t
+        if i >= 2:
+            walls.append(w)
+            dev.append(rep.device_ms * 1e-3)
+    steps = N * M * S
+    return {"traj_steps": steps, "e2e_ms": 1e3 * statistics.median(walls), "device_ms": 1e3 * statistics.median(dev),
+            "e2e_traj_steps_per_s": steps / statistics.median(walls),
+            "device_traj_steps_per_s": steps / statistics.median(dev), "final": y.value,
+            "gpu_launches": int(rep.gpu_launches), "h2d_bytes": int(rep.h2d_bytes), "d2h_bytes": int(rep.d2h_bytes)}
+
+
+def ref_scalar(N, M, S):
+    tool = ROOT / "oracle" / "_ref" / "ref_tool"
+    if not tool.exists():
+        return None
+    cores = os.cpu_count() or 1
+    out = subprocess.run([str(tool), "bench-scalar", "--N", str(N), "--M", str(M), "--S", str(S), "--workers",
+                          str(cores), "--reps", "2"], capture_output=True, text=True, timeout=600, check=True).stdout
+    r = min(json.loads(out), key=lambda x: x["seconds"])
+    return {"value": r["traj_steps"] / r["seconds"], "cores": cores, "kind": "reference",
+            "sample": f"full pint::run_nievergelt(make_model_problem) N={N} M={M} S={S}", "final": r["final"]}
+
+
+def port_logistic(N, M, S, sample=4):
+    import oracle as O
+    from paper_1304_6514_b200 import pint
+
+    dec = O.decompose(0.0, 10.0, N, 10.0 / (N * S))
+    steps, h = dec[2][:sample], dec[3][:sample]
+    nodes = pint.sample_nodes(pint.SECOND_KIND, M, 0.0, 1.25)
+    t = time.perf_counter()
+    O.logistic_rk4_ensemble(steps, h, nodes, 1.0, 1.0)
+    sec = time.perf_counter() - t
+    return {"value": sample * M * S / sec, "cores": 1, "kind": "port",
+            "sample": f"oracle logistic_rk4_ensemble, {sample} of {N} slices x {M} ICs x {S} steps"}
+
+
+def run_lv(ctx, N, Mg, S, reps):
+    import torch
+
+    from paper_1304_6514_b200.dist import LVPlan
+
+    LV = [1.5, 1.0, 1.0, 3.0]
+    un = 0.1 + ((8.0 - 0.1) * np.arange(Mg, dtype=np.float64)) / (Mg - 1)  # uniform grid on [0.1, 8]
+    plan = LVPlan(ctx, LV, 10.0, N, S, un, un)
+    lam0 = torch.tensor([1.0, 1.0], dtype=torch.float64)
+    stream = torch.cuda.current_stream()
+    devs, walls = [], []
+    out = None
+    for i in range(reps + 2):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        plan.build()
+        out = plan.sweep_block(lam0)  # (syncs; the result comes back to the host)
+        e1.record(stream)
+        e1.synchronize()
+        w = time.perf_counter() - t
+        if i >= 2:
+            walls.append(w)
+            devs.append(e0.elapsed_time(e1) * 1e-3)
+    steps = N * Mg * Mg * S
+    return {"traj_steps": steps, "e2e_ms": 1e3 * statistics.median(walls), "device_ms": 1e3 * statistics.median(devs),
+            "e2e_traj_steps_per_s": steps / statistics.median(walls),
+            "device_traj_steps_per_s": steps / statistics.median(devs), "final": [float(x) for x in out.cpu()],
+            "flops_per_traj_step": 54}
+
+
+def port_lv(N, Mg, S, sample=2):
+    import oracle as O
+
+    LV = [1.5, 1.0, 1.0, 3.0]
+    un = O.uniform_nodes(Mg, 0.1, 8.0)
+    dec = O.decompose(0.0, 10.0, N, 10.0 / (N * S))
+    t = time.perf_counter()
+    O.lv_rk4_ensemble(dec[2][:sample], dec[3][:sample], un, un, LV)
+    sec = time.perf_counter() - t
+    return {"value": sample * Mg * Mg * S / sec, "cores": 1, "kind": "port",
+            "sample": f"oracle lv_rk4_ensemble, {sample} of {N} slices x {Mg}^2 ICs x {S} steps"}
+
+
+
+def run_configs(a):
+    import torch
+
+    from paper_1304_6514_b200 import capi
+
+    torch.cuda.set_device(0)
+    ctx = capi.Context(0, stream=torch.cuda.current_stream())
+    peak = C.c_double()
+    ctx.check(ctx.lib.pint_probe_peak(ctx.h, capi.F64, C.byref(peak)))
+
+    def emit(d):
+        print(json.dumps(d), flush=True)
+
+    if "c1ref" in a.configs:
+        for S in (79, 782):
+            r = run_scalar(ctx, capi, "riccati", 64, 512, S, a.config_reps)
+            emit({"config": "c1 reference path (Riccati BE)", "N": 64, "M": 512, "S": S, **r,
+                  "cpu_baseline": ref_scalar(64, 512, S)})
+    if "c1rk4" in a.configs:
+        r = run_scalar(ctx, capi, "logistic", 64, 1024, 977, a.config_reps)
+        emit({"config": "c1 logistic RK4", "N": 64, "M": 1024, "S": 977, **r,
+              "fp64_frac_of_peak_device": r["device_traj_steps_per_s"] * 29 / (peak.value * 1e12),
+              "cpu_baseline": port_logistic(64, 1024, 977)})
+    if "c5" in a.configs:
+        for S in (98, 977, 9766):
+            r = run_scalar(ctx, capi, "logistic", 64, 1024, S, a.config_reps)
+            emit({"config": "c5 logistic RK4", "N": 64, "M": 1024, "S": S, "per_slice_traj_steps": 1024 * S, **r,
+                  "fp64_frac_of_peak_device": r["device_traj_steps_per_s"] * 29 / (peak.value * 1e12),
+                  "cpu_baseline": port_logistic(64, 1024, S, sample=max(1, min(8, 4000 // S)))})
+        for S in (98, 977, 9766):  # (M = 1024: closed-form weights; the reference's product form overflows)
+            r = run_scalar(ctx, capi, "riccati", 64, 1024, S, a.config_reps, closed_weights=True)
+            emit({"config": "c5 Riccati BE", "N": 64, "M": 1024, "S": S, "per_slice_traj_steps": 1024 * S, **r})
+    if "c3" in a.configs:
+        for S in (8, 64):
+            r = run_lv(ctx, 512, 256, S, a.config_reps)
+            emit({"config": "c3 Lotka-Volterra RK4 + bilinear chain", "N": 512, "grid": "256x256", "S": S, **r,
+                  "fp64_frac_of_peak_device": r["device_traj_steps_per_s"] * 54 / (peak.value * 1e12),
+                  "cpu_baseline": port_lv(512, 256, S)})
+
+
+
+CM_TOOL = ROOT / "oracle" / "_ref" / "ref_tool"
+PAPER_ROWS = [(6.103515625e-05, N, 4) for N in (32, 64, 128)] + \
+             [(3.0517578125e-05, N, 5) for N in (32, 64, 128)] + \
+             [(1.52587890625e-05, N, 7) for N in (32, 64, 128)]
+B200_ROWS = [(dt, N, M) for dt in (6.103515625e-05, 1.52587890625e-05) for N in (32, 128) for M in (64, 512)]
+
+def cm_device_total_us(ctx, capi, dt, N, M, reps):
+    rhs = capi.ScalarRHS(capi.RHS_RICCATI_BE, capi.F64, 0.0, 0.0)
+    y, rep, fail = C.c_double(), capi.Report(), capi.Fail()
+    walls = []
+    for i in range(reps + 2):
+        t = time.perf_counter()
+        ctx.check(ctx.lib.pint_run_scalar(ctx.h, C.byref(rhs), 0.0, 0.5, 1.0, N, dt, capi.NODES_SECOND_KIND, M, 0.0,
+                                          2.0, capi.WEIGHTS_PRODUCT, capi.SWEEP_EXACT, C.byref(y), None, None, None,
+                                          C.byref(rep), C.byref(fail)))
+        if i >= 2:
+            walls.append(time.perf_counter() - t)
+    return 1e6 * statistics.median(walls), y.value
+
+
+def cm_serial_us(dt):
+    out = subprocess.run([str(CM_TOOL), "bench-serial", "--dt", repr(dt), "--reps", "5"], capture_output=True,
+                         text=True, check=True, timeout=300).stdout
+    return 1e6 * json.loads(out)["seconds"]
+
+
+def cm_fit(path):
+    out = subprocess.run([str(CM_TOOL), "fit", str(path)], capture_output=True, text=True, check=True).stdout
+    return json.loads(out)
+
+
+
+def run_cost_model(a):
+    import torch
+
+    from paper_1304_6514_b200 import capi
+
+    torch.cuda.set_device(0)
+    ctx = capi.Context(0)
+    lines = ["# B200 (sm_100a) timings for the scalar benchmark, T = 0.5: pint_run_scalar end to end",
+             "# (host buffers), median of the reps; ratio = reference run_serial on one host core / T_total.",
+             "# Columns: dt, N (slices), M (trajectories), T_total (us), cpu/device ratio."]
+    rows = []
+    serial = {}
+    for dt, N, M in PAPER_ROWS + B200_ROWS:
+        if dt not in serial:
+            serial[dt] = cm_serial_us(dt)
+        tot, y = cm_device_total_us(ctx, capi, dt, N, M, a.cm_reps)
+        ratio = serial[dt] / tot
+        rows.append({"dt": dt, "N": N, "M": M, "T_total_us": tot, "ratio": ratio, "final": y})
+        lines.append(f"{dt!r}, {N}, {M}, {tot:.1f}, {ratio:.4f}")
+    prof = ROOT / a.cm_out
+    prof.mkdir(exist_ok=True)
+    fixture = prof / "r01_b200_timings.txt"
+    fixture.write_text("\n".join(lines) + "\n")
+    paper_rows = prof / "r01_b200_timings_paper_rows.txt"
+    paper_rows.write_text("\n".join(lines[:3 + len(PAPER_ROWS)]) + "\n")
+    ref_fixture = ROOT / "oracle" / "_ref" / "dropin" / "data" / "gpu_timings.txt"
+    result = {
+        "b200_fit_all_rows": cm_fit(fixture),
+        "b200_fit_paper_rows": cm_fit(paper_rows),
+        "reference_fixture_fit": cm_fit(ref_fixture) if ref_fixture.exists() else None,
+        "published": {"tau_F": 0.040, "tau_N": 0.701, "tau_K": 137.0, "tau_F_cpu": 0.051},
+        "rows": rows,
+        "serial_us": {repr(k): v for k, v in serial.items()},
+        "units": "microseconds (tau_F per fine step per trajectory, tau_N per slice, tau_K per run)",
+    }
+    (prof / "r01_cost_model.json").write_text(json.dumps(result, indent=1) + "\n")
+    print(json.dumps({k: result[k] for k in ("b200_fit_all_rows", "b200_fit_paper_rows", "reference_fixture_fit")}))
+
+
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -213,6 +453,12 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return reference_arm(args, rank, world)
+    if args.configs is not None:
+        args.configs = args.configs or ["c1ref", "c1rk4", "c5", "c3"]
+        return run_configs(args) or 0
+    if args.cost_model:
+        args.cm_reps, args.cm_out = args.cost_model_reps, args.cost_model_out
+        return run_cost_model(args) or 0
 
     import ctypes as C
 
