@@ -10,6 +10,7 @@
 #include <cmath>
 #include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -373,6 +374,30 @@ void heat_fill_steps(double dx, const pint_slice* slices, int64_t j0, int64_t j1
     if (step_off[j1] - step_off[j0] < 4096 || j1 - j0 < 2) fill(0, j1 - j0);
     else HostPool::get().parallel_for(j1 - j0, fill);
 }
+
+// The same tables for steps [s0, s1) of every slice (0-based step s = i - 1 of the loop above),
+// as one block [j][s - s0] (pitch s1 - s0) so that it travels in one copy.
+void heat_fill_step_range(double dx, const pint_slice* slices, int64_t N, int64_t s0, int64_t s1, double* r,
+                          double* fa, double* fb) {
+    const double inv_dx2 = 1.0 / (dx * dx);
+    auto fill = [&](int64_t a, int64_t b) {
+        for (int64_t j = a; j < b; ++j) {
+            const double tb = slices[j].t_begin, h = slices[j].dt;
+            const int64_t base = j * (s1 - s0) - s0, e = std::min<int64_t>(s1, slices[j].steps);
+            for (int64_t i = s0 + 1; i <= e; ++i) {
+                const double t = tb + static_cast<double>(i) * h;  // ode_core.hpp:83
+                const double st = std::sin(t);
+                const double a = 1.0 + 0.25 * st;
+                const int64_t q = base + i - 1;
+                r[q] = h * a * inv_dx2;
+                fa[q] = -st;
+                fb[q] = a * kPi * kPi * std::cos(t);
+            }
+        }
+    };
+    if (N * (s1 - s0) < 4096 || N < 2) fill(0, N);
+    else HostPool::get().parallel_for(N, fill);
+}
 }  // namespace
 
 int pint_heat_coefficients(double dx, const pint_slice* slices, int64_t N, int64_t* step_off,
@@ -665,7 +690,20 @@ struct HeatDev {
     size_t h2d = 0;
 };
 
-int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, HeatDev& H) {
+// Step segments of the e2e heat run: while the device builds steps [s0, s1) of every slice, the
+// host fills (and the side stream copies and factors) the next segment's tables, so the build
+// starts after the first segment's tables instead of all of them. The first segment is short
+// (the build waits for it); the host fills ~6x faster than the device builds, so it stays ahead.
+constexpr int kHeatSegments = 3;
+int64_t heat_segment_end(int64_t S, int k) {
+    static const int64_t num[kHeatSegments] = {1, 4, 8};  // eighths of S: [0, S/8), [S/8, S/2), [S/2, S)
+    return k + 1 >= kHeatSegments ? S : std::max<int64_t>(1, S * num[k] / 8);
+}
+
+using StepsFn = std::function<int(int64_t s0, int64_t s1)>;
+
+int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, HeatDev& H,
+                const StepsFn* on_steps = nullptr) {
     int64_t n = 0;
     if (const int rc = heat_dim(ctx, dx, &n)) return rc;
     for (const auto& s : sl)
@@ -707,12 +745,38 @@ int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, Hea
     // slice table + sx first, then the per-step tables in chunks of slices (multiples of 32, the
     // forced grid's slice groups): the host pool computes chunk c + 1 (glibc sin/cos) while the
     // copy engine and the record kernel work on chunk c
+    // (step segments: the tables go on the side stream, after the slice table and sx)
+    cudaStream_t tab_stream = ctx->stream;
     auto h2d = [&](const void* src, void* dst, size_t bytes) {
-        return ok(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D heat tables");
+        return ok(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, tab_stream), "H2D heat tables");
     };
     if (!h2d(h_off, H.step_off, sizeof(int64_t) * (N + 1)) || !h2d(h_dt, H.slice_dt, sizeof(double) * N) ||
         !h2d(h_sx, H.sx, sizeof(double) * n))
         return PINT_E_CUDA;
+    if (on_steps) {  // step segments (uniform slices: slice j's steps at j*S in every table)
+        cudaEventRecord(ctx->ev_fork, ctx->stream);  // slice table + sx are on the device
+        cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
+        tab_stream = ctx->side;
+        int64_t s0 = 0;
+        for (int k = 0; k < kHeatSegments && s0 < S; ++k) {
+            const int64_t s1 = std::max(s0 + 1, std::min(S, heat_segment_end(S, k)));
+            // segment k's block at offset N * s0 of each table (the blocks tile the Q = N * S slots)
+            const int64_t o = N * s0, cnt = N * (s1 - s0);
+            heat_fill_step_range(dx, sl.data(), N, s0, s1, h_r + o, h_fa + o, h_fb + o);
+            if (!h2d(h_r + o, H.r + o, sizeof(double) * cnt) || !h2d(h_fa + o, H.fa + o, sizeof(double) * cnt) ||
+                !h2d(h_fb + o, H.fb + o, sizeof(double) * cnt))
+                return PINT_E_CUDA;
+            if (const int rc = launch_heat_factor_block(ctx, ctx->side, n, N, S, 0, N, s0, s1 - s0, s1 - s0,
+                                                        H.step_off, H.slice_dt, H.r + o, H.fa + o, H.fb + o, H.sx,
+                                                        H.factor))
+                return rc;
+            cudaEventRecord(ctx->ev_join, ctx->side);
+            cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);
+            if (const int rc = (*on_steps)(s0, s1)) return rc;
+            s0 = s1;
+        }
+        return PINT_OK;
+    }
     const int64_t chunk = std::max<int64_t>(32, (N / 4 + 31) / 32 * 32);
     for (int64_t j0 = 0; j0 < N; j0 += chunk) {
         const int64_t j1 = std::min(N, j0 + chunk), q0 = h_off[j0], nq = h_off[j1] - q0;
@@ -750,9 +814,9 @@ int pint_run_heat(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int 
         return pint_set_error(ctx, PINT_E_BAD_GRID, "decompose: need N >= 1, T > t0, dt > 0");
     closure_slices(sl.data(), N, dt, sl);
     cudaEventRecord(ctx->ev0, ctx->stream);
-    HeatDev H;
-    if (const int rc = heat_upload(ctx, dx, sl, H)) return rc;
-    const int64_t n = H.n, ldm = pint_affine_ldm(n);
+    int64_t n = 0;
+    if (const int rc = heat_dim(ctx, dx, &n)) return rc;
+    const int64_t ldm = pint_affine_ldm(n);
     const size_t map_elems = static_cast<size_t>(n * ldm);
     // maps (N) + tree scratch (ceil(N/2)) + y0 + y + per-slice timers
     const size_t b_maps = align256(sizeof(double) * map_elems * N);
@@ -766,6 +830,22 @@ int pint_run_heat(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int 
     double* d_y0 = cv.take<double>(n);
     double* d_y = cv.take<double>(n);
     auto* d_ns = cv.take<unsigned long long>(N);
+    // step-segmented first build (uniform slices, register/shared-memory build; PINT_HEAT_SEGMENTS=0
+    // turns it off): launched from inside the upload, segment by segment
+    static const bool seg_env = [] {
+        const char* e = std::getenv("PINT_HEAT_SEGMENTS");
+        return !(e && e[0] == '0');
+    }();
+    bool uniform = true;
+    for (const auto& s : sl) uniform = uniform && s.steps == sl[0].steps;
+    const bool segmented = seg_env && uniform && heat_build_segmentable(n) && sl[0].steps >= 2 * kHeatSegments;
+    if (per_slice_seconds) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
+    HeatDev H;
+    const StepsFn seg_build = [&](int64_t s0, int64_t s1) {
+        return launch_heat_build_steps(ctx, n, N, sl[0].steps, H.step_off, H.factor, d_maps,
+                                       per_slice_seconds ? d_ns : nullptr, 0, s0, s1);
+    };
+    if (const int rc = heat_upload(ctx, dx, sl, H, segmented ? &seg_build : nullptr)) return rc;
     std::vector<double> y0v;
     if (!y0) {
         y0v.resize(static_cast<size_t>(n));
@@ -776,10 +856,12 @@ int pint_run_heat(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int 
     std::vector<unsigned long long> ns;
     int rc = PINT_OK;
     for (int guarded = 0; guarded < 2; ++guarded) {  // second pass only if a range check tripped
-        if (per_slice_seconds) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
-        rc = launch_heat_build(ctx, n, N, H.S, H.step_off, H.slice_dt, H.factor, H.sx, d_maps,
-                               per_slice_seconds ? d_ns : nullptr, guarded);
-        if (rc) return rc;
+        if (guarded || !segmented) {
+            if (per_slice_seconds && guarded) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
+            rc = launch_heat_build(ctx, n, N, H.S, H.step_off, H.slice_dt, H.factor, H.sx, d_maps,
+                                   per_slice_seconds ? d_ns : nullptr, guarded);
+            if (rc) return rc;
+        }
         cudaEventRecord(ctx->evc, ctx->stream);
         if (compose_mode == PINT_COMPOSE_TREE) rc = launch_affine_tree(ctx, n, N, d_maps, d_scr, d_y0, d_y, nullptr);
         else rc = launch_affine_chain(ctx, n, N, d_maps, d_y0, d_y);

@@ -185,6 +185,7 @@ constexpr int kRecChunk = 8;
 constexpr int kRecLane = 4 * kRecChunk + 1;  // padded per-lane stride (doubles)
 
 __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, long long S, long long j0, long long Nc,
+                                                          long long s0, long long Sc, long long tab_pitch,
                                                           const int64_t* __restrict__ step_off,
                                                           const double* __restrict__ slice_dt,
                                                           const double* __restrict__ r_tab,
@@ -194,9 +195,12 @@ __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, lo
     __shared__ double buf[4][32 * kRecLane];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const long long s = t / Nc, j = j0 + (t - s * Nc);  // slices [j0, j0 + Nc) of the N laid out
-    const bool live = t < S * Nc && step_off[j] + s < step_off[j + 1];  // slice j may have fewer steps
-    const long long q = live ? step_off[j] + s : 0;
+    const long long sr = t / Nc, j = j0 + (t - sr * Nc);  // slices [j0, j0 + Nc) of the N laid out,
+    const long long s = s0 + sr;                           // steps [s0, s0 + Sc)
+    const bool live = t < Sc * Nc && step_off[j] + s < step_off[j + 1];  // slice j may have fewer steps
+    // the step tables: slice-major at step_off, or (tab_pitch > 0) this block alone at
+    // [j][s - s0], pitch tab_pitch, from the pointers passed
+    const long long q = !live ? 0 : tab_pitch > 0 ? j * tab_pitch + sr : step_off[j] + s;
     const unsigned live_mask = __ballot_sync(0xffffffffu, live);
     double* mine = buf[w] + lane * kRecLane;
     const double r = live ? r_tab[q] : 0.0;
@@ -294,6 +298,7 @@ struct alignas(64) BuildPlan {
     long long ldm;
     unsigned long long* per_slice_ns;
     FailRec* fail;
+    long long s_begin, s_end;  // the steps this launch runs; s_begin > 0: resume from `maps`
 };
 
 
@@ -632,8 +637,12 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
     double* st = R0 + kBufs * staged_doubles(n, kMode) + (kLS == 32 ? lane : 0);
     // mbarriers of buffer b: forward half at bar0 + 16 b, back half at bar0 + 16 b + 8
     const unsigned bar0 = smem_u32(R0 + kBufs * staged_doubles(n, kMode) + (n - RR) * kLS + kLS * kFwdAhead);
-    const long long my_steps = (kGroup && slice >= P.N) ? 0 : P.step_off[slice + 1] - P.step_off[slice];
-    const long long steps = kGroup ? __reduce_max_sync(0xffffffffu, static_cast<unsigned>(my_steps)) : my_steps;
+    const long long my_all = (kGroup && slice >= P.N) ? 0 : P.step_off[slice + 1] - P.step_off[slice];
+    const long long all = kGroup ? __reduce_max_sync(0xffffffffu, static_cast<unsigned>(my_all)) : my_all;
+    // this launch: steps [s_begin, s_end) of the slice, counted from s0 = s_begin below
+    const long long s0 = P.s_begin;
+    const long long my_steps = max(0ll, min(my_all, P.s_end) - s0);
+    const long long steps = max(0ll, min(all, P.s_end) - s0);
     const RecView V = rec_view(P.rec, n, P.N, P.S);
     auto src = [&](long long s) { return kGroup ? V.fblock(s, g0) : V.rec(g0, s); };
     // forward half: header + (p, rcp) [+ h*b for the forced modes]; back half: c
@@ -647,16 +656,19 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
     // kTiles coordinates: column 2*(slice % 32) of pr2 / lanes (slice % 32) & ~1 of c; block s*N32 + G
     const int tx = static_cast<int>(slice & 31), tg = static_cast<int>(slice >> 5), ng = static_cast<int>(groups32(P.N));
     auto load_fwd = [&](long long s, int b) {
+        s += s0;
         const unsigned dst = smem_u32(buf(b)), bar = bar0 + 16u * b;
         if (kTiles) tile_load(dst, &P.tm_pr, 2 * tx, 0, static_cast<int>(s) * ng + tg, fwd_bytes, bar);
         else bulk_load(dst, src(s), fwd_bytes, bar);
     };
     auto load_back = [&](long long s, int b) {
+        s += s0;
         const unsigned dst = smem_u32(buf(b) + back_off), bar = bar0 + 16u * b + 8u;
         if (kTiles) tile_load(dst, &P.tm_cc, tx & ~1, 0, static_cast<int>(s) * ng + tg, back_bytes, bar);
         else bulk_load(dst, src(s) + back_off, back_bytes, bar);
     };
     auto prefetch = [&](long long s) {
+        s += s0;
         if (kTiles) {
             tile_prefetch(&P.tm_pr, 2 * tx, 0, static_cast<int>(s) * ng + tg);
             tile_prefetch(&P.tm_cc, tx & ~1, 0, static_cast<int>(s) * ng + tg);
@@ -681,6 +693,14 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
 #pragma unroll
     for (int i = 0; i < RR; ++i) reg[i] = (i == k) ? 1.0 : 0.0;  // e_k; the forced run starts at 0
     for (int i = RR; i < n; ++i) st[(i - RR) * kLS] = (i == k) ? 1.0 : 0.0;
+    // a resumed segment starts from the column the previous one stored (the group-forced shadow
+    // lanes read their slice's column too)
+    if (s0 > 0 && (kGroup ? slice < P.N : k <= n)) {
+        const double* gp = P.maps + slice * n * P.ldm + k;
+#pragma unroll
+        for (int i = 0; i < RR; ++i) reg[i] = gp[i * P.ldm];
+        for (int i = RR; i < n; ++i) st[(i - RR) * kLS] = gp[i * P.ldm];
+    }
 
     unsigned qmin = 0xffffffffu;
 #ifdef PINT_HEAT_PROF
@@ -1008,12 +1028,20 @@ int64_t heat_records_doubles(int64_t n, int64_t N, int64_t S) { return records_d
 int launch_heat_factor_range(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, int64_t j0, int64_t Nc,
                              const int64_t* step_off, const double* slice_dt, const double* r, const double* fa,
                              const double* fb, const double* sx, double* records) {
-    if (n < 1 || N < 0 || S < 0 || j0 < 0 || Nc < 0 || j0 + Nc > N)
+    return launch_heat_factor_block(ctx, ctx->stream, n, N, S, j0, Nc, 0, S, 0, step_off, slice_dt, r, fa, fb, sx,
+                                    records);
+}
+
+int launch_heat_factor_block(pint_ctx* ctx, cudaStream_t stream, int64_t n, int64_t N, int64_t S, int64_t j0,
+                             int64_t Nc, int64_t s0, int64_t Sc, int64_t tab_pitch, const int64_t* step_off,
+                             const double* slice_dt, const double* r, const double* fa, const double* fb,
+                             const double* sx, double* records) {
+    if (n < 1 || N < 0 || S < 0 || j0 < 0 || Nc < 0 || j0 + Nc > N || s0 < 0 || Sc < 0 || s0 + Sc > S)
         return pint_set_error(ctx, PINT_E_INVALID, "heat_factor: bad sizes");
-    if (Nc == 0 || S == 0) return PINT_OK;
-    const long long threads = Nc * S;
-    heat_record_kernel<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, ctx->stream>>>(
-        static_cast<int>(n), N, S, j0, Nc, step_off, slice_dt, r, fa, fb, sx, records, ctx->d_fail);
+    if (Nc == 0 || Sc == 0) return PINT_OK;
+    const long long threads = Nc * Sc;
+    heat_record_kernel<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, stream>>>(
+        static_cast<int>(n), N, S, j0, Nc, s0, Sc, tab_pitch, step_off, slice_dt, r, fa, fb, sx, records, ctx->d_fail);
     return pint_check_launch(ctx, "heat_record_kernel");
 }
 
@@ -1028,10 +1056,25 @@ int launch_heat_build(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int6
                       unsigned long long* per_slice_ns, int guarded) {
     if (n < 1 || N < 0) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: bad sizes");
     if (N == 0) return PINT_OK;
-    if (n > (1 << 20) || N > (1 << 26)) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: sizes out of range");
     (void)slice_dt;  // the per-slice step lives in the records (h*b) and step_off
     (void)sx;
+    return launch_heat_build_steps(ctx, n, N, S, step_off, records, maps, per_slice_ns, guarded, 0, S);
+}
+
+bool heat_build_segmentable(int64_t n) { return n >= 1 && !use_tmem(n); }
+
+int launch_heat_build_steps(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
+                            const double* records, double* maps, unsigned long long* per_slice_ns, int guarded,
+                            int64_t s_begin, int64_t s_end) {
+    if (n < 1 || N < 0 || s_begin < 0 || s_end < s_begin)
+        return pint_set_error(ctx, PINT_E_INVALID, "heat_build: bad sizes");
+    if (N == 0 || s_end == s_begin) return PINT_OK;
+    if (n > (1 << 20) || N > (1 << 26)) return pint_set_error(ctx, PINT_E_INVALID, "heat_build: sizes out of range");
+    if ((s_begin > 0 || s_end < S) && !heat_build_segmentable(n))
+        return pint_set_error(ctx, PINT_E_INVALID, "heat_build: step segments need the register/shared-memory build");
     BuildPlan P{};
+    P.s_begin = s_begin;
+    P.s_end = s_end;
     P.n = static_cast<int>(n);
     P.N = static_cast<int>(N);
     P.S = S;
