@@ -693,11 +693,22 @@ struct HeatDev {
 // Step segments of the e2e heat run: while the device builds steps [s0, s1) of every slice, the
 // host fills (and the side stream copies and factors) the next segment's tables, so the build
 // starts after the first segment's tables instead of all of them. The first segment is short
-// (the build waits for it); the host fills ~6x faster than the device builds, so it stays ahead.
+// (the build waits for it); the host fills ~10x faster than the device builds, so it stays ahead.
 constexpr int kHeatSegments = 3;
+// segment ends in eighths of S (the last segment ends at S). Default: [0, S/4), [S/4, S) — measured
+// at C2 (tools/e2e_breakdown.py) e2e 1.70 ms unsegmented, 1.64 with "2", 1.65 "1", 1.69 "1,4",
+// 1.71 "2,5": every extra boundary costs a record-kernel gap. PINT_HEAT_SPLIT: experiments only
 int64_t heat_segment_end(int64_t S, int k) {
-    static const int64_t num[kHeatSegments] = {1, 4, 8};  // eighths of S: [0, S/8), [S/8, S/2), [S/2, S)
-    return k + 1 >= kHeatSegments ? S : std::max<int64_t>(1, S * num[k] / 8);
+    static const std::vector<int64_t> ends = [] {
+        std::vector<int64_t> v;
+        const char* e = std::getenv("PINT_HEAT_SPLIT");
+        for (const char* p = e ? e : "2"; *p && static_cast<int>(v.size()) < kHeatSegments - 1;) {
+            v.push_back(std::strtol(p, const_cast<char**>(&p), 10));
+            while (*p == ',') ++p;
+        }
+        return v;
+    }();
+    return k >= static_cast<int>(ends.size()) ? S : std::max<int64_t>(1, S * ends[k] / 8);
 }
 
 using StepsFn = std::function<int(int64_t s0, int64_t s1)>;
