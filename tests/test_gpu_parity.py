@@ -608,3 +608,25 @@ def test_lv_plan_block_chain(ctx):
     _, _, st, h = O.decompose(0.0, 10.0, N, 10.0 / (N * S))
     lam, _, _ = O.bilinear_sweep(un, vn, O.lv_rk4_ensemble(st, h, un, vn, LV), 1.0, 1.0)
     assert want.tolist() == lam[-1].tolist()
+
+
+@pytest.mark.gpu
+def test_heat_step_segments_match_unsegmented(ctx):
+    """The e2e heat run builds in step segments (capi.cu heat_upload, resumed columns); the same
+    run with PINT_HEAT_SEGMENTS=0 (one launch over all steps) must give bit-identical results."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, sys; sys.path.insert(0, '.'); from paper_1304_6514_b200 import pint; "
+            "N, S = 64, 40; dx, dt = 1.0 / 129.0, 10.0 / (N * S); prob = pint.make_heat_problem(dx, dt, 10.0); "
+            "r = pint.run_nievergelt(prob, N, pint.ExecConfig()); np.save(sys.argv[1], r.final_state)")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        path = os.path.join(root, "gpurun_out", f"_seg{flag}.npy")
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        env = dict(os.environ, PINT_HEAT_SEGMENTS=flag)
+        subprocess.run([sys.executable, "-c", code, path], cwd=root, env=env, check=True, timeout=300)
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
