@@ -2,19 +2,23 @@
 """Benchmark of the Nievergelt slice-map path (BASELINE.json metric: ODE trajectory-steps/s and
 time-to-solution at 1/2/4/8 B200 vs the CPU reference).
 
-Workload (BASELINE.json configs[1]): linear ODE system from the semi-discretised 1-D heat
-equation, n = 128 interior points (dx = 1/129), T = 10, affine propagator per slice from n+1
-basis trajectories, matrix-product (tree) composition. 256 slices x 256 backward-Euler steps per
-GPU (weak scaling: N = 256 x n_gpus slices, dt = T / (N S)). One "step" = one full solve:
-per-step factor tables -> all slice maps (K3) -> log-depth tree compose (K4) -> y = G y0 + c,
-plus, for n_gpus > 1, the NCCL gather of the composed block maps and the root's ordered apply.
+Default workload (BASELINE.json configs[3], the large-slice config the 1->8 GPU target is stated
+on): linear ODE system of the semi-discretised 1-D heat equation, n = 512 interior points
+(dx = 1/513), T = 10, N = 4096 time slices x S = 16 backward-Euler steps (dt = T/(N S)), an
+affine propagator per slice from n+1 basis trajectories, composed into the final state.
+STRONG scaling: the 4096 slices are fixed and split into contiguous blocks over the GPUs.
+`--workload c2` selects configs[1] instead (n = 128, 256 slices x 256 steps).
+One "step" = one full solve: per-step factor records -> all slice maps (K3) -> composition
+(K4) -> y = final state, plus for n_gpus > 1 the one NCCL gather and the root's ordered apply.
 
   python bench.py [--gpus N --steps K --warmup W]            # this implementation
   python bench.py --impl reference [...]                     # the reference CPU path (oracle/_ref)
 
-value: trajectory-steps/s with tables resident in HBM (device events, L2 flushed between steps).
-e2e:   the same metric through the host-buffer C-ABI call pint_run_heat (N=1) / the sharded
-       host path (N>1): host tables + H2D + device + D2H of the final state, wall clock.
+value:  trajectory-steps/s with tables resident in HBM (device events, L2 flushed between steps).
+e2e:    the same metric through the host-buffer C-ABI call (pint_run_heat at N = 1): host
+        tables + H2D + device + D2H of the final state, wall clock.
+parity: the final state of the timed configuration against the unmodified reference's
+        run_nievergelt final state (tests/golden/heat_finals.npz, made by oracle/_ref/ref_tool).
 """
 from __future__ import annotations
 
@@ -35,12 +39,21 @@ import numpy as np
 ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "ODE trajectory-steps/s (heat affine slice maps + tree compose)"
+METRIC = "ODE trajectory-steps/s (heat affine slice maps + composition: time-to-solution)"
+UNIT = "traj-steps/s"
+GOLDEN = ROOT / "tests" / "golden" / "heat_finals.npz"
+
+# name -> (n interior points, N slices (fixed: strong scaling), S steps per slice, reference sample
+# slices, BASELINE.json config)
+WORKLOADS = {
+    "c4": (512, 4096, 16, 512, "configs[3]"),
+    "c2": (128, 256, 256, 256, "configs[1]"),
+}
 
 
 def chain_floor(n: int, slices: int, S: int, lat, build_ms: float, sm_mhz: float) -> dict:
-    """The build's real bound: every column is a chain of S*n dependent rows (forward + back row
-    latencies measured live by pint_probe_latency), run in `waves` rounds of resident columns."""
+    """The exact build's real bound: every column is a chain of S*n dependent rows (forward + back
+    row latencies measured live by pint_probe_latency), run in `waves` rounds of resident columns."""
     row = float(lat[5] + lat[6])
     sms = 148
     if 282 <= n <= 520:  # heat_build_tmem_kernel: one 5-warp CTA per SM per slice quarter
@@ -52,25 +65,27 @@ def chain_floor(n: int, slices: int, S: int, lat, build_ms: float, sm_mhz: float
             "chain_waves": waves}
 
 
-def workload_name(n: int, slices_per_gpu: int, S: int) -> str:
-    """BASELINE.json config the flags select: configs[1] (default) or configs[3]'s per-GPU share."""
-    if n == 512:
-        return f"heat n=512 affine slice maps + tree compose (BASELINE.json configs[3]: {slices_per_gpu} " \
-               f"slices per GPU of 4096 at S={S})"
-    return f"heat n={n} affine slice maps + tree compose (BASELINE.json configs[1])"
-UNIT = "traj-steps/s"
+def workload_name(args) -> str:
+    n, N, S = args.n, args.slices, args.S
+    cfg = WORKLOADS[args.workload][4] if (n, N, S) == WORKLOADS[args.workload][:3] else "custom"
+    return (f"heat n={n} (dx=1/{n + 1}), T={args.T:g}, {N} slices x {S} backward-Euler steps, affine maps from "
+            f"n+1 basis trajectories + composition (BASELINE.json {cfg}); strong scaling: {N} slices split "
+            f"over the GPUs")
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--n", type=int, default=128, help="interior points (dx = 1/(n+1))")
-    p.add_argument("--slices-per-gpu", type=int, default=256)
-    p.add_argument("--S", type=int, default=256, help="backward-Euler steps per slice")
+    p.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    p.add_argument("--n", type=int, default=None, help="interior points (dx = 1/(n+1))")
+    p.add_argument("--slices", type=int, default=None, help="total time slices (fixed over GPU counts)")
+    p.add_argument("--S", type=int, default=None, help="backward-Euler steps per slice")
     p.add_argument("--T", type=float, default=10.0)
+    p.add_argument("--ref-sample", type=int, default=None,
+                   help="slices the reference CPU baseline builds per rep (default: the workload's)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--configs", nargs="*", default=None,
                    help="measure BASELINE configs 1/3/5 instead (cases: c1ref c1rk4 c5 c3; default all)")
@@ -78,7 +93,36 @@ def parse():
     p.add_argument("--cost-model", action="store_true", help="refit the paper's cost model on B200 timings")
     p.add_argument("--cost-model-reps", type=int, default=7)
     p.add_argument("--cost-model-out", default="profiles")
-    return p.parse_args()
+    a = p.parse_args()
+    d = WORKLOADS[a.workload]
+    a.n = a.n or d[0]
+    a.slices = a.slices or d[1]
+    a.S = a.S or d[2]
+    a.ref_sample = min(a.ref_sample or d[3], a.slices)
+    return a
+
+
+def golden_final(n: int, N: int, S: int, T: float):
+    """The unmodified reference's run_nievergelt final state for this configuration, if committed."""
+    if not GOLDEN.exists() or T != 10.0:
+        return None, None
+    z = np.load(GOLDEN)
+    for key in ("c4", "c2"):
+        if tuple(int(x) for x in z[f"{key}_config"]) == (n, N, S):
+            return z[f"{key}_final"], key
+    return None, None
+
+
+def parity_check(y, n: int, N: int, S: int, T: float, tol: float = 1e-12) -> dict:
+    """Final state vs the reference's (bit-exact expected for the exact chain, <= tol relative)."""
+    ref, key = golden_final(n, N, S, T)
+    if ref is None:
+        return {"vs": "no committed reference final state for this configuration", "ok": None}
+    y = np.asarray(y, dtype=np.float64)
+    rel = float(np.max(np.abs(y - ref)) / np.max(np.abs(ref)))
+    return {"vs": f"reference pint::run_nievergelt final_state (tests/golden/heat_finals.npz:{key}_final, "
+                  f"oracle/_ref/ref_tool)", "max_rel_diff": rel, "bit_exact": bool(np.array_equal(y, ref)),
+            "tolerance": tol, "ok": bool(rel <= tol)}
 
 
 def flops_per_slice_step(n: int) -> int:
@@ -152,17 +196,29 @@ def ref_tool():
     return p if p.exists() else None
 
 
-def run_reference_cpu(n, N, S, T, reps, workers=None):
-    """Time the UNMODIFIED reference (oracle/_ref/ref_tool -> pint::run_nievergelt) on host cores."""
+def run_reference_cpu(n, N, S, T, reps, workers=None, sample=None):
+    """Time the UNMODIFIED reference (oracle/_ref/ref_tool) on host cores: pint::run_nievergelt on
+    the full configuration (T_total), or with sample k < N its own build_affine_propagator on the
+    first k slices through parallel_map + compose_sweep (the per-slice body of run_nievergelt,
+    nievergelt.cpp:237-253) — the same per-slice work, a bounded sample of it."""
     tool = ref_tool()
     if tool is None:
         return None
     workers = workers or os.cpu_count() or 1
     cmd = [str(tool), "bench-heat", "--n", str(n), "--N", str(N), "--S", str(S), "--T", repr(T),
            "--workers", str(workers), "--reps", str(reps)]
+    if sample and sample < N:
+        cmd += ["--sample-slices", str(sample)]
     out = subprocess.run(cmd, check=True, capture_output=True, text=True, timeout=1800).stdout
     runs = json.loads(out)
     return {"runs": runs, "workers": workers, "cmd": " ".join(cmd[1:])}
+
+
+def ref_sample_text(n, N, S, k, workers):
+    if k >= N:
+        return f"full pint::run_nievergelt N={N} S={S} n={n} (its T_total, {workers} workers)"
+    return (f"reference build_affine_propagator on the first {k} of {N} slices (parallel_map, {workers} workers) "
+            f"+ compose_sweep; n={n}, S={S}: same per-slice work as the full run")
 
 
 def run_port_cpu(n, N, S, T, slices=4):
@@ -181,37 +237,37 @@ def run_port_cpu(n, N, S, T, slices=4):
 def reference_arm(args, rank, world):
     if rank != 0:
         return 0
-    N = args.slices_per_gpu * args.gpus
-    for _ in range(args.warmup):
-        pass  # the reference has no device state to warm; each rep is a cold full run
-    # each timed step is one full reference solve; bound the whole arm to about a minute
-    res = run_reference_cpu(args.n, N, args.S, args.T, 1)
+    n, N, S, k = args.n, args.slices, args.S, args.ref_sample
+    # no device state to warm: every rep is a cold run of the reference; bound the arm to ~1.5 min
+    res = run_reference_cpu(n, N, S, args.T, 1, sample=k)
     if res is not None and args.steps > 1:
         per = max(res["runs"][0]["seconds"], 1e-3)
-        more = min(args.steps - 1, int(60.0 / per))
+        more = min(args.steps - 1, int(90.0 / per))
         if more > 0:
-            res["runs"] += run_reference_cpu(args.n, N, args.S, args.T, more)["runs"]
+            res["runs"] += run_reference_cpu(n, N, S, args.T, more, sample=k)["runs"]
     if res is None:
-        rp = run_port_cpu(args.n, N, args.S, args.T)
+        rp = run_port_cpu(n, N, S, args.T)
         v = rp["traj_steps"] / rp["seconds"]
         kind, cores, sample, secs = "port", 1, f"oracle heat_build on 4 of {N} slices", rp["seconds"]
+        reps = 1
     else:
-        vals = [r["traj_steps"] / r["seconds"] for r in res["runs"]]
-        v = statistics.mean(vals)
-        secs = statistics.mean(r["seconds"] for r in res["runs"])
-        kind, cores, sample = "reference", res["workers"], f"full run_nievergelt (N={N}, S={args.S}, n={args.n})"
+        tot_steps = sum(r["traj_steps"] for r in res["runs"])
+        secs_all = sum(r["seconds"] for r in res["runs"])
+        v = tot_steps / secs_all
+        secs = N * (n + 1) * S / v  # time-to-solution of the full configuration at the sampled rate
+        kind, cores, sample = "reference", res["workers"], ref_sample_text(n, N, S, k, res["workers"])
+        reps = len(res["runs"])
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args.n, args.slices_per_gpu, args.S), "n": args.n,
-                   "slices": N, "steps_per_slice": args.S, "T": args.T, "compose": "chain (reference)"},
+        "steps": reps, "warmup": 0, "ms_per_step": secs * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args), "n": n, "slices": N, "steps_per_slice": S, "T": args.T,
+                   "compose": "chain (reference compose_sweep)"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
-
 
 
 # ---- configs 1, 3, 5 and the cost-model refit (`--configs`, `--cost-model`) --------------------
@@ -460,13 +516,15 @@ def main():
         args.cm_reps, args.cm_out = args.cost_model_reps, args.cost_model_out
         return run_cost_model(args) or 0
 
-    import ctypes as C
+    return heat_bench(args, rank, world, local)
 
+
+def heat_bench(args, rank, world, local):
     import torch
     import torch.distributed as dist
 
     from paper_1304_6514_b200 import capi, pint
-    from paper_1304_6514_b200.dist import HeatPlan, HeatTablesHost, apply_chain, gather_maps, slice_block
+    from paper_1304_6514_b200.dist import HeatPlan, apply_chain, gather_maps, slice_block
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -475,8 +533,7 @@ def main():
     ctx = capi.Context(local, stream=stream)
     pint.set_context(ctx)
 
-    n, S, T = args.n, args.S, args.T
-    N = args.slices_per_gpu * world
+    n, S, T, N = args.n, args.S, args.T, args.slices
     dx, dt = 1.0 / (n + 1), T / (N * S)
     lo, hi = slice_block(N, world, rank)
     plan = HeatPlan(ctx, dx, dt, T, N, lo, hi)
@@ -500,8 +557,10 @@ def main():
                  P(plan.maps), None, plan.guarded)
         if events:
             events[2].record(stream)
-        plan.compose_local(capi.COMPOSE_TREE, want_composed=world > 1)
-        if world > 1:
+        if world == 1:  # y only: DMMA tree levels + chain tail (n <= 256) / the bit-exact chain (n > 256)
+            plan.compose_local(capi.COMPOSE_TREE, want_composed=False)
+        else:  # this block's composed map, gathered to rank 0, applied in rank order
+            plan.compose_local(capi.COMPOSE_TREE, want_composed=True)
             maps = gather_maps(plan.composed)
             if rank == 0:
                 apply_chain(ctx, plan.n, torch.cat(maps), plan.y0, plan.y)
@@ -516,6 +575,7 @@ def main():
             one_step()
         torch.cuda.synchronize()
         plan.verify()
+    parity = parity_check(plan.y.cpu().numpy(), n, N, S, T) if rank == 0 else None
     if world > 1:
         dist.barrier()
 
@@ -528,6 +588,8 @@ def main():
     for _ in range(args.steps):
         flush.zero_()  # L2 flush between timed iterations (outside the events)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        if world > 1:
+            dist.barrier()
         one_step(ev)
         ev[3].synchronize()
         tot["step"] += ev[0].elapsed_time(ev[3])
@@ -535,7 +597,7 @@ def main():
         tot["build"] += ev[1].elapsed_time(ev[2])
         tot["compose"] += ev[2].elapsed_time(ev[3])
     torch.cuda.synchronize()
-    launches = ctx.launches() - launches0 - 0  # our kernels only (flush is torch's)
+    launches = ctx.launches() - launches0  # our kernels only (the flush is torch's)
     if world > 1:
         t = torch.tensor([tot["step"]], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -545,14 +607,14 @@ def main():
     clocks.stop()
 
     ms_per_step = tot["step"] / args.steps
-    traj_steps_total = N * (n + 1) * S  # every rank's block: all ranks processed all N slices
+    traj_steps_total = N * (n + 1) * S  # all ranks together processed all N slices
     value = traj_steps_total / (ms_per_step * 1e-3)
 
-    # ---- e2e: host buffers through the public API, H2D + D2H inside the timed region
-    y_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    # ---- e2e: host buffers through the public C ABI, H2D + D2H inside the timed region
+    y_np = np.empty(n)
     e2e_secs, h2d, d2h = 0.0, 0, 0
+    e2e_parity = None
     if world == 1:
-        y_np = y_host.numpy()
         rep = capi.Report()
         for i in range(args.warmup + args.steps):
             flush.zero_()
@@ -564,13 +626,18 @@ def main():
             if i >= args.warmup:
                 e2e_secs += dt_s
         h2d, d2h = int(rep.h2d_bytes), int(rep.d2h_bytes)
+        e2e_parity = parity_check(y_np, n, N, S, T)
     else:
+        from paper_1304_6514_b200.dist import HeatTablesHost
+
+        y_host = torch.empty(n, dtype=torch.float64).pin_memory()
+        host = HeatTablesHost(dx, plan.slices)  # pinned staging allocated once, outside the loop
         for i in range(args.warmup + args.steps):
             flush.zero_()
             torch.cuda.synchronize()
             dist.barrier()
             t0 = time.perf_counter()
-            host = HeatTablesHost(dx, plan.slices)
+            host.refill(dx, plan.slices)
             plan.host = host
             b = plan.upload()
             one_step()
@@ -590,25 +657,24 @@ def main():
     build_flops = sum(s.steps for s in plan.slices) * flops_per_slice_step(n)
     achieved = build_flops / (build_ms * 1e-3) / 1e12
     traffic = None
-    prof = ROOT / "profiles" / "r01_build_traffic.json"
+    prof = ROOT / "profiles" / "r02_build_traffic.json"
     if prof.exists():
         try:
             tr = json.loads(prof.read_text())
-            # (only when the capture is of this very configuration)
-            if tuple(tr.get("config", (128, 256, 256))) == (n, args.slices_per_gpu, args.S):
-                traffic = tr.get("dram_bytes_per_launch")
+            # (only when the capture is of this very configuration and build)
+            key = f"n{n}_N{hi - lo}_S{S}"
+            traffic = tr.get(key, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            res = run_reference_cpu(n, N, S, T, 1)
+            res = run_reference_cpu(n, N, S, T, 1, sample=args.ref_sample)
             if res is not None:
                 r0 = res["runs"][0]
                 cpu = {"value": r0["traj_steps"] / r0["seconds"], "unit": UNIT, "cores": res["workers"],
-                       "kind": "reference", "sample": f"full pint::run_nievergelt N={N} S={S} n={n} "
-                       f"(T_total, {res['workers']} workers)"}
+                       "kind": "reference", "sample": ref_sample_text(n, N, S, args.ref_sample, res["workers"])}
             else:
                 rp = run_port_cpu(n, N, S, T)
                 cpu = {"value": rp["traj_steps"] / rp["seconds"], "unit": UNIT, "cores": 1, "kind": "port",
@@ -618,19 +684,22 @@ def main():
 
     if rank == 0:
         csum = clocks.summary(t_region0, t_region1)
+        kern = "heat_build_tmem_kernel" if 282 <= n <= 520 else "heat_build_kernel"  # (heat.cu use_tmem)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(n, args.slices_per_gpu, args.S),
-                       "n": n, "slices": N, "slices_per_gpu": args.slices_per_gpu, "steps_per_slice": S, "T": T,
-                       "dt": dt, "compose": "tree (DMMA)" + (" + NCCL gather" if world > 1 else ""),
-                       "parallelism": f"slice blocks x{world}", "l2": "flushed (256 MB write) between steps",
+            "config": {"workload": workload_name(args), "n": n, "slices": N, "slices_per_gpu": hi - lo,
+                       "steps_per_slice": S, "T": T, "dt": dt, "build": "exact",
+                       "compose": ("chain (bit-exact)" if n > 256 else "tree (DMMA) levels + chain tail") if world == 1
+                       else "block tree (DMMA) + NCCL gather + root chain",
+                       "parallelism": f"slice blocks x{world}",
+                       "l2": "flushed (256 MB write) between steps; maps alone exceed L2",
                        "time_to_solution_ms": ms_per_step, "e2e_time_to_solution_ms": e2e_secs / args.steps * 1e3},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "parity": parity, "e2e_parity": e2e_parity,
             "gpu_launches": launches,
-            "roofline": {"bound": "fp64", "kernel": "heat_build_tmem_kernel" if 282 <= n <= 520 else "heat_build_kernel",  # (heat.cu use_tmem)
-                         "achieved": achieved,
+            "roofline": {"bound": "fp64", "kernel": kern, "achieved": achieved,
                          "peak": peak64.value, "unit": "TFLOP/s", "frac": achieved / peak64.value,
                          "traffic": traffic, "peak_source": "measured DFMA probe (pint_probe_peak)",
                          "flops_per_launch": build_flops, "launch_ms": build_ms,

@@ -105,6 +105,10 @@ int64_t pint_ctx_launch_count(const pint_ctx* ctx);
 /* read (and clear) the device-side failure record; syncs the stream */
 int pint_fail_read(pint_ctx* ctx, pint_fail* out);
 const char* pint_version(void);
+/* test hook: K device-side failures (task idx[t], code[t], value[t]) recorded concurrently through
+   the same path the kernels use; pint_fail_read must return the lowest index with ITS code/value */
+int pint_debug_fail_inject(pint_ctx* ctx, int64_t K, const int64_t* idx, const int* code,
+                           const double* value);
 
 /* ---- host-side tables (bit-identical to the reference's own host arithmetic) ---- */
 /* steps_for (ode_core.cpp:18-24) */

@@ -285,6 +285,11 @@ int cmd_golden(const std::string& dir) {
     return 0;
 }
 
+void write_f64(const std::string& path, const Vector& v) {
+    std::ofstream f(path, std::ios::binary);
+    f.write(reinterpret_cast<const char*>(v.data()), static_cast<std::streamsize>(v.size() * sizeof(double)));
+}
+
 double arg_d(std::map<std::string, std::string>& a, const char* k, double dflt) {
     return a.count(k) ? std::atof(a[k].c_str()) : dflt;
 }
@@ -302,6 +307,8 @@ int cmd_bench_heat(std::map<std::string, std::string> a) {
     if (workers == 0) workers = std::max(1u, std::thread::hardware_concurrency());
     const auto k = static_cast<std::size_t>(arg_d(a, "--sample-slices", static_cast<double>(N)));
     const int reps = static_cast<int>(arg_d(a, "--reps", 1));
+    // --final-out <file>: the full final state of the last rep as raw little-endian f64 (golden)
+    const std::string final_out = a.count("--final-out") ? a["--final-out"] : std::string();
     const double dx = 1.0 / static_cast<double>(n + 1);
     const double dt = T / static_cast<double>(N * S);
     const auto heat = make_heat_problem(dx, dt, T);
@@ -317,6 +324,7 @@ int cmd_bench_heat(std::map<std::string, std::string> a) {
             // here is the reference's T_total only, matching what the reference reports.
             const RunReport r = run_nievergelt(heat, N, e);
             final0 = r.final_state[0];
+            if (!final_out.empty()) write_f64(final_out, r.final_state);
             const double secs = r.T_total;
             std::printf("%s{\"seconds\": %.9g, \"slices\": %zu, \"traj_steps\": %.17g, \"final0\": %.17g}",
                         rep ? "," : "", secs, N, static_cast<double>(N * (n + 1) * S), final0);
@@ -327,6 +335,7 @@ int cmd_bench_heat(std::map<std::string, std::string> a) {
             SweepStats stats;
             const Vector y = compose_sweep(maps, heat.y0, 0.0, stats);
             final0 = y[0];
+            if (!final_out.empty()) write_f64(final_out, y);
             const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             std::printf("%s{\"seconds\": %.9g, \"slices\": %zu, \"traj_steps\": %.17g, \"final0\": %.17g}",
                         rep ? "," : "", secs, k, static_cast<double>(k * (n + 1) * S), final0);

@@ -73,6 +73,7 @@ _SIGS = {
     "pint_ctx_set_stream": (_int, [_vp, _vp]),
     "pint_ctx_launch_count": (_i, [_vp]),
     "pint_fail_read": (_int, [_vp, C.POINTER(Fail)]),
+    "pint_debug_fail_inject": (_int, [_vp, _i, _vp, _vp, _vp]),
     "pint_steps_for": (_i, [_d, _d]),
     "pint_decompose": (_int, [_d, _d, _i, _d, C.POINTER(Slice)]),
     "pint_sample_nodes": (_int, [_int, _i, _d, _d, _vp]),

@@ -302,6 +302,22 @@ int pint_fail_read(pint_ctx* ctx, pint_fail* out) {
     return PINT_OK;
 }
 
+namespace {
+// Test hook for the failure-record protocol: thread t records (idx[t], code[t], value[t]).
+__global__ void fail_inject_kernel(int64_t K, const int64_t* idx, const int* code, const double* value, FailRec* rec) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < K) pint_dev::record_failure(rec, idx[t], code[t], value[t]);
+}
+}  // namespace
+
+int pint_debug_fail_inject(pint_ctx* ctx, int64_t K, const int64_t* idx, const int* code, const double* value) {
+    if (!ctx || K < 0) return PINT_E_INVALID;
+    if (K == 0) return PINT_OK;
+    fail_inject_kernel<<<static_cast<unsigned>((K + 255) / 256), 256, 0, ctx->stream>>>(K, idx, code, value,
+                                                                                    ctx->d_fail);
+    return pint_check_launch(ctx, "fail_inject_kernel");
+}
+
 // ---- host tables ---------------------------------------------------------------------------------
 
 int64_t pint_steps_for(double width, double dt) {
