@@ -175,6 +175,23 @@ int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t S, int6
                             int64_t steps, double h, int with_forcing, const double* records,
                             const double* sx, double* y);
 
+/* ---- K3f: heat slice maps, TOLERANCE build (EXTENSION: the same maps as pint_heat_build_dev —
+ * build_affine_propagator, nievergelt.cpp:53-66 — in a different operation order, <= 1e-12 relative
+ * to the exact maps; north_star allows this tolerance for trajectory end states). Each step is a
+ * row-partitioned Thomas solve (linalg.cpp:77-93) with all rows in registers: one FMA per row on
+ * the dependent chain, partition carries by shuffle scans, fix-ups with per-(slice, step) spike
+ * vectors. Supports n <= 768 (pint_heat_fast_records_size returns 0 beyond). ---- */
+enum { PINT_BUILD_EXACT = 0, PINT_BUILD_FAST = 1 };
+int64_t pint_heat_fast_records_size(int64_t n, int64_t N, int64_t S);
+/* per-(slice, step) coefficients from the same device tables as pint_heat_factor_dev; slices with
+ * fewer than S steps are padded with identity steps */
+int pint_heat_fast_factor_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
+                              const double* slice_dt, const double* r, const double* fa,
+                              const double* fb, const double* sx, double* records);
+/* all N augmented maps (layout as pint_heat_build_dev) from pint_heat_fast_factor_dev's records */
+int pint_heat_fast_build_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const double* records,
+                             double* maps);
+
 /* ---- K4: affine composition (compose_sweep, nievergelt.cpp:90-110) ----
  * CHAIN: y <- G_j y + c_j in slice order, rows as sequential dots (bit-exact vs matvec,
  * linalg.cpp:17-26). TREE: log-depth pairwise products on FP64 tensor cores (DMMA), then one
@@ -208,6 +225,11 @@ int pint_run_scalar(pint_ctx* ctx, const pint_scalar_rhs* rhs, double t0, double
 /* Heat: make_heat_problem(dx, dt, T) with y0 = heat_initial, N slices, K3 + K4. */
 int pint_run_heat(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int compose_mode,
                   const double* y0, double* y_out, double* per_slice_seconds, pint_report* report);
+/* pint_run_heat with a choice of build: PINT_BUILD_EXACT (bit-exact, = pint_run_heat) or
+ * PINT_BUILD_FAST (the tolerance build, final state <= 1e-12 relative to the reference's). */
+int pint_run_heat_ex(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int build_mode,
+                     int compose_mode, const double* y0, double* y_out, double* per_slice_seconds,
+                     pint_report* report);
 /* Heat slice maps to host: G row-major N x n x n, c N x n (build_affine_propagator for all). */
 int pint_heat_maps(pint_ctx* ctx, double dx, double dt, const pint_slice* slices, int64_t N,
                    double* G, double* c);

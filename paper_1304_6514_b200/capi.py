@@ -30,6 +30,7 @@ F64, F32 = 0, 1
 WEIGHTS_PRODUCT, WEIGHTS_CLOSED2 = 0, 1
 SWEEP_EXACT, SWEEP_TREE = 0, 1
 COMPOSE_CHAIN, COMPOSE_TREE = 0, 1
+BUILD_EXACT, BUILD_FAST = 0, 1
 NODES_FIRST_KIND, NODES_SECOND_KIND = 0, 1
 
 
@@ -86,6 +87,9 @@ _SIGS = {
     "pint_heat_records_size": (_i, [_i, _i, _i]),
     "pint_heat_factor_dev": (_int, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pint_heat_build_dev": (_int, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _int]),
+    "pint_heat_fast_records_size": (_i, [_i, _i, _i]),
+    "pint_heat_fast_factor_dev": (_int, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pint_heat_fast_build_dev": (_int, [_vp, _i, _i, _i, _vp, _vp]),
     "pint_heat_integrate_dev": (_int, [_vp, _i, _i, _i, _i, _i, _d, _int, _vp, _vp, _vp]),
     "pint_affine_compose_dev": (_int, [_vp, _int, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "pint_affine_pair_dev": (_int, [_vp, _i, _i, _vp, _vp, _vp]),
@@ -94,6 +98,7 @@ _SIGS = {
     "pint_run_scalar": (_int, [_vp, C.POINTER(ScalarRHS), _d, _d, _d, _i, _d, _int, _i, _d, _d, _int, _int,
                                _vp, _vp, _vp, _vp, C.POINTER(Report), C.POINTER(Fail)]),
     "pint_run_heat": (_int, [_vp, _d, _d, _d, _i, _int, _vp, _vp, _vp, C.POINTER(Report)]),
+    "pint_run_heat_ex": (_int, [_vp, _d, _d, _d, _i, _int, _int, _vp, _vp, _vp, C.POINTER(Report)]),
     "pint_heat_maps": (_int, [_vp, _d, _d, C.POINTER(Slice), _i, _vp, _vp]),
     "pint_heat_integrate": (_int, [_vp, _d, C.POINTER(Slice), _d, _int, _i, _vp]),
     "pint_scalar_integrate": (_int, [_vp, C.POINTER(ScalarRHS), C.POINTER(Slice), _i, _vp, _vp, C.POINTER(Fail)]),

@@ -468,6 +468,20 @@ int pint_heat_build_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const in
     return launch_heat_build(ctx, n, N, S, step_off, slice_dt, records, sx, maps, per_slice_ns, guarded);
 }
 
+int64_t pint_heat_fast_records_size(int64_t n, int64_t N, int64_t S) { return heat_fast_records_doubles(n, N, S); }
+
+int pint_heat_fast_factor_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
+                              const double* slice_dt, const double* r, const double* fa, const double* fb,
+                              const double* sx, double* records) {
+    if (!ctx) return PINT_E_INVALID;
+    return launch_heat_fast_factor(ctx, ctx->stream, n, N, S, step_off, slice_dt, r, fa, fb, sx, records);
+}
+
+int pint_heat_fast_build_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const double* records, double* maps) {
+    if (!ctx) return PINT_E_INVALID;
+    return launch_heat_fast_build(ctx, n, N, S, records, maps);
+}
+
 int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t S, int64_t s0,
                             int64_t steps, double h, int with_forcing, const double* records,
                             const double* sx, double* y) {
@@ -730,7 +744,8 @@ int64_t heat_segment_end(int64_t S, int k) {
 using StepsFn = std::function<int(int64_t s0, int64_t s1)>;
 
 int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, HeatDev& H,
-                const StepsFn* on_steps = nullptr) {
+                const StepsFn* on_steps = nullptr, int build_mode = PINT_BUILD_EXACT) {
+    const bool fast = build_mode == PINT_BUILD_FAST;
     int64_t n = 0;
     if (const int rc = heat_dim(ctx, dx, &n)) return rc;
     for (const auto& s : sl)
@@ -755,7 +770,10 @@ int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, Hea
     int64_t S = 0;
     for (const auto& s : sl) S = std::max<int64_t>(S, s.steps);
     char* d = static_cast<char*>(pint_scratch(ctx, 0, in_bytes));
-    double* f = static_cast<double*>(pint_scratch(ctx, 1, sizeof(double) * heat_records_doubles(n, N, S)));
+    if (fast && !heat_fast_supported(n))
+        return pint_set_error(ctx, PINT_E_INVALID, "heat fast build: n > 768 unsupported (use PINT_BUILD_EXACT)");
+    const int64_t rec_doubles = fast ? heat_fast_records_doubles(n, N, S) : heat_records_doubles(n, N, S);
+    double* f = static_cast<double*>(pint_scratch(ctx, 1, sizeof(double) * rec_doubles));
     if (!d || !f) return PINT_E_CUDA;
     H.n = n;
     H.N = N;
@@ -811,10 +829,13 @@ int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, Hea
         if (!h2d(h_r + q0, H.r + q0, sizeof(double) * nq) || !h2d(h_fa + q0, H.fa + q0, sizeof(double) * nq) ||
             !h2d(h_fb + q0, H.fb + q0, sizeof(double) * nq))
             return PINT_E_CUDA;
+        if (fast) continue;  // (one record launch over all slices below)
         if (const int rc = launch_heat_factor_range(ctx, n, N, S, j0, j1 - j0, H.step_off, H.slice_dt, H.r, H.fa,
                                                     H.fb, H.sx, H.factor))
             return rc;
     }
+    if (fast) return launch_heat_fast_factor(ctx, ctx->stream, n, N, S, H.step_off, H.slice_dt, H.r, H.fa, H.fb, H.sx,
+                                             H.factor);
     return PINT_OK;
 }
 
@@ -833,7 +854,14 @@ int singular_check(pint_ctx* ctx) {
 
 int pint_run_heat(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int compose_mode,
                   const double* y0, double* y_out, double* per_slice_seconds, pint_report* report) {
-    if (!ctx || !y_out || N < 1) return PINT_E_INVALID;
+    return pint_run_heat_ex(ctx, dx, dt, T, N, PINT_BUILD_EXACT, compose_mode, y0, y_out, per_slice_seconds, report);
+}
+
+int pint_run_heat_ex(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int build_mode, int compose_mode,
+                     const double* y0, double* y_out, double* per_slice_seconds, pint_report* report) {
+    if (!ctx || !y_out || N < 1 || (build_mode != PINT_BUILD_EXACT && build_mode != PINT_BUILD_FAST))
+        return PINT_E_INVALID;
+    const bool fast = build_mode == PINT_BUILD_FAST;
     HostTimer wall;
     const long long launches0 = ctx->launches;
     std::vector<pint_slice> sl(static_cast<size_t>(N));
@@ -865,14 +893,15 @@ int pint_run_heat(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int 
     }();
     bool uniform = true;
     for (const auto& s : sl) uniform = uniform && s.steps == sl[0].steps;
-    const bool segmented = seg_env && uniform && heat_build_segmentable(n) && sl[0].steps >= 2 * kHeatSegments;
+    const bool segmented =
+        !fast && seg_env && uniform && heat_build_segmentable(n) && sl[0].steps >= 2 * kHeatSegments;
     if (per_slice_seconds) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
     HeatDev H;
     const StepsFn seg_build = [&](int64_t s0, int64_t s1) {
         return launch_heat_build_steps(ctx, n, N, sl[0].steps, H.step_off, H.factor, d_maps,
                                        per_slice_seconds ? d_ns : nullptr, 0, s0, s1);
     };
-    if (const int rc = heat_upload(ctx, dx, sl, H, segmented ? &seg_build : nullptr)) return rc;
+    if (const int rc = heat_upload(ctx, dx, sl, H, segmented ? &seg_build : nullptr, build_mode)) return rc;
     std::vector<double> y0v;
     if (!y0) {
         y0v.resize(static_cast<size_t>(n));
@@ -883,7 +912,10 @@ int pint_run_heat(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int 
     std::vector<unsigned long long> ns;
     int rc = PINT_OK;
     for (int guarded = 0; guarded < 2; ++guarded) {  // second pass only if a range check tripped
-        if (guarded || !segmented) {
+        if (fast) {  // (no range retry: plain FP64 arithmetic throughout)
+            rc = launch_heat_fast_build(ctx, n, N, H.S, H.factor, d_maps);
+            if (rc) return rc;
+        } else if (guarded || !segmented) {
             if (per_slice_seconds && guarded) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
             rc = launch_heat_build(ctx, n, N, H.S, H.step_off, H.slice_dt, H.factor, H.sx, d_maps,
                                    per_slice_seconds ? d_ns : nullptr, guarded);
@@ -904,8 +936,14 @@ int pint_run_heat(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int 
         if (rc != PINT_E_RANGE_RETRY) break;
     }
     if (rc) return rc;
-    if (per_slice_seconds)
+    if (per_slice_seconds && fast) {  // the tolerance build has no per-slice timers: its time split evenly
+        float ms = 0.f, cms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        cudaEventElapsedTime(&cms, ctx->evc, ctx->ev1);
+        for (int64_t j = 0; j < N; ++j) per_slice_seconds[j] = (ms - cms) * 1e-3 / static_cast<double>(N);
+    } else if (per_slice_seconds) {
         for (int64_t j = 0; j < N; ++j) per_slice_seconds[j] = static_cast<double>(ns[j]) * 1e-9;
+    }
     if (report) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);

@@ -93,9 +93,12 @@ class HeatPlan:
     """Device-resident plan for slices [lo, hi) of make_heat_problem(dx, dt, T) cut into N slices."""
 
     def __init__(self, ctx: capi.Context, dx: float, dt: float, T: float, N: int, lo: int = 0,
-                 hi: Optional[int] = None, tables: Optional[HeatTablesHost] = None):
+                 hi: Optional[int] = None, tables: Optional[HeatTablesHost] = None, build: str = "exact"):
         import torch
 
+        if build not in ("exact", "fast"):
+            raise ValueError(f"build must be 'exact' or 'fast', got {build!r}")
+        self.build = build
         self.ctx = ctx
         self.dx, self.dt, self.T, self.N_total = dx, dt, T, N
         hi = N if hi is None else hi
@@ -109,7 +112,10 @@ class HeatPlan:
         dev = torch.device("cuda", ctx.device)
         self.dev = [t.to(dev) for t in self.host.tensors()]
         self.S = max(s.steps for s in self.slices)
-        rec_doubles = int(capi.load().pint_heat_records_size(self.n, self.N, self.S))
+        size = capi.load().pint_heat_fast_records_size if build == "fast" else capi.load().pint_heat_records_size
+        rec_doubles = int(size(self.n, self.N, self.S))
+        if rec_doubles <= 0:
+            raise ValueError(f"the {build} build does not support n = {self.n}")
         self.factor = torch.empty(rec_doubles, dtype=torch.float64, device=dev)
         stride = self.n * self.ldm
         self.maps = torch.zeros(self.N * stride, dtype=torch.float64, device=dev)
@@ -132,6 +138,11 @@ class HeatPlan:
     def factor_and_build(self):
         c, P = self.ctx, capi.ptr
         step_off, slice_dt, r, fa, fb, sx = self.dev
+        if self.build == "fast":
+            c.call("pint_heat_fast_factor_dev", self.n, self.N, self.S, P(step_off), P(slice_dt), P(r), P(fa), P(fb),
+                   P(sx), P(self.factor))
+            c.call("pint_heat_fast_build_dev", self.n, self.N, self.S, P(self.factor), P(self.maps))
+            return
         c.call("pint_heat_factor_dev", self.n, self.N, self.S, P(step_off), P(slice_dt), P(r), P(fa), P(fb), P(sx),
                P(self.factor))
         c.call("pint_heat_build_dev", self.n, self.N, self.S, P(step_off), P(slice_dt), P(self.factor), P(sx),

@@ -1,0 +1,132 @@
+"""GPU parity of the TOLERANCE heat build (heat_fast.cu, PINT_BUILD_FAST) against the reference.
+
+The fast build computes the same slice maps as build_affine_propagator (nievergelt.cpp:53-66) in a
+different operation order, so it is held to the north_star tolerance, written here:
+  * maps: max |G_fast - G_ref| <= 1e-12 max |G_ref| (and the same for c) against the C oracle
+    (oracle/pint_oracle.c, pinned bit-exactly to the reference), for every partition shape;
+  * final states against the unmodified reference's run_nievergelt final state at the full bench
+    configurations (tests/golden/heat_finals.npz): <= 1e-12 relative (max-norm) at C2. At C4 the
+    reference's OWN FP64 rounding puts it 2.6e-12 from the long-double solve stored beside it
+    (heat_truth.c), so no differently-ordered FP64 computation can be held to 1e-12 of it there;
+    the test holds the fast build to the reference's own accuracy instead: its distance to the
+    long-double answer is <= 1.5x the reference's + 1e-12, and its gap to the reference <= 5e-12.
+"""
+import ctypes as C
+import pathlib
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1304_6514_b200 import capi, pint
+from paper_1304_6514_b200.dist import HeatPlan, HeatTablesHost
+
+pytestmark = pytest.mark.gpu
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+MAP_TOL = 1e-12
+REL_F64 = 1e-12
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return pint.context()
+
+
+def fast_maps(ctx, dx, dt, T, N):
+    plan = HeatPlan(ctx, dx, dt, T, N, build="fast")
+    plan.factor_and_build()
+    ctx.sync()
+    assert ctx.fail().index < 0
+    m = plan.maps.view(plan.N, plan.n, plan.ldm).cpu().numpy()
+    return plan, m[:, :, : plan.n], m[:, :, plan.n]
+
+
+def close(a, ref, tol):
+    scale = max(np.max(np.abs(ref)), 1e-300)
+    return np.max(np.abs(a - ref)) <= tol * scale
+
+
+# every partition shape (P, R): n <= 32 -> (1, 32); 64 -> (2, 32); 97 -> (4, 32) ... 512 -> (16, 32);
+# 700 -> (16, 48); with padded rows (n not a multiple of P R) and CTAs spanning several slices
+@pytest.mark.parametrize("n,N,S", [(9, 4, 5), (31, 3, 4), (40, 3, 4), (64, 2, 3), (97, 3, 3), (128, 5, 4),
+                                   (150, 2, 3), (200, 3, 2), (255, 2, 3), (300, 2, 3), (384, 2, 2), (512, 3, 4),
+                                   (700, 2, 2)])
+def test_fast_maps_vs_oracle(ctx, n, N, S):
+    dx, dt = 1.0 / (n + 1), 1e-3
+    T = N * S * dt
+    plan, G, c = fast_maps(ctx, dx, dt, T, N)
+    for j, s in enumerate(plan.slices):
+        Gw, cw = O.heat_build(dx, s.t_begin, s.t_end, dt)
+        assert close(G[j], Gw, MAP_TOL), (n, j, np.max(np.abs(G[j] - Gw)))
+        assert close(c[j], cw, MAP_TOL), (n, j, np.max(np.abs(c[j] - cw)))
+
+
+def test_fast_maps_heat9_golden(ctx, golden):
+    """The reference's own heat9 slice maps (test_nievergelt.cpp:76-90 problem) within tolerance."""
+    _, G, c = fast_maps(ctx, 0.1, 0.005, 10.0, 4)
+    for j in range(4):
+        assert close(G[j], golden["heat9_G"][j], MAP_TOL)
+        assert close(c[j], golden["heat9_c"][j], MAP_TOL)
+
+
+def test_fast_uneven_slices_identity_padding(ctx):
+    """Slices with different step counts: the shorter ones are padded with identity steps."""
+    import torch
+
+    n, dx = 128, 1.0 / 129
+    slices = [capi.Slice(0.0, 0.01, 2, 0.005), capi.Slice(0.01, 0.04, 6, 0.005), capi.Slice(0.04, 0.045, 1, 0.005)]
+    host = HeatTablesHost(dx, slices)
+    dev = [t.cuda() for t in host.tensors()]
+    N, S = len(slices), 6
+    ldm = int(capi.load().pint_affine_ldm(n))
+    rec = torch.empty(int(capi.load().pint_heat_fast_records_size(n, N, S)), dtype=torch.float64, device="cuda")
+    maps = torch.zeros(N * n * ldm, dtype=torch.float64, device="cuda")
+    P = capi.ptr
+    ctx.call("pint_heat_fast_factor_dev", n, N, S, *[P(t) for t in dev], P(rec))
+    ctx.call("pint_heat_fast_build_dev", n, N, S, P(rec), P(maps))
+    ctx.sync()
+    m = maps.view(N, n, ldm).cpu().numpy()
+    for j, s in enumerate(slices):
+        Gw, cw = O.heat_build(dx, s.t_begin, s.t_end, s.dt)
+        assert close(m[j, :, :n], Gw, MAP_TOL) and close(m[j, :, n], cw, MAP_TOL), j
+
+
+def test_fast_records_size_bounds():
+    lib = capi.load()
+    assert lib.pint_heat_fast_records_size(768, 4, 4) > 0
+    assert lib.pint_heat_fast_records_size(769, 4, 4) == 0  # -> PINT_BUILD_EXACT only
+
+
+@pytest.mark.parametrize("key", ["c2", "c4"])
+def test_fast_run_final_vs_reference(ctx, key):
+    """pint_run_heat_ex(PINT_BUILD_FAST) at the full bench configurations against the unmodified
+    reference's run_nievergelt final state and the long-double answer (see the module docstring)."""
+    z = np.load(ROOT / "tests" / "golden" / "heat_finals.npz")
+    n, N, S = (int(v) for v in z[f"{key}_config"])
+    ref, truth = z[f"{key}_final"], z[f"{key}_truth"]
+    scale = np.max(np.abs(truth))
+    ref_err = np.max(np.abs(ref - truth)) / scale
+    dx, dt = 1.0 / (n + 1), 10.0 / (N * S)
+    for mode in (capi.COMPOSE_CHAIN, capi.COMPOSE_TREE):
+        y = np.empty(n)
+        rep = capi.Report()
+        ctx.check(ctx.lib.pint_run_heat_ex(ctx.h, dx, dt, 10.0, N, capi.BUILD_FAST, mode, None, capi.ptr(y), None,
+                                           C.byref(rep)))
+        gap = np.max(np.abs(y - ref)) / np.max(np.abs(ref))
+        err = np.max(np.abs(y - truth)) / scale
+        if key == "c2":
+            assert gap <= REL_F64, (key, mode, gap)
+        else:
+            assert gap <= 5e-12 and err <= 1.5 * ref_err + 1e-12, (key, mode, gap, err, ref_err)
+        assert rep.traj_steps == N * S * (n + 1)
+
+
+def test_fast_unsupported_n_raises(ctx):
+    y = np.empty(1023)
+    rc = ctx.lib.pint_run_heat_ex(ctx.h, 1.0 / 1024, 1e-3, 4e-3, 2, capi.BUILD_FAST, capi.COMPOSE_CHAIN, None,
+                                  capi.ptr(y), None, None)
+    assert rc == capi.PINT_E_INVALID
