@@ -51,18 +51,18 @@ WORKLOADS = {
 }
 
 
-def chain_floor(n: int, slices: int, S: int, lat, build_ms: float, sm_mhz: float) -> dict:
+def chain_floor(n: int, slices: int, S: int, lat, build_ms: float, sm_mhz: float, sms: int = 148) -> dict:
     """The exact build's real bound: every column is a chain of S*n dependent rows (forward + back
-    row latencies measured live by pint_probe_latency), run in `waves` rounds of resident columns."""
+    row latencies measured live by pint_probe_latency), run in `waves` rounds of resident columns
+    on the `sms` SMs the build has (148, or 132 beside the concurrent 16-CTA chain)."""
     row = float(lat[5] + lat[6])
-    sms = 148
     if 282 <= n <= 520:  # heat_build_tmem_kernel: one 5-warp CTA per SM per slice quarter
         waves = -(-slices * -(-(-(-n // 32)) // 4) // sms)
     else:  # one-warp CTAs; at C2 every warp is resident at once
         waves = 1
     floor_ms = waves * S * n * row / (sm_mhz * 1e3)
     return {"chain_floor_ms": floor_ms, "frac_of_chain_floor": floor_ms / build_ms, "chain_row_cycles": row,
-            "chain_waves": waves}
+            "chain_waves": waves, "build_sms": sms}
 
 
 def workload_name(args) -> str:
@@ -544,6 +544,11 @@ def heat_bench(args, rank, world, local):
     lat = np.zeros(8)
     ctx.check(ctx.lib.pint_probe_latency(ctx.h, capi.ptr(lat)))  # [5] forward row, [6] back row
 
+    # n in [282, 520] (the TMEM build, C4): at N = 1 the bit-exact chain runs CONCURRENTLY with the
+    # build (pint_heat_build_chain_dev: it consumes each map once its builder CTAs have stored it)
+    overlap = world == 1 and 282 <= n <= 520
+    phase = [C.c_double(), C.c_double()]
+
     def one_step(events=None):
         if events:
             events[0].record(stream)
@@ -553,6 +558,13 @@ def heat_bench(args, rank, world, local):
                  P(plan.factor))
         if events:
             events[1].record(stream)
+        if overlap:
+            ctx.call("pint_heat_build_chain_dev", plan.n, plan.N, plan.S, P(step_off), P(slice_dt), P(plan.factor),
+                     P(sx), P(plan.maps), P(plan.y0), P(plan.y), plan.guarded)
+            if events:
+                events[2].record(stream)
+                events[3].record(stream)
+            return
         ctx.call("pint_heat_build_dev", plan.n, plan.N, plan.S, P(step_off), P(slice_dt), P(plan.factor), P(sx),
                  P(plan.maps), None, plan.guarded)
         if events:
@@ -594,8 +606,13 @@ def heat_bench(args, rank, world, local):
         ev[3].synchronize()
         tot["step"] += ev[0].elapsed_time(ev[3])
         tot["factor"] += ev[0].elapsed_time(ev[1])
-        tot["build"] += ev[1].elapsed_time(ev[2])
-        tot["compose"] += ev[2].elapsed_time(ev[3])
+        if overlap:  # the build kernel's own events (main stream) and the chain's exposed tail (side stream)
+            ctx.check(ctx.lib.pint_ctx_build_chain_ms(ctx.h, C.byref(phase[0]), C.byref(phase[1])))
+            tot["build"] += phase[0].value
+            tot["compose"] += phase[1].value
+        else:
+            tot["build"] += ev[1].elapsed_time(ev[2])
+            tot["compose"] += ev[2].elapsed_time(ev[3])
     torch.cuda.synchronize()
     launches = ctx.launches() - launches0  # our kernels only (the flush is torch's)
     if world > 1:
@@ -691,7 +708,8 @@ def heat_bench(args, rank, world, local):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(args), "n": n, "slices": N, "slices_per_gpu": hi - lo,
                        "steps_per_slice": S, "T": T, "dt": dt, "build": "exact",
-                       "compose": ("chain (bit-exact)" if n > 256 else "tree (DMMA) levels + chain tail") if world == 1
+                       "compose": ("chain (bit-exact), concurrent with the build" if overlap else "chain (bit-exact)"
+                                   if n > 256 else "tree (DMMA) levels + chain tail") if world == 1
                        else "block tree (DMMA) + NCCL gather + root chain",
                        "parallelism": f"slice blocks x{world}",
                        "l2": "flushed (256 MB write) between steps; maps alone exceed L2",
@@ -704,8 +722,13 @@ def heat_bench(args, rank, world, local):
                          "traffic": traffic, "peak_source": "measured DFMA probe (pint_probe_peak)",
                          "flops_per_launch": build_flops, "launch_ms": build_ms,
                          "share_of_step": build_ms / ms_per_step,
-                         "factor_ms": tot["factor"] / args.steps, "compose_ms": tot["compose"] / args.steps,
-                         **chain_floor(n, hi - lo, S, lat, build_ms, csum.get("sm_mhz") or 1965.0)},
+                         "factor_ms": tot["factor"] / args.steps,
+                         ("compose_tail_ms" if overlap else "compose_ms"): tot["compose"] / args.steps,
+                         "launch_ms_source": ("build kernel span on the device (first CTA start to last CTA end, "
+                                              "%globaltimer), the chain running beside it") if overlap
+                                             else "CUDA events around the launch on its stream",
+                         **chain_floor(n, hi - lo, S, lat, build_ms, csum.get("sm_mhz") or 1965.0,
+                                       148 - 16 if overlap else 148)},
             "clocks": csum,
             "cpu_baseline": cpu,
         }

@@ -200,6 +200,17 @@ int pint_heat_fast_build_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, con
  * composed augmented map (TREE only). y0, y: device n-vectors. */
 int pint_affine_compose_dev(pint_ctx* ctx, int mode, int64_t n, int64_t N, double* maps,
                             double* scratch, const double* y0, double* y, double* composed);
+/* K3 + K4 fused in time: all N maps (pint_heat_build_dev's exact build, guarded as there) and the
+ * bit-exact CHAIN to y. For n in [282, 520] the chain runs concurrently with the build on the
+ * context's side stream, fetching each map as soon as all its builder CTAs have stored it;
+ * otherwise build then chain. Replaces the build + compose_sweep pair of run_nievergelt
+ * (nievergelt.cpp:237-246). y0, y: device n-vectors; result bit-identical to build + CHAIN. */
+int pint_heat_build_chain_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
+                              const double* slice_dt, const double* records, const double* sx,
+                              double* maps, const double* y0, double* y, int guarded);
+/* after an overlapped pint_heat_build_chain_dev: the build kernel's span on the device (first CTA
+ * start to last CTA end, %globaltimer) and the chain's exposed tail past it; syncs the stream */
+int pint_ctx_build_chain_ms(pint_ctx* ctx, double* build_ms, double* tail_ms);
 /* Compose two augmented maps: out = later ∘ earlier (EXTENSION, the tree's pair step). */
 int pint_affine_pair_dev(pint_ctx* ctx, int64_t n, int64_t P, const double* earlier,
                          const double* later, double* out);

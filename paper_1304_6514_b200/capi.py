@@ -91,6 +91,8 @@ _SIGS = {
     "pint_heat_fast_factor_dev": (_int, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pint_heat_fast_build_dev": (_int, [_vp, _i, _i, _i, _vp, _vp]),
     "pint_heat_integrate_dev": (_int, [_vp, _i, _i, _i, _i, _i, _d, _int, _vp, _vp, _vp]),
+    "pint_heat_build_chain_dev": (_int, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _int]),
+    "pint_ctx_build_chain_ms": (_int, [_vp, C.POINTER(_d), C.POINTER(_d)]),
     "pint_affine_compose_dev": (_int, [_vp, _int, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "pint_affine_pair_dev": (_int, [_vp, _i, _i, _vp, _vp, _vp]),
     "pint_lv_ensemble_dev": (_int, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),

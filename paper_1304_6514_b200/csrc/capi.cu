@@ -198,6 +198,17 @@ int pint_check_launch(pint_ctx* ctx, const char* what) {
     return PINT_OK;
 }
 
+void pint_kernel_attrs(const void* fn) {
+    static std::mutex m;
+    static std::vector<const void*> done;
+    std::lock_guard<std::mutex> lk(m);
+    if (std::find(done.begin(), done.end(), fn) != done.end()) return;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    done.push_back(fn);
+}
+
 void* pint_scratch(pint_ctx* ctx, int slot, size_t bytes) {
     if (ctx->scratch_bytes[slot] < bytes) {
         if (ctx->scratch[slot]) cudaFree(ctx->scratch[slot]);
@@ -252,7 +263,7 @@ void pint_ctx_destroy(pint_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    for (int i = 0; i < 5; ++i)
+    for (int i = 0; i < pint_ctx::kSlots; ++i)
         if (ctx->scratch[i]) cudaFree(ctx->scratch[i]);
     if (ctx->d_fail) cudaFree(ctx->d_fail);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -487,6 +498,31 @@ int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t S, int6
                             const double* sx, double* y) {
     if (!ctx) return PINT_E_INVALID;
     return launch_heat_integrate(ctx, n, K, S, s0, steps, h, with_forcing, records, sx, y);
+}
+
+int pint_ctx_build_chain_ms(pint_ctx* ctx, double* build_ms, double* tail_ms) {
+    if (!ctx) return PINT_E_INVALID;
+    if (!ctx->span_words) return pint_set_error(ctx, PINT_E_INVALID, "no overlapped build + chain ran on this context");
+    unsigned long long w[3];
+    if (!ok(ctx, cudaMemcpyAsync(w, ctx->span_words, sizeof w, cudaMemcpyDeviceToHost, ctx->stream), "span D2H") ||
+        !ok(ctx, cudaStreamSynchronize(ctx->stream), "span sync"))
+        return PINT_E_CUDA;
+    if (build_ms) *build_ms = static_cast<double>(w[1] - w[0]) * 1e-6;
+    if (tail_ms) *tail_ms = w[2] > w[1] ? static_cast<double>(w[2] - w[1]) * 1e-6 : 0.0;
+    return PINT_OK;
+}
+
+namespace {
+int heat_build_chain(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
+                     const double* slice_dt, const double* records, const double* sx, double* maps,
+                     const double* y0, double* y, unsigned long long* per_slice_ns, int guarded);
+}  // namespace
+
+int pint_heat_build_chain_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
+                              const double* slice_dt, const double* records, const double* sx, double* maps,
+                              const double* y0, double* y, int guarded) {
+    if (!ctx) return PINT_E_INVALID;
+    return heat_build_chain(ctx, n, N, S, step_off, slice_dt, records, sx, maps, y0, y, nullptr, guarded);
 }
 
 int pint_affine_compose_dev(pint_ctx* ctx, int mode, int64_t n, int64_t N, double* maps,
@@ -839,6 +875,41 @@ int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, Hea
     return PINT_OK;
 }
 
+// All N maps and the bit-exact chain to y. Where the build signals per-slice completion (the
+// TMEM build, n in [282, 520]) the chain runs CONCURRENTLY: the 16-CTA cluster chain holds 16 SMs
+// and fetches map j once ready[j] counts all of slice j's builder CTAs, while the build fills the
+// other SMs. The chain is launched first and the build right behind it on the same stream with
+// programmatic stream serialization: build CTAs are dispatched only once every chain CTA is
+// resident (the chain triggers at its start), so the cluster never queues behind the build grid;
+// nothing may sit between the two launches (an event record would make the build wait for the
+// chain). The build never waits on the chain (deadlock-free; the chain's waits are bounded and
+// fail loudly). Kernel attributes are set before the launches: cudaFuncSetAttribute waits for a
+// running kernel, here for the chain that waits for the build.
+int heat_build_chain(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
+                     const double* slice_dt, const double* records, const double* sx, double* maps,
+                     const double* y0, double* y, unsigned long long* per_slice_ns, int guarded) {
+    const int target = heat_build_ready_target(n);
+    // ready[N] counters, then {build start, build end, chain end} globaltimer words
+    const size_t ready_bytes = sizeof(int) * static_cast<size_t>((N + 1) & ~1ll);
+    int* ready = target ? static_cast<int*>(pint_scratch(ctx, 5, ready_bytes + 32)) : nullptr;
+    if (!target || !ready || n > 512) {
+        if (const int rc = launch_heat_build(ctx, n, N, S, step_off, slice_dt, records, sx, maps, per_slice_ns, guarded))
+            return rc;
+        cudaEventRecord(ctx->evc, ctx->stream);
+        return launch_affine_chain(ctx, n, N, maps, y0, y);
+    }
+    heat_build_prepare(n);
+    cudaMemsetAsync(ready, 0, ready_bytes, ctx->stream);
+    cudaMemsetAsync(reinterpret_cast<char*>(ready) + ready_bytes, 0xff, 8, ctx->stream);  // (min start)
+    cudaMemsetAsync(reinterpret_cast<char*>(ready) + ready_bytes + 8, 0, 16, ctx->stream);
+    ctx->span_words = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ready) + ready_bytes);
+    if (const int rc = launch_affine_chain_on(ctx, ctx->stream, n, N, maps, y0, y, ready, target)) return rc;
+    if (const int rc = launch_heat_build_steps(ctx, n, N, S, step_off, records, maps, per_slice_ns, guarded, 0, S, ready))
+        return rc;
+    cudaEventRecord(ctx->evc, ctx->stream);
+    return PINT_OK;
+}
+
 int singular_check(pint_ctx* ctx) {
     pint_fail fr;
     if (const int rc = pint_fail_read(ctx, &fr)) return rc;
@@ -912,7 +983,14 @@ int pint_run_heat_ex(pint_ctx* ctx, double dx, double dt, double T, int64_t N, i
     std::vector<unsigned long long> ns;
     int rc = PINT_OK;
     for (int guarded = 0; guarded < 2; ++guarded) {  // second pass only if a range check tripped
-        if (fast) {  // (no range retry: plain FP64 arithmetic throughout)
+        const bool overlap = !fast && !segmented && heat_build_ready_target(n) > 0 &&
+                             (compose_mode == PINT_COMPOSE_CHAIN || n > 256);  // (only-y TREE at n > 256 IS the chain)
+        if (overlap) {
+            if (per_slice_seconds && guarded) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
+            rc = heat_build_chain(ctx, n, N, H.S, H.step_off, H.slice_dt, H.factor, H.sx, d_maps, d_y0, d_y,
+                                  per_slice_seconds ? d_ns : nullptr, guarded);
+            if (rc) return rc;
+        } else if (fast) {  // (no range retry: plain FP64 arithmetic throughout)
             rc = launch_heat_fast_build(ctx, n, N, H.S, H.factor, d_maps);
             if (rc) return rc;
         } else if (guarded || !segmented) {
@@ -921,10 +999,12 @@ int pint_run_heat_ex(pint_ctx* ctx, double dx, double dt, double T, int64_t N, i
                                    per_slice_seconds ? d_ns : nullptr, guarded);
             if (rc) return rc;
         }
-        cudaEventRecord(ctx->evc, ctx->stream);
-        if (compose_mode == PINT_COMPOSE_TREE) rc = launch_affine_tree(ctx, n, N, d_maps, d_scr, d_y0, d_y, nullptr);
-        else rc = launch_affine_chain(ctx, n, N, d_maps, d_y0, d_y);
-        if (rc) return rc;
+        if (!overlap) {
+            cudaEventRecord(ctx->evc, ctx->stream);
+            if (compose_mode == PINT_COMPOSE_TREE) rc = launch_affine_tree(ctx, n, N, d_maps, d_scr, d_y0, d_y, nullptr);
+            else rc = launch_affine_chain(ctx, n, N, d_maps, d_y0, d_y);
+            if (rc) return rc;
+        }
         cudaEventRecord(ctx->ev1, ctx->stream);
         cudaMemcpyAsync(y_out, d_y, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream);
         if (per_slice_seconds) {

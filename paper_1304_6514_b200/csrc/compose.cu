@@ -82,8 +82,12 @@ constexpr int kRing = 4;        // maps in flight (bulk-copy latency ~ 2 map app
 __global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long long N, int ldm, int ring,
                                                                   const double* __restrict__ maps,
                                                                   const double* __restrict__ y0,
-                                                                  double* __restrict__ y) {
+                                                                  double* __restrict__ y, const int* ready,
+                                                                  int target, FailRec* fail) {
     extern __shared__ __align__(16) double sm[];
+    // waiting on builders launched behind this grid on the same stream (programmatic dependent
+    // launch): let them start now that this CTA is resident
+    if (ready) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     cg::cluster_group cluster = cg::this_cluster();
     const unsigned rank = cluster.block_rank();
     const unsigned csize = cluster.num_blocks();
@@ -102,7 +106,25 @@ __global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long lo
     }
     __syncwarp();
     const bool mine = lane < rows;
+    bool gave_up = false;
+    // (ready: maps arrive while this kernel runs — wait until map j's builders have all stored it,
+    // then order that acquire before the bulk copy's async-proxy read)
     auto fetch = [&](long long j, int b) {  // this CTA's rows of map j (contiguous) into block b
+        if (lane == 0 && ready && !gave_up) {
+            int v;
+            const unsigned long long t0 = pint_dev::globaltimer();
+            do {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(ready + j) : "memory");
+                // never hang: a map not ready 1 s after the wait began means its builder is not
+                // running; fail loudly (the result is not used) and stop waiting for the rest
+                if (v < target && pint_dev::globaltimer() - t0 > 1000000000ull) {
+                    pint_dev::record_failure(fail, j, PINT_E_CUDA, static_cast<double>(v));
+                    gave_up = true;
+                    break;
+                }
+            } while (v < target);
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        }
         if (lane == 0)
             bulk_load(smem_u32(blk + b * 32 * ldm), maps + j * mstride + static_cast<long long>(r0) * ldm, blk_bytes,
                       bar0 + 8u * b);
@@ -129,7 +151,7 @@ __global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long lo
         mbar_wait(bar0 + 8u * b, static_cast<unsigned>((j / ring) & 1));
         // the block after the ring's next into L2 now, so its bulk copy (issued once this block is
         // consumed) reads L2 rather than HBM — with a 1-deep ring (n > ~220) that copy is exposed
-        if (lane == 0 && j + ring < N)
+        if (lane == 0 && j + ring < N && (!ready || *reinterpret_cast<const volatile int*>(ready + j + ring) >= target))
             prefetch_l2(maps + (j + ring) * mstride + static_cast<long long>(r0) * ldm, blk_bytes);
         CHAIN_MARK(tw);
         const double2* g2 = reinterpret_cast<const double2*>(blk + (b * 32 + lane) * ldm);
@@ -190,6 +212,8 @@ __global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long lo
                tf / N, ts / N);
 #endif
     if (mine) y[r0 + lane] = ys[(N & 1) * ny + r0 + lane];
+    if (ready && rank == 0 && lane == 0)  // (the span words behind the counters: chain end)
+        reinterpret_cast<unsigned long long*>(const_cast<int*>(ready) + ((N + 1) & ~1ll))[2] = pint_dev::globaltimer();
     cluster.sync();  // no CTA leaves while a peer may still write into its shared memory
 }
 
@@ -365,6 +389,11 @@ int launch_pairs(pint_ctx* ctx, long long n, long long P, const double* earlier,
 
 int launch_affine_chain(pint_ctx* ctx, int64_t n, int64_t N, const double* maps, const double* y0,
                         double* y) {
+    return launch_affine_chain_on(ctx, ctx->stream, n, N, maps, y0, y, nullptr, 0);
+}
+
+int launch_affine_chain_on(pint_ctx* ctx, cudaStream_t stream, int64_t n, int64_t N, const double* maps,
+                           const double* y0, double* y, const int* ready, int target) {
     if (n < 1 || N < 0) return pint_set_error(ctx, PINT_E_INVALID, "affine_chain: bad sizes");
     if (n <= 32 * kClusterMax && N > 0) {
         const int ldm = static_cast<int>(pint_affine_ldm(n));
@@ -373,15 +402,13 @@ int launch_affine_chain(pint_ctx* ctx, int64_t n, int64_t N, const double* maps,
         const size_t rest = sizeof(double) * (2 * ny + 4 * kChainAhead) + 8 * (kRing + 2);
         const int ring = static_cast<int>(std::min<size_t>(kRing, (227 * 1024 - rest) / blk));
         const size_t smem = ring * blk + rest;
-        cudaFuncSetAttribute(affine_chain_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+        pint_kernel_attrs(reinterpret_cast<const void*>(affine_chain_cluster_kernel));
         const unsigned C = static_cast<unsigned>((n + 31) / 32);
-        if (C > 8) cudaFuncSetAttribute(affine_chain_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(C, 1, 1);
         cfg.blockDim = dim3(32, 1, 1);
         cfg.dynamicSmemBytes = smem;
-        cfg.stream = ctx->stream;
+        cfg.stream = stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = C;
@@ -390,13 +417,14 @@ int launch_affine_chain(pint_ctx* ctx, int64_t n, int64_t N, const double* maps,
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         if (cudaLaunchKernelEx(&cfg, affine_chain_cluster_kernel, static_cast<int>(n), static_cast<long long>(N), ldm,
-                               ring, maps, y0, y) != cudaSuccess)
+                               ring, maps, y0, y, ready, target, ctx->d_fail) != cudaSuccess)
             return pint_check_launch(ctx, "affine_chain_cluster_kernel");
         return pint_check_launch(ctx, "affine_chain_cluster_kernel");
     }
     if (n > 4 * kChainThreads) return pint_set_error(ctx, PINT_E_INVALID, "affine_chain: n > 1024 unsupported");
+    if (ready) return pint_set_error(ctx, PINT_E_INVALID, "affine_chain: waiting on builders needs n <= 512");
     const size_t smem = sizeof(double) * static_cast<size_t>(n);
-    affine_chain_kernel<<<1, kChainThreads, smem, ctx->stream>>>(n, N, pint_affine_ldm(n), maps, y0, y);
+    affine_chain_kernel<<<1, kChainThreads, smem, stream>>>(n, N, pint_affine_ldm(n), maps, y0, y);
     return pint_check_launch(ctx, "affine_chain_kernel");
 }
 

@@ -299,6 +299,8 @@ struct alignas(64) BuildPlan {
     unsigned long long* per_slice_ns;
     FailRec* fail;
     long long s_begin, s_end;  // the steps this launch runs; s_begin > 0: resume from `maps`
+    int* ready;                // (TMEM build) per-slice count of CTAs whose part of the map is stored
+    unsigned long long* span;  // (with ready) {first CTA start, last CTA end} globaltimer of the launch
 };
 
 
@@ -882,6 +884,14 @@ __global__ void __launch_bounds__(160, 1) heat_build_tmem_kernel(const __grid_co
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(*tslot) : "memory");
+    // this CTA's columns of the map are stored: count it (a chain consuming maps as they complete
+    // waits for cps counts, launch_heat_build_chain)
+    if (P.ready && threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(P.ready + slice, 1);
+        atomicMin(P.span, t_start);
+        atomicMax(P.span + 1, pint_dev::globaltimer());
+    }
 }
 
 // ---- integrate: K caller columns of one slice (records with N = 1), guarded division ----------
@@ -934,9 +944,8 @@ __global__ void __launch_bounds__(32) heat_integrate_kernel(IntegratePlan P) {
 }
 
 template <class K>
-void smem_attrs(K kern, size_t smem) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+void smem_attrs(K kern, size_t) {
+    pint_kernel_attrs(reinterpret_cast<const void*>(kern));
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -1063,9 +1072,18 @@ int launch_heat_build(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int6
 
 bool heat_build_segmentable(int64_t n) { return n >= 1 && !use_tmem(n); }
 
+void heat_build_prepare(int64_t n) {
+    if (use_tmem(n)) {
+        smem_attrs(heat_build_tmem_kernel<false>, 0);
+        smem_attrs(heat_build_tmem_kernel<true>, 0);
+    }
+}
+
+int heat_build_ready_target(int64_t n) { return use_tmem(n) ? static_cast<int>(((n + 31) / 32 + 3) / 4) : 0; }
+
 int launch_heat_build_steps(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
                             const double* records, double* maps, unsigned long long* per_slice_ns, int guarded,
-                            int64_t s_begin, int64_t s_end) {
+                            int64_t s_begin, int64_t s_end, int* ready) {
     if (n < 1 || N < 0 || s_begin < 0 || s_end < s_begin)
         return pint_set_error(ctx, PINT_E_INVALID, "heat_build: bad sizes");
     if (N == 0 || s_end == s_begin) return PINT_OK;
@@ -1085,12 +1103,30 @@ int launch_heat_build_steps(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, cons
     P.ldm = pint_affine_ldm(n);
     P.per_slice_ns = per_slice_ns;
     P.fail = ctx->d_fail;
+    P.ready = ready;
+    P.span = ready ? reinterpret_cast<unsigned long long*>(ready + ((N + 1) & ~1ll)) : nullptr;
     if (use_tmem(n)) {
         const size_t smem = sizeof(double) * tm_smem_doubles(n);
         auto kern = guarded ? heat_build_tmem_kernel<true> : heat_build_tmem_kernel<false>;
         smem_attrs(kern, smem);
         const long long ctas = N * ((P.wps + 3) / 4);
-        kern<<<static_cast<unsigned>(ctas), 160, smem, ctx->stream>>>(P);
+        if (!ready) {
+            kern<<<static_cast<unsigned>(ctas), 160, smem, ctx->stream>>>(P);
+            return pint_check_launch(ctx, "heat_build_tmem_kernel");
+        }
+        // signalling build: launched behind the waiting chain on the same stream, allowed to start
+        // while it runs (programmatic stream serialization; the chain triggers at its start)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(ctas), 1, 1);
+        cfg.blockDim = dim3(160, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, P);
         return pint_check_launch(ctx, "heat_build_tmem_kernel");
     }
     static_assert(reg_rows(kRegRows + 2) == kRegRows, "reg_rows");
