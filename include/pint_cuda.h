@@ -169,11 +169,14 @@ int pint_heat_factor_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const i
 int pint_heat_build_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
                         const double* slice_dt, const double* records, const double* sx,
                         double* maps, unsigned long long* per_slice_ns, int guarded);
-/* Integrate K state vectors y[k*n ...] in place through steps [s0, s0+steps) of ONE slice's
- * records (built with N = 1, S steps): the integrate closure, or run_serial over the interval. */
-int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t S, int64_t s0,
-                            int64_t steps, double h, int with_forcing, const double* records,
-                            const double* sx, double* y);
+/* Integrate K state vectors y[k*n ...] in place through the `steps` steps of ONE slice whose device
+ * tables (pint_heat_coefficients with N = 1: step_off[2], slice_dt[1], r/fa/fb[steps], sx[n]) are
+ * given: the integrate closure (pde_problems.cpp:86-98) or run_serial (nievergelt.cpp:126-143),
+ * bit-exact. Records are built in bounded chunks internally (O(chunk), not O(steps), scratch).
+ * guarded as pint_heat_build_dev (read the failure record; re-run with guarded = 1 on RANGE_RETRY). */
+int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t steps, const int64_t* step_off,
+                            const double* slice_dt, const double* r, const double* fa,
+                            const double* fb, const double* sx, int with_forcing, double* y, int guarded);
 
 /* ---- K3f: heat slice maps, TOLERANCE build (EXTENSION: the same maps as pint_heat_build_dev —
  * build_affine_propagator, nievergelt.cpp:53-66 — in a different operation order, <= 1e-12 relative
@@ -247,6 +250,12 @@ int pint_heat_maps(pint_ctx* ctx, double dx, double dt, const pint_slice* slices
 /* Heat integrate closure on host vectors: K states y[k*n..] over one slice, in place. */
 int pint_heat_integrate(pint_ctx* ctx, double dx, const pint_slice* slice, double dt_nominal,
                         int with_forcing, int64_t K, double* y);
+/* run_serial(make_heat_problem(dx, dt, T)) in the BACKGROUND on the context's own serial stream
+ * (nievergelt.cpp:126-143, bit-exact): begin enqueues it and returns; end waits and writes the final
+ * state. Concurrent device work on the context (e.g. pint_run_heat) proceeds meanwhile — how the
+ * drop-in's run_nievergelt overlaps the serial reference run with the parallel one. */
+int pint_heat_serial_begin(pint_ctx* ctx, double dx, double dt, double T, const double* y0);
+int pint_heat_serial_end(pint_ctx* ctx, double* y_out);
 /* Scalar integrate (integrate_scalar, nievergelt.cpp:29-35) for K initial values on one slice. */
 int pint_scalar_integrate(pint_ctx* ctx, const pint_scalar_rhs* rhs, const pint_slice* slice,
                           int64_t K, const double* y0, double* y_out, pint_fail* fail);

@@ -248,13 +248,16 @@ int pint_ctx_create(int device, pint_ctx** out) {
         cudaEventCreate(&ctx->evc) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->serial, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc(&ctx->d_fail_serial, sizeof(FailRec)) != cudaSuccess) {
         delete ctx;
         return PINT_E_CUDA;
     }
     ctx->own_stream = true;
     FailRec init{pint_dev::kNoFail, 0, 0, 0.0};
     cudaMemcpy(ctx->d_fail, &init, sizeof init, cudaMemcpyHostToDevice);
+    cudaMemcpy(ctx->d_fail_serial, &init, sizeof init, cudaMemcpyHostToDevice);
     *out = ctx;
     return PINT_OK;
 }
@@ -265,7 +268,10 @@ void pint_ctx_destroy(pint_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (int i = 0; i < pint_ctx::kSlots; ++i)
         if (ctx->scratch[i]) cudaFree(ctx->scratch[i]);
+    if (ctx->serial) cudaStreamSynchronize(ctx->serial);
     if (ctx->d_fail) cudaFree(ctx->d_fail);
+    if (ctx->d_fail_serial) cudaFree(ctx->d_fail_serial);
+    if (ctx->serial) cudaStreamDestroy(ctx->serial);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->evc) cudaEventDestroy(ctx->evc);
@@ -293,6 +299,28 @@ int pint_ctx_set_stream(pint_ctx* ctx, void* stream) {
 }
 
 int64_t pint_ctx_launch_count(const pint_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+namespace {
+// read and clear failure record `f` on `st` (pint_fail_read semantics)
+int fail_read_on(pint_ctx* ctx, FailRec* f, cudaStream_t st, pint_fail* out) {
+    FailRec rec{};
+    if (!ok(ctx, cudaMemcpyAsync(&rec, f, sizeof rec, cudaMemcpyDeviceToHost, st), "fail read") ||
+        !ok(ctx, cudaStreamSynchronize(st), "fail read sync"))
+        return PINT_E_CUDA;
+    FailRec init{pint_dev::kNoFail, 0, 0, 0.0};
+    if (rec.index != pint_dev::kNoFail &&
+        (!ok(ctx, cudaMemcpyAsync(f, &init, sizeof init, cudaMemcpyHostToDevice, st), "fail reset") ||
+         !ok(ctx, cudaStreamSynchronize(st), "fail reset sync")))
+        return PINT_E_CUDA;
+    if (out) {
+        out->index = rec.index == pint_dev::kNoFail ? -1 : static_cast<int64_t>(rec.index);
+        out->code = rec.index == pint_dev::kNoFail ? 0 : rec.code;
+        out->pad = 0;
+        out->value = rec.value;
+    }
+    return PINT_OK;
+}
+}  // namespace
 
 int pint_fail_read(pint_ctx* ctx, pint_fail* out) {
     FailRec rec{};
@@ -493,11 +521,76 @@ int pint_heat_fast_build_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, con
     return launch_heat_fast_build(ctx, n, N, S, records, maps);
 }
 
-int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t S, int64_t s0,
-                            int64_t steps, double h, int with_forcing, const double* records,
-                            const double* sx, double* y) {
+namespace {
+// ---- integrate (the closure, run_serial): one slice's steps for K device columns ----------------
+struct IntegTables {
+    int64_t n = 0, Q = 0;
+    int64_t* step_off = nullptr;
+    double *dt = nullptr, *r = nullptr, *fa = nullptr, *fb = nullptr, *sx = nullptr;
+};
+
+// Host tables of slice `s` (the reference's arithmetic, as heat_upload) into scratch `slot`, copied
+// on `st` and synchronised (the thread's pinned staging is free again on return).
+int integ_upload(pint_ctx* ctx, cudaStream_t st, int slot, double dx, const pint_slice& s, IntegTables& T) {
+    int64_t n = 0;
+    if (const int rc = heat_dim(ctx, dx, &n)) return rc;
+    if (const int rc = check_integral(ctx, s.t_end - s.t_begin, s.dt)) return rc;
+    const int64_t Q = s.steps;
+    const size_t b_off = align256(2 * sizeof(int64_t)), b_dt = align256(sizeof(double));
+    const size_t b_q = align256(sizeof(double) * Q), b_sx = align256(sizeof(double) * n);
+    const size_t bytes = b_off + b_dt + 3 * b_q + b_sx;
+    char* h = static_cast<char*>(pinned(bytes));
+    char* d = static_cast<char*>(pint_scratch(ctx, slot, bytes));
+    if (!h || !d) return pint_set_error(ctx, PINT_E_CUDA, "integrate: table allocation failed");
+    auto* h_off = reinterpret_cast<int64_t*>(h);
+    h_off[0] = 0;
+    h_off[1] = Q;
+    reinterpret_cast<double*>(h + b_off)[0] = s.dt;
+    heat_fill_steps(dx, &s, 0, 1, h_off, reinterpret_cast<double*>(h + b_off + b_dt),
+                    reinterpret_cast<double*>(h + b_off + b_dt + b_q), reinterpret_cast<double*>(h + b_off + b_dt + 2 * b_q));
+    auto* h_sx = reinterpret_cast<double*>(h + b_off + b_dt + 3 * b_q);
+    for (int64_t i = 0; i < n; ++i) h_sx[i] = std::sin(kPi * (static_cast<double>(i + 1) * dx));
+    if (!ok(ctx, cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st), "H2D integrate tables") ||
+        !ok(ctx, cudaStreamSynchronize(st), "H2D integrate tables sync"))
+        return PINT_E_CUDA;
+    T.n = n;
+    T.Q = Q;
+    T.step_off = reinterpret_cast<int64_t*>(d);
+    T.dt = reinterpret_cast<double*>(d + b_off);
+    T.r = reinterpret_cast<double*>(d + b_off + b_dt);
+    T.fa = reinterpret_cast<double*>(d + b_off + b_dt + b_q);
+    T.fb = reinterpret_cast<double*>(d + b_off + b_dt + 2 * b_q);
+    T.sx = reinterpret_cast<double*>(d + b_off + b_dt + 3 * b_q);
+    return PINT_OK;
+}
+
+// the steps in bounded chunks on `st`: slice-major records of chunk c into `rec` (heat_integrate_chunk
+// steps of room), then the integrate kernel over them — O(chunk) records, never O(Q)
+int integ_enqueue(pint_ctx* ctx, cudaStream_t st, const IntegTables& T, double* rec, int with_forcing, int64_t K,
+                  double* d_y, FailRec* fail, int guarded) {
+    const int64_t chunk = heat_integrate_chunk(T.n);
+    for (int64_t s0 = 0; s0 < T.Q; s0 += chunk) {
+        const int64_t sc = std::min(chunk, T.Q - s0);
+        if (const int rc = launch_heat_factor_block(ctx, st, T.n, 1, chunk, 0, 1, s0, sc, 0, T.step_off, T.dt, T.r,
+                                                    T.fa, T.fb, T.sx, rec, s0, true))
+            return rc;
+        if (const int rc = launch_heat_integrate_steps(ctx, st, T.n, K, sc, with_forcing, rec, d_y, fail, s0, guarded))
+            return rc;
+    }
+    return PINT_OK;
+}
+
+}  // namespace
+
+int pint_heat_integrate_dev(pint_ctx* ctx, int64_t n, int64_t K, int64_t steps, const int64_t* step_off,
+                            const double* slice_dt, const double* r, const double* fa, const double* fb,
+                            const double* sx, int with_forcing, double* y, int guarded) {
     if (!ctx) return PINT_E_INVALID;
-    return launch_heat_integrate(ctx, n, K, S, s0, steps, h, with_forcing, records, sx, y);
+    const IntegTables T{n, steps, const_cast<int64_t*>(step_off), const_cast<double*>(slice_dt), const_cast<double*>(r),
+                        const_cast<double*>(fa), const_cast<double*>(fb), const_cast<double*>(sx)};
+    double* rec = static_cast<double*>(pint_scratch(ctx, 1, sizeof(double) * heat_integrate_records_doubles(n)));
+    if (!rec) return PINT_E_CUDA;
+    return integ_enqueue(ctx, ctx->stream, T, rec, with_forcing, K, y, ctx->d_fail, guarded);
 }
 
 int pint_ctx_build_chain_ms(pint_ctx* ctx, double* build_ms, double* tail_ms) {
@@ -1079,17 +1172,78 @@ int pint_heat_integrate(pint_ctx* ctx, double dx, const pint_slice* slice, doubl
     if (K == 0) return PINT_OK;
     std::vector<pint_slice> sl;
     closure_slices(slice, 1, dt_nominal, sl);
-    HeatDev H;
-    if (const int rc = heat_upload(ctx, dx, sl, H)) return rc;
-    const int64_t n = H.n;
-    double* d_y = static_cast<double*>(pint_scratch(ctx, 2, sizeof(double) * n * K));
-    if (!d_y) return PINT_E_CUDA;
+    IntegTables T;
+    if (const int rc = integ_upload(ctx, ctx->stream, 0, dx, sl[0], T)) return rc;
+    const int64_t n = T.n;
+    double* rec = static_cast<double*>(pint_scratch(ctx, 1, sizeof(double) * heat_integrate_records_doubles(n)));
+    double* d_y = static_cast<double*>(pint_scratch(ctx, 2, 2 * sizeof(double) * n * K));
+    if (!rec || !d_y) return PINT_E_CUDA;
+    double* d_y0 = d_y + n * K;  // (the start states, for a guarded re-run)
     cudaMemcpyAsync(d_y, y, sizeof(double) * n * K, cudaMemcpyHostToDevice, ctx->stream);
-    int rc = launch_heat_integrate(ctx, n, K, H.S, 0, H.Q, sl[0].dt, with_forcing, H.factor, H.sx, d_y);
+    cudaMemcpyAsync(d_y0, d_y, sizeof(double) * n * K, cudaMemcpyDeviceToDevice, ctx->stream);
+    int rc = PINT_OK;
+    for (int guarded = 0; guarded < 2; ++guarded) {  // second pass only if a range check tripped
+        if (guarded) cudaMemcpyAsync(d_y, d_y0, sizeof(double) * n * K, cudaMemcpyDeviceToDevice, ctx->stream);
+        if ((rc = integ_enqueue(ctx, ctx->stream, T, rec, with_forcing, K, d_y, ctx->d_fail, guarded))) return rc;
+        rc = singular_check(ctx);  // (synchronises)
+        if (rc != PINT_E_RANGE_RETRY) break;
+    }
     if (rc) return rc;
     cudaMemcpyAsync(y, d_y, sizeof(double) * n * K, cudaMemcpyDeviceToHost, ctx->stream);
-    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "heat_integrate sync")) return PINT_E_CUDA;
-    return singular_check(ctx);
+    return ok(ctx, cudaStreamSynchronize(ctx->stream), "heat_integrate sync") ? PINT_OK : PINT_E_CUDA;
+}
+
+int pint_heat_serial_begin(pint_ctx* ctx, double dx, double dt, double T, const double* y0) {
+    if (!ctx || !y0) return PINT_E_INVALID;
+    auto& R = ctx->serial_run;
+    if (R.active) return pint_set_error(ctx, PINT_E_INVALID, "heat_serial_begin: a serial run is already in flight");
+    // run_serial's single slice (nievergelt.cpp:126-143) as the integrate closure steps it
+    const int64_t steps = pint_steps_for(T, dt);
+    const pint_slice whole{0.0, T, steps, T / static_cast<double>(steps)};
+    std::vector<pint_slice> sl;
+    closure_slices(&whole, 1, dt, sl);
+    IntegTables Tb;
+    if (const int rc = integ_upload(ctx, ctx->serial, 6, dx, sl[0], Tb)) return rc;
+    const int64_t n = Tb.n, rec_doubles = heat_integrate_records_doubles(n);
+    double* d = static_cast<double*>(pint_scratch(ctx, 7, sizeof(double) * (rec_doubles + 2 * n)));
+    if (!d) return PINT_E_CUDA;
+    R.n = n;
+    R.Q = Tb.Q;
+    R.rec = d;
+    R.y = d + rec_doubles;
+    R.y0 = R.y + n;
+    R.step_off = Tb.step_off, R.dt = Tb.dt, R.r = Tb.r, R.fa = Tb.fa, R.fb = Tb.fb, R.sx = Tb.sx;
+    if (!ok(ctx, cudaMemcpyAsync(R.y0, y0, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->serial), "H2D serial y0") ||
+        !ok(ctx, cudaMemcpyAsync(R.y, R.y0, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->serial), "serial y") ||
+        !ok(ctx, cudaStreamSynchronize(ctx->serial), "serial y0 sync"))  // (y0 is the caller's buffer)
+        return PINT_E_CUDA;
+    if (const int rc = integ_enqueue(ctx, ctx->serial, Tb, R.rec, 1, 1, R.y, ctx->d_fail_serial, 0)) return rc;
+    R.active = true;
+    return PINT_OK;
+}
+
+int pint_heat_serial_end(pint_ctx* ctx, double* y_out) {
+    if (!ctx || !y_out) return PINT_E_INVALID;
+    auto& R = ctx->serial_run;
+    if (!R.active) return pint_set_error(ctx, PINT_E_INVALID, "heat_serial_end: no serial run in flight");
+    R.active = false;
+    const IntegTables Tb{R.n, R.Q, R.step_off, R.dt, R.r, R.fa, R.fb, R.sx};
+    for (int guarded = 0; guarded < 2; ++guarded) {
+        pint_fail f;
+        if (const int rc = fail_read_on(ctx, ctx->d_fail_serial, ctx->serial, &f)) return rc;  // (synchronises)
+        if (f.index < 0) break;
+        if (f.code != PINT_E_RANGE_RETRY || guarded) {
+            char buf[96];
+            std::snprintf(buf, sizeof buf, "thomas_solve: zero pivot at row %d", static_cast<int>(f.value));
+            return pint_set_error(ctx, PINT_E_SINGULAR, buf);
+        }
+        cudaMemcpyAsync(R.y, R.y0, sizeof(double) * R.n, cudaMemcpyDeviceToDevice, ctx->serial);
+        if (const int rc = integ_enqueue(ctx, ctx->serial, Tb, R.rec, 1, 1, R.y, ctx->d_fail_serial, 1)) return rc;
+    }
+    return ok(ctx, cudaMemcpyAsync(y_out, R.y, sizeof(double) * R.n, cudaMemcpyDeviceToHost, ctx->serial), "D2H serial") &&
+                   ok(ctx, cudaStreamSynchronize(ctx->serial), "serial sync")
+               ? PINT_OK
+               : PINT_E_CUDA;
 }
 
 int pint_affine_compose(pint_ctx* ctx, int mode, int64_t n, int64_t N, const double* G, const double* c,

@@ -79,7 +79,9 @@ constexpr int kBackAhead = 8;  // back row: 2 dependent ops (~16 cycles)
 // group_forced): basis columns on 2-D tiles of it (kBasisGroup) and 32 forced columns per warp on
 // its halves (kForcedGroup). Otherwise (large n) slice-major records: basis columns (kBasis) and
 // one forced column per warp (kForcedSingle).
-enum : int { kBasis = 0, kForcedGroup = 1, kForcedSingle = 2, kBasisGroup = 3 };
+enum : int { kBasis = 0, kForcedGroup = 1, kForcedSingle = 2, kBasisGroup = 3, kBasisForced = 4 };
+// (kBasisForced: lane-interleaved columns on slice-major records like kBasis, each adding the forcing
+// increment like kForcedSingle — the integrate closure's forced runs from caller states)
 // kBasisGroup staging: [-r, 0, (p, rcp) x n][pad] | c pairs [n][2] (the 2-lane tile of c)
 __host__ __device__ constexpr long long bg_fwd(long long n) { return round16(2 * (n + 1)); }
 __host__ __device__ constexpr long long staged_doubles(long long n, int mode) {
@@ -186,6 +188,7 @@ constexpr int kRecLane = 4 * kRecChunk + 1;  // padded per-lane stride (doubles)
 
 __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, long long S, long long j0, long long Nc,
                                                           long long s0, long long Sc, long long tab_pitch,
+                                                          long long rec_s0, bool slice_major,
                                                           const int64_t* __restrict__ step_off,
                                                           const double* __restrict__ slice_dt,
                                                           const double* __restrict__ r_tab,
@@ -210,8 +213,9 @@ __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, lo
     if (live && !(r >= 0.0 && r <= 0x1p40)) record_failure(fail, kRetryIndex + q, PINT_E_RANGE_RETRY, r);
     unsigned hb_max = 0;
     const bool fast_c = r >= 0x1p-960 && r <= 0x1p40;
-    const bool group = group_forced(n);
-    double* const myrec = rec + (j * S + s) * record_stride(n);  // slice-major: this lane's record
+    // slice-major records hold steps [rec_s0, rec_s0 + S) (the integrate path's bounded chunks)
+    const bool group = group_forced(n) && !slice_major;
+    double* const myrec = rec + (j * S + s - rec_s0) * record_stride(n);  // slice-major: this lane's record
     double* const fblk = rec + (s * groups32(N) + j / 32) * fblock_stride(n);  // slice-group block
     double2* const pr2 = reinterpret_cast<double2*>(fblk) + (j & 31);
     if (live && group) pr2[0] = make_double2(negr, 0.0);
@@ -301,6 +305,7 @@ struct alignas(64) BuildPlan {
     long long s_begin, s_end;  // the steps this launch runs; s_begin > 0: resume from `maps`
     int* ready;                // (TMEM build) per-slice count of CTAs whose part of the map is stored
     unsigned long long* span;  // (with ready) {first CTA start, last CTA end} globaltimer of the launch
+    int only;                  // timing experiments (PINT_HEAT_ONLY): 1 basis columns only, 2 forced only
 };
 
 
@@ -317,7 +322,7 @@ template <int kMode>
 struct StagedStep {
     const double* R;
     int n, lane, parity;
-    static constexpr bool kForced = kMode == kForcedGroup || kMode == kForcedSingle;
+    static constexpr bool kForced = kMode == kForcedGroup || kMode == kForcedSingle || kMode == kBasisForced;
     static constexpr int kS = kMode == kForcedGroup ? 32 : 1;                             // p, rcp, h*b
     static constexpr int kSc = kMode == kForcedGroup ? 32 : kMode == kBasisGroup ? 2 : 1;  // c
     __device__ __forceinline__ double negr() const {
@@ -770,9 +775,9 @@ __global__ void __launch_bounds__(160, 1) heat_build_tmem_kernel(const __grid_co
     const int cta = static_cast<int>(blockIdx.x - slice * cps);
     const bool forced = warp == 4;
     const int g = 4 * cta + warp;
-    const bool wlive = forced ? cta == 0 : g < P.wps;  // this warp has columns
+    const bool wlive = forced ? cta == 0 && P.only != 1 : g < P.wps && P.only != 2;  // this warp has columns
     const int k = forced ? n : 32 * g + lane;
-    const int nlive = min(4, P.wps - 4 * cta) + (cta == 0 ? 1 : 0);
+    const int nlive = (P.only == 2 ? 0 : min(4, P.wps - 4 * cta)) + (cta == 0 && P.only != 1 ? 1 : 0);
     const int nb = tm_rows(n) / kTmBody;
     const long long M = tm_shared_rows(n);
     double* R = smem;
@@ -894,53 +899,96 @@ __global__ void __launch_bounds__(160, 1) heat_build_tmem_kernel(const __grid_co
     }
 }
 
-// ---- integrate: K caller columns of one slice (records with N = 1), guarded division ----------
-struct IntegratePlan {
+// ---- integrate: K caller columns through consecutive steps of ONE slice ------------------------
+// The integrate closure (pde_problems.cpp:86-98) and run_serial (nievergelt.cpp:126-143): the same
+// bit-exact row recurrence as the build, one warp per 32 caller columns (lane = column; a single
+// trajectory runs on lane 0 with the others idle), rows [0, RR) in registers and the rest
+// lane-interleaved in shared memory, each step's slice-major record (forward half: header, (p,
+// rcp), h*b; back half: c) staged by two bulk copies — the back half while the forward pass runs,
+// the next forward half while the back pass runs, the step after next pulled into L2. Steps go in
+// bounded chunks (launch_heat_integrate_steps): the records of one chunk at a time.
+struct IntegPlan {
     int n;
-    long long K, s0, steps, S;
-    double h;
-    int with_forcing;
+    long long K, steps;  // columns; steps of this chunk (records [0, steps) of `rec`)
     const double* rec;
-    const double* sx;
-    double* y;
+    double* y;           // [K][n], in place
+    FailRec* fail;
+    long long fail_base;  // step index of the chunk's first step (range-retry index)
 };
 
-__global__ void __launch_bounds__(32) heat_integrate_kernel(IntegratePlan P) {
+template <int RR, int kMode, bool kGuard>
+__global__ void __maxnreg__(255) heat_integrate_kernel(const IntegPlan P) {
+    static_assert(kMode == kBasis || kMode == kBasisForced, "integrate modes");
     extern __shared__ __align__(128) double smem[];
     const int n = P.n;
     const int lane = threadIdx.x;
     const long long col = static_cast<long long>(blockIdx.x) * 32 + lane;
-    const bool active = col < P.K;
-    double* sx = smem;
-    double* st = smem + even(n) + lane;
-    for (int i = lane; i < n; i += 32) sx[i] = P.sx[i];
-    for (int i = 0; i < n; ++i) st[i * 32] = active ? P.y[col * n + i] : 0.0;
+    const bool live = col < P.K;
+    double* R0 = smem + front_pad(n, kMode);
+    double* st = R0 + staged_doubles(n, kMode) + lane;
+    const unsigned bar0 = smem_u32(R0 + staged_doubles(n, kMode) + (n - RR) * 32 + 32 * kFwdAhead);
+    const unsigned fwd_bytes = 8u * static_cast<unsigned>(cc_offset(n));  // header, (p, rcp), h*b
+    const unsigned back_bytes = 8u * static_cast<unsigned>(even(n));
+    auto rec = [&](long long s) { return P.rec + s * record_stride(n); };
+    if (lane == 0) {
+        mbar_init(bar0);
+        mbar_init(bar0 + 8u);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
     __syncwarp();
-    const RecView V = rec_view(P.rec, n, 1, P.S);
-    const bool forcing = P.with_forcing != 0;
-    const bool group = group_forced(n);  // records of ONE slice: slice-group block, lane 0
-    for (long long s = P.s0; s < P.s0 + P.steps; ++s) {
-        const double* B = group ? V.fblock(s, 0) : V.rec(0, s);
-        const double2* PR = group ? reinterpret_cast<const double2*>(B) + 32 : reinterpret_cast<const double2*>(B + pr_offset());
-        const double* HB = group ? B + fblock_hb(n) : B + hb_offset(n);
-        const double* CC = group ? B + fblock_cc(n) : B + cc_offset(n);
-        const int ks = group ? 32 : 1;
-        const double negr = __ldg(B);
-        double d = 0.0;
-        for (int i = 0; i < n; ++i) {
-            double x = st[i * 32];
-            if (forcing) x = __dadd_rn(x, __ldg(HB + i * ks));  // state += h*b (pde_problems.cpp:93)
-            const double num = (i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d));
-            d = div_guarded(num, __ldg(PR + i * ks));
-            st[i * 32] = d;
-        }
-        for (int i = n - 2; i >= 0; --i) {
-            d = __dsub_rn(st[i * 32], __dmul_rn(__ldg(CC + i * ks), d));
-            st[i * 32] = d;
+    if (lane == 0 && P.steps > 0) {
+        bulk_load(smem_u32(R0), rec(0), fwd_bytes, bar0);
+        bulk_load(smem_u32(R0 + cc_offset(n)), rec(0) + cc_offset(n), back_bytes, bar0 + 8u);
+        if (P.steps > 1) prefetch_l2(rec(1), 8u * static_cast<unsigned>(record_stride(n)));
+    }
+    double reg[RR > 0 ? RR : 1];
+    const double* yc = P.y + (live ? col : 0) * n;
+#pragma unroll
+    for (int i = 0; i < RR; ++i) reg[i] = live ? yc[i] : 0.0;
+    for (int i = RR; i < n; ++i) st[(i - RR) * 32] = live ? yc[i] : 0.0;
+    unsigned qmin = 0xffffffffu;
+    for (long long s = 0; s < P.steps; ++s) {
+        const unsigned parity = static_cast<unsigned>(s & 1);
+        const StagedStep<kMode> SV{R0, n, lane, 0};
+        mbar_wait(bar0, parity);
+        double dm1 = 0.0;
+        double d = column_forward<RR, kMode, kGuard>(reg, st, SV, dm1, qmin);
+        qmin = min(qmin, hi_abs(d) - 1u);
+        __syncwarp();  // every lane is done with the forward half
+        if (lane == 0 && s + 1 < P.steps) bulk_load(smem_u32(R0), rec(s + 1), fwd_bytes, bar0);
+        mbar_wait(bar0 + 8u, parity);
+        column_back<RR, kMode>(reg, st, SV, d, dm1, qmin);
+        __syncwarp();
+        if (lane == 0 && s + 1 < P.steps) {
+            bulk_load(smem_u32(R0 + cc_offset(n)), rec(s + 1) + cc_offset(n), back_bytes, bar0 + 8u);
+            if (s + 2 < P.steps) prefetch_l2(rec(s + 2), 8u * static_cast<unsigned>(record_stride(n)));
         }
     }
-    if (active)
-        for (int i = 0; i < n; ++i) P.y[col * n + i] = st[i * 32];
+    if (live) {
+        double* yo = P.y + col * n;
+#pragma unroll
+        for (int i = 0; i < RR; ++i) yo[i] = reg[i];
+        for (int i = RR; i < n; ++i) yo[i] = st[(i - RR) * 32];
+        if (!kGuard && qmin < kQuotLo - 1u) record_failure(P.fail, kRetryIndex + P.fail_base, PINT_E_RANGE_RETRY, 0.0);
+    }
+}
+
+template <int RR, int kMode, bool kGuard>
+int launch_integ(pint_ctx* ctx, cudaStream_t stream, const IntegPlan& P) {
+    const size_t smem = sizeof(double) * warp_smem_doubles(P.n, kMode);
+    if (smem > 227 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "heat_integrate: n too large for shared memory");
+    auto kern = heat_integrate_kernel<RR, kMode, kGuard>;
+    pint_kernel_attrs(reinterpret_cast<const void*>(kern));
+    kern<<<static_cast<unsigned>((P.K + 31) / 32), 32, smem, stream>>>(P);
+    return pint_check_launch(ctx, "heat_integrate_kernel");
+}
+
+template <int RR>
+int launch_integ_rr(pint_ctx* ctx, cudaStream_t stream, const IntegPlan& P, bool forcing, bool guarded) {
+    if (forcing)
+        return guarded ? launch_integ<RR, kBasisForced, true>(ctx, stream, P)
+                       : launch_integ<RR, kBasisForced, false>(ctx, stream, P);
+    return guarded ? launch_integ<RR, kBasis, true>(ctx, stream, P) : launch_integ<RR, kBasis, false>(ctx, stream, P);
 }
 
 template <class K>
@@ -1044,13 +1092,13 @@ int launch_heat_factor_range(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, int
 int launch_heat_factor_block(pint_ctx* ctx, cudaStream_t stream, int64_t n, int64_t N, int64_t S, int64_t j0,
                              int64_t Nc, int64_t s0, int64_t Sc, int64_t tab_pitch, const int64_t* step_off,
                              const double* slice_dt, const double* r, const double* fa, const double* fb,
-                             const double* sx, double* records) {
-    if (n < 1 || N < 0 || S < 0 || j0 < 0 || Nc < 0 || j0 + Nc > N || s0 < 0 || Sc < 0 || s0 + Sc > S)
+                             const double* sx, double* records, int64_t rec_s0, bool slice_major) {
+    if (n < 1 || N < 0 || S < 0 || j0 < 0 || Nc < 0 || j0 + Nc > N || s0 < rec_s0 || Sc < 0 || s0 + Sc > rec_s0 + S)
         return pint_set_error(ctx, PINT_E_INVALID, "heat_factor: bad sizes");
     if (Nc == 0 || Sc == 0) return PINT_OK;
     const long long threads = Nc * Sc;
     heat_record_kernel<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, stream>>>(
-        static_cast<int>(n), N, S, j0, Nc, s0, Sc, tab_pitch, step_off, slice_dt, r, fa, fb, sx, records, ctx->d_fail);
+        static_cast<int>(n), N, S, j0, Nc, s0, Sc, tab_pitch, rec_s0, slice_major, step_off, slice_dt, r, fa, fb, sx, records, ctx->d_fail);
     return pint_check_launch(ctx, "heat_record_kernel");
 }
 
@@ -1104,6 +1152,7 @@ int launch_heat_build_steps(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, cons
     P.per_slice_ns = per_slice_ns;
     P.fail = ctx->d_fail;
     P.ready = ready;
+    if (const char* o = std::getenv("PINT_HEAT_ONLY")) P.only = std::strcmp(o, "basis") == 0 ? 1 : std::strcmp(o, "forced") == 0 ? 2 : 0;
     P.span = ready ? reinterpret_cast<unsigned long long*>(ready + ((N + 1) & ~1ll)) : nullptr;
     if (use_tmem(n)) {
         const size_t smem = sizeof(double) * tm_smem_doubles(n);
@@ -1135,14 +1184,18 @@ int launch_heat_build_steps(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, cons
     return guarded ? launch_build<0, true>(ctx, P) : launch_build<0, false>(ctx, P);
 }
 
-int launch_heat_integrate(pint_ctx* ctx, int64_t n, int64_t K, int64_t S, int64_t s0, int64_t steps, double h,
-                          int with_forcing, const double* records, const double* sx, double* y) {
-    if (n < 1 || K < 0) return pint_set_error(ctx, PINT_E_INVALID, "heat_integrate: bad sizes");
-    if (K == 0) return PINT_OK;
-    IntegratePlan P{static_cast<int>(n), K, s0, steps, S, h, with_forcing, records, sx, y};
-    const size_t smem = sizeof(double) * (static_cast<size_t>(n) * 32 + even(n));
-    if (smem > 227 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "heat_integrate: n too large");
-    smem_attrs(heat_integrate_kernel, smem);
-    heat_integrate_kernel<<<static_cast<unsigned>((K + 31) / 32), 32, smem, ctx->stream>>>(P);
-    return pint_check_launch(ctx, "heat_integrate_kernel");
+int64_t heat_integrate_chunk(int64_t n) {  // steps per chunk: ~16 MB of records
+    return std::max<int64_t>(16, (int64_t{2} << 20) / record_stride(n));
+}
+
+int64_t heat_integrate_records_doubles(int64_t n) { return heat_integrate_chunk(n) * record_stride(n); }
+
+int launch_heat_integrate_steps(pint_ctx* ctx, cudaStream_t stream, int64_t n, int64_t K, int64_t steps,
+                                int with_forcing, const double* records, double* y, FailRec* fail, int64_t fail_base,
+                                int guarded) {
+    if (n < 1 || K < 0 || steps < 0) return pint_set_error(ctx, PINT_E_INVALID, "heat_integrate: bad sizes");
+    if (K == 0 || steps == 0) return PINT_OK;
+    const IntegPlan P{static_cast<int>(n), K, steps, records, y, fail, fail_base};
+    return reg_rows(n) == kRegRows ? launch_integ_rr<kRegRows>(ctx, stream, P, with_forcing != 0, guarded != 0)
+                                   : launch_integ_rr<0>(ctx, stream, P, with_forcing != 0, guarded != 0);
 }
