@@ -38,7 +38,8 @@ enum {
                                        host-buffer entry points re-run with the guarded kernel */
     PINT_E_INVALID = 16,            /* bad argument to this ABI */
     PINT_E_CUDA = 17,               /* CUDA runtime failure (no CPU fallback exists) */
-    PINT_E_NO_DEVICE = 18
+    PINT_E_NO_DEVICE = 18,
+    PINT_E_NCCL = 19                /* multi-GPU transport failure (NCCL or a caller callback) */
 };
 
 typedef struct pint_ctx pint_ctx;
@@ -282,6 +283,36 @@ int pint_wave_integrate(pint_ctx* ctx, int64_t d, const double* D2, double dt_na
 int pint_run_wave(pint_ctx* ctx, int64_t d, const double* D2, double dt_native, double T, int64_t N,
                   double dt_nominal, int compose_mode, const double* y0, double* y_out,
                   double* per_slice_seconds, pint_report* report);
+
+/* ---- multi-GPU (north_star subsystem 4): one context per GPU (a process or a
+ * thread each). Slices go to ranks in contiguous blocks [floor(rN/W), floor((r+1)N/W)) of the
+ * reference decomposition (ode_core.cpp:26-45, identical on every rank: slice assignment is
+ * bit-exact); the only exchange is the final compose step. Replaces the reference's simulated
+ * wire (inject_latency + counters, nievergelt.cpp:73-79, 95-101) and ExecConfig::workers' thread
+ * pool (exec_harness.hpp:17-21, 51-101) with GPUs. ---- */
+/* NCCL: rank 0 makes the id (128 bytes, an ncclUniqueId) and the caller distributes it */
+int pint_comm_unique_id(void* id_out);
+int pint_comm_init(pint_ctx* ctx, const void* id, int rank, int world);
+/* one process driving `world` GPUs: ctxs[r] on its own device becomes rank r */
+int pint_comm_init_all(pint_ctx** ctxs, int world);
+/* a caller-provided transport of HOST buffers (MPI, a socket, torch.distributed ...); each call
+ * returns 0 on success; device data is staged through pinned memory */
+typedef int (*pint_send_fn)(void* user, int peer, const void* buf, size_t bytes);
+typedef int (*pint_recv_fn)(void* user, int peer, void* buf, size_t bytes);
+int pint_comm_init_callbacks(pint_ctx* ctx, int rank, int world, pint_send_fn send, pint_recv_fn recv,
+                             void* user);
+int pint_comm_rank(const pint_ctx* ctx, int* rank, int* world);
+int pint_comm_destroy(pint_ctx* ctx);
+/* run_nievergelt(make_heat_problem(dx, dt, T), N) over the communicator's ranks (call on every
+ * rank). Each rank builds its block's maps (build_mode as pint_run_heat_ex). compose_mode
+ * PINT_COMPOSE_TREE: the block's maps tree-composed (DMMA) into one augmented map, ONE gather of
+ * the W maps to rank 0, which applies them in rank order (the paper's single final gather/compose;
+ * <= 1e-12 vs the chain). PINT_COMPOSE_CHAIN: the running state handed rank to rank (W messages of
+ * n doubles), each rank applying its block's maps with the bit-exact chain — bit-identical to
+ * pint_run_heat. y_out (n doubles) is written on rank 0 (may be NULL elsewhere); report->
+ * message_count / bytes_communicated count this rank's real transfers. */
+int pint_run_heat_sharded(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int build_mode,
+                          int compose_mode, const double* y0, double* y_out, pint_report* report);
 
 /* Host-buffer barycentric weights (interp.cpp:43-55 / closed form); DuplicateNodes -> code 5. */
 int pint_bary_weights(pint_ctx* ctx, int kind, int64_t M, const double* nodes, double* w);

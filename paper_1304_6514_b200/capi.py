@@ -23,6 +23,7 @@ PINT_E_RANGE_RETRY = 6
 PINT_E_INVALID = 16
 PINT_E_CUDA = 17
 PINT_E_NO_DEVICE = 18
+PINT_E_NCCL = 19
 
 RHS_RICCATI_BE = 0
 RHS_LOGISTIC_RK4 = 1
@@ -64,6 +65,9 @@ class Report(C.Structure):
 
 
 _vp, _d, _i, _int = C.c_void_p, C.c_double, C.c_int64, C.c_int
+# pint_send_fn / pint_recv_fn: int (*)(void* user, int peer, [const] void* buf, size_t bytes)
+SEND_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_size_t)
+RECV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_size_t)
 _SIGS = {
     "pint_version": (C.c_char_p, []),
     "pint_ctx_create": (_int, [_int, C.POINTER(_vp)]),
@@ -103,6 +107,13 @@ _SIGS = {
                                _vp, _vp, _vp, _vp, C.POINTER(Report), C.POINTER(Fail)]),
     "pint_run_heat": (_int, [_vp, _d, _d, _d, _i, _int, _vp, _vp, _vp, C.POINTER(Report)]),
     "pint_run_heat_ex": (_int, [_vp, _d, _d, _d, _i, _int, _int, _vp, _vp, _vp, C.POINTER(Report)]),
+    "pint_comm_unique_id": (_int, [_vp]),
+    "pint_comm_init": (_int, [_vp, _vp, _int, _int]),
+    "pint_comm_init_all": (_int, [C.POINTER(_vp), _int]),
+    "pint_comm_init_callbacks": (_int, [_vp, _int, _int, SEND_FN, RECV_FN, _vp]),
+    "pint_comm_rank": (_int, [_vp, C.POINTER(_int), C.POINTER(_int)]),
+    "pint_comm_destroy": (_int, [_vp]),
+    "pint_run_heat_sharded": (_int, [_vp, _d, _d, _d, _i, _int, _int, _vp, _vp, C.POINTER(Report)]),
     "pint_heat_maps": (_int, [_vp, _d, _d, C.POINTER(Slice), _i, _vp, _vp]),
     "pint_heat_integrate": (_int, [_vp, _d, C.POINTER(Slice), _d, _int, _i, _vp]),
     "pint_scalar_integrate": (_int, [_vp, C.POINTER(ScalarRHS), C.POINTER(Slice), _i, _vp, _vp, C.POINTER(Fail)]),

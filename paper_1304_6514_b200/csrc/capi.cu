@@ -269,6 +269,7 @@ void pint_ctx_destroy(pint_ctx* ctx) {
     for (int i = 0; i < pint_ctx::kSlots; ++i)
         if (ctx->scratch[i]) cudaFree(ctx->scratch[i]);
     if (ctx->serial) cudaStreamSynchronize(ctx->serial);
+    comm_free(ctx);
     if (ctx->d_fail) cudaFree(ctx->d_fail);
     if (ctx->d_fail_serial) cudaFree(ctx->d_fail_serial);
     if (ctx->serial) cudaStreamDestroy(ctx->serial);
@@ -1131,6 +1132,123 @@ int pint_run_heat_ex(pint_ctx* ctx, double dx, double dt, double T, int64_t N, i
         float cms = 0.f;
         cudaEventElapsedTime(&cms, ctx->evc, ctx->ev1);
         report->compose_ms = cms;
+        report->total_ms = wall.ms();
+    }
+    return PINT_OK;
+}
+
+int pint_run_heat_sharded(pint_ctx* ctx, double dx, double dt, double T, int64_t N, int build_mode,
+                          int compose_mode, const double* y0, double* y_out, pint_report* report) {
+    if (!ctx || N < 1 || (build_mode != PINT_BUILD_EXACT && build_mode != PINT_BUILD_FAST) ||
+        (compose_mode != PINT_COMPOSE_CHAIN && compose_mode != PINT_COMPOSE_TREE))
+        return PINT_E_INVALID;
+    if (!ctx->comm) return pint_set_error(ctx, PINT_E_INVALID, "run_heat_sharded: no communicator (pint_comm_init*)");
+    int rank = 0, W = 1;
+    pint_comm_rank(ctx, &rank, &W);
+    if (rank == 0 && !y_out) return PINT_E_INVALID;
+    comm_counters(ctx, nullptr, nullptr, true);
+    if (W == 1) {  // one rank: the single-GPU run itself (bit-identical by construction)
+        const int rc = pint_run_heat_ex(ctx, dx, dt, T, N, build_mode, compose_mode, y0, y_out, nullptr, report);
+        if (report) report->message_count = report->bytes_communicated = 0;  // (no transfers)
+        return rc;
+    }
+    HostTimer wall;
+    const long long launches0 = ctx->launches;
+    std::vector<pint_slice> all(static_cast<size_t>(N));
+    if (pint_decompose(0.0, T, N, dt, all.data()) != PINT_OK)
+        return pint_set_error(ctx, PINT_E_BAD_GRID, "decompose: need N >= 1, T > t0, dt > 0");
+    closure_slices(all.data(), N, dt, all);
+    const int64_t lo = rank * N / W, hi = (rank + 1) * N / W, Nb = hi - lo;  // this rank's block
+    const std::vector<pint_slice> sl(all.begin() + lo, all.begin() + hi);
+    int64_t n = 0;
+    if (const int rc = heat_dim(ctx, dx, &n)) return rc;
+    cudaEventRecord(ctx->ev0, ctx->stream);
+    const int64_t ldm = pint_affine_ldm(n);
+    const size_t map_elems = static_cast<size_t>(n * ldm);
+    const bool tree = compose_mode == PINT_COMPOSE_TREE;
+    const size_t total = align256(sizeof(double) * map_elems * std::max<int64_t>(Nb, 1)) +
+                         (tree ? align256(sizeof(double) * map_elems * ((Nb + 1) / 2 + 1)) : 0) +
+                         (tree ? align256(sizeof(double) * map_elems) : 0) +
+                         (tree && rank == 0 ? align256(sizeof(double) * map_elems * W) : 0) +
+                         3 * align256(sizeof(double) * n) + 1024;
+    char* d = static_cast<char*>(pint_scratch(ctx, 2, total));
+    if (!d) return PINT_E_CUDA;
+    Carve cv{d};
+    double* d_maps = cv.take<double>(map_elems * std::max<int64_t>(Nb, 1));
+    double* d_scr = tree ? cv.take<double>(map_elems * ((Nb + 1) / 2 + 1)) : nullptr;
+    double* d_comp = tree ? cv.take<double>(map_elems) : nullptr;
+    double* d_gath = tree && rank == 0 ? cv.take<double>(map_elems * W) : nullptr;
+    double* d_y0 = cv.take<double>(n);
+    double* d_y = cv.take<double>(n);
+    double* d_lam = cv.take<double>(n);
+    std::vector<double> y0v;
+    if (!y0) {
+        y0v.resize(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) y0v[i] = std::sin(kPi * static_cast<double>(i + 1) * dx);  // heat_initial
+        y0 = y0v.data();
+    }
+    cudaMemcpyAsync(d_y0, y0, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream);
+    // this block's maps (its slices' records, then the build; a tripped range check re-runs guarded)
+    HeatDev H;
+    if (Nb > 0) {
+        if (const int rc = heat_upload(ctx, dx, sl, H, nullptr, build_mode)) return rc;
+        for (int guarded = 0; guarded < 2; ++guarded) {
+            int rc = build_mode == PINT_BUILD_FAST
+                         ? launch_heat_fast_build(ctx, n, Nb, H.S, H.factor, d_maps)
+                         : launch_heat_build(ctx, n, Nb, H.S, H.step_off, H.slice_dt, H.factor, H.sx, d_maps, nullptr,
+                                             guarded);
+            if (rc) return rc;
+            rc = singular_check(ctx);  // (synchronises)
+            if (rc == PINT_OK) break;
+            if (rc != PINT_E_RANGE_RETRY) return rc;
+        }
+    }
+    cudaEventRecord(ctx->evc, ctx->stream);
+    if (tree) {  // the block map, ONE gather of the W block maps, rank 0 applies them in rank order
+        if (Nb > 0) {
+            if (const int rc = launch_affine_tree(ctx, n, Nb, d_maps, d_scr, d_y0, d_lam, d_comp)) return rc;
+        } else {  // an empty block composes to the identity map [I | 0]
+            std::vector<double> id(map_elems, 0.0);
+            for (int64_t i = 0; i < n; ++i) id[static_cast<size_t>(i * ldm + i)] = 1.0;
+            cudaMemcpyAsync(d_comp, id.data(), sizeof(double) * map_elems, cudaMemcpyHostToDevice, ctx->stream);
+            cudaStreamSynchronize(ctx->stream);
+        }
+        if (const int rc = comm_gather(ctx, d_comp, d_gath, sizeof(double) * map_elems, 0)) return rc;
+        if (rank == 0)
+            if (const int rc = launch_affine_chain(ctx, n, W, d_gath, d_y0, d_y)) return rc;
+    } else {  // the running state handed rank to rank (0 -> 1 -> ... -> W-1 -> 0), each block chained
+        const double* in = d_y0;
+        if (rank > 0) {
+            if (const int rc = comm_recv(ctx, d_lam, sizeof(double) * n, rank - 1)) return rc;
+            in = d_lam;
+        }
+        if (Nb > 0) {
+            if (const int rc = launch_affine_chain(ctx, n, Nb, d_maps, in, d_y)) return rc;
+        } else {
+            cudaMemcpyAsync(d_y, in, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream);
+        }
+        if (const int rc = comm_send(ctx, d_y, sizeof(double) * n, (rank + 1) % W)) return rc;
+        if (rank == 0)
+            if (const int rc = comm_recv(ctx, d_y, sizeof(double) * n, W - 1)) return rc;
+    }
+    cudaEventRecord(ctx->ev1, ctx->stream);
+    if (rank == 0) cudaMemcpyAsync(y_out, d_y, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream);
+    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "run_heat_sharded sync")) return PINT_E_CUDA;
+    if (report) {
+        float ms = 0.f, cms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        cudaEventElapsedTime(&cms, ctx->evc, ctx->ev1);
+        int64_t msgs = 0, bytes = 0;
+        comm_counters(ctx, &msgs, &bytes, false);
+        report->message_count = msgs;
+        report->bytes_communicated = bytes;
+        report->extrapolation_count = 0;
+        report->device_ms = ms;
+        report->compose_ms = cms;
+        report->traj_steps = (Nb > 0 ? H.Q : 0) * (n + 1);
+        report->gpu_launches = ctx->launches - launches0;
+        report->h2d_bytes = static_cast<int64_t>((Nb > 0 ? H.h2d : 0) + sizeof(double) * n);
+        report->d2h_bytes = rank == 0 ? static_cast<int64_t>(sizeof(double) * n) : 0;
         report->total_ms = wall.ms();
     }
     return PINT_OK;

@@ -220,6 +220,76 @@ def sharded_heat_step(plan: HeatPlan, group=None) -> None:
         plan.ctx.sync()
 
 
+# ---- the sharded run behind the C ABI (pint_run_heat_sharded) -----------------------------------
+
+class TorchDistTransport:
+    """pint_comm_init_callbacks transport over torch.distributed point-to-point (e.g. gloo): the
+    library hands host buffers to these callbacks. Keep the object alive while the context uses it."""
+
+    def __init__(self, ctx: capi.Context, group=None):
+        import torch.distributed as dist
+
+        self.ctx, self.group = ctx, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+
+        def _send(user, peer, buf, nbytes):
+            try:
+                import torch
+
+                arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_uint8)), shape=(nbytes,))
+                dist.send(torch.from_numpy(arr.copy()), peer, group=group)
+                return 0
+            except Exception:  # (reported to the library as a transport failure)
+                return 1
+
+        def _recv(user, peer, buf, nbytes):
+            try:
+                import torch
+
+                t = torch.empty(nbytes, dtype=torch.uint8)
+                dist.recv(t, peer, group=group)
+                C.memmove(buf, t.numpy().ctypes.data, nbytes)
+                return 0
+            except Exception:
+                return 1
+
+        self._send, self._recv = capi.SEND_FN(_send), capi.RECV_FN(_recv)
+        ctx.check(ctx.lib.pint_comm_init_callbacks(ctx.h, self.rank, self.world, self._send, self._recv, None))
+
+
+def nccl_comm_init(ctx: capi.Context, group=None) -> None:
+    """pint_comm_init over NCCL: rank 0 makes the unique id, torch.distributed broadcasts it."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    uid = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        ctx.check(ctx.lib.pint_comm_unique_id(capi.ptr(uid.numpy())))
+    if dist.get_backend(group) == "nccl":
+        u = uid.cuda()
+        dist.broadcast(u, 0, group=group)
+        uid = u.cpu()
+    else:
+        dist.broadcast(uid, 0, group=group)
+    ctx.check(ctx.lib.pint_comm_init(ctx.h, capi.ptr(uid.numpy()), rank, world))
+
+
+def run_heat_sharded(ctx: capi.Context, dx: float, dt: float, T: float, N: int, build: str = "exact",
+                     compose: str = "chain", y0=None):
+    """pint_run_heat_sharded on this rank (every rank calls it): returns (y or None, report)."""
+    rank, world = C.c_int(), C.c_int()
+    ctx.check(ctx.lib.pint_comm_rank(ctx.h, C.byref(rank), C.byref(world)))
+    n = int(round(1.0 / dx)) - 1
+    y = np.empty(n) if rank.value == 0 else None
+    y0a = None if y0 is None else np.ascontiguousarray(y0, dtype=np.float64)
+    rep = capi.Report()
+    ctx.check(ctx.lib.pint_run_heat_sharded(ctx.h, dx, dt, T, N, capi.BUILD_FAST if build == "fast" else capi.BUILD_EXACT,
+                                            capi.COMPOSE_TREE if compose == "tree" else capi.COMPOSE_CHAIN,
+                                            capi.ptr(y0a), capi.ptr(y), C.byref(rep)))
+    return y, rep
+
+
 # ---- nonlinear composition across ranks (SURVEY.md §8e) ---------------------------------------
 
 def block_sizes(N: int, world: int) -> List[int]:
