@@ -87,6 +87,8 @@ def parse():
     p.add_argument("--ref-sample", type=int, default=None,
                    help="slices the reference CPU baseline builds per rep (default: the workload's)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--transport", default="nccl", choices=["nccl", "host"],
+                   help="N > 1: NCCL, or the host-callback transport over gloo (several ranks on one GPU: tests)")
     p.add_argument("--configs", nargs="*", default=None,
                    help="measure BASELINE configs 1/3/5 instead (cases: c1ref c1rk4 c5 c3; default all)")
     p.add_argument("--config-reps", type=int, default=5)
@@ -516,7 +518,98 @@ def main():
         args.cm_reps, args.cm_out = args.cost_model_reps, args.cost_model_out
         return run_cost_model(args) or 0
 
+    if world > 1:
+        return heat_bench_sharded(args, rank, world, local)
     return heat_bench(args, rank, world, local)
+
+
+def heat_bench_sharded(args, rank, world, local):
+    """N > 1 GPUs: every step is ONE pint_run_heat_sharded call per rank (the C ABI with host
+    buffers: tables H2D, the block's maps, the block tree, one NCCL gather of the W block maps to
+    rank 0, rank 0's ordered apply, y D2H). value: the device time of that call (CUDA events on each
+    rank's stream), max over ranks; e2e: its wall time, max over ranks. --transport host runs the
+    same code over the host-callback transport (gloo; e.g. several ranks on one GPU, for testing)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1304_6514_b200 import capi
+    from paper_1304_6514_b200.dist import TorchDistTransport, nccl_comm_init, slice_block
+
+    host = args.transport == "host"
+    if host:  # (test mode: ranks may share a GPU; each kernel still runs on its own rank's stream)
+        local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo" if host else "nccl", **({} if host else {"device_id": torch.device("cuda", local)}))
+    ctx = capi.Context(local)
+    keep = TorchDistTransport(ctx) if host else nccl_comm_init(ctx)
+    n, S, T, N = args.n, args.S, args.T, args.slices
+    dx, dt = 1.0 / (n + 1), T / (N * S)
+    lo, hi = slice_block(N, world, rank)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    y = np.empty(n)
+    rep = capi.Report()
+    compose = capi.COMPOSE_TREE
+
+    def one():
+        ctx.check(ctx.lib.pint_run_heat_sharded(ctx.h, dx, dt, T, N, capi.BUILD_EXACT, compose, None,
+                                                capi.ptr(y) if rank == 0 else None, C.byref(rep)))
+
+    for _ in range(args.warmup):
+        one()
+    parity = parity_check(y, n, N, S, T, tol=1e-12) if rank == 0 else None
+    clocks = ClockSampler(local)
+    clocks.start()
+    clocks.wait_first_sample()
+    dev_ms, wall_s, comp_ms = 0.0, 0.0, 0.0
+    t_region0 = time.time()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        one()
+        wall_s += time.perf_counter() - t0
+        dev_ms += rep.device_ms
+        comp_ms += rep.compose_ms
+    agg = torch.tensor([dev_ms, wall_s, comp_ms], dtype=torch.float64)
+    dist.all_reduce(agg, op=dist.ReduceOp.MAX)
+    t_region1 = time.time()
+    clocks.stop()
+    dev_ms, wall_s, comp_ms = (float(v) for v in agg)
+    ms_per_step = dev_ms / args.steps
+    traj_steps_total = N * (n + 1) * S
+    if rank == 0:
+        build_ms = (dev_ms - comp_ms) / args.steps  # (tables H2D + records + build of the largest block)
+        flops = (hi - lo) * S * flops_per_slice_step(n)
+        peak64 = C.c_double()
+        ctx.check(ctx.lib.pint_probe_peak(ctx.h, capi.F64, C.byref(peak64)))
+        achieved = flops / (build_ms * 1e-3) / 1e12
+        line = {
+            "metric": METRIC, "value": traj_steps_total / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args), "n": n, "slices": N, "slices_per_gpu": hi - lo,
+                       "steps_per_slice": S, "T": T, "dt": dt, "build": "exact",
+                       "compose": "block tree (DMMA) + one gather to rank 0 + rank 0's ordered apply",
+                       "transport": "host callbacks (gloo)" if host else "NCCL", "parallelism": f"slice blocks x{world}",
+                       "l2": "flushed (256 MB write) between steps; maps alone exceed L2",
+                       "time_to_solution_ms": ms_per_step, "e2e_time_to_solution_ms": wall_s / args.steps * 1e3,
+                       "entry": "pint_run_heat_sharded (C ABI, host buffers)"},
+            "e2e": {"value": traj_steps_total / (wall_s / args.steps), "unit": UNIT,
+                    "h2d_bytes_per_step": int(rep.h2d_bytes), "d2h_bytes_per_step": int(rep.d2h_bytes)},
+            "parity": parity, "gpu_launches": int(rep.gpu_launches) * args.steps,
+            "roofline": {"bound": "fp64", "kernel": "heat build (rank 0's block, incl. tables + records)",
+                         "achieved": achieved, "peak": peak64.value, "unit": "TFLOP/s",
+                         "frac": achieved / peak64.value, "traffic": None, "launch_ms": build_ms,
+                         "compose_ms": comp_ms / args.steps},
+            "clocks": clocks.summary(t_region0, t_region1), "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    del keep
+    ctx.close()
+    dist.destroy_process_group()
+    return 0
 
 
 def heat_bench(args, rank, world, local):
@@ -527,8 +620,6 @@ def heat_bench(args, rank, world, local):
     from paper_1304_6514_b200.dist import HeatPlan, apply_chain, gather_maps, slice_block
 
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
     ctx = capi.Context(local, stream=stream)
     pint.set_context(ctx)
