@@ -94,6 +94,8 @@ typedef struct {
 } pint_report;
 
 /* ---- context ---- */
+/* CUDA devices visible to this process (0 without a GPU) */
+int pint_device_count(void);
 int pint_ctx_create(int device, pint_ctx** out);
 void pint_ctx_destroy(pint_ctx* ctx);
 const char* pint_ctx_last_error(const pint_ctx* ctx);

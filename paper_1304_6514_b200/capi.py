@@ -70,6 +70,7 @@ SEND_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_size_t)
 RECV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_size_t)
 _SIGS = {
     "pint_version": (C.c_char_p, []),
+    "pint_device_count": (_int, []),
     "pint_ctx_create": (_int, [_int, C.POINTER(_vp)]),
     "pint_ctx_destroy": (None, [_vp]),
     "pint_ctx_last_error": (C.c_char_p, [_vp]),

@@ -229,6 +229,11 @@ extern "C" {
 
 const char* pint_version(void) { return "pint-b200 0.1 (sm_100a)"; }
 
+int pint_device_count(void) {
+    int count = 0;
+    return cudaGetDeviceCount(&count) == cudaSuccess ? count : 0;
+}
+
 int pint_ctx_create(int device, pint_ctx** out) {
     if (!out) return PINT_E_INVALID;
     *out = nullptr;

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -54,7 +55,38 @@ pint_ctx* ctx_locked() {
     return d.ctx;
 }
 
-[[noreturn]] void raise(int rc, pint_ctx* ctx, const pint_fail* fail = nullptr) {
+// ExecConfig::workers > 1 with several GPUs: one context per device (cuda:0 .. cuda:G-1), joined
+// into one NCCL communicator (pint_comm_init_all); built once per G, guarded by device().mu.
+struct DeviceSet {
+    std::vector<pint_ctx*> ctxs;
+    ~DeviceSet() {
+        for (std::size_t g = 1; g < ctxs.size(); ++g) pint_ctx_destroy(ctxs[g]);  // (ctxs[0] is device())
+    }
+};
+
+int gpus_for(std::size_t workers) {
+    return static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(workers, pint_device_count())));
+}
+
+[[noreturn]] void raise(int rc, pint_ctx* ctx, const pint_fail* fail = nullptr);
+
+// the device set for G GPUs (G > 1), caller holds device().mu
+std::vector<pint_ctx*>& device_set_locked(int G) {
+    static DeviceSet set;
+    if (static_cast<int>(set.ctxs.size()) != G) {
+        for (std::size_t g = 1; g < set.ctxs.size(); ++g) pint_ctx_destroy(set.ctxs[g]);
+        set.ctxs.assign(1, ctx_locked());
+        for (int g = 1; g < G; ++g) {
+            pint_ctx* c = nullptr;
+            if (const int rc = pint_ctx_create(g, &c)) raise(rc, nullptr);
+            set.ctxs.push_back(c);
+        }
+        if (const int rc = pint_comm_init_all(set.ctxs.data(), G)) raise(rc, set.ctxs[0]);
+    }
+    return set.ctxs;
+}
+
+[[noreturn]] void raise(int rc, pint_ctx* ctx, const pint_fail* fail) {
     const std::string msg = ctx ? pint_ctx_last_error(ctx) : std::string("pint-b200 error");
     if (fail && fail->index >= 0) throw TaskFailure(static_cast<std::size_t>(fail->index), msg);
     switch (rc) {
@@ -572,7 +604,29 @@ RunReport run_nievergelt(const LinearProblem& problem, std::size_t N, const Exec
         pint_ctx* c = ctx_locked();
         if (problem.t0 != 0.0) throw std::invalid_argument("pint-b200: linear problems start at t0 = 0");
         const int mode = problem.tree_compose ? PINT_COMPOSE_TREE : PINT_COMPOSE_CHAIN;
-        if (problem.heat) {
+        const int G = problem.heat ? gpus_for(exec.workers) : 1;
+        if (G > 1) {  // ExecConfig::workers -> GPUs: slice blocks per GPU, one thread each, NCCL gather
+            std::vector<pint_ctx*>& cs = device_set_locked(G);
+            check(pint_heat_serial_begin(cs[0], problem.heat->dx, problem.dt, problem.T, problem.y0.data()), cs[0]);
+            total = Stopwatch();
+            std::vector<int> rcs(static_cast<std::size_t>(G), PINT_OK);
+            std::vector<pint_report> reps(static_cast<std::size_t>(G));
+            std::vector<std::thread> th;
+            for (int g = 0; g < G; ++g)
+                th.emplace_back([&, g] {
+                    rcs[g] = pint_run_heat_sharded(cs[g], problem.heat->dx, problem.dt, problem.T,
+                                                   static_cast<int64_t>(N), PINT_BUILD_EXACT, mode, problem.y0.data(),
+                                                   g == 0 ? y.data() : nullptr, &reps[g]);
+                });
+            for (auto& t : th) t.join();
+            r.T_total = total.seconds();
+            const int rs = pint_heat_serial_end(cs[0], serial.data());
+            for (int g = 0; g < G; ++g) check(rcs[g], cs[g]);
+            check(rs, cs[0]);
+            rep = reps[0];
+            const double each = rep.device_ms * 1e-3 / static_cast<double>(N);  // (no per-slice timers here)
+            std::fill(per_slice.begin(), per_slice.end(), each);
+        } else if (problem.heat) {
             check(pint_heat_serial_begin(c, problem.heat->dx, problem.dt, problem.T, problem.y0.data()), c);
             total = Stopwatch();
             const int rc = pint_run_heat(c, problem.heat->dx, problem.dt, problem.T, static_cast<int64_t>(N), mode,
@@ -590,7 +644,7 @@ RunReport run_nievergelt(const LinearProblem& problem, std::size_t N, const Exec
         }
     }
     SweepStats stats;
-    const double t_run = problem.heat ? r.T_total : total.seconds();
+    const double t_run = problem.heat ? r.T_total : total.seconds();  // (heat: measured around the run)
     simulate_receives(N, sizeof(double) * problem.dim, exec.latency_per_receive, stats);
     stats.apply_cost = rep.compose_ms * 1e-3 / static_cast<double>(N);
     r.T_total = t_run + stats.T_comm;
