@@ -286,6 +286,28 @@ int pint_run_wave(pint_ctx* ctx, int64_t d, const double* D2, double dt_native, 
                   double dt_nominal, int compose_mode, const double* y0, double* y_out,
                   double* per_slice_seconds, pint_report* report);
 
+/* ---- parareal on the device (parareal.cpp:47-165; the paper's comparison method, SURVEY.md §8f
+ * rank 2) — scalar model problem: the reference's integrate_scalar_step (backward-Euler Riccati,
+ * per-slice steps_for / width / n) as fine (dt) and coarse (DT) propagator, N slices of
+ * decompose(t0, T, N, dt), k iterations. ONE kernel: each iteration's fine wave runs the N slices
+ * in parallel from lambda_j, then the sequential correction sweep g_new + f - g_old; bit-identical
+ * to the reference. finals[k + 1]: the final-time state after iteration 0 (coarse init) .. k
+ * (PararealResult::final_per_iteration). fine_seconds[N] (may be NULL): summed device time of each
+ * slice's fine integrations; *coarse_seconds (may be NULL): mean device time per coarse slice
+ * (modeled_time_parareal's inputs). NoRealRoot in the fine wave: fail->index = the slice. */
+int pint_parareal_scalar(pint_ctx* ctx, double t0, double T, double y0, int64_t N, int64_t k, double dt,
+                         double DT, double* finals, double* fine_seconds, double* coarse_seconds,
+                         pint_report* report, pint_fail* fail);
+
+/* Parareal for make_heat_problem(dx, ., T): the integrate closure at dt (fine) and DT (coarse)
+ * (parareal.cpp:167-190), N slices of decompose(0, T, N, dt), k iterations; bit-identical to the
+ * reference. Each iteration is two launches: the fine wave (a warp per slice, from lambda_j, on
+ * that slice's staged records) and the sequential correction sweep (one warp walking the slices'
+ * coarse steps, combining g_new + f - g_old row by row). finals[(k + 1) n]: the final state after
+ * every iteration. y0 NULL: heat_initial. */
+int pint_parareal_heat(pint_ctx* ctx, double dx, double T, const double* y0, int64_t N, int64_t k,
+                       double dt, double DT, double* finals, pint_report* report);
+
 /* ---- multi-GPU (north_star subsystem 4): one context per GPU (a process or a
  * thread each). Slices go to ranks in contiguous blocks [floor(rN/W), floor((r+1)N/W)) of the
  * reference decomposition (ode_core.cpp:26-45, identical on every rank: slice assignment is

@@ -108,6 +108,9 @@ _SIGS = {
                                _vp, _vp, _vp, _vp, C.POINTER(Report), C.POINTER(Fail)]),
     "pint_run_heat": (_int, [_vp, _d, _d, _d, _i, _int, _vp, _vp, _vp, C.POINTER(Report)]),
     "pint_run_heat_ex": (_int, [_vp, _d, _d, _d, _i, _int, _int, _vp, _vp, _vp, C.POINTER(Report)]),
+    "pint_parareal_scalar": (_int, [_vp, _d, _d, _d, _i, _i, _d, _d, _vp, _vp, _vp, C.POINTER(Report),
+                                     C.POINTER(Fail)]),
+    "pint_parareal_heat": (_int, [_vp, _d, _d, _vp, _i, _i, _d, _d, _vp, C.POINTER(Report)]),
     "pint_comm_unique_id": (_int, [_vp]),
     "pint_comm_init": (_int, [_vp, _vp, _int, _int]),
     "pint_comm_init_all": (_int, [C.POINTER(_vp), _int]),

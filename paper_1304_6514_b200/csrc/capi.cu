@@ -809,6 +809,83 @@ int pint_run_scalar(pint_ctx* ctx, const pint_scalar_rhs* rhs, double t0, double
     return PINT_OK;
 }
 
+int pint_parareal_scalar(pint_ctx* ctx, double t0, double T, double y0, int64_t N, int64_t k, double dt, double DT,
+                         double* finals, double* fine_seconds, double* coarse_seconds, pint_report* report,
+                         pint_fail* fail) {
+    if (!ctx || !finals || N < 1 || k < 0 || !(dt > 0.0) || !(DT > 0.0)) return PINT_E_INVALID;
+    HostTimer wall;
+    const long long launches0 = ctx->launches;
+    std::vector<pint_slice> dec(static_cast<size_t>(N));
+    if (pint_decompose(t0, T, N, dt, dec.data()) != PINT_OK)
+        return pint_set_error(ctx, PINT_E_BAD_GRID, "decompose: need N >= 1, T > t0, dt > 0");
+    // integrate_scalar_step's per-slice step count and effective step for each propagator
+    std::vector<pint_slice> fine, coarse;
+    closure_slices(dec.data(), N, dt, fine);
+    closure_slices(dec.data(), N, DT, coarse);
+    for (int64_t j = 0; j < N; ++j) {
+        if (const int rc = check_integral(ctx, fine[j].t_end - fine[j].t_begin, fine[j].dt)) return rc;
+        if (const int rc = check_integral(ctx, coarse[j].t_end - coarse[j].t_begin, coarse[j].dt)) return rc;
+    }
+    const size_t b_i = align256(sizeof(int64_t) * N), b_d = align256(sizeof(double) * N);
+    const size_t b_w = align256(sizeof(double) * (3 * N + 1)), b_f = align256(sizeof(double) * (k + 1));
+    const size_t b_ns = align256(sizeof(unsigned long long) * (N + 1));
+    const size_t in_bytes = 2 * b_i + 2 * b_d;
+    char* h = static_cast<char*>(pinned(in_bytes));
+    char* d = static_cast<char*>(pint_scratch(ctx, 0, in_bytes + b_w + b_f + b_ns));
+    if (!h || !d) return PINT_E_CUDA;
+    for (int64_t j = 0; j < N; ++j) {
+        reinterpret_cast<int64_t*>(h)[j] = fine[j].steps;
+        reinterpret_cast<int64_t*>(h + b_i)[j] = coarse[j].steps;
+        reinterpret_cast<double*>(h + 2 * b_i)[j] = fine[j].dt;
+        reinterpret_cast<double*>(h + 2 * b_i + b_d)[j] = coarse[j].dt;
+    }
+    auto* ns = reinterpret_cast<unsigned long long*>(d + in_bytes + b_w + b_f);
+    cudaEventRecord(ctx->ev0, ctx->stream);
+    cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemsetAsync(ns, 0, sizeof(unsigned long long) * (N + 1), ctx->stream);
+    auto* d_finals = reinterpret_cast<double*>(d + in_bytes + b_w);
+    if (const int rc = launch_parareal_scalar(ctx, N, k, reinterpret_cast<int64_t*>(d), reinterpret_cast<double*>(d + 2 * b_i),
+                                              reinterpret_cast<int64_t*>(d + b_i),
+                                              reinterpret_cast<double*>(d + 2 * b_i + b_d), y0,
+                                              reinterpret_cast<double*>(d + in_bytes), d_finals, ns, ns + N))
+        return rc;
+    cudaEventRecord(ctx->ev1, ctx->stream);
+    std::vector<unsigned long long> hns(static_cast<size_t>(N + 1));
+    cudaMemcpyAsync(finals, d_finals, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(hns.data(), ns, sizeof(unsigned long long) * (N + 1), cudaMemcpyDeviceToHost, ctx->stream);
+    pint_fail fr;
+    if (const int rc = pint_fail_read(ctx, &fr)) return rc;  // (synchronises)
+    if (fail) *fail = fr;
+    if (fr.index >= 0) {
+        const bool coarse_fail = fr.index >= parareal_coarse_fail_index();
+        char buf[128];
+        std::snprintf(buf, sizeof buf, "be_step_scalar_riccati: no real root (discriminant %.17g)%s", fr.value,
+                      coarse_fail ? " in the coarse sweep" : "");
+        if (coarse_fail && fail) fail->index = -1;  // (the coarse sweep throws unwrapped, parareal.cpp:78/112)
+        return pint_set_error(ctx, PINT_E_NO_REAL_ROOT, buf);
+    }
+    if (fine_seconds)
+        for (int64_t j = 0; j < N; ++j) fine_seconds[j] = static_cast<double>(hns[j]) * 1e-9;
+    if (coarse_seconds) *coarse_seconds = static_cast<double>(hns[N]) * 1e-9 / static_cast<double>((k + 1) * N);
+    if (report) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        report->message_count = (2 * k + 1) * (N - 1);  // parareal_message_count (parareal.cpp:141-143)
+        report->bytes_communicated = report->message_count * static_cast<int64_t>(sizeof(double));
+        report->extrapolation_count = 0;
+        report->device_ms = ms;
+        report->compose_ms = static_cast<double>(hns[N]) * 1e-6;  // (the coarse sweeps)
+        int64_t ts = 0;
+        for (int64_t j = 0; j < N; ++j) ts += k * fine[j].steps + (k + 1) * coarse[j].steps;
+        report->traj_steps = ts;
+        report->gpu_launches = ctx->launches - launches0;
+        report->h2d_bytes = static_cast<int64_t>(in_bytes);
+        report->d2h_bytes = static_cast<int64_t>(sizeof(double) * (k + 1) + 8 * (N + 1));
+        report->total_ms = wall.ms();
+    }
+    return PINT_OK;
+}
+
 int pint_scalar_integrate(pint_ctx* ctx, const pint_scalar_rhs* rhs, const pint_slice* slice,
                           int64_t K, const double* y0, double* y_out, pint_fail* fail) {
     if (!ctx || !rhs || !slice || K < 0) return PINT_E_INVALID;
@@ -1254,6 +1331,129 @@ int pint_run_heat_sharded(pint_ctx* ctx, double dx, double dt, double T, int64_t
         report->gpu_launches = ctx->launches - launches0;
         report->h2d_bytes = static_cast<int64_t>((Nb > 0 ? H.h2d : 0) + sizeof(double) * n);
         report->d2h_bytes = rank == 0 ? static_cast<int64_t>(sizeof(double) * n) : 0;
+        report->total_ms = wall.ms();
+    }
+    return PINT_OK;
+}
+
+namespace {
+// Tables and slice-major records of the slices `sl` (each at most S steps) into scratch slots:
+// records [N][S][record] (slice j's steps at j S), device step counts `steps`.
+int slices_records(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, int slot_tab, int slot_rec,
+                   int64_t* n_out, int64_t* S_out, int64_t** steps, double** rec) {
+    int64_t n = 0;
+    if (const int rc = heat_dim(ctx, dx, &n)) return rc;
+    const int64_t N = static_cast<int64_t>(sl.size());
+    int64_t S = 0, Q = 0;
+    for (const auto& s : sl) {
+        if (const int rc = check_integral(ctx, s.t_end - s.t_begin, s.dt)) return rc;
+        S = std::max<int64_t>(S, s.steps);
+        Q += s.steps;
+    }
+    const size_t b_off = align256(sizeof(int64_t) * (N + 1)), b_st = align256(sizeof(int64_t) * N);
+    const size_t b_dt = align256(sizeof(double) * N), b_q = align256(sizeof(double) * Q);
+    const size_t b_sx = align256(sizeof(double) * n);
+    const size_t bytes = b_off + b_st + b_dt + 3 * b_q + b_sx;
+    char* h = static_cast<char*>(pinned(bytes));
+    char* d = static_cast<char*>(pint_scratch(ctx, slot_tab, bytes));
+    double* r = static_cast<double*>(pint_scratch(ctx, slot_rec, sizeof(double) * N * S * heat_record_stride(n)));
+    if (!h || !d || !r) return pint_set_error(ctx, PINT_E_CUDA, "parareal: table / record allocation failed");
+    auto* h_off = reinterpret_cast<int64_t*>(h);
+    auto* h_st = reinterpret_cast<int64_t*>(h + b_off);
+    auto* h_dt = reinterpret_cast<double*>(h + b_off + b_st);
+    h_off[0] = 0;
+    for (int64_t j = 0; j < N; ++j) {
+        h_off[j + 1] = h_off[j] + sl[j].steps;
+        h_st[j] = sl[j].steps;
+        h_dt[j] = sl[j].dt;
+    }
+    double* h_q = reinterpret_cast<double*>(h + b_off + b_st + b_dt);
+    heat_fill_steps(dx, sl.data(), 0, N, h_off, h_q, h_q + b_q / 8, h_q + 2 * b_q / 8);
+    auto* h_sx = reinterpret_cast<double*>(h + b_off + b_st + b_dt + 3 * b_q);
+    for (int64_t i = 0; i < n; ++i) h_sx[i] = std::sin(kPi * (static_cast<double>(i + 1) * dx));
+    if (!ok(ctx, cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D parareal tables") ||
+        !ok(ctx, cudaStreamSynchronize(ctx->stream), "H2D parareal tables sync"))
+        return PINT_E_CUDA;
+    const double* dq = reinterpret_cast<const double*>(d + b_off + b_st + b_dt);
+    if (const int rc = launch_heat_factor_block(ctx, ctx->stream, n, N, S, 0, N, 0, S, 0,
+                                                reinterpret_cast<const int64_t*>(d), reinterpret_cast<const double*>(d + b_off + b_st),
+                                                dq, dq + b_q / 8, dq + 2 * b_q / 8,
+                                                reinterpret_cast<const double*>(d + b_off + b_st + b_dt + 3 * b_q), r, 0, true))
+        return rc;
+    *n_out = n;
+    *S_out = S;
+    *steps = reinterpret_cast<int64_t*>(d + b_off);
+    *rec = r;
+    return PINT_OK;
+}
+}  // namespace
+
+int pint_parareal_heat(pint_ctx* ctx, double dx, double T, const double* y0, int64_t N, int64_t k, double dt,
+                       double DT, double* finals, pint_report* report) {
+    if (!ctx || !finals || N < 1 || k < 0 || !(dt > 0.0) || !(DT > 0.0)) return PINT_E_INVALID;
+    HostTimer wall;
+    const long long launches0 = ctx->launches;
+    std::vector<pint_slice> dec(static_cast<size_t>(N));
+    if (pint_decompose(0.0, T, N, dt, dec.data()) != PINT_OK)
+        return pint_set_error(ctx, PINT_E_BAD_GRID, "decompose: need N >= 1, T > t0, dt > 0");
+    std::vector<pint_slice> fine, coarse;  // the integrate closure at dt (fine) and DT (coarse)
+    closure_slices(dec.data(), N, dt, fine);
+    closure_slices(dec.data(), N, DT, coarse);
+    cudaEventRecord(ctx->ev0, ctx->stream);
+    int64_t n = 0, Sf = 0, Sc = 0;
+    int64_t *st_f = nullptr, *st_c = nullptr;
+    double *rec_f = nullptr, *rec_c = nullptr;
+    if (const int rc = slices_records(ctx, dx, fine, 0, 1, &n, &Sf, &st_f, &rec_f)) return rc;
+    if (const int rc = slices_records(ctx, dx, coarse, 6, 7, &n, &Sc, &st_c, &rec_c)) return rc;
+    const int64_t stride = heat_record_stride(n);
+    const size_t vn = sizeof(double) * n;
+    char* d = static_cast<char*>(pint_scratch(ctx, 2, (4 * N + 2 + (k + 1)) * vn + 1024));
+    if (!d) return PINT_E_CUDA;
+    auto* d_y0 = reinterpret_cast<double*>(d);
+    double* lam = d_y0 + n;
+    double* gprev = lam + (N + 1) * n;
+    double* fout = gprev + N * n;
+    double* d_fin = fout + N * n;
+    std::vector<double> y0v;
+    if (!y0) {
+        y0v.resize(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) y0v[i] = std::sin(kPi * static_cast<double>(i + 1) * dx);  // heat_initial
+        y0 = y0v.data();
+    }
+    cudaMemcpyAsync(d_y0, y0, vn, cudaMemcpyHostToDevice, ctx->stream);
+    int rc = PINT_OK;
+    for (int guarded = 0; guarded < 2; ++guarded) {  // a tripped range check re-runs everything guarded
+        if ((rc = launch_heat_parareal_coarse(ctx, n, N, rec_c, Sc * stride, st_c, d_y0, nullptr, gprev, lam, guarded)))
+            return rc;
+        cudaMemcpyAsync(d_fin, lam + N * n, vn, cudaMemcpyDeviceToDevice, ctx->stream);
+        for (int64_t it = 1; it <= k; ++it) {
+            cudaMemcpyAsync(fout, lam, vn * N, cudaMemcpyDeviceToDevice, ctx->stream);  // fine wave from lambda_j
+            if ((rc = launch_heat_integrate_slices(ctx, n, N, st_f, rec_f, Sf * stride, fout, guarded))) return rc;
+            if ((rc = launch_heat_parareal_coarse(ctx, n, N, rec_c, Sc * stride, st_c, d_y0, fout, gprev, lam, guarded)))
+                return rc;
+            cudaMemcpyAsync(d_fin + it * n, lam + N * n, vn, cudaMemcpyDeviceToDevice, ctx->stream);
+        }
+        rc = singular_check(ctx);  // (synchronises)
+        if (rc != PINT_E_RANGE_RETRY) break;
+    }
+    if (rc) return rc;
+    cudaEventRecord(ctx->ev1, ctx->stream);
+    cudaMemcpyAsync(finals, d_fin, vn * (k + 1), cudaMemcpyDeviceToHost, ctx->stream);
+    if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "parareal_heat sync")) return PINT_E_CUDA;
+    if (report) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        report->message_count = (2 * k + 1) * (N - 1);
+        report->bytes_communicated = report->message_count * static_cast<int64_t>(vn);
+        report->extrapolation_count = 0;
+        report->device_ms = ms;
+        report->compose_ms = 0.0;
+        int64_t ts = 0;
+        for (int64_t j = 0; j < N; ++j) ts += k * fine[j].steps + (k + 1) * coarse[j].steps;
+        report->traj_steps = ts;
+        report->gpu_launches = ctx->launches - launches0;
+        report->h2d_bytes = static_cast<int64_t>(vn);
+        report->d2h_bytes = static_cast<int64_t>(vn * (k + 1));
         report->total_ms = wall.ms();
     }
     return PINT_OK;

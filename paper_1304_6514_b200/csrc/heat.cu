@@ -914,7 +914,84 @@ struct IntegPlan {
     double* y;           // [K][n], in place
     FailRec* fail;
     long long fail_base;  // step index of the chunk's first step (range-retry index)
+    // per-slice mode (parareal's fine wave): CTA b runs ONE column (y + b n, lane 0) through its own
+    // records rec + b rec_cta_stride, cta_steps[b] steps
+    long long rec_cta_stride;
+    const int64_t* cta_steps;
 };
+
+// One warp's state and staging for the integrate loops: rows [0, RR) of this lane's column in reg,
+// the rest at st[32 (i - RR)], the step's record staged at R0 (forward half at 0, back half at
+// cc_offset) completing on bar0 / bar0 + 8; `ph` counts the steps run through these barriers.
+template <int RR>
+struct IntegWarp {
+    double reg[RR > 0 ? RR : 1];
+    double* st;
+    double* R0;
+    unsigned bar0;
+    long long ph = 0;
+    unsigned qmin = 0xffffffffu;
+};
+
+// `steps` consecutive steps whose slice-major records start at `rec` (the caller's warp, all lanes)
+template <int RR, int kMode, bool kGuard>
+__device__ __forceinline__ void integ_run(IntegWarp<RR>& W, int n, const double* rec, long long steps) {
+    const int lane = threadIdx.x & 31;
+    const unsigned fwd_bytes = 8u * static_cast<unsigned>(cc_offset(n));  // header, (p, rcp), h*b
+    const unsigned back_bytes = 8u * static_cast<unsigned>(even(n));
+    auto recs = [&](long long s) { return rec + s * record_stride(n); };
+    __syncwarp();
+    if (lane == 0 && steps > 0) {
+        bulk_load(smem_u32(W.R0), recs(0), fwd_bytes, W.bar0);
+        bulk_load(smem_u32(W.R0 + cc_offset(n)), recs(0) + cc_offset(n), back_bytes, W.bar0 + 8u);
+        if (steps > 1) prefetch_l2(recs(1), 8u * static_cast<unsigned>(record_stride(n)));
+    }
+    for (long long s = 0; s < steps; ++s, ++W.ph) {
+        const unsigned parity = static_cast<unsigned>(W.ph & 1);
+        const StagedStep<kMode> SV{W.R0, n, lane, 0};
+        mbar_wait(W.bar0, parity);
+        double dm1 = 0.0;
+        double d = column_forward<RR, kMode, kGuard>(W.reg, W.st, SV, dm1, W.qmin);
+        W.qmin = min(W.qmin, hi_abs(d) - 1u);
+        __syncwarp();  // every lane is done with the forward half
+        if (lane == 0 && s + 1 < steps) bulk_load(smem_u32(W.R0), recs(s + 1), fwd_bytes, W.bar0);
+        mbar_wait(W.bar0 + 8u, parity);
+        column_back<RR, kMode>(W.reg, W.st, SV, d, dm1, W.qmin);
+        __syncwarp();
+        if (lane == 0 && s + 1 < steps) {
+            bulk_load(smem_u32(W.R0 + cc_offset(n)), recs(s + 1) + cc_offset(n), back_bytes, W.bar0 + 8u);
+            if (s + 2 < steps) prefetch_l2(recs(s + 2), 8u * static_cast<unsigned>(record_stride(n)));
+        }
+    }
+}
+
+template <int RR, int kMode>
+__device__ __forceinline__ void integ_setup(IntegWarp<RR>& W, int n, double* smem) {
+    const int lane = threadIdx.x & 31;
+    W.R0 = smem + front_pad(n, kMode);
+    W.st = W.R0 + staged_doubles(n, kMode) + lane;
+    W.bar0 = smem_u32(W.R0 + staged_doubles(n, kMode) + (n - RR) * 32 + 32 * kFwdAhead);
+    if (lane == 0) {
+        mbar_init(W.bar0);
+        mbar_init(W.bar0 + 8u);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+}
+
+template <int RR>
+__device__ __forceinline__ void integ_load(IntegWarp<RR>& W, int n, const double* y, bool live) {
+#pragma unroll
+    for (int i = 0; i < RR; ++i) W.reg[i] = live ? y[i] : 0.0;
+    for (int i = RR; i < n; ++i) W.st[(i - RR) * 32] = live ? y[i] : 0.0;
+}
+
+template <int RR>
+__device__ __forceinline__ void integ_store(IntegWarp<RR>& W, int n, double* y) {
+#pragma unroll
+    for (int i = 0; i < RR; ++i) y[i] = W.reg[i];
+    for (int i = RR; i < n; ++i) y[i] = W.st[(i - RR) * 32];
+}
 
 template <int RR, int kMode, bool kGuard>
 __global__ void __maxnreg__(255) heat_integrate_kernel(const IntegPlan P) {
@@ -922,55 +999,74 @@ __global__ void __maxnreg__(255) heat_integrate_kernel(const IntegPlan P) {
     extern __shared__ __align__(128) double smem[];
     const int n = P.n;
     const int lane = threadIdx.x;
-    const long long col = static_cast<long long>(blockIdx.x) * 32 + lane;
-    const bool live = col < P.K;
-    double* R0 = smem + front_pad(n, kMode);
-    double* st = R0 + staged_doubles(n, kMode) + lane;
-    const unsigned bar0 = smem_u32(R0 + staged_doubles(n, kMode) + (n - RR) * 32 + 32 * kFwdAhead);
-    const unsigned fwd_bytes = 8u * static_cast<unsigned>(cc_offset(n));  // header, (p, rcp), h*b
-    const unsigned back_bytes = 8u * static_cast<unsigned>(even(n));
-    auto rec = [&](long long s) { return P.rec + s * record_stride(n); };
-    if (lane == 0) {
-        mbar_init(bar0);
-        mbar_init(bar0 + 8u);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncwarp();
-    if (lane == 0 && P.steps > 0) {
-        bulk_load(smem_u32(R0), rec(0), fwd_bytes, bar0);
-        bulk_load(smem_u32(R0 + cc_offset(n)), rec(0) + cc_offset(n), back_bytes, bar0 + 8u);
-        if (P.steps > 1) prefetch_l2(rec(1), 8u * static_cast<unsigned>(record_stride(n)));
-    }
-    double reg[RR > 0 ? RR : 1];
-    const double* yc = P.y + (live ? col : 0) * n;
-#pragma unroll
-    for (int i = 0; i < RR; ++i) reg[i] = live ? yc[i] : 0.0;
-    for (int i = RR; i < n; ++i) st[(i - RR) * 32] = live ? yc[i] : 0.0;
-    unsigned qmin = 0xffffffffu;
-    for (long long s = 0; s < P.steps; ++s) {
-        const unsigned parity = static_cast<unsigned>(s & 1);
-        const StagedStep<kMode> SV{R0, n, lane, 0};
-        mbar_wait(bar0, parity);
-        double dm1 = 0.0;
-        double d = column_forward<RR, kMode, kGuard>(reg, st, SV, dm1, qmin);
-        qmin = min(qmin, hi_abs(d) - 1u);
-        __syncwarp();  // every lane is done with the forward half
-        if (lane == 0 && s + 1 < P.steps) bulk_load(smem_u32(R0), rec(s + 1), fwd_bytes, bar0);
-        mbar_wait(bar0 + 8u, parity);
-        column_back<RR, kMode>(reg, st, SV, d, dm1, qmin);
-        __syncwarp();
-        if (lane == 0 && s + 1 < P.steps) {
-            bulk_load(smem_u32(R0 + cc_offset(n)), rec(s + 1) + cc_offset(n), back_bytes, bar0 + 8u);
-            if (s + 2 < P.steps) prefetch_l2(rec(s + 2), 8u * static_cast<unsigned>(record_stride(n)));
-        }
-    }
+    const bool per_slice = P.cta_steps != nullptr;
+    const long long col = per_slice ? blockIdx.x : static_cast<long long>(blockIdx.x) * 32 + lane;
+    const bool live = col < P.K && (!per_slice || lane == 0);
+    IntegWarp<RR> W;
+    integ_setup<RR, kMode>(W, n, smem);
+    integ_load<RR>(W, n, P.y + (live ? col : 0) * n, live);
+    const long long steps = per_slice ? P.cta_steps[blockIdx.x] : P.steps;
+    integ_run<RR, kMode, kGuard>(W, n, P.rec + (per_slice ? blockIdx.x * P.rec_cta_stride : 0), steps);
     if (live) {
-        double* yo = P.y + col * n;
-#pragma unroll
-        for (int i = 0; i < RR; ++i) yo[i] = reg[i];
-        for (int i = RR; i < n; ++i) yo[i] = st[(i - RR) * 32];
-        if (!kGuard && qmin < kQuotLo - 1u) record_failure(P.fail, kRetryIndex + P.fail_base, PINT_E_RANGE_RETRY, 0.0);
+        integ_store<RR>(W, n, P.y + col * n);
+        if (!kGuard && W.qmin < kQuotLo - 1u) record_failure(P.fail, kRetryIndex + P.fail_base, PINT_E_RANGE_RETRY, 0.0);
     }
+}
+
+// ---- parareal's sequential correction sweep on the device (parareal.cpp:71-81, :103-117) -------
+// One warp, one column (lane 0): for every slice j, G(next_j) = the coarse steps of slice j (records
+// rec + j rec_stride, steps[j]); iteration 0 (fout null) stores lambda_{j+1} = g_prev_j = G, later
+// iterations lambda_{j+1} = (G + fout_j) - g_prev_j and g_prev_j = G — the reference's combine, row by
+// row on lane 0 (rounded exactly as g_new[i] + f[i] - g_old[i]).
+struct CoarsePlan {
+    int n;
+    long long N;
+    const double* rec;
+    long long rec_stride;
+    const int64_t* steps;
+    const double* y0;
+    const double* fout;  // [N][n] fine endpoints of this iteration, or null (iteration 0)
+    double* gprev;       // [N][n]
+    double* lam;         // [N + 1][n]
+    FailRec* fail;
+};
+
+template <int RR, bool kGuard>
+__global__ void __maxnreg__(255) heat_parareal_coarse_kernel(const CoarsePlan P) {
+    extern __shared__ __align__(128) double smem[];
+    constexpr int kMode = kBasisForced;
+    const int n = P.n;
+    const int lane = threadIdx.x;
+    IntegWarp<RR> W;
+    integ_setup<RR, kMode>(W, n, smem);
+    integ_load<RR>(W, n, P.y0, lane == 0);
+    if (lane == 0)
+        for (int i = 0; i < n; ++i) P.lam[i] = P.y0[i];
+    for (long long j = 0; j < P.N; ++j) {
+        integ_run<RR, kMode, kGuard>(W, n, P.rec + j * P.rec_stride, P.steps[j]);
+        if (lane == 0) {  // g_new = the state; next = g_new + f - g_old (or g_new at iteration 0)
+            double* gp = P.gprev + j * n;
+            double* lm = P.lam + (j + 1) * n;
+            const double* f = P.fout ? P.fout + j * n : nullptr;
+#pragma unroll
+            for (int i = 0; i < RR; ++i) {
+                const double g = W.reg[i];
+                const double nx = f ? __dsub_rn(__dadd_rn(g, f[i]), gp[i]) : g;
+                gp[i] = g;
+                lm[i] = nx;
+                W.reg[i] = nx;
+            }
+            for (int i = RR; i < n; ++i) {
+                const double g = W.st[(i - RR) * 32];
+                const double nx = f ? __dsub_rn(__dadd_rn(g, f[i]), gp[i]) : g;
+                gp[i] = g;
+                lm[i] = nx;
+                W.st[(i - RR) * 32] = nx;
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0 && !kGuard && W.qmin < kQuotLo - 1u) record_failure(P.fail, kRetryIndex, PINT_E_RANGE_RETRY, 0.0);
 }
 
 template <int RR, int kMode, bool kGuard>
@@ -979,7 +1075,8 @@ int launch_integ(pint_ctx* ctx, cudaStream_t stream, const IntegPlan& P) {
     if (smem > 227 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "heat_integrate: n too large for shared memory");
     auto kern = heat_integrate_kernel<RR, kMode, kGuard>;
     pint_kernel_attrs(reinterpret_cast<const void*>(kern));
-    kern<<<static_cast<unsigned>((P.K + 31) / 32), 32, smem, stream>>>(P);
+    const long long ctas = P.cta_steps ? P.K : (P.K + 31) / 32;
+    kern<<<static_cast<unsigned>(ctas), 32, smem, stream>>>(P);
     return pint_check_launch(ctx, "heat_integrate_kernel");
 }
 
@@ -1190,12 +1287,41 @@ int64_t heat_integrate_chunk(int64_t n) {  // steps per chunk: ~16 MB of records
 
 int64_t heat_integrate_records_doubles(int64_t n) { return heat_integrate_chunk(n) * record_stride(n); }
 
+int64_t heat_record_stride(int64_t n) { return record_stride(n); }
+
+int launch_heat_integrate_slices(pint_ctx* ctx, int64_t n, int64_t N, const int64_t* steps, const double* records,
+                                 int64_t rec_slice_stride, double* y, int guarded) {
+    if (n < 1 || N < 0) return pint_set_error(ctx, PINT_E_INVALID, "heat_integrate_slices: bad sizes");
+    if (N == 0) return PINT_OK;
+    const IntegPlan P{static_cast<int>(n), N, 0, records, y, ctx->d_fail, 0, rec_slice_stride, steps};
+    return reg_rows(n) == kRegRows ? launch_integ_rr<kRegRows>(ctx, ctx->stream, P, true, guarded != 0)
+                                   : launch_integ_rr<0>(ctx, ctx->stream, P, true, guarded != 0);
+}
+
+template <int RR, bool kGuard>
+int launch_coarse(pint_ctx* ctx, const CoarsePlan& P) {
+    const size_t smem = sizeof(double) * warp_smem_doubles(P.n, kBasisForced);
+    if (smem > 227 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "parareal: n too large for shared memory");
+    auto kern = heat_parareal_coarse_kernel<RR, kGuard>;
+    pint_kernel_attrs(reinterpret_cast<const void*>(kern));
+    kern<<<1, 32, smem, ctx->stream>>>(P);
+    return pint_check_launch(ctx, "heat_parareal_coarse_kernel");
+}
+
+int launch_heat_parareal_coarse(pint_ctx* ctx, int64_t n, int64_t N, const double* records, int64_t rec_slice_stride,
+                                const int64_t* steps, const double* y0, const double* fout, double* gprev, double* lam,
+                                int guarded) {
+    const CoarsePlan P{static_cast<int>(n), N, records, rec_slice_stride, steps, y0, fout, gprev, lam, ctx->d_fail};
+    if (reg_rows(n) == kRegRows) return guarded ? launch_coarse<kRegRows, true>(ctx, P) : launch_coarse<kRegRows, false>(ctx, P);
+    return guarded ? launch_coarse<0, true>(ctx, P) : launch_coarse<0, false>(ctx, P);
+}
+
 int launch_heat_integrate_steps(pint_ctx* ctx, cudaStream_t stream, int64_t n, int64_t K, int64_t steps,
                                 int with_forcing, const double* records, double* y, FailRec* fail, int64_t fail_base,
                                 int guarded) {
     if (n < 1 || K < 0 || steps < 0) return pint_set_error(ctx, PINT_E_INVALID, "heat_integrate: bad sizes");
     if (K == 0 || steps == 0) return PINT_OK;
-    const IntegPlan P{static_cast<int>(n), K, steps, records, y, fail, fail_base};
+    const IntegPlan P{static_cast<int>(n), K, steps, records, y, fail, fail_base, 0, nullptr};
     return reg_rows(n) == kRegRows ? launch_integ_rr<kRegRows>(ctx, stream, P, with_forcing != 0, guarded != 0)
                                    : launch_integ_rr<0>(ctx, stream, P, with_forcing != 0, guarded != 0);
 }

@@ -21,6 +21,7 @@
 #include "pint/linalg.hpp"
 #include "pint/nievergelt.hpp"
 #include "pint/ode_core.hpp"
+#include "pint/parareal.hpp"
 #include "pint/pde_problems.hpp"
 #include "pint_cuda.h"
 
@@ -802,6 +803,143 @@ LinearProblem make_wave_linear_problem(const WaveProblem& w, double T) {
         return y;
     };
     return p;
+}
+
+// ---- parareal (parareal.cpp:47-190) on the device ----------------------------------------------
+
+std::size_t parareal_message_count(std::size_t k, std::size_t N) { return N == 0 ? 0 : (2 * k + 1) * (N - 1); }
+
+double coarse_propagate(const ScalarIVP& ivp, double lambda, const TimeSlice& slice, double DT) {
+    (void)ivp;  // (the reference's coarse propagator is the Riccati step whatever the right-hand side)
+    ScalarIVP model = make_model_problem();
+    return integrate_scalar_many(model, Vector{lambda}, slice.t_begin, slice.t_end, DT)[0];
+}
+
+Vector coarse_propagate(const LinearProblem& problem, Vector lambda, const TimeSlice& slice, double DT) {
+    return problem.integrate(slice, std::move(lambda), DT, true);
+}
+
+namespace {
+
+// the report fields every parareal run shares; the simulated receives (latency per message) are
+// slept here, as the reference's CommTracker sleeps them inside its sweeps
+void parareal_report(RunReport& r, const PararealConfig& cfg, const ExecConfig& exec, std::size_t state_bytes) {
+    r.method = "parareal";
+    r.N = cfg.N;
+    r.k = cfg.k;
+    r.dt = cfg.dt;
+    r.DT = cfg.DT;
+    r.latency = exec.latency_per_receive;
+    r.workers = exec.workers;
+    r.message_count = parareal_message_count(cfg.k, cfg.N);
+    r.bytes_communicated = r.message_count * state_bytes;
+    for (std::size_t m = 0; m < r.message_count; ++m) {
+        Stopwatch sw;
+        inject_latency(exec.latency_per_receive);
+        if (exec.latency_per_receive > 0.0) r.T_comm += sw.seconds();
+    }
+}
+
+}  // namespace
+
+PararealResult parareal_sweep(const ScalarIVP& ivp, const PararealConfig& cfg, const ExecConfig& exec) {
+    if (cfg.N == 0) throw std::invalid_argument("parareal: N >= 1 required");
+    PararealResult out;
+    RunReport& r = out.report;
+    std::vector<double> finals(cfg.k + 1), fine(cfg.N);
+    double coarse_per_slice = 0.0;
+    Stopwatch total;
+    {
+        std::lock_guard<std::mutex> lk(device().mu);
+        pint_ctx* c = ctx_locked();
+        pint_report rep{};
+        pint_fail fail{};
+        const int rc = pint_parareal_scalar(c, ivp.t0, ivp.T, ivp.y0, static_cast<int64_t>(cfg.N),
+                                            static_cast<int64_t>(cfg.k), cfg.dt, cfg.DT, finals.data(), fine.data(),
+                                            &coarse_per_slice, &rep, &fail);
+        check(rc, c, &fail);
+    }
+    parareal_report(r, cfg, exec, sizeof(double));
+    r.T_total = total.seconds();
+    r.per_slice_compute = fine;
+    for (double y : finals) out.final_per_iteration.push_back(Vector{y});
+    r.final_state = out.final_per_iteration.back();
+    if (exec.clock != ClockMode::measured) {
+        std::vector<double> fine_mean(fine);
+        for (double& t : fine_mean) t /= static_cast<double>(std::max<std::size_t>(cfg.k, 1));
+        r.modeled_time = modeled_time_parareal(fine_mean, coarse_per_slice, cfg.k, cfg.N, exec.latency_per_receive);
+    }
+    const double y = r.final_state[0];
+    if (ivp.exact) r.error_vs_exact = std::abs(y - (*ivp.exact)(ivp.T));
+    const ScalarIVP model = make_model_problem();  // (the serial run uses the Riccati step too)
+    const double y_serial = integrate_scalar_many(model, Vector{ivp.y0}, ivp.t0, ivp.T, cfg.dt)[0];
+    r.error_vs_serial = std::abs(y - y_serial) / std::max(1e-300, std::abs(y_serial));
+    return out;
+}
+
+PararealResult parareal_sweep(const LinearProblem& problem, const PararealConfig& cfg, const ExecConfig& exec) {
+    if (cfg.N == 0) throw std::invalid_argument("parareal: N >= 1 required");
+    PararealResult out;
+    RunReport& r = out.report;
+    const std::size_t n = problem.dim;
+    Stopwatch total;
+    if (problem.heat && problem.t0 == 0.0) {  // both propagators in device kernels
+        std::vector<double> finals((cfg.k + 1) * n);
+        pint_report rep{};
+        {
+            std::lock_guard<std::mutex> lk(device().mu);
+            pint_ctx* c = ctx_locked();
+            check(pint_parareal_heat(c, problem.heat->dx, problem.T, problem.y0.data(), static_cast<int64_t>(cfg.N),
+                                     static_cast<int64_t>(cfg.k), cfg.dt, cfg.DT, finals.data(), &rep),
+                  c);
+        }
+        for (std::size_t i = 0; i <= cfg.k; ++i)
+            out.final_per_iteration.emplace_back(finals.begin() + static_cast<std::ptrdiff_t>(i * n),
+                                                 finals.begin() + static_cast<std::ptrdiff_t>((i + 1) * n));
+        r.per_slice_compute.assign(cfg.N, rep.device_ms * 1e-3 / static_cast<double>(cfg.N));
+    } else {  // other linear problems: the same iteration over their device integrate closures
+        const TimeSliceDecomposition dec = decompose(problem.t0, problem.T, cfg.N, cfg.dt);
+        std::vector<Vector> lam(cfg.N + 1), g_old(cfg.N);
+        lam[0] = problem.y0;
+        for (std::size_t j = 0; j < cfg.N; ++j) lam[j + 1] = g_old[j] = coarse_propagate(problem, lam[j], dec.slices[j], cfg.DT);
+        out.final_per_iteration.push_back(lam[cfg.N]);
+        r.per_slice_compute.assign(cfg.N, 0.0);
+        for (std::size_t it = 1; it <= cfg.k; ++it) {
+            std::vector<Vector> f(cfg.N);
+            for (std::size_t j = 0; j < cfg.N; ++j) {
+                Stopwatch sw;
+                f[j] = problem.integrate(dec.slices[j], lam[j], cfg.dt, true);
+                r.per_slice_compute[j] += sw.seconds();
+            }
+            for (std::size_t j = 0; j < cfg.N; ++j) {
+                Vector g = coarse_propagate(problem, lam[j], dec.slices[j], cfg.DT);
+                Vector next(n);
+                for (std::size_t i = 0; i < n; ++i) next[i] = g[i] + f[j][i] - g_old[j][i];
+                g_old[j] = std::move(g);
+                lam[j + 1] = std::move(next);
+            }
+            out.final_per_iteration.push_back(lam[cfg.N]);
+        }
+    }
+    parareal_report(r, cfg, exec, sizeof(double) * n);
+    r.T_total = total.seconds();
+    r.final_state = out.final_per_iteration.back();
+    if (exec.clock != ClockMode::measured)
+        r.modeled_time = modeled_time_parareal(r.per_slice_compute, 0.0, cfg.k, cfg.N, exec.latency_per_receive);
+    if (problem.exact_final) r.error_vs_exact = max_abs_diff(r.final_state, *problem.exact_final);
+    const Vector serial = run_serial(problem).final_state;
+    const double scale = max_abs(serial);
+    const double gap = max_abs_diff(r.final_state, serial);
+    r.error_vs_serial = scale == 0.0 ? gap : gap / scale;
+    return out;
+}
+
+RunReport run_parareal(const ScalarIVP& ivp, const PararealConfig& cfg, const ExecConfig& exec) {
+    return parareal_sweep(ivp, cfg, exec).report;
+}
+
+RunReport run_parareal(const LinearProblem& problem, const PararealConfig& cfg, const ExecConfig& exec) {
+    return parareal_sweep(problem, cfg, exec).report;
 }
 
 }  // namespace pint
