@@ -47,9 +47,12 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kScanTab = 64;
 __host__ __device__ constexpr long long fast_blk(long long NP) { return 4 * NP + 2 * kScanTab; }
 
-// Partition shape for n: the fewest partitions (a power of two) with R <= 48 rows each (64 rows
-// of state plus the coefficient pipeline overflow the 255 registers), R in {32, 48} so that
-// NP = P R is a multiple of 32 (the record kernel's lanes); P = 1 only with R = 32.
+// Partition shape for n: R rows per partition, P (a power of two <= 16) partitions per column,
+// C = 64 / R columns per thread (64 rows of state in registers: 128 of the 255), so that NP = P R
+// is a multiple of 32 (the record kernel's lanes). Shorter partitions give each thread more
+// independent chains and amortise every coefficient load over more columns (C), at the price of a
+// deeper carry scan: R = 16 (C = 4) up to n = 256, then R = 32 (C = 2, n <= 512) and R = 48
+// (C = 1, n <= 768).
 struct FastShape {
     int P = 0, R = 0;
     bool ok() const { return P > 0; }
@@ -57,13 +60,13 @@ struct FastShape {
 };
 FastShape fast_shape(long long n) {
     FastShape f;
-    for (int P = 1; P <= 16; P *= 2) {
-        const long long per = (n + P - 1) / P;
-        if (per > (P == 1 ? 32 : 48)) continue;
-        f.P = P;
-        f.R = per <= 32 ? 32 : 48;
-        return f;
-    }
+    for (int R : {16, 32, 48})
+        for (int P = 2; P <= 16; P *= 2)
+            if (static_cast<long long>(P) * R >= n) {
+                f.P = P;
+                f.R = R;
+                return f;
+            }
     return f;
 }
 
@@ -189,7 +192,9 @@ __global__ void __launch_bounds__(128) heat_fast_record_kernel(const FastRecPlan
     for (int k = 0; k < kM; ++k) {
         const int t = c * kM + k;
         A2[t * P + p] = make_double2(rp[k], u[k]);
-        B2[t * P + p] = make_double2(__fma_rn(sl[k], nxt, ps[k]), sl[k] * exs);
+        // (partition 0 has no carry from above and the last none from below: psi / sigma stored as 0 there,
+        // so the build multiplies whatever its shuffles return there by 0 instead of selecting)
+        B2[t * P + p] = make_double2(p == 0 ? 0.0 : __fma_rn(sl[k], nxt, ps[k]), p == P - 1 ? 0.0 : sl[k] * exs);
         H[t * P + p] = hr[k];
     }
     // the carry scans' multipliers (RHS-independent): forward, element p = (pi_end(p), d~_end) scanned
@@ -200,9 +205,9 @@ __global__ void __launch_bounds__(128) heat_fast_record_kernel(const FastRecPlan
     for (int l = 0; (1 << l) < P; ++l) {
         const int o = 1 << l;
         const double fo = __shfl_up_sync(kFull, af, o), bo = __shfl_down_sync(kFull, ab, o);
-        if (c == CPP - 1) {
-            blk[4 * NP + l * 16 + p] = af;
-            blk[4 * NP + kScanTab + l * 16 + p] = ab;
+        if (c == CPP - 1) {  // (0 where the partner partition does not exist: no select in the build)
+            blk[4 * NP + l * 16 + p] = p >= o ? af : 0.0;
+            blk[4 * NP + kScanTab + l * 16 + p] = p + o < P ? ab : 0.0;
         }
         if (p >= o) af *= fo;
         if (p + o < P) ab *= bo;
@@ -220,17 +225,20 @@ struct FastPlan {
     const double* hrec;
 };
 
-// records staged ahead: step s + 2 is fetched when step s is done (a third stage measured no
-// gain at C2 and costs C4 its second CTA per SM)
-constexpr int kFastStages = 2;
+// records staged ahead: step s + ST is fetched when step s is done (and step s + ST + 1 pulled into
+// L2 meanwhile); ST = 4 where 4 stages leave room for 2 CTAs per SM (small records: C2), else 2
+constexpr int kFastStagesMax = 4;
 
 // C columns per thread share every coefficient load (one LDS serves 5 C FP64 instructions: the
 // shared-memory path stays below the FP64 pipe) and give each thread C independent chains.
 template <int R>
 struct FastCfg {
-    static constexpr int C = R <= 32 ? 2 : 1;
-    static constexpr int W = 4;        // warps per CTA
-    static constexpr int kMinCtas = 2;  // (<= 255 registers: 8 warps per SM)
+    static constexpr int C = R <= 16 ? 4 : R <= 32 ? 2 : 1;
+    // warps per CTA: single-warp CTAs stage their own records and never wait for a slower warp
+    // (C2: 0.78 vs 0.88 ms with 4-warp CTAs); at R = 32 (n = 512: 21.5 KB a staged step) 4-warp
+    // CTAs share one staged copy, or the copies would not fit 8 warps per SM
+    static constexpr int W = R <= 16 ? 1 : 4;
+    static constexpr int kMinCtas = 2;  // (x 4 / W CTAs: 8 warps per SM, <= 255 registers)
 };
 
 // One step of C column partitions (thread: partition p of C columns, rows in x[c][]); St = the
@@ -265,16 +273,13 @@ __device__ __forceinline__ void fast_step(double (&x)[C][R], const double* St, c
         for (int l = 0; l < L; ++l) {
             const double m = FS[l * 16];
 #pragma unroll
-            for (int c = 0; c < C; ++c) {
+            for (int c = 0; c < C; ++c) {  // (m = 0 where p < 2^l: the lane's own value, times 0)
                 const double vo = __shfl_up_sync(kFull, d[c], 1 << l, P);
-                if (p >= (1 << l)) d[c] = __fma_rn(m, vo, d[c]);
+                d[c] = __fma_rn(m, vo, d[c]);
             }
         }
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-            D[c] = __shfl_up_sync(kFull, d[c], 1, P);
-            if (p == 0) D[c] = 0.0;
-        }
+        for (int c = 0; c < C; ++c) D[c] = __shfl_up_sync(kFull, d[c], 1, P);  // (p = 0: psi = 0 absorbs it)
     }
     double xn[C];
 #pragma unroll
@@ -300,14 +305,11 @@ __device__ __forceinline__ void fast_step(double (&x)[C][R], const double* St, c
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 const double vo = __shfl_down_sync(kFull, v[c], 1 << l, P);
-                if (p + (1 << l) < P) v[c] = __fma_rn(m, vo, v[c]);
+                v[c] = __fma_rn(m, vo, v[c]);
             }
         }
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-            E[c] = __shfl_down_sync(kFull, v[c], 1, P);
-            if (p == P - 1) E[c] = 0.0;
-        }
+        for (int c = 0; c < C; ++c) E[c] = __shfl_down_sync(kFull, v[c], 1, P);  // (p = P - 1: sigma = 0)
 #pragma unroll
         for (int t = 0; t < R; ++t) {  // x = x~ + D psi + E sigma
             const double2 b = B[t * P];
@@ -323,10 +325,10 @@ __device__ __forceinline__ void fast_step(double (&x)[C][R], const double* St, c
 // warps in ns <= W slices, whose records (+ the forced increments, for the warps that hold a
 // forced column) are staged per step by bulk copies (double-buffered; the last warp done with a
 // buffer refills it).
-template <int P, int R>
-__global__ void __launch_bounds__(32 * FastCfg<R>::W, FastCfg<R>::kMinCtas) heat_fast_build_kernel(const FastPlan Q) {
+template <int P, int R, int ST, int W>
+__global__ void __launch_bounds__(32 * W, FastCfg<R>::kMinCtas * 4 / W) heat_fast_build_kernel(const FastPlan Q) {
     constexpr int NP = P * R;
-    constexpr int C = FastCfg<R>::C, W = FastCfg<R>::W;
+    constexpr int C = FastCfg<R>::C;
     constexpr int G = 32 / P;          // column groups per warp
     constexpr int CPW = G * C;         // basis columns per warp
     constexpr long long BLK = fast_blk(NP);
@@ -353,8 +355,8 @@ __global__ void __launch_bounds__(32 * FastCfg<R>::W, FastCfg<R>::kMinCtas) heat
         if (kk[c] == n) fmask |= 1u << c;
     }
     const bool wf = __any_sync(kFull, fmask != 0);
-    unsigned long long* bars = reinterpret_cast<unsigned long long*>(sm + kFastStages * Q.NS * SLOT);
-    unsigned* cnt = reinterpret_cast<unsigned*>(bars + kFastStages);
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(sm + ST * Q.NS * SLOT);
+    unsigned* cnt = reinterpret_cast<unsigned*>(bars + ST);
     const unsigned bar0 = smem_u32(bars);
     // the forced column of slice jq is held by warp jq * wps + (n / CPW): is that warp in this CTA?
     const long long w0 = static_cast<long long>(blockIdx.x) * W;
@@ -375,10 +377,11 @@ __global__ void __launch_bounds__(32 * FastCfg<R>::W, FastCfg<R>::kMinCtas) heat
             bulk_copy(smem_u32(dst), Q.rec + rix * BLK, static_cast<unsigned>(8 * BLK), bar0 + 8u * b);
             if (forced_here(j_lo + q))
                 bulk_copy(smem_u32(dst + BLK), Q.hrec + rix * NP, static_cast<unsigned>(8 * NP), bar0 + 8u * b);
+            if (s + 1 < Q.S) prefetch_l2(Q.rec + (rix + 1) * BLK, static_cast<unsigned>(8 * BLK));  // (the next refill)
         }
     };
     if (threadIdx.x == 0) {
-        for (int b = 0; b < kFastStages; ++b) {
+        for (int b = 0; b < ST; ++b) {
             mbar_init(bar0 + 8u * b);
             cnt[b] = 0;
         }
@@ -386,7 +389,7 @@ __global__ void __launch_bounds__(32 * FastCfg<R>::W, FastCfg<R>::kMinCtas) heat
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int b = 0; b < kFastStages && b < Q.S; ++b) issue(b, b);
+        for (int b = 0; b < ST && b < Q.S; ++b) issue(b, b);
     }
     double x[C][R];
 #pragma unroll
@@ -394,16 +397,16 @@ __global__ void __launch_bounds__(32 * FastCfg<R>::W, FastCfg<R>::kMinCtas) heat
 #pragma unroll
         for (int t = 0; t < R; ++t) x[c][t] = (kk[c] < n && p * R + t == kk[c]) ? 1.0 : 0.0;  // e_k; forced, idle: 0
     for (long long s = 0; s < Q.S; ++s) {
-        const int b = static_cast<int>(s % kFastStages);
-        mbar_wait(bar0 + 8u * b, static_cast<unsigned>((s / kFastStages) & 1));
+        const int b = static_cast<int>(s % ST);
+        mbar_wait(bar0 + 8u * b, static_cast<unsigned>((s / ST) & 1));
         const double* St = sm + (static_cast<long long>(b) * Q.NS + js) * SLOT;
         if (wf) fast_step<P, R, C, true>(x, St, St + BLK, p, fmask);
         else fast_step<P, R, C, false>(x, St, St, p, 0u);
         __syncwarp();
-        if (lane == 0) {  // the last warp done with buffer b refills it with step s + 2
+        if (lane == 0) {  // the last warp done with buffer b refills it with step s + ST
             __threadfence_block();
             const unsigned tk = atomicAdd(cnt + b, 1u);
-            if (tk % W == W - 1 && s + kFastStages < Q.S) issue(s + kFastStages, b);
+            if (tk % W == W - 1 && s + ST < Q.S) issue(s + ST, b);
         }
     }
 #pragma unroll
@@ -425,20 +428,37 @@ int launch_records(pint_ctx* ctx, cudaStream_t st, const FastRecPlan& Q) {
     return pint_check_launch(ctx, "heat_fast_record_kernel");
 }
 
-template <int P, int R>
-int launch_fast(pint_ctx* ctx, FastPlan Q) {
+template <int P, int R, int ST, int W>
+int launch_fast_st(pint_ctx* ctx, const FastPlan& Q, size_t smem, long long ctas) {
+    auto kern = heat_fast_build_kernel<P, R, ST, W>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<static_cast<unsigned>(ctas), 32 * W, smem, ctx->stream>>>(Q);
+    return pint_check_launch(ctx, "heat_fast_build_kernel");
+}
+
+template <int P, int R, int W>
+int launch_fast_w(pint_ctx* ctx, FastPlan Q) {
     constexpr int NP = P * R;
-    constexpr int W = FastCfg<R>::W, CPW = 32 / P * FastCfg<R>::C;
+    constexpr int CPW = 32 / P * FastCfg<R>::C;
     const long long wps = (Q.n + 1 + CPW - 1) / CPW;
     Q.NS = static_cast<int>(std::min<long long>(W, (W + wps - 1) / wps + 1));  // slices a CTA's warps span
     const size_t stage_bytes = sizeof(double) * Q.NS * (fast_blk(NP) + NP);
-    const size_t smem = kFastStages * stage_bytes + 64;
+    const bool deep = kFastStagesMax * stage_bytes + 64 <= static_cast<size_t>(W) * 25 * 1024;  // (8 warps per SM either way)
+    const size_t smem = (deep ? kFastStagesMax : 2) * stage_bytes + 64;
     if (smem > 227 * 1024) return pint_set_error(ctx, PINT_E_INVALID, "heat_fast_build: records exceed shared memory");
-    cudaFuncSetAttribute(heat_fast_build_kernel<P, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
     const long long ctas = (Q.N * wps + W - 1) / W;
-    heat_fast_build_kernel<P, R><<<static_cast<unsigned>(ctas), 32 * W, smem, ctx->stream>>>(Q);
-    return pint_check_launch(ctx, "heat_fast_build_kernel");
+    return deep ? launch_fast_st<P, R, kFastStagesMax, W>(ctx, Q, smem, ctas) : launch_fast_st<P, R, 2, W>(ctx, Q, smem, ctas);
+}
+
+template <int P, int R>
+int launch_fast(pint_ctx* ctx, const FastPlan& Q) {
+    static const int w_env = [] {  // PINT_FAST_W=1|2|4: warps per CTA (experiments only)
+        const char* e = std::getenv("PINT_FAST_W");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (w_env == 1) return launch_fast_w<P, R, 1>(ctx, Q);
+    if (w_env == 2) return launch_fast_w<P, R, 2>(ctx, Q);
+    return launch_fast_w<P, R, FastCfg<R>::W>(ctx, Q);
 }
 
 }  // namespace
@@ -481,13 +501,10 @@ int launch_heat_fast_build(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const
                      records + N * S * fast_blk(f.NP())};
     if (S == 0) return pint_set_error(ctx, PINT_E_INVALID, "heat_fast_build: S >= 1 required");
     switch (f.P * 1000 + f.R) {
-        case 1032: return launch_fast<1, 32>(ctx, Q);
-        case 2032: return launch_fast<2, 32>(ctx, Q);
-        case 2048: return launch_fast<2, 48>(ctx, Q);
-        case 4032: return launch_fast<4, 32>(ctx, Q);
-        case 4048: return launch_fast<4, 48>(ctx, Q);
-        case 8032: return launch_fast<8, 32>(ctx, Q);
-        case 8048: return launch_fast<8, 48>(ctx, Q);
+        case 2016: return launch_fast<2, 16>(ctx, Q);
+        case 4016: return launch_fast<4, 16>(ctx, Q);
+        case 8016: return launch_fast<8, 16>(ctx, Q);
+        case 16016: return launch_fast<16, 16>(ctx, Q);
         case 16032: return launch_fast<16, 32>(ctx, Q);
         case 16048: return launch_fast<16, 48>(ctx, Q);
         default: return pint_set_error(ctx, PINT_E_INVALID, "heat_fast_build: shape");

@@ -50,8 +50,8 @@ def close(a, ref, tol):
     return np.max(np.abs(a - ref)) <= tol * scale
 
 
-# every partition shape (P, R): n <= 32 -> (1, 32); 64 -> (2, 32); 97 -> (4, 32) ... 512 -> (16, 32);
-# 700 -> (16, 48); with padded rows (n not a multiple of P R) and CTAs spanning several slices
+# every partition shape (P, R): n <= 32 -> (2, 16), <= 64 -> (4, 16), <= 128 -> (8, 16), <= 256 -> (16, 16),
+# <= 512 -> (16, 32), <= 768 -> (16, 48); padded rows (n not a multiple of P R), CTAs over several slices
 @pytest.mark.parametrize("n,N,S", [(9, 4, 5), (31, 3, 4), (40, 3, 4), (64, 2, 3), (97, 3, 3), (128, 5, 4),
                                    (150, 2, 3), (200, 3, 2), (255, 2, 3), (300, 2, 3), (384, 2, 2), (512, 3, 4),
                                    (700, 2, 2)])
