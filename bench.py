@@ -87,6 +87,7 @@ def parse():
     p.add_argument("--ref-sample", type=int, default=None,
                    help="slices the reference CPU baseline builds per rep (default: the workload's)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-fast", action="store_true", help="skip the tolerance-build secondary measurement")
     p.add_argument("--transport", default="nccl", choices=["nccl", "host"],
                    help="N > 1: NCCL, or the host-callback transport over gloo (several ranks on one GPU: tests)")
     p.add_argument("--configs", nargs="*", default=None,
@@ -125,6 +126,79 @@ def parity_check(y, n: int, N: int, S: int, T: float, tol: float = 1e-12) -> dic
     return {"vs": f"reference pint::run_nievergelt final_state (tests/golden/heat_finals.npz:{key}_final, "
                   f"oracle/_ref/ref_tool)", "max_rel_diff": rel, "bit_exact": bool(np.array_equal(y, ref)),
             "tolerance": tol, "ok": bool(rel <= tol)}
+
+
+def truth_check(y, n: int, N: int, S: int, T: float) -> dict:
+    """Distance of y and of the reference's own final state to the long-double solve of the same
+    problem (tests/golden/heat_truth.c): what any differently-ordered FP64 result is measured against."""
+    if not GOLDEN.exists() or T != 10.0:
+        return {}
+    z = np.load(GOLDEN)
+    for key in ("c4", "c2"):
+        if f"{key}_truth" in z and tuple(int(x) for x in z[f"{key}_config"]) == (n, N, S):
+            tr, ref = z[f"{key}_truth"], z[f"{key}_final"]
+            sc = float(np.max(np.abs(tr)))
+            return {"vs_long_double": float(np.max(np.abs(np.asarray(y) - tr)) / sc),
+                    "reference_vs_long_double": float(np.max(np.abs(ref - tr)) / sc)}
+    return {}
+
+
+def fast_parity(y, n, N, S, T) -> dict:
+    """The tolerance build's parity, as tests/test_gpu_fast.py states it: <= 1e-12 relative to the
+    reference where the reference's own rounding allows that (C2); at C4 the reference is itself
+    2.6e-12 from the long-double solve, so the build is held to the reference's accuracy instead
+    (its distance to the long-double answer <= 1.5x the reference's + 1e-12, gap <= 5e-12)."""
+    pc, tc = parity_check(y, n, N, S, T), truth_check(y, n, N, S, T)
+    out = {**pc, **tc}
+    if tc and tc["reference_vs_long_double"] > 1e-12:
+        out["criterion"] = ("reference's own accuracy: |y - y_long_double| <= 1.5 |y_ref - y_long_double| + 1e-12 "
+                            "and |y - y_ref| <= 5e-12 (the reference is > 1e-12 from the long-double answer here)")
+        out["ok"] = bool(tc["vs_long_double"] <= 1.5 * tc["reference_vs_long_double"] + 1e-12
+                         and pc.get("max_rel_diff", 1.0) <= 5e-12)
+    else:
+        out["criterion"] = "<= 1e-12 relative to the reference's final state"
+    return out
+
+
+def fast_build_measure(ctx, capi, plan, n, N, S, T, reps, flush, stream, peak):
+    """The tolerance build (PINT_BUILD_FAST, heat_fast.cu) at the same workload, device-resident:
+    its records + build + the bit-exact chain to y, CUDA events, L2 flushed between reps."""
+    import torch
+
+    from paper_1304_6514_b200.dist import HeatPlan
+
+    fp = HeatPlan(ctx, plan.dx, plan.dt, T, N, build="fast")
+    P = capi.ptr
+    step_off, slice_dt, r, fa, fb, sx = fp.dev
+    tot = [0.0, 0.0, 0.0]
+    for i in range(reps + 1):
+        flush.zero_()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(stream)
+        ctx.call("pint_heat_fast_factor_dev", n, fp.N, fp.S, P(step_off), P(slice_dt), P(r), P(fa), P(fb), P(sx),
+                 P(fp.factor))
+        ev[1].record(stream)
+        ctx.call("pint_heat_fast_build_dev", n, fp.N, fp.S, P(fp.factor), P(fp.maps))
+        ev[2].record(stream)
+        fp.compose_local(capi.COMPOSE_CHAIN, want_composed=False)
+        ev[3].record(stream)
+        ev[3].synchronize()
+        if i:
+            tot[0] += ev[0].elapsed_time(ev[3])
+            tot[1] += ev[1].elapsed_time(ev[2])
+            tot[2] += ev[2].elapsed_time(ev[3])
+    y = fp.y.cpu().numpy()
+    build_ms = tot[1] / reps
+    achieved = N * S * flops_per_slice_step(n) / (build_ms * 1e-3) / 1e12
+    out = {"build": "fast (tolerance; heat_fast.cu)", "time_to_solution_ms": tot[0] / reps,
+           "value": N * (n + 1) * S / (tot[0] / reps * 1e-3), "build_ms": build_ms, "compose_ms": tot[2] / reps,
+           "compose": "chain (bit-exact over the tolerance maps)",
+           "roofline": {"bound": "fp64", "kernel": "heat_fast_build_kernel", "achieved": achieved, "peak": peak,
+                        "unit": "TFLOP/s", "frac": achieved / peak},
+           "parity": fast_parity(y, n, N, S, T)}
+    del fp
+    torch.cuda.empty_cache()
+    return out
 
 
 def flops_per_slice_step(n: int) -> int:
@@ -790,6 +864,12 @@ def heat_bench(args, rank, world, local):
         except Exception as e:  # the baseline is reported, never the target
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
+    fast = None
+    if rank == 0 and not args.no_fast:
+        try:
+            fast = fast_build_measure(ctx, capi, plan, n, N, S, T, max(3, args.steps // 4), flush, stream, peak64.value)
+        except Exception as e:  # a secondary measurement: reported, never the headline
+            fast = {"error": str(e)}
     if rank == 0:
         csum = clocks.summary(t_region0, t_region1)
         kern = "heat_build_tmem_kernel" if 282 <= n <= 520 else "heat_build_kernel"  # (heat.cu use_tmem)
@@ -822,6 +902,7 @@ def heat_bench(args, rank, world, local):
                                        148 - 16 if overlap else 148)},
             "clocks": csum,
             "cpu_baseline": cpu,
+            "fast_build": fast,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
