@@ -203,14 +203,17 @@ __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, lo
     const bool live = t < Sc * Nc && step_off[j] + s < step_off[j + 1];  // slice j may have fewer steps
     // the step tables: slice-major at step_off, or (tab_pitch > 0) this block alone at
     // [j][s - s0], pitch tab_pitch, from the pointers passed
-    const long long q = !live ? 0 : tab_pitch > 0 ? j * tab_pitch + sr : step_off[j] + s;
+    // table index: slice-major at step_off, or (tab_pitch > 0) this block alone at [j - j0][s - s0];
+    // failures always carry the global task index step_off[j] + s (lowest-index semantics)
+    const long long q = !live ? 0 : tab_pitch > 0 ? (j - j0) * tab_pitch + sr : step_off[j] + s;
+    const long long qf = !live ? 0 : step_off[j] + s;
     const unsigned live_mask = __ballot_sync(0xffffffffu, live);
     double* mine = buf[w] + lane * kRecLane;
     const double r = live ? r_tab[q] : 0.0;
     const double negr = -r;                                  // pde_problems.cpp:55
     const double diag = __dadd_rn(1.0, __dmul_rn(2.0, r));   // 1.0 + 2.0 * r
     const double h = live ? slice_dt[j] : 0.0, fq = live ? fa[q] : 0.0, gq = live ? fb[q] : 0.0;
-    if (live && !(r >= 0.0 && r <= 0x1p40)) record_failure(fail, kRetryIndex + q, PINT_E_RANGE_RETRY, r);
+    if (live && !(r >= 0.0 && r <= 0x1p40)) record_failure(fail, kRetryIndex + qf, PINT_E_RANGE_RETRY, r);
     unsigned hb_max = 0;
     const bool fast_c = r >= 0x1p-960 && r <= 0x1p40;
     // slice-major records hold steps [rec_s0, rec_s0 + S) (the integrate path's bounded chunks)
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, lo
     if (group) {
         for (int i = 0; i < n; ++i) {
             if (i > 0) p = __dsub_rn(diag, __dmul_rn(negr, c));  // pivot = diag - sub*c[i-1] (:84-88)
-            if (live && p == 0.0) record_failure(fail, q, PINT_E_SINGULAR, static_cast<double>(i));
+            if (live && p == 0.0) record_failure(fail, qf, PINT_E_SINGULAR, static_cast<double>(i));
             const double rcp = __drcp_rn(p);
             c = (i < n - 1) ? (fast_c ? div_fast(negr, make_double2(p, rcp)) : __ddiv_rn(negr, p)) : 0.0;
             const double si = sx[i];
@@ -236,7 +239,7 @@ __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, lo
                 fblk[fblock_cc(n) + i * 32 + (j & 31)] = c;
             }
         }
-        if (live && hb_max >= ((1023u + 900u) << 20)) record_failure(fail, kRetryIndex + q, PINT_E_RANGE_RETRY, 0.0);
+        if (live && hb_max >= ((1023u + 900u) << 20)) record_failure(fail, kRetryIndex + qf, PINT_E_RANGE_RETRY, 0.0);
         return;
     }
     for (int i0 = 0; i0 < n; i0 += kRecChunk) {
@@ -244,7 +247,7 @@ __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, lo
         for (int u = 0; u < rows; ++u) {
             const int i = i0 + u;
             if (i > 0) p = __dsub_rn(diag, __dmul_rn(negr, c));  // pivot = diag - sub*c[i-1] (:84-88)
-            if (live && p == 0.0) record_failure(fail, q, PINT_E_SINGULAR, static_cast<double>(i));
+            if (live && p == 0.0) record_failure(fail, qf, PINT_E_SINGULAR, static_cast<double>(i));
             const double rcp = __drcp_rn(p);
             // c[i] = sup / pivot: the Markstein division with the reciprocal the record carries
             // anyway when r in [2^-960, 2^40] (then p in [1 + r, 1 + 2r], |c| < 1: exact), IEEE otherwise
@@ -280,7 +283,7 @@ __global__ void __launch_bounds__(128) heat_record_kernel(int n, long long N, lo
         }
         __syncwarp();
     }
-    if (live && hb_max >= ((1023u + 900u) << 20)) record_failure(fail, kRetryIndex + q, PINT_E_RANGE_RETRY, 0.0);
+    if (live && hb_max >= ((1023u + 900u) << 20)) record_failure(fail, kRetryIndex + qf, PINT_E_RANGE_RETRY, 0.0);
 }
 
 __device__ __forceinline__ double div_guarded(double x, double2 pr) {
@@ -702,7 +705,7 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
     for (int i = RR; i < n; ++i) st[(i - RR) * kLS] = (i == k) ? 1.0 : 0.0;
     // a resumed segment starts from the column the previous one stored (the group-forced shadow
     // lanes read their slice's column too)
-    if (s0 > 0 && (kGroup ? slice < P.N : k <= n)) {
+    if (s0 > 0 && (kGroup ? slice < P.N : (kForced || k < n))) {  // (only lanes that own a column)
         const double* gp = P.maps + slice * n * P.ldm + k;
 #pragma unroll
         for (int i = 0; i < RR; ++i) reg[i] = gp[i * P.ldm];

@@ -611,16 +611,23 @@ def test_lv_plan_block_chain(ctx):
 
 
 @pytest.mark.gpu
-def test_heat_step_segments_match_unsegmented(ctx):
+@pytest.mark.parametrize("n,N,S,dt", [(128, 64, 40, None), (9, 33, 24, None), (97, 33, 24, None),
+                                      (255, 5, 24, None), (270, 3, 24, None), (128, 4, 12, 1e-9)])
+def test_heat_step_segments_match_unsegmented(ctx, n, N, S, dt):
     """The e2e heat run builds in step segments (capi.cu heat_upload, resumed columns); the same
-    run with PINT_HEAT_SEGMENTS=0 (one launch over all steps) must give bit-identical results."""
+    run with PINT_HEAT_SEGMENTS=0 (one launch over all steps) must give bit-identical results —
+    for the slice-group layout (n = 9, 97, 128; N = 33 leaves a partial group), the slice-major
+    basis / single-forced layout (n = 255, 270), and dt = 1e-9, where the fast division's range
+    check trips AFTER a segmented build and the guarded re-run must still match."""
     import os
     import subprocess
     import sys
 
+    T = 10.0 if dt is None else N * S * dt
+    dt = T / (N * S) if dt is None else dt
     code = ("import numpy as np, sys; sys.path.insert(0, '.'); from paper_1304_6514_b200 import pint; "
-            "N, S = 64, 40; dx, dt = 1.0 / 129.0, 10.0 / (N * S); prob = pint.make_heat_problem(dx, dt, 10.0); "
-            "r = pint.run_nievergelt(prob, N, pint.ExecConfig()); np.save(sys.argv[1], r.final_state)")
+            f"prob = pint.make_heat_problem(1.0 / {n + 1}, {dt!r}, {T!r}); "
+            f"r = pint.run_nievergelt(prob, {N}, pint.ExecConfig()); np.save(sys.argv[1], r.final_state)")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
     for flag in ("1", "0"):
@@ -630,3 +637,10 @@ def test_heat_step_segments_match_unsegmented(ctx):
         subprocess.run([sys.executable, "-c", code, path], cwd=root, env=env, check=True, timeout=300)
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
+    if n <= 128:  # and against the oracle's chain over the oracle's maps
+        dec = pint.decompose(0.0, T, N, dt)
+        G = np.empty((N, n, n))
+        c = np.empty((N, n))
+        for j, s in enumerate(dec.slices):
+            G[j], c[j] = O.heat_build(1.0 / (n + 1), s.t_begin, s.t_end, dt)
+        assert np.array_equal(outs[0], O.affine_chain(G, c, np.asarray(pint.heat_initial(1.0 / (n + 1)))))
