@@ -314,7 +314,10 @@ int pint_parareal_heat(pint_ctx* ctx, double dx, double T, const double* y0, int
  * bit-exact); the only exchange is the final compose step. Replaces the reference's simulated
  * wire (inject_latency + counters, nievergelt.cpp:73-79, 95-101) and ExecConfig::workers' thread
  * pool (exec_harness.hpp:17-21, 51-101) with GPUs. ---- */
-/* NCCL: rank 0 makes the id (128 bytes, an ncclUniqueId) and the caller distributes it */
+/* NCCL: rank 0 makes the id (128 bytes, an ncclUniqueId) and the caller distributes it. NCCL is
+ * resolved at run time (dlopen "libnccl.so.2" at the first NCCL call), never linked, so loading this
+ * library does not pin an NCCL build: in a process that also uses PyTorch, import torch first and its
+ * NCCL is the one used (paper_1304_6514_b200/dist.py nccl_comm_init does). */
 int pint_comm_unique_id(void* id_out);
 int pint_comm_init(pint_ctx* ctx, const void* id, int rank, int world);
 /* one process driving `world` GPUs: ctxs[r] on its own device becomes rank r */
