@@ -36,6 +36,9 @@ enum {
     PINT_E_DUPLICATE_NODES = 5,     /* DuplicateNodes      errors.hpp:29 */
     PINT_E_RANGE_RETRY = 6,         /* internal: a fast-division range check tripped; the
                                        host-buffer entry points re-run with the guarded kernel */
+    PINT_E_SERIALIZED = 7,          /* internal: the chain of pint_heat_build_chain_dev could not
+                                       run beside the build (kernels serialised, e.g. under a
+                                       profiler); the maps are complete: re-run the compose */
     PINT_E_INVALID = 16,            /* bad argument to this ABI */
     PINT_E_CUDA = 17,               /* CUDA runtime failure (no CPU fallback exists) */
     PINT_E_NO_DEVICE = 18,

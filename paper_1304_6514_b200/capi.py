@@ -20,6 +20,7 @@ PINT_E_BAD_GRID = 3
 PINT_E_NON_INTEGER_STEPS = 4
 PINT_E_DUPLICATE_NODES = 5
 PINT_E_RANGE_RETRY = 6
+PINT_E_SERIALIZED = 7
 PINT_E_INVALID = 16
 PINT_E_CUDA = 17
 PINT_E_NO_DEVICE = 18

@@ -1068,7 +1068,11 @@ int heat_build_chain(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64
     // ready[N] counters, then {build start, build end, chain end} globaltimer words
     const size_t ready_bytes = sizeof(int) * static_cast<size_t>((N + 1) & ~1ll);
     int* ready = target ? static_cast<int*>(pint_scratch(ctx, 5, ready_bytes + 32)) : nullptr;
-    if (!target || !ready || n > 512) {
+    static const int overlap_env = [] {  // PINT_OVERLAP=0: build, then chain (experiments, debugging)
+        const char* e = std::getenv("PINT_OVERLAP");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (!target || !ready || n > 512 || overlap_env == 0) {
         if (const int rc = launch_heat_build(ctx, n, N, S, step_off, slice_dt, records, sx, maps, per_slice_ns, guarded))
             return rc;
         cudaEventRecord(ctx->evc, ctx->stream);
@@ -1080,6 +1084,7 @@ int heat_build_chain(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64
     cudaMemsetAsync(reinterpret_cast<char*>(ready) + ready_bytes + 8, 0, 16, ctx->stream);
     ctx->span_words = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ready) + ready_bytes);
     if (const int rc = launch_affine_chain_on(ctx, ctx->stream, n, N, maps, y0, y, ready, target)) return rc;
+    if (overlap_env == 2) cudaEventRecord(ctx->evc, ctx->stream);  // (test hook: serialise the build behind the chain)
     if (const int rc = launch_heat_build_steps(ctx, n, N, S, step_off, records, maps, per_slice_ns, guarded, 0, S, ready))
         return rc;
     cudaEventRecord(ctx->evc, ctx->stream);
@@ -1091,6 +1096,7 @@ int singular_check(pint_ctx* ctx) {
     if (const int rc = pint_fail_read(ctx, &fr)) return rc;
     if (fr.index >= 0) {
         if (fr.code == PINT_E_RANGE_RETRY) return PINT_E_RANGE_RETRY;  // caller re-runs guarded
+        if (fr.code == PINT_E_SERIALIZED) return PINT_E_SERIALIZED;    // caller re-runs the compose
         char buf[96];
         std::snprintf(buf, sizeof buf, "thomas_solve: zero pivot at row %d", static_cast<int>(fr.value));
         return pint_set_error(ctx, PINT_E_SINGULAR, buf);
@@ -1189,6 +1195,13 @@ int pint_run_heat_ex(pint_ctx* ctx, double dx, double dt, double T, int64_t N, i
         }
         if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "run_heat sync")) return PINT_E_CUDA;
         rc = singular_check(ctx);
+        if (rc == PINT_E_SERIALIZED) {  // the concurrent chain could not run beside the build: the maps
+            if ((rc = launch_affine_chain(ctx, n, N, d_maps, d_y0, d_y))) return rc;  // are done, chain them now
+            cudaEventRecord(ctx->ev1, ctx->stream);
+            cudaMemcpyAsync(y_out, d_y, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream);
+            if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "run_heat sync")) return PINT_E_CUDA;
+            rc = singular_check(ctx);
+        }
         if (rc != PINT_E_RANGE_RETRY) break;
     }
     if (rc) return rc;

@@ -29,6 +29,9 @@ namespace {
 using namespace pint_async;
 
 constexpr int kChainThreads = 256;
+// a concurrent chain that gave up waiting (PINT_E_SERIALIZED): above every task and range-retry
+// index, so a real failure of the same run is the one reported first
+constexpr long long kSerializedIndex = 0x7FFFFFFFFFFFFFFEll;
 
 // One CTA; thread t owns rows t, t+256, ... Dynamic smem: y[n].
 __global__ void __launch_bounds__(kChainThreads)
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long lo
                 // never hang: a map not ready 1 s after the wait began means its builder is not
                 // running; fail loudly (the result is not used) and stop waiting for the rest
                 if (v < target && pint_dev::globaltimer() - t0 > 1000000000ull) {
-                    pint_dev::record_failure(fail, j, PINT_E_CUDA, static_cast<double>(v));
+                    pint_dev::record_failure(fail, kSerializedIndex, PINT_E_SERIALIZED, static_cast<double>(j));
                     gave_up = true;
                     break;
                 }

@@ -154,6 +154,10 @@ class HeatPlan:
         f = self.ctx.fail()
         if f.index < 0:
             return True
+        if f.code == capi.PINT_E_SERIALIZED:  # the concurrent chain ran alone: the maps are complete
+            self.compose_local(capi.COMPOSE_CHAIN, want_composed=False)
+            self.ctx.sync()
+            return self.verify()
         if f.code == capi.PINT_E_RANGE_RETRY:
             self.guarded = 1
             return False
