@@ -474,34 +474,57 @@ def run_configs(a):
     peak = C.c_double()
     ctx.check(ctx.lib.pint_probe_peak(ctx.h, capi.F64, C.byref(peak)))
 
-    def emit(d):
-        print(json.dumps(d), flush=True)
+    def emit(name, params, r, flops_per_step, cpu, parity=None, kernel="scalar ensemble (K1) + ordered sweep (K2)"):
+        """One BENCH-shaped line per configuration: device value + e2e (host buffers) + roofline of
+        the device time against the measured FP64 FMA peak + the CPU baseline + parity."""
+        achieved = r["device_traj_steps_per_s"] * flops_per_step / 1e12
+        line = {"metric": "ODE trajectory-steps/s (time to solution)", "value": r["device_traj_steps_per_s"],
+                "unit": UNIT, "n_gpus": 1, "ms_per_step": r["device_ms"], "higher_is_better": True,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": name, **params, "time_to_solution_ms": r["device_ms"],
+                           "e2e_time_to_solution_ms": r["e2e_ms"], "final": r["final"]},
+                "e2e": {"value": r["e2e_traj_steps_per_s"], "unit": UNIT,
+                        "h2d_bytes_per_step": r.get("h2d_bytes"), "d2h_bytes_per_step": r.get("d2h_bytes")},
+                "gpu_launches": r.get("gpu_launches"),
+                "roofline": {"bound": "fp64", "kernel": kernel + " (whole device time)", "achieved": achieved,
+                             "peak": peak.value, "unit": "TFLOP/s", "frac": achieved / peak.value,
+                             "flops_per_traj_step": flops_per_step},
+                "cpu_baseline": cpu, "parity": parity}
+        print(json.dumps(line), flush=True)
 
+    def ref_parity(y, cpu):
+        if not cpu or "final" not in cpu:
+            return None
+        return {"vs": "reference pint::run_nievergelt final_state (oracle/_ref/ref_tool bench-scalar)",
+                "bit_exact": y == cpu["final"], "ok": y == cpu["final"]}
+
+    ext = {"vs": "EXTENSION (no reference counterpart): bit-exact against the oracle in tests/test_gpu_parity.py"}
     if "c1ref" in a.configs:
         for S in (79, 782):
             r = run_scalar(ctx, capi, "riccati", 64, 512, S, a.config_reps)
-            emit({"config": "c1 reference path (Riccati BE)", "N": 64, "M": 512, "S": S, **r,
-                  "cpu_baseline": ref_scalar(64, 512, S)})
+            cpu = ref_scalar(64, 512, S)
+            emit("c1 reference path: make_model_problem, Riccati BE, 64 slices x 512 ICs (BASELINE configs[0])",
+                 {"N": 64, "M": 512, "S": S}, r, 6, cpu, ref_parity(r["final"], cpu))
     if "c1rk4" in a.configs:
         r = run_scalar(ctx, capi, "logistic", 64, 1024, 977, a.config_reps)
-        emit({"config": "c1 logistic RK4", "N": 64, "M": 1024, "S": 977, **r,
-              "fp64_frac_of_peak_device": r["device_traj_steps_per_s"] * 29 / (peak.value * 1e12),
-              "cpu_baseline": port_logistic(64, 1024, 977)})
+        emit("c1 logistic RK4, 64 slices x 1024 ICs", {"N": 64, "M": 1024, "S": 977}, r, 29,
+             port_logistic(64, 1024, 977), ext)
     if "c5" in a.configs:
         for S in (98, 977, 9766):
             r = run_scalar(ctx, capi, "logistic", 64, 1024, S, a.config_reps)
-            emit({"config": "c5 logistic RK4", "N": 64, "M": 1024, "S": S, "per_slice_traj_steps": 1024 * S, **r,
-                  "fp64_frac_of_peak_device": r["device_traj_steps_per_s"] * 29 / (peak.value * 1e12),
-                  "cpu_baseline": port_logistic(64, 1024, S, sample=max(1, min(8, 4000 // S)))})
+            emit("c5 logistic RK4 sweep (BASELINE configs[4])", {"N": 64, "M": 1024, "S": S,
+                 "per_slice_traj_steps": 1024 * S}, r, 29,
+                 port_logistic(64, 1024, S, sample=max(1, min(8, 4000 // S))), ext)
         for S in (98, 977, 9766):  # (M = 1024: closed-form weights; the reference's product form overflows)
             r = run_scalar(ctx, capi, "riccati", 64, 1024, S, a.config_reps, closed_weights=True)
-            emit({"config": "c5 Riccati BE", "N": 64, "M": 1024, "S": S, "per_slice_traj_steps": 1024 * S, **r})
+            emit("c5 Riccati BE sweep (BASELINE configs[4])", {"N": 64, "M": 1024, "S": S,
+                 "per_slice_traj_steps": 1024 * S}, r, 6, None, ext)
     if "c3" in a.configs:
         for S in (8, 64):
             r = run_lv(ctx, 512, 256, S, a.config_reps)
-            emit({"config": "c3 Lotka-Volterra RK4 + bilinear chain", "N": 512, "grid": "256x256", "S": S, **r,
-                  "fp64_frac_of_peak_device": r["device_traj_steps_per_s"] * 54 / (peak.value * 1e12),
-                  "cpu_baseline": port_lv(512, 256, S)})
+            emit("c3 Lotka-Volterra RK4 + bilinear chain, 512 slices x 256^2 grid (BASELINE configs[2])",
+                 {"N": 512, "grid": "256x256", "S": S}, r, 54, port_lv(512, 256, S), ext,
+                 kernel="LV tensor-grid RK4 + bilinear sweep")
 
 
 
