@@ -372,6 +372,8 @@ def run_scalar(ctx, capi, kind, N, M, S, reps, closed_weights=False):
         t0, T, y0, a, b, wk = 0.0, 10.0, 0.1, 0.0, 1.25, capi.WEIGHTS_CLOSED2
     if closed_weights:
         wk = capi.WEIGHTS_CLOSED2
+    # EXTENSION runs (closed-form weights, no reference sum order to keep) sweep in tree order
+    sweep = capi.SWEEP_TREE if wk == capi.WEIGHTS_CLOSED2 else capi.SWEEP_EXACT
     dt = (T - t0) / (N * S)
     y = C.c_double()
     rep, fail = capi.Report(), capi.Fail()
@@ -379,7 +381,7 @@ def run_scalar(ctx, capi, kind, N, M, S, reps, closed_weights=False):
     for i in range(reps + 2):
         t = time.perf_counter()
         ctx.check(ctx.lib.pint_run_scalar(ctx.h, C.byref(rhs), t0, T, y0, N, dt, capi.NODES_SECOND_KIND, M, a, b,
-                                          wk, capi.SWEEP_EXACT, C.byref(y), None, None, None, C.byref(rep),
+                                          wk, sweep, C.byref(y), None, None, None, C.byref(rep),
                                           C.byref(fail)))
         w = time.perf_counter() - t
         if i >= 2:

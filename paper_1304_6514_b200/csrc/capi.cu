@@ -263,6 +263,10 @@ int pint_ctx_create(int device, pint_ctx** out) {
     FailRec init{pint_dev::kNoFail, 0, 0, 0.0};
     cudaMemcpy(ctx->d_fail, &init, sizeof init, cudaMemcpyHostToDevice);
     cudaMemcpy(ctx->d_fail_serial, &init, sizeof init, cudaMemcpyHostToDevice);
+    if (cudaHostAlloc(&ctx->h_small, 256, cudaHostAllocDefault) != cudaSuccess) {
+        pint_ctx_destroy(ctx);
+        return PINT_E_CUDA;
+    }
     *out = ctx;
     return PINT_OK;
 }
@@ -277,6 +281,7 @@ void pint_ctx_destroy(pint_ctx* ctx) {
     comm_free(ctx);
     if (ctx->d_fail) cudaFree(ctx->d_fail);
     if (ctx->d_fail_serial) cudaFree(ctx->d_fail_serial);
+    if (ctx->h_small) cudaFreeHost(ctx->h_small);
     if (ctx->serial) cudaStreamDestroy(ctx->serial);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -753,13 +758,16 @@ int pint_run_scalar(pint_ctx* ctx, const pint_scalar_rhs* rhs, double t0, double
     }
     cudaEventRecord(ctx->ev1, ctx->stream);
     int64_t d2h = 0;
-    if (!ok(ctx, cudaMemcpyAsync(&y, d_y, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H y"))
+    // y, the extrapolation count and the failure record land in the pinned small block: one batch
+    auto* hs = static_cast<char*>(ctx->h_small);
+    if (!ok(ctx, cudaMemcpyAsync(hs, d_y, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H y"))
         return PINT_E_CUDA;
     d2h += sizeof(double);
     if (!serial) {
-        cudaMemcpyAsync(&ext, d_ext, sizeof ext, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(hs + 8, d_ext, sizeof ext, cudaMemcpyDeviceToHost, ctx->stream);
         d2h += sizeof ext;
     }
+    cudaMemcpyAsync(hs + 16, ctx->d_fail, sizeof(FailRec), cudaMemcpyDeviceToHost, ctx->stream);
     if (endpoints_out) {
         cudaMemcpyAsync(endpoints_out, d_ends, esz * N * Mn, cudaMemcpyDeviceToHost, ctx->stream);
         d2h += esz * N * Mn;
@@ -774,9 +782,15 @@ int pint_run_scalar(pint_ctx* ctx, const pint_scalar_rhs* rhs, double t0, double
         cudaMemcpyAsync(ns.data(), d_ns, sizeof(unsigned long long) * N, cudaMemcpyDeviceToHost, ctx->stream);
     }
     if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "run_scalar sync")) return PINT_E_CUDA;
+    std::memcpy(&y, hs, sizeof y);
+    if (!serial) std::memcpy(&ext, hs + 8, sizeof ext);
     if (f32) y = static_cast<double>(*reinterpret_cast<float*>(&y));
-    pint_fail fr;
-    if ((rc = pint_fail_read(ctx, &fr))) return rc;
+    FailRec frec;
+    std::memcpy(&frec, hs + 16, sizeof frec);
+    pint_fail fr{-1, 0, 0, 0.0};
+    if (frec.index != pint_dev::kNoFail) {  // (rare) read it properly, which also clears it
+        if ((rc = pint_fail_read(ctx, &fr))) return rc;
+    }
     if (fail) *fail = fr;
     if (fr.index >= 0) {
         char buf[160];

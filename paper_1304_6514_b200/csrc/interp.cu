@@ -107,74 +107,94 @@ __global__ void bary_closed2_kernel(long long M, double* __restrict__ w) {
     w[j] = (j == 0 || j == M - 1) ? 0.5 * sgn : sgn;
 }
 
-constexpr int kSweepThreads = 256;
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
+// TREE mode (EXTENSION, within 1e-12 of EXACT: the sums in tree order): one CTA of 1024 threads
+// walks the N slices in order; thread t owns nodes t, t + 1024, ... (PER of them, in registers —
+// loaded once when the slices share their nodes, the usual case), the values of slice j + 1 are
+// loaded while slice j is evaluated, and the node snap (interp.cpp:70-72: the lowest node within
+// 1e-14 relative returns its value) rides in the same block reduction as (num, den): ONE pass and
+// two barriers per slice — the slice's critical path is a divide and two 5-level shuffle trees.
+constexpr int kTreeThreads = 1024;
 
-// TREE mode (EXTENSION): one CTA walks the N slices in order; per slice the snap test, then
-// num/den by warp-tree reduction.
-__global__ void __launch_bounds__(kSweepThreads)
+template <int PER>
+__global__ void __launch_bounds__(kTreeThreads)
 scalar_sweep_tree_kernel(long long N, long long M, const double* __restrict__ nodes, long long node_stride,
                          const double* __restrict__ weights, const double* __restrict__ values,
                          const double* __restrict__ a_arr, const double* __restrict__ b_arr,
                          long long ab_stride, double y0, double* lambdas, double* y_out,
                          long long* extrapolations) {
+    __shared__ double2 red[kTreeThreads / 32];
+    __shared__ unsigned red_hit[kTreeThreads / 32];
     __shared__ double y_s;
-    __shared__ unsigned long long hit_s;
-    __shared__ double red_num[kSweepThreads / 32], red_den[kSweepThreads / 32];
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double xr[PER], wr[PER], vr[PER], vn[PER];
+    auto load_nodes = [&](long long j) {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const long long k = tid + q * kTreeThreads;
+            xr[q] = k < M ? nodes[j * node_stride + k] : 0.0;
+            wr[q] = k < M ? weights[j * node_stride + k] : 0.0;
+        }
+    };
+    auto load_values = [&](long long j, double (&dst)[PER]) {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const long long k = tid + q * kTreeThreads;
+            dst[q] = (k < M && j < N) ? values[j * M + k] : 0.0;
+        }
+    };
+    load_nodes(0);
+    load_values(0, vr);
     double y = y0;
     long long ext = 0;
     for (long long j = 0; j < N; ++j) {
-        const double* x = nodes + j * node_stride;
-        const double* w = weights + j * node_stride;
-        const double* v = values + j * M;
+        load_values(j + 1, vn);  // (independent of y: in flight while this slice is evaluated)
+        if (node_stride && j > 0) load_nodes(j);
         const double a = a_arr[j * ab_stride], b = b_arr[j * ab_stride];
         if (y < a || y > b) ++ext;  // nievergelt.cpp:83
-        if (tid == 0) hit_s = static_cast<unsigned long long>(M);
-        __syncthreads();
-        // node snap: the lowest node within 1e-14 (relative) returns its value (interp.cpp:70-72)
-        for (long long k = tid; k < M; k += kSweepThreads) {
-            const double xk = x[k];
-            if (fabs(__dsub_rn(y, xk)) <= __dmul_rn(1e-14, fmax(1.0, fabs(xk)))) {
-                atomicMin(&hit_s, static_cast<unsigned long long>(k));
-                break;
-            }
-        }
-        __syncthreads();
-        const long long hit = static_cast<long long>(hit_s);
-        if (hit < M) {
-            y = v[hit];
-        } else {
-            double num = 0.0, den = 0.0;
-            for (long long k = tid; k < M; k += kSweepThreads) {
-                const double r = w[k] / (y - x[k]);
-                num = fma(r, v[k], num);
+        double num = 0.0, den = 0.0;
+        unsigned hit = 0xffffffffu;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const long long k = tid + q * kTreeThreads;
+            if (k < M) {
+                const double d = __dsub_rn(y, xr[q]);
+                if (fabs(d) <= __dmul_rn(1e-14, fmax(1.0, fabs(xr[q]))) && hit == 0xffffffffu)
+                    hit = static_cast<unsigned>(k);
+                const double r = wr[q] / d;
+                num = fma(r, vr[q], num);
                 den += r;
             }
-            num = warp_sum(num);
-            den = warp_sum(den);
-            if ((tid & 31) == 0) {
-                red_num[tid >> 5] = num;
-                red_den[tid >> 5] = den;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                double sn = 0.0, sd = 0.0;
-                for (int q = 0; q < kSweepThreads / 32; ++q) {
-                    sn += red_num[q];
-                    sd += red_den[q];
-                }
-                y_s = sn / sd;
-            }
-            __syncthreads();
-            y = y_s;
         }
-        if (tid == 0 && lambdas) lambdas[j] = y;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            num += __shfl_xor_sync(0xffffffffu, num, o);
+            den += __shfl_xor_sync(0xffffffffu, den, o);
+        }
+        hit = __reduce_min_sync(0xffffffffu, hit);
+        if (lane == 0) {
+            red[warp] = make_double2(num, den);
+            red_hit[warp] = hit;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double2 t = red[lane];
+            unsigned h = __reduce_min_sync(0xffffffffu, red_hit[lane]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                t.x += __shfl_xor_sync(0xffffffffu, t.x, o);
+                t.y += __shfl_xor_sync(0xffffffffu, t.y, o);
+            }
+            if (lane == 0) {
+                const double yn = h != 0xffffffffu ? values[j * M + h] : t.x / t.y;
+                y_s = yn;
+                if (lambdas) lambdas[j] = yn;
+            }
+        }
+        __syncthreads();
+        y = y_s;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) vr[q] = vn[q];
     }
     if (tid == 0) {
         if (y_out) *y_out = y;
@@ -513,8 +533,12 @@ int launch_scalar_sweep(pint_ctx* ctx, int mode, int64_t N, int64_t M, const dou
         scalar_sweep_exact_kernel<<<1, kExactThreads, smem, ctx->stream>>>(
             N, M, nodes, node_stride, weights, values, a, b, ab_stride, y0, lambdas, y_out, extrapolations);
     } else if (mode == PINT_SWEEP_TREE) {
-        scalar_sweep_tree_kernel<<<1, kSweepThreads, 0, ctx->stream>>>(
-            N, M, nodes, node_stride, weights, values, a, b, ab_stride, y0, lambdas, y_out, extrapolations);
+        if (M > 8 * kTreeThreads) return pint_set_error(ctx, PINT_E_INVALID, "scalar_sweep: M > 8192 unsupported in TREE mode");
+        const int per = static_cast<int>((M + kTreeThreads - 1) / kTreeThreads);
+        auto k = per <= 1 ? scalar_sweep_tree_kernel<1> : per <= 2 ? scalar_sweep_tree_kernel<2>
+               : per <= 4 ? scalar_sweep_tree_kernel<4> : scalar_sweep_tree_kernel<8>;
+        k<<<1, kTreeThreads, 0, ctx->stream>>>(N, M, nodes, node_stride, weights, values, a, b, ab_stride, y0,
+                                               lambdas, y_out, extrapolations);
     } else {
         return pint_set_error(ctx, PINT_E_INVALID, "scalar_sweep: unknown mode");
     }
