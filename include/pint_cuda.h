@@ -217,6 +217,9 @@ int pint_affine_compose_dev(pint_ctx* ctx, int mode, int64_t n, int64_t N, doubl
 int pint_heat_build_chain_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
                               const double* slice_dt, const double* records, const double* sx,
                               double* maps, const double* y0, double* y, int guarded);
+/* the same with the TOLERANCE build (pint_heat_fast_factor_dev's records) */
+int pint_heat_fast_build_chain_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const double* records,
+                                   double* maps, const double* y0, double* y);
 /* after an overlapped pint_heat_build_chain_dev: the build kernel's span on the device (first CTA
  * start to last CTA end, %globaltimer) and the chain's exposed tail past it; syncs the stream */
 int pint_ctx_build_chain_ms(pint_ctx* ctx, double* build_ms, double* tail_ms);

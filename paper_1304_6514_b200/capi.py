@@ -100,6 +100,7 @@ _SIGS = {
     "pint_heat_serial_begin": (_int, [_vp, _d, _d, _d, _vp]),
     "pint_heat_serial_end": (_int, [_vp, _vp]),
     "pint_heat_build_chain_dev": (_int, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _int]),
+    "pint_heat_fast_build_chain_dev": (_int, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "pint_ctx_build_chain_ms": (_int, [_vp, C.POINTER(_d), C.POINTER(_d)]),
     "pint_affine_compose_dev": (_int, [_vp, _int, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "pint_affine_pair_dev": (_int, [_vp, _i, _i, _vp, _vp, _vp]),

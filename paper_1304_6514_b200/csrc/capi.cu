@@ -619,7 +619,8 @@ int pint_ctx_build_chain_ms(pint_ctx* ctx, double* build_ms, double* tail_ms) {
 namespace {
 int heat_build_chain(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
                      const double* slice_dt, const double* records, const double* sx, double* maps,
-                     const double* y0, double* y, unsigned long long* per_slice_ns, int guarded);
+                     const double* y0, double* y, unsigned long long* per_slice_ns, int guarded,
+                     int build_mode = PINT_BUILD_EXACT);
 }  // namespace
 
 int pint_heat_build_chain_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
@@ -627,6 +628,12 @@ int pint_heat_build_chain_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, co
                               const double* y0, double* y, int guarded) {
     if (!ctx) return PINT_E_INVALID;
     return heat_build_chain(ctx, n, N, S, step_off, slice_dt, records, sx, maps, y0, y, nullptr, guarded);
+}
+
+int pint_heat_fast_build_chain_dev(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const double* records,
+                                   double* maps, const double* y0, double* y) {
+    if (!ctx) return PINT_E_INVALID;
+    return heat_build_chain(ctx, n, N, S, nullptr, nullptr, records, nullptr, maps, y0, y, nullptr, 0, PINT_BUILD_FAST);
 }
 
 int pint_affine_compose_dev(pint_ctx* ctx, int mode, int64_t n, int64_t N, double* maps,
@@ -1077,8 +1084,10 @@ int heat_upload(pint_ctx* ctx, double dx, const std::vector<pint_slice>& sl, Hea
 // running kernel, here for the chain that waits for the build.
 int heat_build_chain(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
                      const double* slice_dt, const double* records, const double* sx, double* maps,
-                     const double* y0, double* y, unsigned long long* per_slice_ns, int guarded) {
-    const int target = heat_build_ready_target(n);
+                     const double* y0, double* y, unsigned long long* per_slice_ns, int guarded,
+                     int build_mode) {
+    const bool fast = build_mode == PINT_BUILD_FAST;
+    const int target = fast ? heat_fast_ready_target(n) : heat_build_ready_target(n);
     // ready[N] counters, then {build start, build end, chain end} globaltimer words
     const size_t ready_bytes = sizeof(int) * static_cast<size_t>((N + 1) & ~1ll);
     int* ready = target ? static_cast<int*>(pint_scratch(ctx, 5, ready_bytes + 32)) : nullptr;
@@ -1087,19 +1096,24 @@ int heat_build_chain(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64
         return e ? std::atoi(e) : 1;
     }();
     if (!target || !ready || n > 512 || overlap_env == 0) {
-        if (const int rc = launch_heat_build(ctx, n, N, S, step_off, slice_dt, records, sx, maps, per_slice_ns, guarded))
+        if (const int rc = fast ? launch_heat_fast_build(ctx, n, N, S, records, maps)
+                                : launch_heat_build(ctx, n, N, S, step_off, slice_dt, records, sx, maps, per_slice_ns,
+                                                    guarded))
             return rc;
         cudaEventRecord(ctx->evc, ctx->stream);
         return launch_affine_chain(ctx, n, N, maps, y0, y);
     }
-    heat_build_prepare(n);
+    if (fast) heat_fast_prepare(n);
+    else heat_build_prepare(n);
     cudaMemsetAsync(ready, 0, ready_bytes, ctx->stream);
     cudaMemsetAsync(reinterpret_cast<char*>(ready) + ready_bytes, 0xff, 8, ctx->stream);  // (min start)
     cudaMemsetAsync(reinterpret_cast<char*>(ready) + ready_bytes + 8, 0, 16, ctx->stream);
     ctx->span_words = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ready) + ready_bytes);
     if (const int rc = launch_affine_chain_on(ctx, ctx->stream, n, N, maps, y0, y, ready, target)) return rc;
     if (overlap_env == 2) cudaEventRecord(ctx->evc, ctx->stream);  // (test hook: serialise the build behind the chain)
-    if (const int rc = launch_heat_build_steps(ctx, n, N, S, step_off, records, maps, per_slice_ns, guarded, 0, S, ready))
+    if (const int rc = fast ? launch_heat_fast_build(ctx, n, N, S, records, maps, ready)
+                            : launch_heat_build_steps(ctx, n, N, S, step_off, records, maps, per_slice_ns, guarded, 0,
+                                                      S, ready))
         return rc;
     cudaEventRecord(ctx->evc, ctx->stream);
     return PINT_OK;
@@ -1179,12 +1193,14 @@ int pint_run_heat_ex(pint_ctx* ctx, double dx, double dt, double T, int64_t N, i
     std::vector<unsigned long long> ns;
     int rc = PINT_OK;
     for (int guarded = 0; guarded < 2; ++guarded) {  // second pass only if a range check tripped
-        const bool overlap = !fast && !segmented && heat_build_ready_target(n) > 0 &&
-                             (compose_mode == PINT_COMPOSE_CHAIN || n > 256);  // (only-y TREE at n > 256 IS the chain)
+        const bool overlap = !segmented && n <= 512 &&
+                             (fast ? heat_fast_ready_target(n) > 0 && compose_mode == PINT_COMPOSE_CHAIN
+                                   : heat_build_ready_target(n) > 0 &&
+                                         (compose_mode == PINT_COMPOSE_CHAIN || n > 256));  // (only-y TREE at n > 256 IS the chain)
         if (overlap) {
             if (per_slice_seconds && guarded) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
             rc = heat_build_chain(ctx, n, N, H.S, H.step_off, H.slice_dt, H.factor, H.sx, d_maps, d_y0, d_y,
-                                  per_slice_seconds ? d_ns : nullptr, guarded);
+                                  per_slice_seconds ? d_ns : nullptr, guarded, build_mode);
             if (rc) return rc;
         } else if (fast) {  // (no range retry: plain FP64 arithmetic throughout)
             rc = launch_heat_fast_build(ctx, n, N, H.S, H.factor, d_maps);

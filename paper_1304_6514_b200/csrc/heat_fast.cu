@@ -223,6 +223,8 @@ struct FastPlan {
     long long ldm;
     const double* rec;
     const double* hrec;
+    int* ready;  // (may be null) per-slice count of warps whose columns of the map are stored
+    unsigned long long* span;  // (with ready) {first warp start, last warp end} globaltimer
 };
 
 // records staged ahead: step s + ST is fetched when step s is done (and step s + ST + 1 pulled into
@@ -334,6 +336,7 @@ __global__ void __launch_bounds__(32 * W, FastCfg<R>::kMinCtas * 4 / W) heat_fas
     constexpr long long BLK = fast_blk(NP);
     constexpr long long SLOT = BLK + NP;
     extern __shared__ __align__(128) double sm[];
+    const unsigned long long t_start = Q.ready ? pint_dev::globaltimer() : 0;
     const int n = Q.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cg = lane / P, p = lane % P;
@@ -419,6 +422,16 @@ __global__ void __launch_bounds__(32 * W, FastCfg<R>::kMinCtas * 4 / W) heat_fas
             if (i < n) gp[static_cast<long long>(i) * Q.ldm] = x[c][t];
         }
     }
+    // this warp's columns of slice j are stored: count it (a concurrent chain waits for all wps)
+    if (Q.ready && wlive) {
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicAdd(Q.ready + j, 1);
+            atomicMin(Q.span, t_start);
+            atomicMax(Q.span + 1, pint_dev::globaltimer());
+        }
+    }
 }
 
 template <int kM>
@@ -431,8 +444,23 @@ int launch_records(pint_ctx* ctx, cudaStream_t st, const FastRecPlan& Q) {
 template <int P, int R, int ST, int W>
 int launch_fast_st(pint_ctx* ctx, const FastPlan& Q, size_t smem, long long ctas) {
     auto kern = heat_fast_build_kernel<P, R, ST, W>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    kern<<<static_cast<unsigned>(ctas), 32 * W, smem, ctx->stream>>>(Q);
+    pint_kernel_attrs(reinterpret_cast<const void*>(kern));  // (once: never between the chain and the build)
+    if (!Q.ready) {
+        kern<<<static_cast<unsigned>(ctas), 32 * W, smem, ctx->stream>>>(Q);
+        return pint_check_launch(ctx, "heat_fast_build_kernel");
+    }
+    // signalling build: behind the waiting chain on the same stream, allowed to start while it runs
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(ctas), 1, 1);
+    cfg.blockDim = dim3(32 * W, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, Q);
     return pint_check_launch(ctx, "heat_fast_build_kernel");
 }
 
@@ -493,12 +521,35 @@ int launch_heat_fast_factor(pint_ctx* ctx, cudaStream_t stream, int64_t n, int64
     }
 }
 
-int launch_heat_fast_build(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const double* records, double* maps) {
+int heat_fast_ready_target(int64_t n) {  // warps per slice (each adds 1 to ready[j] after its stores)
+    const FastShape f = fast_shape(n);
+    if (!f.ok()) return 0;
+    const int cpw = 32 / f.P * (f.R <= 16 ? FastCfg<16>::C : f.R <= 32 ? FastCfg<32>::C : FastCfg<48>::C);
+    return static_cast<int>((n + 1 + cpw - 1) / cpw);
+}
+
+void heat_fast_prepare(int64_t n) {  // every kernel variant the build for n may launch, attributes set
+    const FastShape f = fast_shape(n);
+    auto set = [](auto k) { pint_kernel_attrs(reinterpret_cast<const void*>(k)); };
+    switch (f.P * 1000 + f.R) {
+        case 2016: set(heat_fast_build_kernel<2, 16, 4, 1>); set(heat_fast_build_kernel<2, 16, 2, 1>); break;
+        case 4016: set(heat_fast_build_kernel<4, 16, 4, 1>); set(heat_fast_build_kernel<4, 16, 2, 1>); break;
+        case 8016: set(heat_fast_build_kernel<8, 16, 4, 1>); set(heat_fast_build_kernel<8, 16, 2, 1>); break;
+        case 16016: set(heat_fast_build_kernel<16, 16, 4, 1>); set(heat_fast_build_kernel<16, 16, 2, 1>); break;
+        case 16032: set(heat_fast_build_kernel<16, 32, 4, 4>); set(heat_fast_build_kernel<16, 32, 2, 4>); break;
+        case 16048: set(heat_fast_build_kernel<16, 48, 4, 4>); set(heat_fast_build_kernel<16, 48, 2, 4>); break;
+        default: break;
+    }
+}
+
+int launch_heat_fast_build(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const double* records, double* maps,
+                           int* ready) {
     const FastShape f = fast_shape(n);
     if (!f.ok() || N < 0 || S < 0) return pint_set_error(ctx, PINT_E_INVALID, "heat_fast_build: unsupported n");
     if (N == 0) return PINT_OK;
     const FastPlan Q{static_cast<int>(n), N, S, 0, maps, pint_affine_ldm(n), records,
-                     records + N * S * fast_blk(f.NP())};
+                     records + N * S * fast_blk(f.NP()), ready,
+                     ready ? reinterpret_cast<unsigned long long*>(ready + ((N + 1) & ~1ll)) : nullptr};
     if (S == 0) return pint_set_error(ctx, PINT_E_INVALID, "heat_fast_build: S >= 1 required");
     switch (f.P * 1000 + f.R) {
         case 2016: return launch_fast<2, 16>(ctx, Q);
