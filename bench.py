@@ -54,7 +54,7 @@ WORKLOADS = {
 def chain_floor(n: int, slices: int, S: int, lat, build_ms: float, sm_mhz: float, sms: int = 148) -> dict:
     """The exact build's real bound: every column is a chain of S*n dependent rows (forward + back
     row latencies measured live by pint_probe_latency), run in `waves` rounds of resident columns
-    on the `sms` SMs the build has (148, or 132 beside the concurrent 16-CTA chain)."""
+    on the `sms` SMs the build has (148, or fewer beside the concurrent chain: chain_sms)."""
     row = float(lat[5] + lat[6])
     if 282 <= n <= 520:  # heat_build_tmem_kernel: one 5-warp CTA per SM per slice quarter
         waves = -(-slices * -(-(-(-n // 32)) // 4) // sms)
@@ -63,6 +63,12 @@ def chain_floor(n: int, slices: int, S: int, lat, build_ms: float, sm_mhz: float
     floor_ms = waves * S * n * row / (sm_mhz * 1e3)
     return {"chain_floor_ms": floor_ms, "frac_of_chain_floor": floor_ms / build_ms, "chain_row_cycles": row,
             "chain_waves": waves, "build_sms": sms}
+
+
+def chain_sms(n: int) -> int:
+    """SMs the concurrent chain holds beside the build (launch_affine_chain_on): the wide chain
+    (128 rows per CTA) when 256 < n <= 512 and n % 16 == 0, else one 32-row CTA per SM."""
+    return -(-n // 128) if 256 < n <= 512 and n % 16 == 0 else -(-n // 32)
 
 
 def workload_name(args) -> str:
@@ -929,7 +935,7 @@ def heat_bench(args, rank, world, local):
                                               "%globaltimer), the chain running beside it") if overlap
                                              else "CUDA events around the launch on its stream",
                          **chain_floor(n, hi - lo, S, lat, build_ms, csum.get("sm_mhz") or 1965.0,
-                                       148 - 16 if overlap else 148)},
+                                       148 - chain_sms(n) if overlap else 148)},
             "clocks": csum,
             "cpu_baseline": cpu,
             "fast_build": fast,

@@ -1109,7 +1109,8 @@ int heat_build_chain(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64
     cudaMemsetAsync(reinterpret_cast<char*>(ready) + ready_bytes, 0xff, 8, ctx->stream);  // (min start)
     cudaMemsetAsync(reinterpret_cast<char*>(ready) + ready_bytes + 8, 0, 16, ctx->stream);
     ctx->span_words = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ready) + ready_bytes);
-    if (const int rc = launch_affine_chain_on(ctx, ctx->stream, n, N, maps, y0, y, ready, target)) return rc;
+    if (const int rc = launch_affine_chain_on(ctx, ctx->stream, n, N, maps, y0, y, ready, target, fast ? 0 : 128))
+        return rc;
     if (overlap_env == 2) cudaEventRecord(ctx->evc, ctx->stream);  // (test hook: serialise the build behind the chain)
     if (const int rc = fast ? launch_heat_fast_build(ctx, n, N, S, records, maps, ready)
                             : launch_heat_build_steps(ctx, n, N, S, step_off, records, maps, per_slice_ns, guarded, 0,

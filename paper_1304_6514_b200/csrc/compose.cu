@@ -16,6 +16,8 @@
 // Maps are the row-major augmented blocks [G | c] with leading dimension ldm (pint_cuda.h).
 // Roofline: TREE is FP64 tensor (2 n^3 flops per pair); CHAIN is latency/L2 bound.
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -220,6 +222,202 @@ __global__ void __launch_bounds__(32) affine_chain_cluster_kernel(int n, long lo
     cluster.sync();  // no CTA leaves while a peer may still write into its shared memory
 }
 
+// ---- the WIDE chain: 32 W rows per CTA, maps streamed by TMA (n in (256, 512], n % 16 == 0) -----
+// Bit-exact like the cluster chain above (lane = row, sum_k G(i,k) y_k sequential in k, then + c_i).
+// A CTA's 32W x (n+1) block does not sit in shared memory, so each consumer warp streams its 32 rows
+// through a ring of 16 KB boxes: the maps seen as a 4-D tensor {16 columns, n rows, n/16 column
+// blocks, N maps} (strides 8 B, 8 ldm B, 128 B, 8 n ldm B), box {16, 32, 4, 1} = 64 columns x 32
+// rows with the 128-byte swizzle, so lane = row reads its 16-byte pairs conflict-free. One producer
+// warp issues every box (full/empty mbarrier pairs per slot); the consumers only wait, sum and
+// release, loading one 8-pair group ahead of the DADD chain. Beside the exact build W = 4 (4 SMs at
+// n = 512 instead of 16: the build gets 144), see launch_affine_chain_on.
+constexpr int kWideBlk = 4, kWideCols = 16 * kWideBlk, kWideRingTotal = 12;
+constexpr int kWideSlot = 32 * kWideCols;  // doubles
+
+template <int kWideWarps>
+__global__ void __launch_bounds__(32 * (kWideWarps + 1)) affine_chain_wide_kernel(
+    const __grid_constant__ CUtensorMap tm, int n, long long N, int ldm, const double* __restrict__ maps,
+    const double* __restrict__ y0, double* __restrict__ y, const int* ready, int target, FailRec* fail) {
+    constexpr int kRows = 32 * kWideWarps, kRing = kWideRingTotal / kWideWarps;
+    extern __shared__ __align__(1024) double sm_raw[];
+    if (ready) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    // (1024-byte alignment for the swizzled boxes, by offsetting sm_raw itself: the pointer stays a
+    // shared-window pointer, so the row reads compile to LDS, not generic loads)
+    double* sm = sm_raw + ((((smem_u32(sm_raw) + 1023u) & ~1023u) - smem_u32(sm_raw)) >> 3);
+    cg::cluster_group cluster = cg::this_cluster();
+    const unsigned rank = cluster.block_rank(), csize = cluster.num_blocks();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ny = (n + kWideCols - 1) / kWideCols * kWideCols;
+    const int nch = (n + kWideCols - 1) / kWideCols;
+    // [warps][kRing][kWideBlk][32 rows][16] | y [2][ny] | full [warps][kRing] | empty [..] | 2 y barriers
+    double* ys = sm + kWideWarps * kRing * kWideSlot;
+    const unsigned full0 = smem_u32(ys + 2 * ny), empty0 = full0 + 8u * kWideWarps * kRing;
+    const unsigned ybar0 = empty0 + 8u * kWideWarps * kRing;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2 * kWideWarps * kRing + 2; ++b) mbar_init(full0 + 8u * b);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    for (int i = threadIdx.x; i < 2 * ny; i += blockDim.x) ys[i] = (i < n) ? y0[i] : 0.0;
+    cluster.sync();  // barriers and y initialised everywhere before any copy lands or remote write
+    const long long total = N * nch;
+    if (warp == kWideWarps) {  // ---- the producer: lane 0 issues every box of every consumer warp
+        if (lane == 0) {
+            bool gave_up = false;
+            long long j = 0;
+            int c = 0, slot = 0;
+            unsigned use = 0;  // uses of `slot` so far
+            for (long long q = 0; q < total; ++q) {
+                if (c == 0 && ready && !gave_up) {  // map j must be complete (its builders counted)
+                    int v;
+                    const unsigned long long t0 = pint_dev::globaltimer();
+                    do {
+                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(ready + j) : "memory");
+                        if (v < target && pint_dev::globaltimer() - t0 > 1000000000ull) {
+                            pint_dev::record_failure(fail, kSerializedIndex, PINT_E_SERIALIZED, static_cast<double>(j));
+                            gave_up = true;
+                            break;
+                        }
+                    } while (v < target);
+                    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+                }
+                for (int w = 0; w < kWideWarps; ++w) {
+                    const int row0 = static_cast<int>(rank) * kRows + 32 * w;
+                    if (row0 >= n) break;
+                    const unsigned fb = full0 + 8u * (w * kRing + slot), eb = empty0 + 8u * (w * kRing + slot);
+                    if (use > 0) mbar_wait(eb, (use - 1) & 1);  // the consumer released the slot
+                    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(fb),
+                                 "r"(8u * kWideSlot)
+                                 : "memory");
+                    asm volatile(
+                        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
+                        "{%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(sm + (w * kRing + slot) * kWideSlot)),
+                        "l"(reinterpret_cast<unsigned long long>(&tm)), "r"(0), "r"(row0), "r"(c * kWideBlk),
+                        "r"(static_cast<int>(j)), "r"(fb)
+                        : "memory");
+                }
+                if (++slot == kRing) slot = 0, ++use;
+                if (++c == nch) c = 0, ++j;
+            }
+        }
+    } else {  // ---- consumers: lane = row
+        const int row0 = static_cast<int>(rank) * kRows + warp * 32, row = row0 + lane;
+        const bool mine = row < n;
+        const double* ring = sm + warp * kRing * kWideSlot + lane * 16;
+        const unsigned wfull = full0 + 8u * warp * kRing, wempty = empty0 + 8u * warp * kRing;
+// the 128-byte swizzle: 16-byte chunk i of row r sits at chunk i ^ (r & 7) of its 128-byte line
+        int off[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) off[u] = 2 * (u ^ (lane & 7));
+        int slot = 0;
+        unsigned use = 0;
+#ifdef PINT_CHAIN_PROF
+        long long tb = 0, tyw = 0, tcp = 0, tst = 0, tp = clock64();
+#define WMARK(v) do { const long long t1 = clock64(); v += t1 - tp; tp = t1; } while (0)
+#else
+#define WMARK(v) do { } while (0)
+#endif
+        for (long long j = 0; j < N; ++j) {
+            const int yb = static_cast<int>(j & 1);
+            const double2* y2 = reinterpret_cast<const double2*>(ys + yb * ny);
+            double s = 0.0;
+            if (row0 < n) {
+                // the map's n/2 column pairs in order, in 8-pair groups (a 16-column block of a box),
+                // each group's operands loaded during the previous group's DADDs. The box loop is
+                // straight-line (a warp issues in order: branches between groups would serialise the
+                // integer work with the DADD chain); a box's slot is released once it is summed.
+                const double* cur = ring + slot * kWideSlot;
+                WMARK(tcp);
+                mbar_wait(wfull + 8u * slot, use & 1);
+                WMARK(tb);
+                // c_i once map j's first box has landed: the producer acquired map j before issuing
+                // it, and the barrier's phase carries that here (the build writes c: an L2 load)
+                const double cc =
+                    mine ? __ldcg(maps + j * static_cast<long long>(n) * ldm + static_cast<long long>(row) * ldm + n) : 0.0;
+                double2 gv[8], yq[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) gv[u] = *reinterpret_cast<const double2*>(cur + off[u]), yq[u] = y2[u];
+                for (int c = 0; c < nch; ++c) {
+                    const int nb = min(kWideBlk, (n - c * kWideCols) / 16);  // 16-column blocks in box c
+                    int nslot = slot + 1;
+                    unsigned nuse = use;
+                    if (nslot == kRing) nslot = 0, ++nuse;
+                    const double* nxt = ring + nslot * kWideSlot;
+                    const bool more = c + 1 < nch;
+                    const double2* yc = y2 + c * (kWideCols / 2);
+                    if (nb == kWideBlk) {  // a full box: 4 groups, straight-line
+#pragma unroll
+                        for (int b = 0; b < kWideBlk; ++b) {
+                            if (b == kWideBlk - 1 && more) {
+                                WMARK(tcp);
+                                mbar_wait(wfull + 8u * nslot, nuse & 1);
+                                WMARK(tb);
+                            }
+                            const double* gn = b + 1 < kWideBlk ? cur + (b + 1) * 32 * 16 : nxt;
+                            const double2* yn = yc + (b + 1) * 8;
+                            const bool ld = b + 1 < kWideBlk || more;
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {  // matvec order: k sequential
+                                s = __dadd_rn(s, __dmul_rn(gv[u].x, yq[u].x));
+                                s = __dadd_rn(s, __dmul_rn(gv[u].y, yq[u].y));
+                                if (ld) gv[u] = *reinterpret_cast<const double2*>(gn + off[u]), yq[u] = yn[u];
+                            }
+                        }
+                    } else {  // the last, partial box (n % 64 != 0)
+                        for (int b = 0; b < nb; ++b) {
+                            const bool ld = b + 1 < nb;
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                s = __dadd_rn(s, __dmul_rn(gv[u].x, yq[u].x));
+                                s = __dadd_rn(s, __dmul_rn(gv[u].y, yq[u].y));
+                                if (ld)
+                                    gv[u] = *reinterpret_cast<const double2*>(cur + (b + 1) * 32 * 16 + off[u]),
+                                    yq[u] = yc[(b + 1) * 8 + u];
+                            }
+                        }
+                    }
+                    __syncwarp();  // box c is summed: hand its slot back to the producer
+                    if (lane == 0)
+                        asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(wempty + 8u * slot)
+                                     : "memory");
+                    slot = nslot, use = nuse, cur = nxt;
+                }
+                s = __dadd_rn(s, cc);  // + c_i
+            }
+            WMARK(tcp);
+            // y_{j+1}: every CTA's rows land in every CTA's buffer yb ^ 1 (8n bytes expected per map)
+            const unsigned ybar = ybar0 + 8u * (yb ^ 1);
+            if (threadIdx.x == 0)
+                asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(ybar),
+                             "r"(8u * static_cast<unsigned>(n))
+                             : "memory");
+            if (mine) {
+                const unsigned la = smem_u32(ys + (yb ^ 1) * ny + row);
+                for (unsigned cc2 = 0; cc2 < csize; ++cc2) {
+                    unsigned ra, rb;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(la), "r"(cc2));
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(ybar), "r"(cc2));
+                    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(ra),
+                                 "d"(s), "r"(rb)
+                                 : "memory");
+                }
+            }
+            WMARK(tst);
+            mbar_wait(ybar, static_cast<unsigned>((j >> 1) & 1));  // y_{j+1} complete here
+            WMARK(tyw);
+        }
+#ifdef PINT_CHAIN_PROF
+        if (lane == 0 && (rank == 0 || rank == csize - 1))
+            printf("wide rank %u warp %d: per map box-wait %lld compute %lld send %lld y-wait %lld cycles\n", rank, warp,
+                   tb / N, tcp / N, tst / N, tyw / N);
+#endif
+#undef WMARK
+        if (mine) y[row] = ys[(N & 1) * ny + row];
+        if (ready && rank == 0 && threadIdx.x == 0)  // (the span words behind the counters: chain end)
+            reinterpret_cast<unsigned long long*>(const_cast<int*>(ready) + ((N + 1) & ~1ll))[2] = pint_dev::globaltimer();
+    }
+    cluster.sync();  // no CTA leaves while a peer may still write into its shared memory
+}
+
 // ---- DMMA pair kernel ------------------------------------------------------------------------
 // CTA = 2 x 2 warps, warp tile (8 MI) x 32: BM = 16 MI rows, BN = 64 columns (+ the extra fragment).
 constexpr int BN = 64, BK = 16, kStages = 3;
@@ -396,8 +594,57 @@ int launch_affine_chain(pint_ctx* ctx, int64_t n, int64_t N, const double* maps,
 }
 
 int launch_affine_chain_on(pint_ctx* ctx, cudaStream_t stream, int64_t n, int64_t N, const double* maps,
-                           const double* y0, double* y, const int* ready, int target) {
+                           const double* y0, double* y, const int* ready, int target, int wide_chain_rows) {
     if (n < 1 || N < 0) return pint_set_error(ctx, PINT_E_INVALID, "affine_chain: bad sizes");
+    // the wide chain (TMA-streamed, 32 W rows per CTA) for 256 < n <= 512 with n % 16 == 0: W = 4
+    // beside the exact build (wide_rows 128: it keeps up with the build on 4 SMs, the build gets
+    // 144), else W = 2 (the fastest shape: 3.6 us per map at n = 512 on 8 SMs, against 4.8 us for the
+    // 16-CTA cluster chain). PINT_WIDE_CHAIN=0 turns it off, PINT_WIDE_W forces W (experiments).
+    static const int wide_env = [] {
+        const char* e = std::getenv("PINT_WIDE_CHAIN");
+        return e ? std::atoi(e) : 1;
+    }();
+    static const int wide_w = [] {
+        const char* e = std::getenv("PINT_WIDE_W");
+        const int w = e ? std::atoi(e) : 0;
+        return w == 1 || w == 2 || w == 4 ? w : 0;
+    }();
+    const int W = wide_w ? wide_w : (ready && wide_chain_rows >= 128) ? 4 : 2;
+    if (wide_env && n > 256 && n <= 512 && n % 16 == 0 && N > 0 && (n + 32 * W - 1) / (32 * W) <= 16) {
+        const int ldm = static_cast<int>(pint_affine_ldm(n));
+        auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(pint_tensor_map_encoder());
+        if (!enc) return pint_set_error(ctx, PINT_E_CUDA, "affine_chain: cuTensorMapEncodeTiled unavailable");
+        CUtensorMap tm;
+        const cuuint64_t dims[4] = {16, static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(n / 16),
+                                    static_cast<cuuint64_t>(N)};
+        const cuuint64_t strides[3] = {static_cast<cuuint64_t>(8 * ldm), 128,
+                                       static_cast<cuuint64_t>(8 * static_cast<int64_t>(n) * ldm)};
+        const cuuint32_t box[4] = {16, 32, kWideBlk, 1}, estr[4] = {1, 1, 1, 1};
+        if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(maps), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return pint_set_error(ctx, PINT_E_CUDA, "affine_chain: tensor map failed");
+        const size_t ny = static_cast<size_t>((n + kWideCols - 1) / kWideCols * kWideCols);
+        const size_t smem = 1024 + sizeof(double) * (kWideRingTotal * kWideSlot + 2 * ny) + 8 * (2 * kWideRingTotal + 2);
+        auto kern = W == 4 ? affine_chain_wide_kernel<4> : W == 2 ? affine_chain_wide_kernel<2> : affine_chain_wide_kernel<1>;
+        pint_kernel_attrs(reinterpret_cast<const void*>(kern));
+        const unsigned C = static_cast<unsigned>((n + 32 * W - 1) / (32 * W));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(C, 1, 1);
+        cfg.blockDim = dim3(32 * (W + 1), 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, tm, static_cast<int>(n), static_cast<long long>(N), ldm, maps, y0, y, ready,
+                           target, ctx->d_fail);
+        return pint_check_launch(ctx, "affine_chain_wide_kernel");
+    }
     if (n <= 32 * kClusterMax && N > 0) {
         const int ldm = static_cast<int>(pint_affine_ldm(n));
         const size_t ny = static_cast<size_t>((n + 15) & ~15);

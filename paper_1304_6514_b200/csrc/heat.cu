@@ -1180,6 +1180,8 @@ int launch_build(pint_ctx* ctx, BuildPlan P) {
 
 }  // namespace
 
+void* pint_tensor_map_encoder() { return reinterpret_cast<void*>(tensor_map_encoder()); }
+
 int64_t heat_records_doubles(int64_t n, int64_t N, int64_t S) { return records_doubles(n, N, S); }
 
 int launch_heat_factor_range(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, int64_t j0, int64_t Nc,

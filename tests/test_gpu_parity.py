@@ -447,6 +447,21 @@ def test_affine_tree_random_maps(ctx):
         assert np.max(np.abs(y - chain)) <= 1e-11 * scale
 
 
+@pytest.mark.parametrize("N,n", [(5, 272), (9, 320), (3, 400), (11, 512), (2, 496)])
+def test_affine_chain_wide_random_maps(ctx, N, n):
+    """The TMA-streamed wide chain (256 < n <= 512, n % 16 == 0; compose.cu affine_chain_wide_kernel):
+    bit-exact against the oracle's compose_sweep order — full and partial 64-column boxes, one or
+    several CTAs, rows past n in the last CTA."""
+    rng = np.random.default_rng(n)
+    G = rng.uniform(-1, 1, (N, n, n)) / np.sqrt(n)
+    c = rng.uniform(-1, 1, (N, n))
+    y0 = rng.uniform(-1, 1, n)
+    y = np.empty(n)
+    ctx.check(ctx.lib.pint_affine_compose(ctx.h, capi.COMPOSE_CHAIN, n, N, capi.ptr(G), capi.ptr(c), capi.ptr(y0),
+                                          capi.ptr(y)))
+    assert np.array_equal(y, O.affine_chain(G, c, y0))
+
+
 def test_affine_compose_order(ctx):
     """test_nievergelt.cpp:104-118: maps applied in slice order."""
     maps = []

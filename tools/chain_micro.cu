@@ -1,9 +1,21 @@
-// Section timing of affine_chain_cluster_kernel (-DPINT_CHAIN_PROF): tools/_chain_micro n N
+// Section timing of affine_chain_cluster_kernel / affine_chain_wide_kernel (-DPINT_CHAIN_PROF):
+//   tools/_chain_micro n N      (PINT_WIDE_CHAIN=2 PINT_WIDE_W=1|2|4: the wide chain)
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
 
 #include "../paper_1304_6514_b200/csrc/compose.cu"
+
+void* pint_tensor_map_encoder() {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess) p = nullptr;
+    return p;
+}
+void pint_kernel_attrs(const void* f) {
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+}
 
 int pint_set_error(pint_ctx*, int code, const std::string& msg) {
     std::fprintf(stderr, "error %d: %s\n", code, msg.c_str());
@@ -29,7 +41,18 @@ int main(int argc, char** argv) {
     cudaMemcpy(d, h.data(), 8 * h.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(dy0, y0.data(), 8 * n, cudaMemcpyHostToDevice);
     pint_ctx ctx;
-    launch_affine_chain(&ctx, n, N, d, dy0, dy);
-    cudaDeviceSynchronize();
+    for (int rep = 0; rep < 2; ++rep) {
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0);
+        launch_affine_chain(&ctx, n, N, d, dy0, dy);
+        cudaEventRecord(e1);
+        cudaDeviceSynchronize();
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        std::printf("chain n=%d N=%d: %.3f ms (%.2f us per map) %s\n", n, N, ms, 1e3 * ms / N,
+                    cudaGetErrorString(cudaGetLastError()));
+    }
     return 0;
 }
