@@ -551,6 +551,230 @@ affine_pair_kernel(long long n, long long ldm, const double* __restrict__ earlie
     }
 }
 
+// ---- DMMA pair kernel, TMA-fed (16 | n) ---------------------------------------------------------
+// The same augmented product out_p = later_p o earlier_p, CTA tile 128 x 128 (8 warps of 64 x 32;
+// thread 0 also issues the copies), k tiles of 16 in a kPairStages-deep ring filled by TMA with full /
+// empty mbarriers — no per-thread address arithmetic and no __syncthreads in the k loop (the
+// cp.async kernel above spends as many integer instructions on its copies as it issues DMMAs).
+//  * A (later, rows x k): 3-D tensor {n, n, pairs}, box {16 k, 128 rows} with the 128-byte swizzle:
+//    row r's 16-byte chunk i at i ^ (r & 7).
+//  * B (earlier, k x columns): 4-D tensor {16 columns, n rows, n/16 column blocks, pairs}, box
+//    {16, 16, 8, 1} = [8 column blocks][16 k][16 columns], swizzled per 128-byte k line.
+//  * the translation column (c1 = earlier's column n) for the last column tile: a {8, 16} box of
+//    the {n+1, n, pairs} tensor (columns past n zero-filled), unswizzled.
+//  A k step uses k offsets {0, 1, 4, 5} (+ 0, 2, 8, 10) for the four k lanes instead of 0..3: the
+//  fragment reads then touch each bank twice (2 wavefronts, the minimum) for A and for B — with
+//  consecutive k, B's four rows XOR into the same half of the 128-byte line (4 wavefronts).
+constexpr int kPairStages = 4;  // (a power of 2)
+constexpr unsigned kPairA = 128 * 16 * 8, kPairB = 8 * 16 * 16 * 8, kPairX = 16 * 8 * 8;  // bytes per stage
+constexpr unsigned kPairStage = kPairA + kPairB + kPairX;
+struct PairMaps {
+    CUtensorMap a, b, x;
+};
+constexpr size_t pair_tma_smem() { return 1024 + kPairStages * kPairStage + 16 * kPairStages; }
+
+__global__ void __launch_bounds__(256, 1)
+affine_pair_tma_kernel(const __grid_constant__ PairMaps tm, int n, long long ldm, int pairs,
+                       const double* __restrict__ later, long long l_stride, double* __restrict__ out,
+                       long long o_stride) {
+    extern __shared__ __align__(1024) unsigned char pt_raw[];
+    unsigned char* sm = pt_raw + ((((smem_u32(pt_raw) + 1023u) & ~1023u) - smem_u32(pt_raw)));
+    const unsigned base = smem_u32(sm);
+    const unsigned full0 = base + kPairStages * kPairStage, empty0 = full0 + 8 * kPairStages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kTiles = (n + 15) / 16, tiles1 = (n + 127) / 128;
+    const int tiles = pairs * tiles1 * tiles1;
+    // this CTA's tiles are blockIdx.x, + gridDim.x, ... (one by default, see launch_pairs_tma); their
+    // k tiles form one sequence q = (local tile) * kTiles + kt through the ring
+    const int my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const long long total_q = static_cast<long long>(my_tiles) * kTiles;
+    struct Tile {
+        int p, row0, col0;
+        bool xtile;
+    };
+    auto tile_of = [&](int lt) {
+        const int t = blockIdx.x + lt * gridDim.x;
+        Tile T;
+        T.p = t / (tiles1 * tiles1);
+        const int r = t - T.p * tiles1 * tiles1;
+        T.row0 = (r / tiles1) * 128;
+        T.col0 = (r % tiles1) * 128;
+        T.xtile = T.col0 + 128 >= n;  // the tile holding the last columns also computes column n
+        return T;
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kPairStages; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(full0 + 8 * s) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;\n" ::"r"(empty0 + 8 * s) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    // thread 0 also feeds the ring: step q into stage q % kPairStages once every warp has released
+    // the stage's previous step (a 9th, producer warp would cap the registers at 168: 3 warps on
+    // one SM sub-partition)
+    // (the producer walks its own (tile, k tile) cursor: no 64-bit divisions on thread 0, whose warp
+    // every other warp waits for through the ring)
+    long long pq = 0;
+    int pkt = 0, plt = 0;
+    Tile PT = tile_of(0);
+    auto produce_next = [&]() {
+        const int s = static_cast<int>(pq & (kPairStages - 1));
+        if (pq >= kPairStages) mbar_wait(empty0 + 8 * s, static_cast<unsigned>((pq / kPairStages) - 1) & 1);
+        const unsigned fb = full0 + 8 * s, dst = base + s * kPairStage;
+        asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(fb),
+                     "r"(kPairA + kPairB + (PT.xtile ? kPairX : 0u))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+            "%3, %4}], [%5];\n" ::"r"(dst),
+            "l"(reinterpret_cast<unsigned long long>(&tm.a)), "r"(16 * pkt), "r"(PT.row0), "r"(PT.p), "r"(fb)
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+            "%3, %4, %5}], [%6];\n" ::"r"(dst + kPairA),
+            "l"(reinterpret_cast<unsigned long long>(&tm.b)), "r"(0), "r"(16 * pkt), "r"(PT.col0 / 16), "r"(PT.p),
+            "r"(fb)
+            : "memory");
+        if (PT.xtile)
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
+                "{%2, %3, %4}], [%5];\n" ::"r"(dst + kPairA + kPairB),
+                "l"(reinterpret_cast<unsigned long long>(&tm.x)), "r"(n), "r"(16 * pkt), "r"(PT.p), "r"(fb)
+                : "memory");
+        ++pq;
+        if (++pkt == kTiles) {
+            pkt = 0;
+            if (++plt < my_tiles) PT = tile_of(plt);
+        }
+    };
+    if (threadIdx.x == 0)
+        while (pq < kPairStages && pq < total_q) produce_next();
+    // warp (wm, wn) owns rows wm*64 .. +63, columns wn*32 .. +31 of a tile
+    const int wm = warp >> 2, wn = warp & 3;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int kofs = (t4 & 1) + 4 * (t4 >> 1);  // k lane -> k offset {0, 1, 4, 5}
+    long long q = 0;
+    for (int lt = 0; lt < my_tiles; ++lt) {
+        const Tile T = tile_of(lt);
+        const bool extra = T.xtile && wn == 3;  // + the 8-column fragment holding column n
+        double acc[8][5][2];
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 5; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+        for (int kt = 0; kt < kTiles; ++kt, ++q) {
+            const int s = static_cast<int>(q & (kPairStages - 1));
+            mbar_wait(full0 + 8 * s, static_cast<unsigned>(q / kPairStages) & 1);
+            const unsigned char* As = sm + s * kPairStage;
+            const unsigned char* Bs = As + kPairA;
+            const double* Xs = reinterpret_cast<const double*>(Bs + kPairB);
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {  // k = kb + kofs, kb in {0, 2, 8, 10}
+                const int k = 2 * (ks & 1) + 8 * (ks >> 1) + kofs;
+                double af[8], bf[4];
+#pragma unroll
+                for (int mi = 0; mi < 8; ++mi) {  // A[row][k]: row & 7 == g
+                    const int r = wm * 64 + mi * 8 + g;
+                    af[mi] = *reinterpret_cast<const double*>(As + r * 128 + (((k >> 1) ^ g) << 4) + ((k & 1) << 3));
+                }
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) {  // B[k][c]: block c / 16, k line, chunk (c & 15) / 2 ^ (k & 7)
+                    const int c = wn * 32 + ni * 8 + g;
+                    bf[ni] = *reinterpret_cast<const double*>(Bs + (c >> 4) * 2048 + k * 128 +
+                                                              ((((c & 15) >> 1) ^ (k & 7)) << 4) + ((c & 1) << 3));
+                }
+#pragma unroll
+                for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+                if (extra) {
+                    const double bx = Xs[k * 8 + g];
+#pragma unroll
+                    for (int mi = 0; mi < 8; ++mi) dmma(acc[mi][4][0], acc[mi][4][1], af[mi], bx);
+                }
+            }
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(empty0 + 8 * s)
+                             : "memory");
+            if (threadIdx.x == 0 && pq < total_q) produce_next();
+        }
+        const double* L = later + T.p * l_stride;
+        double* O = out + T.p * o_stride;
+        const long long nc = n + 1;
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi) {
+            const long long r = T.row0 + wm * 64 + mi * 8 + g;
+            if (r >= n) continue;
+#pragma unroll
+            for (int ni = 0; ni < 5; ++ni) {
+                if (ni == 4 && !extra) continue;
+                const long long c = ni == 4 ? n + t4 * 2 : T.col0 + wn * 32 + ni * 8 + t4 * 2;
+                if (ni < 4 && c >= n) continue;
+                double v0 = acc[mi][ni][0], v1 = acc[mi][ni][1];
+                if (c == n) v0 += L[r * ldm + n];  // + c2
+                if (c + 1 < n) {
+                    *reinterpret_cast<double2*>(O + r * ldm + c) = make_double2(v0, v1);
+                } else if (c < nc) {
+                    O[r * ldm + c] = v0;
+                }
+            }
+        }
+    }
+}
+
+int launch_pairs_tma(pint_ctx* ctx, long long n, long long P, const double* earlier, long long e_stride,
+                     const double* later, long long l_stride, double* out, long long o_stride) {
+    auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(pint_tensor_map_encoder());
+    if (!enc) return pint_set_error(ctx, PINT_E_CUDA, "affine_pair: cuTensorMapEncodeTiled unavailable");
+    const long long ldm = pint_affine_ldm(n);
+    PairMaps M;
+    const cuuint32_t e1[4] = {1, 1, 1, 1};
+    {
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(P)};
+        const cuuint64_t str[2] = {static_cast<cuuint64_t>(8 * ldm), static_cast<cuuint64_t>(8 * l_stride)};
+        const cuuint32_t box[3] = {16, 128, 1};
+        if (enc(&M.a, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(later), dims, str, box, e1,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return pint_set_error(ctx, PINT_E_CUDA, "affine_pair: tensor map A failed");
+    }
+    {
+        const cuuint64_t dims[4] = {16, static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(n / 16),
+                                    static_cast<cuuint64_t>(P)};
+        const cuuint64_t str[3] = {static_cast<cuuint64_t>(8 * ldm), 128, static_cast<cuuint64_t>(8 * e_stride)};
+        const cuuint32_t box[4] = {16, 16, 8, 1};
+        if (enc(&M.b, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(earlier), dims, str, box, e1,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return pint_set_error(ctx, PINT_E_CUDA, "affine_pair: tensor map B failed");
+    }
+    {
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(n + 1), static_cast<cuuint64_t>(n),
+                                    static_cast<cuuint64_t>(P)};
+        const cuuint64_t str[2] = {static_cast<cuuint64_t>(8 * ldm), static_cast<cuuint64_t>(8 * e_stride)};
+        const cuuint32_t box[3] = {8, 16, 1};
+        if (enc(&M.x, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(earlier), dims, str, box, e1,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return pint_set_error(ctx, PINT_E_CUDA, "affine_pair: tensor map x failed");
+    }
+    pint_kernel_attrs(reinterpret_cast<const void*>(affine_pair_tma_kernel));
+    const long long t = (n + 127) / 128, tiles = P * t * t;
+    // one tile per CTA by default: measured at n = 512, 128 pairs, a persistent grid of one CTA per SM
+    // (14 tiles each) ran 26.6 TFLOP/s against 29.8 for one tile per CTA (PINT_PAIR_GRID: experiments)
+    static const long long grid_env = [] {
+        const char* e = std::getenv("PINT_PAIR_GRID");
+        return e ? std::atoll(e) : 0ll;
+    }();
+    const unsigned grid = static_cast<unsigned>(grid_env ? std::min<long long>(tiles, grid_env) : tiles);
+    affine_pair_tma_kernel<<<grid, 256, pair_tma_smem(), ctx->stream>>>(M, static_cast<int>(n), ldm,
+                                                                        static_cast<int>(P), later, l_stride, out,
+                                                                        o_stride);
+    return pint_check_launch(ctx, "affine_pair_tma_kernel");
+}
+
 template <int MI>
 int launch_pairs_mi(pint_ctx* ctx, long long n, long long P, const double* earlier, long long e_stride,
                     const double* later, long long l_stride, double* out, long long o_stride) {
@@ -580,7 +804,21 @@ int launch_pairs(pint_ctx* ctx, long long n, long long P, const double* earlier,
     }();
     // 128-row tiles (warp tile 64 x 32: half the B-fragment loads per DMMA) pay once the grid is
     // large enough to fill the SMs anyway (n = 512: tree -9%); at n = 128 the 64-row tiles win
-    const int mi = mi_env ? mi_env : n >= 384 ? 8 : 4;
+    // the TMA-fed 128 x 128 kernel where 16 | n (PINT_PAIR_TMA=0: the cp.async kernel)
+    static const int tma_env = [] {
+        const char* e = std::getenv("PINT_PAIR_TMA");
+        return e ? std::atoi(e) : 1;
+    }();
+    // Measured (tools/prof_pair.py, n = 512): the TMA kernel from 8 pairs up (29.8-30.7 TFLOP/s at
+    // 128 pairs, cuBLAS batched DGEMM 30.9), the 128 x 64 cp.async tiles otherwise, and 64 x 64 tiles
+    // when even those leave SMs idle (2-4 pairs: 11.7-17.2 against 7.3-14.1). Where 128 does not
+    // divide n the 128-wide TMA tiles waste work (n = 144: 5.9 against 8.0); below n = 384 the
+    // cp.async kernel is as fast.
+    const long long t128 = n / 128;
+    if (tma_env && !mi_env && n % 128 == 0 && n >= 384 && 2 * P * t128 * t128 >= ctx->sm_count)
+        return launch_pairs_tma(ctx, n, P, earlier, e_stride, later, l_stride, out, o_stride);
+    int mi = mi_env ? mi_env : n >= 384 ? 8 : 4;
+    if (!mi_env && mi == 8 && P * ((n + 127) / 128) * ((n + BN - 1) / BN) < ctx->sm_count) mi = 4;
     if (mi == 8) return launch_pairs_mi<8>(ctx, n, P, earlier, e_stride, later, l_stride, out, o_stride);
     if (mi == 6) return launch_pairs_mi<6>(ctx, n, P, earlier, e_stride, later, l_stride, out, o_stride);
     return launch_pairs_mi<4>(ctx, n, P, earlier, e_stride, later, l_stride, out, o_stride);
