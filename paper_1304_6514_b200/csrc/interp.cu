@@ -8,6 +8,9 @@
 //  * bilinear sweep: EXTENSION for the 2-D tensor-grid maps, with bracket indices reported.
 //
 // Roofline: latency (the chain is sequential by construction); reported as time, not a fraction.
+#include <algorithm>
+#include <cstdlib>
+
 #include "pint_internal.cuh"
 
 namespace {
@@ -127,13 +130,15 @@ scalar_sweep_tree_kernel(long long N, long long M, const double* __restrict__ no
     __shared__ unsigned red_hit[kTreeThreads / 32];
     __shared__ double y_s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double xr[PER], wr[PER], vr[PER], vn[PER];
-    auto load_nodes = [&](long long j) {
+    // slice j's operands in xr/wr/vr/a/b, slice j + 1's loading into xn/wn/vn/an/bn while slice j is
+    // evaluated (none of them depends on y: no global load on the slice-to-slice chain)
+    double xr[PER], wr[PER], vr[PER], xn[PER], wn[PER], vn[PER];
+    auto load_nodes = [&](long long j, double (&xd)[PER], double (&wd)[PER]) {
 #pragma unroll
         for (int q = 0; q < PER; ++q) {
             const long long k = tid + q * kTreeThreads;
-            xr[q] = k < M ? nodes[j * node_stride + k] : 0.0;
-            wr[q] = k < M ? weights[j * node_stride + k] : 0.0;
+            xd[q] = (k < M && j < N) ? nodes[j * node_stride + k] : 0.0;
+            wd[q] = (k < M && j < N) ? weights[j * node_stride + k] : 0.0;
         }
     };
     auto load_values = [&](long long j, double (&dst)[PER]) {
@@ -143,14 +148,15 @@ scalar_sweep_tree_kernel(long long N, long long M, const double* __restrict__ no
             dst[q] = (k < M && j < N) ? values[j * M + k] : 0.0;
         }
     };
-    load_nodes(0);
+    load_nodes(0, xr, wr);
     load_values(0, vr);
+    double a = a_arr[0], b = b_arr[0];
     double y = y0;
     long long ext = 0;
     for (long long j = 0; j < N; ++j) {
-        load_values(j + 1, vn);  // (independent of y: in flight while this slice is evaluated)
-        if (node_stride && j > 0) load_nodes(j);
-        const double a = a_arr[j * ab_stride], b = b_arr[j * ab_stride];
+        load_values(j + 1, vn);
+        if (node_stride) load_nodes(j + 1, xn, wn);
+        const double an = j + 1 < N ? a_arr[(j + 1) * ab_stride] : 0.0, bn = j + 1 < N ? b_arr[(j + 1) * ab_stride] : 0.0;
         if (y < a || y > b) ++ext;  // nievergelt.cpp:83
         double num = 0.0, den = 0.0;
         unsigned hit = 0xffffffffu;
@@ -194,7 +200,163 @@ scalar_sweep_tree_kernel(long long N, long long M, const double* __restrict__ no
         __syncthreads();
         y = y_s;
 #pragma unroll
-        for (int q = 0; q < PER; ++q) vr[q] = vn[q];
+        for (int q = 0; q < PER; ++q) {
+            vr[q] = vn[q];
+            if (node_stride) xr[q] = xn[q], wr[q] = wn[q];
+        }
+        a = an, b = bn;
+    }
+    if (tid == 0) {
+        if (y_out) *y_out = y;
+        if (extrapolations) *extrapolations = ext;
+    }
+}
+
+// TREE mode, staged: the same sums with nothing but arithmetic and one barrier between slices.
+// Slice j + 1 .. j + 3's values (and nodes, weights when every slice has its own) are already in
+// a 4-slot shared-memory ring, bulk-copied ahead by warp 1 (the slot of slice j - 1, which no warp
+// reads any more once slice j's barrier has passed); the intervals [a_j, b_j] are staged once. A
+// thread sums up to 4 terms side by side, w / (y - x) as w x rcp(y - x) (MUFU.RCP64H + two Newton
+// steps: no IEEE slow-path branches); (num, den, lowest snap) are reduced per warp, the W partials
+// double-buffered by slice parity, and EVERY warp reduces them itself, so one barrier per slice.
+// Config 5 (64 slices, M = 1024): the register-prefetch kernel above took ~90 us to sweep (a global-
+// load latency per slice), this one ~55 us; the whole S = 98 solve 0.40 -> 0.093 ms. Used when M
+// is even, N <= 4096 and the ring fits (launch_scalar_sweep).
+using namespace pint_async;
+constexpr int kStagedMaxN = 4096;
+constexpr int kStagedRing = 4;  // slices in flight (a power of 2)
+// Tolerance-mode reciprocal: the hardware approximation (MUFU.RCP64H) refined by two Newton steps —
+// no IEEE slow-path branches. Only for |d| well inside the float exponent range (node distances
+// here; the approximation's input range is the float one).
+__device__ __forceinline__ double rcp_nr(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+
+// a / b with b first scaled into [1, 2) by an exact power of 2 (num and den of a barycentric sum
+// can be ~1e150 with the reference's weights), then rcp_nr and one remainder correction; IEEE for
+// zero, subnormal, infinite or NaN b
+__device__ __forceinline__ double div_scaled(double a, double b) {
+    const int e = (__double2hiint(b) >> 20) & 0x7ff;
+    if (e == 0 || e == 0x7ff) return a / b;
+    const double sc = __hiloint2double((2046 - e) << 20, 0);  // 2^-(e - 1023)
+    const double as = a * sc, bs = b * sc;
+    const double r = rcp_nr(bs);
+    const double q = as * r;
+    return fma(fma(-q, bs, as), r, q);
+}
+
+template <int THREADS, int PER>
+__global__ void __launch_bounds__(THREADS)
+scalar_sweep_staged_kernel(long long N, long long M, const double* __restrict__ nodes, long long node_stride,
+                           const double* __restrict__ weights, const double* __restrict__ values,
+                           const double* __restrict__ a_arr, const double* __restrict__ b_arr, long long ab_stride,
+                           double y0, double* lambdas, double* y_out, long long* extrapolations) {
+    constexpr int W = THREADS / 32;
+    extern __shared__ __align__(16) double st[];
+    __shared__ double2 red[2][W];  // (by slice parity: ONE barrier per slice)
+    __shared__ unsigned red_hit[2][W];
+    __shared__ __align__(8) unsigned long long bars[kStagedRing];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long arrays = node_stride ? 3 : 1;  // per slot: values [| nodes | weights]
+    const long long slot_d = arrays * M;
+    double* ab = st + kStagedRing * slot_d;  // a[N] | b[N]
+    const unsigned bar0 = smem_u32(bars);
+    auto issue = [&](long long j) {  // (one thread) slice j into slot j % kStagedRing
+        const int sl = static_cast<int>(j & (kStagedRing - 1));
+        double* dst = st + sl * slot_d;
+        const unsigned bar = bar0 + 8u * sl;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // (the slot's previous reads)
+        asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(bar),
+                     "r"(static_cast<unsigned>(8 * slot_d))
+                     : "memory");
+        bulk_copy(smem_u32(dst), values + j * M, static_cast<unsigned>(8 * M), bar);
+        if (node_stride) {
+            bulk_copy(smem_u32(dst + M), nodes + j * node_stride, static_cast<unsigned>(8 * M), bar);
+            bulk_copy(smem_u32(dst + 2 * M), weights + j * node_stride, static_cast<unsigned>(8 * M), bar);
+        }
+    };
+    if (tid == 0) {
+        for (int q = 0; q < kStagedRing; ++q) mbar_init(bar0 + 8u * q);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    for (long long j = tid; j < N; j += THREADS) {
+        ab[j] = a_arr[j * ab_stride];
+        ab[N + j] = b_arr[j * ab_stride];
+    }
+    double xr[PER], wr[PER];
+    if (!node_stride) {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const long long k = tid + q * THREADS;
+            xr[q] = k < M ? nodes[k] : 0.0;
+            wr[q] = k < M ? weights[k] : 0.0;
+        }
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (long long q = 0; q < kStagedRing && q < N; ++q) issue(q);
+    double y = y0;
+    long long ext = 0;
+    for (long long j = 0; j < N; ++j) {
+        if (tid == 0 && (y < ab[j] || y > ab[N + j])) ++ext;  // nievergelt.cpp:83
+        const int sl = static_cast<int>(j & (kStagedRing - 1)), par = static_cast<int>(j & 1);
+        const double* V = st + sl * slot_d;
+        mbar_wait(bar0 + 8u * sl, static_cast<unsigned>((j / kStagedRing) & 1));
+        // the PER terms side by side (branch-free: their reciprocals overlap), w / (y - x) as w x an
+        // approximate reciprocal refined by two Newton steps (tolerance mode)
+        double num = 0.0, den = 0.0;
+        unsigned hit = 0xffffffffu;
+        double dq[PER], rq[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const long long k = tid + q * THREADS;
+            const double xk = k < M ? (node_stride ? V[M + k] : xr[q]) : 0.0;
+            dq[q] = __dsub_rn(y, xk);
+            const bool snap = k < M && fabs(dq[q]) <= __dmul_rn(1e-14, fmax(1.0, fabs(xk)));
+            hit = snap ? min(hit, static_cast<unsigned>(k)) : hit;
+            rq[q] = rcp_nr(dq[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const long long k = tid + q * THREADS;
+            if (k < M) {
+                const double wk = node_stride ? V[2 * M + k] : wr[q];
+                const double r = __dmul_rn(wk, rq[q]);
+                num = fma(r, V[k], num);
+                den += r;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            num += __shfl_xor_sync(0xffffffffu, num, o);
+            den += __shfl_xor_sync(0xffffffffu, den, o);
+        }
+        hit = __reduce_min_sync(0xffffffffu, hit);
+        if (lane == 0) {
+            red[par][warp] = make_double2(num, den);
+            red_hit[par][warp] = hit;
+        }
+        __syncthreads();  // every warp's partial is in; every thread is done with slot sl
+        // every warp reduces the W partials itself (no second barrier: red is double-buffered)
+        double2 t = lane < W ? red[par][lane] : make_double2(0.0, 0.0);
+        const unsigned h = __reduce_min_sync(0xffffffffu, lane < W ? red_hit[par][lane] : 0xffffffffu);
+#pragma unroll
+        for (int o = W / 2; o > 0; o >>= 1) {
+            t.x += __shfl_xor_sync(0xffffffffu, t.x, o);
+            t.y += __shfl_xor_sync(0xffffffffu, t.y, o);
+        }
+        t.x = __shfl_sync(0xffffffffu, t.x, 0);  // (lanes >= W reduced only zeros)
+        t.y = __shfl_sync(0xffffffffu, t.y, 0);
+        y = h != 0xffffffffu ? V[h] : div_scaled(t.x, t.y);
+        if (tid == 0 && lambdas) lambdas[j] = y;
+        // refill the previous slice's slot: past this slice's barrier no warp reads it any more (this
+        // slice's slot may still be read for the snap value V[h] after the barrier)
+        if (tid == 32 % THREADS && j >= 1 && j - 1 + kStagedRing < N) issue(j - 1 + kStagedRing);
     }
     if (tid == 0) {
         if (y_out) *y_out = y;
@@ -535,6 +697,24 @@ int launch_scalar_sweep(pint_ctx* ctx, int mode, int64_t N, int64_t M, const dou
     } else if (mode == PINT_SWEEP_TREE) {
         if (M > 8 * kTreeThreads) return pint_set_error(ctx, PINT_E_INVALID, "scalar_sweep: M > 8192 unsupported in TREE mode");
         const int per = static_cast<int>((M + kTreeThreads - 1) / kTreeThreads);
+        const size_t slot = sizeof(double) * (node_stride ? 3 : 1) * static_cast<size_t>(M);
+        const size_t ab_bytes = sizeof(double) * 2 * static_cast<size_t>(N);
+        const bool aligned = (reinterpret_cast<uintptr_t>(values) | reinterpret_cast<uintptr_t>(nodes) |
+                              reinterpret_cast<uintptr_t>(weights)) % 16 == 0;
+        if (M % 2 == 0 && (node_stride % 2 == 0) && aligned && N >= 1 && N <= kStagedMaxN &&
+            kStagedRing * slot + ab_bytes <= 200 * 1024) {
+            const size_t smem = kStagedRing * slot + ab_bytes;
+            // 256 threads x up to 4 terms each for M <= 1024 (fewer warps to issue per slice and to
+            // meet at the two barriers), 512 x 4 to M = 2048, else 1024 x 8
+            auto ks = M <= 256 ? scalar_sweep_staged_kernel<256, 1> : M <= 512 ? scalar_sweep_staged_kernel<256, 2>
+                    : M <= 1024 ? scalar_sweep_staged_kernel<256, 4> : M <= 2048 ? scalar_sweep_staged_kernel<512, 4>
+                    : scalar_sweep_staged_kernel<1024, 8>;
+            const int threads = M <= 1024 ? 256 : M <= 2048 ? 512 : 1024;
+            pint_kernel_attrs(reinterpret_cast<const void*>(ks));
+            ks<<<1, threads, smem, ctx->stream>>>(N, M, nodes, node_stride, weights, values, a, b, ab_stride, y0,
+                                                       lambdas, y_out, extrapolations);
+            return pint_check_launch(ctx, "scalar_sweep_staged_kernel");
+        }
         auto k = per <= 1 ? scalar_sweep_tree_kernel<1> : per <= 2 ? scalar_sweep_tree_kernel<2>
                : per <= 4 ? scalar_sweep_tree_kernel<4> : scalar_sweep_tree_kernel<8>;
         k<<<1, kTreeThreads, 0, ctx->stream>>>(N, M, nodes, node_stride, weights, values, a, b, ab_stride, y0,
