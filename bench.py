@@ -365,7 +365,7 @@ def reference_arm(args, rank, world):
 # legs; the GPU side goes through the C ABI like every other measurement here.
 #
 #   python bench.py --configs [c1ref c1rk4 c5 c3]      -> one JSON line per case (profiles/r01_configs.*)
-#   python bench.py --cost-model [--cost-model-out DIR] -> r01_b200_timings*.txt, r01_cost_model.json
+#   python bench.py --cost-model [--cost-model-out DIR] -> r02_b200_timings*.txt, r02_cost_model.json
 #
 # c1ref  config 1 on the reference path: y' = y^2 (make_model_problem), backward-Euler Riccati,
 #        N = 64, M = 512, S in {79, 782}, vs the reference (ref_tool bench-scalar, all host cores).
@@ -573,6 +573,9 @@ def cm_fit(path):
 
 
 
+CM_ROUND = "r02"  # (file prefix of the cost-model outputs under profiles/)
+
+
 def run_cost_model(a):
     import torch
 
@@ -594,9 +597,9 @@ def run_cost_model(a):
         lines.append(f"{dt!r}, {N}, {M}, {tot:.1f}, {ratio:.4f}")
     prof = ROOT / a.cm_out
     prof.mkdir(exist_ok=True)
-    fixture = prof / "r01_b200_timings.txt"
+    fixture = prof / f"{CM_ROUND}_b200_timings.txt"
     fixture.write_text("\n".join(lines) + "\n")
-    paper_rows = prof / "r01_b200_timings_paper_rows.txt"
+    paper_rows = prof / f"{CM_ROUND}_b200_timings_paper_rows.txt"
     paper_rows.write_text("\n".join(lines[:3 + len(PAPER_ROWS)]) + "\n")
     ref_fixture = ROOT / "oracle" / "_ref" / "dropin" / "data" / "gpu_timings.txt"
     result = {
@@ -608,7 +611,7 @@ def run_cost_model(a):
         "serial_us": {repr(k): v for k, v in serial.items()},
         "units": "microseconds (tau_F per fine step per trajectory, tau_N per slice, tau_K per run)",
     }
-    (prof / "r01_cost_model.json").write_text(json.dumps(result, indent=1) + "\n")
+    (prof / f"{CM_ROUND}_cost_model.json").write_text(json.dumps(result, indent=1) + "\n")
     print(json.dumps({k: result[k] for k in ("b200_fit_all_rows", "b200_fit_paper_rows", "reference_fixture_fit")}))
 
 
