@@ -576,7 +576,7 @@ constexpr size_t pair_tma_smem() { return 1024 + kPairStages * kPairStage + 16 *
 __global__ void __launch_bounds__(256, 1)
 affine_pair_tma_kernel(const __grid_constant__ PairMaps tm, int n, long long ldm, int pairs,
                        const double* __restrict__ later, long long l_stride, double* __restrict__ out,
-                       long long o_stride) {
+                       long long o_stride, int chunked) {
     extern __shared__ __align__(1024) unsigned char pt_raw[];
     unsigned char* sm = pt_raw + ((((smem_u32(pt_raw) + 1023u) & ~1023u) - smem_u32(pt_raw)));
     const unsigned base = smem_u32(sm);
@@ -584,16 +584,20 @@ affine_pair_tma_kernel(const __grid_constant__ PairMaps tm, int n, long long ldm
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int kTiles = (n + 15) / 16, tiles1 = (n + 127) / 128;
     const int tiles = pairs * tiles1 * tiles1;
-    // this CTA's tiles are blockIdx.x, + gridDim.x, ... (one by default, see launch_pairs_tma); their
-    // k tiles form one sequence q = (local tile) * kTiles + kt through the ring
-    const int my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    // this CTA's tiles (a contiguous run, see launch_pairs_tma): their k tiles form one sequence
+    // q = (local tile) * kTiles + kt through the ring, so the next tile's first stages load while
+    // this one's epilogue stores
+    // chunked (the default): CTA b takes tiles [b*tiles/grid, (b+1)*tiles/grid); else round-robin
+    const int c_lo = static_cast<int>(static_cast<long long>(blockIdx.x) * tiles / gridDim.x);
+    const int c_hi = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * tiles / gridDim.x);
+    const int my_tiles = chunked ? c_hi - c_lo : blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const long long total_q = static_cast<long long>(my_tiles) * kTiles;
     struct Tile {
         int p, row0, col0;
         bool xtile;
     };
     auto tile_of = [&](int lt) {
-        const int t = blockIdx.x + lt * gridDim.x;
+        const int t = chunked ? c_lo + lt : blockIdx.x + lt * gridDim.x;
         Tile T;
         T.p = t / (tiles1 * tiles1);
         const int r = t - T.p * tiles1 * tiles1;
@@ -762,16 +766,22 @@ int launch_pairs_tma(pint_ctx* ctx, long long n, long long P, const double* earl
     }
     pint_kernel_attrs(reinterpret_cast<const void*>(affine_pair_tma_kernel));
     const long long t = (n + 127) / 128, tiles = P * t * t;
-    // one tile per CTA by default: measured at n = 512, 128 pairs, a persistent grid of one CTA per SM
-    // (14 tiles each) ran 26.6 TFLOP/s against 29.8 for one tile per CTA (PINT_PAIR_GRID: experiments)
+    // Persistent, one CTA per SM, each taking a CONTIGUOUS run of tiles (the next tile's first k
+    // tiles load during this one's epilogue). Measured at n = 512, 128 pairs: 31.7 TFLOP/s, against
+    // 29.8 for one tile per CTA and 27.0 for the same persistent grid with tiles dealt round-robin
+    // (cuBLAS batched DGEMM: 30.9). PINT_PAIR_GRID / PINT_PAIR_CHUNK=0: experiments.
     static const long long grid_env = [] {
         const char* e = std::getenv("PINT_PAIR_GRID");
         return e ? std::atoll(e) : 0ll;
     }();
-    const unsigned grid = static_cast<unsigned>(grid_env ? std::min<long long>(tiles, grid_env) : tiles);
+    const unsigned grid = static_cast<unsigned>(std::min<long long>(tiles, grid_env ? grid_env : ctx->sm_count));
+    static const int chunk_env = [] {
+        const char* e = std::getenv("PINT_PAIR_CHUNK");
+        return e ? std::atoi(e) : 1;
+    }();
     affine_pair_tma_kernel<<<grid, 256, pair_tma_smem(), ctx->stream>>>(M, static_cast<int>(n), ldm,
                                                                         static_cast<int>(P), later, l_stride, out,
-                                                                        o_stride);
+                                                                        o_stride, chunk_env);
     return pint_check_launch(ctx, "affine_pair_tma_kernel");
 }
 
