@@ -203,7 +203,11 @@ void pint_kernel_attrs(const void* fn) {
     static std::vector<const void*> done;
     std::lock_guard<std::mutex> lk(m);
     if (std::find(done.begin(), done.end(), fn) != done.end()) return;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    // (227 KB per block including the kernel's static shared memory: asking for more fails and
+    // would leave the 48 KB default in place)
+    cudaFuncAttributes fa{};
+    const size_t stat = cudaFuncGetAttributes(&fa, fn) == cudaSuccess ? fa.sharedSizeBytes : 0;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(227 * 1024 - stat));
     cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     done.push_back(fn);

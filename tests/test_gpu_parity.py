@@ -161,6 +161,39 @@ def test_tree_sweep_within_tolerance(ctx):
     assert abs(y_tree - y_exact) <= REL_F64 * abs(y_exact)
 
 
+@pytest.mark.parametrize("M,per_slice,snap", [(6, True, False), (30, True, True), (48, False, True), (64, True, False),
+                                               (1024, True, False), (1024, False, True)])
+def test_sweep_modes_agree(ctx, M, per_slice, snap):
+    """pint_scalar_sweep with per-slice or shared nodes: the TREE sweep (the staged kernel) within
+    1e-12 of the bit-exact EXACT sweep (the one-warp kernel for M <= 32), identical extrapolation
+    counts, and a start value ON a node snapping to that node's value in both."""
+    N = 40
+    rng = np.random.default_rng(M)
+    a = np.sort(rng.uniform(0.0, 0.2, N))
+    b = a + 2.0
+    xs = np.stack([O.cheb_nodes(M, a[j], b[j]) for j in range(N)]) if per_slice else O.cheb_nodes(M, 0.0, 2.0)[None]
+    ws = np.stack([O.bary_weights_closed2(M) for _ in range(xs.shape[0])])
+    # smooth, contracting slice maps (y -> 0.1 + 0.9 y + 0.05 sin 3y): random values would make the
+    # sweep chaotic and amplify any rounding difference
+    xv = np.broadcast_to(xs, (N, M))
+    vals = np.ascontiguousarray(0.1 + 0.9 * xv + 0.05 * np.sin(3.0 * xv))
+    y0 = float(xs[0, M // 3]) if snap else 1.0
+    out = {}
+    for mode in (capi.SWEEP_EXACT, capi.SWEEP_TREE):
+        y, ext = C.c_double(), C.c_longlong()
+        lam = np.empty(N)
+        ctx.check(ctx.lib.pint_scalar_sweep(ctx.h, mode, N, M, capi.ptr(np.ascontiguousarray(xs)), M if per_slice else 0,
+                                            capi.ptr(np.ascontiguousarray(ws)), capi.ptr(vals), capi.ptr(a), capi.ptr(b),
+                                            1, y0, capi.ptr(lam), C.byref(y), C.byref(ext)))
+        out[mode] = (lam, y.value, ext.value)
+    le, ye, ee = out[capi.SWEEP_EXACT]
+    lt, yt, et = out[capi.SWEEP_TREE]
+    assert np.all(np.isfinite(lt)) and ee == et
+    assert np.max(np.abs(lt - le)) <= REL_F64 * np.max(np.abs(le))
+    if snap:
+        assert le[0] == vals[0, M // 3] and lt[0] == vals[0, M // 3]
+
+
 def test_scalar_M1024_closed_form(ctx):
     """Config 1 at M=1024 (reference weights overflow): closed-form weights vs the oracle."""
     N, M = 64, 1024
@@ -460,6 +493,27 @@ def test_affine_chain_wide_random_maps(ctx, N, n):
     ctx.check(ctx.lib.pint_affine_compose(ctx.h, capi.COMPOSE_CHAIN, n, N, capi.ptr(G), capi.ptr(c), capi.ptr(y0),
                                           capi.ptr(y)))
     assert np.array_equal(y, O.affine_chain(G, c, y0))
+
+
+@pytest.mark.parametrize("n,P", [(384, 9), (384, 40), (512, 5), (512, 37)])
+def test_affine_pair_tma_kernel(ctx, n, P):
+    """The TMA-fed persistent pair kernel (compose.cu affine_pair_tma_kernel; 128 | n, n >= 384):
+    out_p = later_p o earlier_p as augmented products, within 1e-12 of the host product — one and
+    several tiles per CTA (9 P or 16 P tiles over the SMs), the translation column n included."""
+    import torch
+
+    ldm = int(capi.load().pint_affine_ldm(n))
+    rng = np.random.default_rng(n + P)
+    Eh = rng.uniform(-1, 1, (P, n, ldm)) / np.sqrt(n)
+    Lh = rng.uniform(-1, 1, (P, n, ldm)) / np.sqrt(n)
+    E, L = torch.as_tensor(Eh).cuda(), torch.as_tensor(Lh).cuda()
+    O_ = torch.full_like(E, float("nan"))
+    ctx.call("pint_affine_pair_dev", n, P, capi.ptr(E), capi.ptr(L), capi.ptr(O_))
+    ctx.sync()
+    want = np.matmul(Lh[:, :, :n], Eh[:, :, : n + 1])
+    want[:, :, n] += Lh[:, :, n]
+    got = O_.cpu().numpy()[:, :, : n + 1]
+    assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.max(np.abs(want)))
 
 
 def test_affine_compose_order(ctx):
