@@ -480,12 +480,13 @@ int launch_fast_w(pint_ctx* ctx, FastPlan Q) {
 
 template <int P, int R>
 int launch_fast(pint_ctx* ctx, const FastPlan& Q) {
-    static const int w_env = [] {  // PINT_FAST_W=1|2|4: warps per CTA (experiments only)
+    static const int w_env = [] {  // PINT_FAST_W=1|2|8: warps per CTA (experiments only)
         const char* e = std::getenv("PINT_FAST_W");
         return e ? std::atoi(e) : 0;
     }();
     if (w_env == 1) return launch_fast_w<P, R, 1>(ctx, Q);
     if (w_env == 2) return launch_fast_w<P, R, 2>(ctx, Q);
+    if (w_env == 8 && R >= 32) return launch_fast_w<P, R, 8>(ctx, Q);
     return launch_fast_w<P, R, FastCfg<R>::W>(ctx, Q);
 }
 

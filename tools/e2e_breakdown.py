@@ -1,5 +1,5 @@
 """Where the end-to-end time of pint_run_heat goes (bench config): wall vs device time, and the
-host-side table computation alone.   python tools/e2e_breakdown.py"""
+host-side table computation alone.   python tools/e2e_breakdown.py [c2|c4]"""
 import ctypes as C
 import json
 import pathlib
@@ -18,7 +18,9 @@ def main():
     from paper_1304_6514_b200.dist import HeatTablesHost, closure_slices
 
     ctx = capi.Context(0, stream=torch.cuda.current_stream())
-    n, N, S, T = 128, 256, 256, 10.0
+    c4 = len(sys.argv) > 1 and sys.argv[1] == "c4"
+    n, N, S, T = (512, 4096, 16, 10.0) if c4 else (128, 256, 256, 10.0)
+    mode = capi.COMPOSE_CHAIN if c4 else capi.COMPOSE_TREE
     dx, dt = 1.0 / (n + 1), T / (N * S)
     y = np.empty(n)
     rep = capi.Report()
@@ -26,7 +28,7 @@ def main():
     for i in range(12):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ctx.check(ctx.lib.pint_run_heat(ctx.h, dx, dt, T, N, capi.COMPOSE_TREE, None, capi.ptr(y), None,
+        ctx.check(ctx.lib.pint_run_heat(ctx.h, dx, dt, T, N, mode, None, capi.ptr(y), None,
                                         C.byref(rep)))
         wall = (time.perf_counter() - t0) * 1e3
         rows.append((wall, rep.total_ms, rep.device_ms, rep.compose_ms))
@@ -40,7 +42,7 @@ def main():
                       "compose_ms": w[:, 3].mean(), "host_tables_ms(py, incl. pinned alloc)": tables_ms}))
 
 
-if __name__ == "__main__" and len(sys.argv) == 1:
+if __name__ == "__main__" and (len(sys.argv) == 1 or sys.argv[1] in ("c2", "c4")):
     main()
 
 
