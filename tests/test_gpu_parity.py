@@ -480,7 +480,7 @@ def test_affine_tree_random_maps(ctx):
         assert np.max(np.abs(y - chain)) <= 1e-11 * scale
 
 
-@pytest.mark.parametrize("N,n", [(5, 272), (9, 320), (3, 400), (11, 512), (2, 496)])
+@pytest.mark.parametrize("N,n", [(5, 272), (9, 320), (3, 400), (11, 512), (2, 496), (1, 512)])
 def test_affine_chain_wide_random_maps(ctx, N, n):
     """The TMA-streamed wide chain (256 < n <= 512, n % 16 == 0; compose.cu affine_chain_wide_kernel):
     bit-exact against the oracle's compose_sweep order — full and partial 64-column boxes, one or
