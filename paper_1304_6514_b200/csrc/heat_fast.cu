@@ -43,8 +43,9 @@ using namespace pint_async;
 
 constexpr unsigned kFull = 0xffffffffu;
 
-// Kogge-Stone multipliers of the two carry scans, [level][partition] (levels <= 4, P <= 16)
-constexpr int kScanTab = 64;
+// Kogge-Stone multipliers of the two carry scans, [level][partition] (levels <= 5, P <= 32)
+constexpr int kScanLevelStride = 32;
+constexpr int kScanTab = 5 * kScanLevelStride;
 __host__ __device__ constexpr long long fast_blk(long long NP) { return 4 * NP + 2 * kScanTab; }
 
 // Partition shape for n: R rows per partition, P (a power of two <= 16) partitions per column,
@@ -59,9 +60,13 @@ struct FastShape {
     int NP() const { return P * R; }
 };
 FastShape fast_shape(long long n) {
+    static const int p32 = [] {  // PINT_FAST_P32=1: 32 partitions of 16 rows up to n = 512 (experiment)
+        const char* e = std::getenv("PINT_FAST_P32");
+        return e ? std::atoi(e) : 1;
+    }();
     FastShape f;
     for (int R : {16, 32, 48})
-        for (int P = 2; P <= 16; P *= 2)
+        for (int P = 2; P <= (R == 16 && p32 ? 32 : 16); P *= 2)
             if (static_cast<long long>(P) * R >= n) {
                 f.P = P;
                 f.R = R;
@@ -206,8 +211,8 @@ __global__ void __launch_bounds__(128) heat_fast_record_kernel(const FastRecPlan
         const int o = 1 << l;
         const double fo = __shfl_up_sync(kFull, af, o), bo = __shfl_down_sync(kFull, ab, o);
         if (c == CPP - 1) {  // (0 where the partner partition does not exist: no select in the build)
-            blk[4 * NP + l * 16 + p] = p >= o ? af : 0.0;
-            blk[4 * NP + kScanTab + l * 16 + p] = p + o < P ? ab : 0.0;
+            blk[4 * NP + l * kScanLevelStride + p] = p >= o ? af : 0.0;
+            blk[4 * NP + kScanTab + l * kScanLevelStride + p] = p + o < P ? ab : 0.0;
         }
         if (p >= o) af *= fo;
         if (p + o < P) ab *= bo;
@@ -239,7 +244,7 @@ struct FastCfg {
     // warps per CTA: single-warp CTAs stage their own records and never wait for a slower warp
     // (C2: 0.78 vs 0.88 ms with 4-warp CTAs); at R = 32 (n = 512: 21.5 KB a staged step) 4-warp
     // CTAs share one staged copy, or the copies would not fit 8 warps per SM
-    static constexpr int W = R <= 16 ? 1 : 4;
+    static constexpr int W = R <= 16 ? 1 : 4;  // (P = 32, R = 16: see fast_warps)
     static constexpr int kMinCtas = 2;  // (x 4 / W CTAs: 8 warps per SM, <= 255 registers)
 };
 
@@ -268,12 +273,12 @@ __device__ __forceinline__ void fast_step(double (&x)[C][R], const double* St, c
         }
     }
     double D[C], E[C];
-    constexpr int L = P >= 16 ? 4 : P >= 8 ? 3 : P >= 4 ? 2 : P >= 2 ? 1 : 0;
+    constexpr int L = P >= 32 ? 5 : P >= 16 ? 4 : P >= 8 ? 3 : P >= 4 ? 2 : P >= 2 ? 1 : 0;
     if constexpr (P > 1) {  // carry-in of the forward recurrence: upward scan of (pi_end, d~_end)
         const double* FS = St + 4 * NP + p;
 #pragma unroll
         for (int l = 0; l < L; ++l) {
-            const double m = FS[l * 16];
+            const double m = FS[l * kScanLevelStride];
 #pragma unroll
             for (int c = 0; c < C; ++c) {  // (m = 0 where p < 2^l: the lane's own value, times 0)
                 const double vo = __shfl_up_sync(kFull, d[c], 1 << l, P);
@@ -303,7 +308,7 @@ __device__ __forceinline__ void fast_step(double (&x)[C][R], const double* St, c
         for (int c = 0; c < C; ++c) v[c] = __fma_rn(D[c], psi0, x[c][0]);
 #pragma unroll
         for (int l = 0; l < L; ++l) {
-            const double m = BS[l * 16];
+            const double m = BS[l * kScanLevelStride];
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 const double vo = __shfl_down_sync(kFull, v[c], 1 << l, P);
@@ -537,6 +542,10 @@ void heat_fast_prepare(int64_t n) {  // every kernel variant the build for n may
         case 4016: set(heat_fast_build_kernel<4, 16, 4, 1>); set(heat_fast_build_kernel<4, 16, 2, 1>); break;
         case 8016: set(heat_fast_build_kernel<8, 16, 4, 1>); set(heat_fast_build_kernel<8, 16, 2, 1>); break;
         case 16016: set(heat_fast_build_kernel<16, 16, 4, 1>); set(heat_fast_build_kernel<16, 16, 2, 1>); break;
+        case 32016:
+            set(heat_fast_build_kernel<32, 16, 4, 4>), set(heat_fast_build_kernel<32, 16, 2, 4>);
+            set(heat_fast_build_kernel<32, 16, 4, 8>), set(heat_fast_build_kernel<32, 16, 2, 8>);
+            break;
         case 16032: set(heat_fast_build_kernel<16, 32, 4, 4>); set(heat_fast_build_kernel<16, 32, 2, 4>); break;
         case 16048: set(heat_fast_build_kernel<16, 48, 4, 4>); set(heat_fast_build_kernel<16, 48, 2, 4>); break;
         default: break;
@@ -557,6 +566,10 @@ int launch_heat_fast_build(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const
         case 4016: return launch_fast<4, 16>(ctx, Q);
         case 8016: return launch_fast<8, 16>(ctx, Q);
         case 16016: return launch_fast<16, 16>(ctx, Q);
+        case 32016: {  // (records of 512 rows: 4 warps share a staged copy; PINT_FAST_W=8: experiment)
+            static const int w8 = [] { const char* e = std::getenv("PINT_FAST_W"); return e && std::atoi(e) == 8; }();
+            return w8 ? launch_fast_w<32, 16, 8>(ctx, Q) : launch_fast_w<32, 16, 4>(ctx, Q);
+        }
         case 16032: return launch_fast<16, 32>(ctx, Q);
         case 16048: return launch_fast<16, 48>(ctx, Q);
         default: return pint_set_error(ctx, PINT_E_INVALID, "heat_fast_build: shape");
