@@ -48,12 +48,13 @@ constexpr int kScanLevelStride = 32;
 constexpr int kScanTab = 5 * kScanLevelStride;
 __host__ __device__ constexpr long long fast_blk(long long NP) { return 4 * NP + 2 * kScanTab; }
 
-// Partition shape for n: R rows per partition, P (a power of two <= 16) partitions per column,
+// Partition shape for n: R rows per partition, P (a power of two <= 32) partitions per column,
 // C = 64 / R columns per thread (64 rows of state in registers: 128 of the 255), so that NP = P R
 // is a multiple of 32 (the record kernel's lanes). Shorter partitions give each thread more
 // independent chains and amortise every coefficient load over more columns (C), at the price of a
-// deeper carry scan: R = 16 (C = 4) up to n = 256, then R = 32 (C = 2, n <= 512) and R = 48
-// (C = 1, n <= 768).
+// deeper carry scan: R = 16 (C = 4) up to n = 512 (P = 32 above n = 256: one column per warp; the
+// R = 32, C = 2 shape spilled and ran 3.5% slower at config 4), then R = 32 (C = 2, only with
+// PINT_FAST_P32=0) and R = 48 (C = 1, n <= 768).
 struct FastShape {
     int P = 0, R = 0;
     bool ok() const { return P > 0; }
