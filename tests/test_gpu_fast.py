@@ -51,7 +51,7 @@ def close(a, ref, tol):
 
 
 # every partition shape (P, R): n <= 32 -> (2, 16), <= 64 -> (4, 16), <= 128 -> (8, 16), <= 256 -> (16, 16),
-# <= 512 -> (16, 32), <= 768 -> (16, 48); padded rows (n not a multiple of P R), CTAs over several slices
+# <= 512 -> (32, 16), <= 768 -> (16, 48); padded rows (n not a multiple of P R), CTAs over several slices
 @pytest.mark.parametrize("n,N,S", [(9, 4, 5), (31, 3, 4), (40, 3, 4), (64, 2, 3), (97, 3, 3), (128, 5, 4),
                                    (150, 2, 3), (200, 3, 2), (255, 2, 3), (300, 2, 3), (384, 2, 2), (512, 3, 4),
                                    (700, 2, 2)])
