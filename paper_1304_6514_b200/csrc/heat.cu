@@ -110,6 +110,10 @@ __host__ __device__ constexpr bool group_forced(long long n) {
 // both look-ahead rings (kTmAhead and kBackAhead), so every ring slot is a compile-time index.
 constexpr int kTmBody = 16;
 constexpr int kTmAhead = 4;  // forward (p, rcp) look-ahead over the TMEM rows
+#ifndef PINT_TM_ROW_STORES
+#define PINT_TM_ROW_STORES 1
+#endif
+constexpr bool kTmRowStores = PINT_TM_ROW_STORES;  // a tcgen05.st per row instead of per 8-row chunk
 
 // ---- large n: heat_build_tmem_kernel --------------------------------------------------------
 // When a warp's state no longer fits 4 times into shared memory (n >~ 280 with the one-warp-CTA
@@ -384,6 +388,12 @@ __device__ __forceinline__ void tm_st(unsigned addr, const Tm8& t) {
         : "memory");  // (also keeps the look-ahead loads from being hoisted across chunks)
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+// one row (a double: two 32-bit TMEM columns) straight from the register that holds it
+__device__ __forceinline__ void tm_st1(unsigned addr, double v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(addr),
+                 "r"(static_cast<unsigned>(__double2loint(v))), "r"(static_cast<unsigned>(__double2hiint(v)))
+                 : "memory");
+}
 
 // Forward rows [RR, RR + 16 nb) from TMEM (base row RR at column 0): chunk c + 1 is loaded while
 // chunk c is eliminated, (p, rcp) read kTmAhead rows ahead. Quotients are range-checked here.
@@ -413,10 +423,11 @@ __device__ __forceinline__ void tmem_forward(unsigned tm, int nb, const double2*
                 const int rr = 8 * c + u;
                 d = divide(__dsub_rn(cur.get(u), __dmul_rn(negr, d)), pv[rr % kTmAhead]);
                 pv[rr % kTmAhead] = pr[kTmBody * b + rr + kTmAhead];
-                cur.put(u, d);
+                if (kTmRowStores) tm_st1(tm + 16u * ch + 2u * u, d);
+                else cur.put(u, d);
                 qmin = min(qmin, hi_abs(d) - 1u);
             }
-            tm_st(tm + 16u * ch, cur);
+            if (!kTmRowStores) tm_st(tm + 16u * ch, cur);
             if (more) tm_wait_ld(nxt);
         }
     }
@@ -448,9 +459,10 @@ __device__ __forceinline__ void tmem_back(unsigned tm, int nb, const double* cc,
                 const int u = 7 - v;
                 d = __dsub_rn(cur.get(u), __dmul_rn(cv[v], d));
                 cv[v] = cc[8 * ch + u - 8];
-                cur.put(u, d);
+                if (kTmRowStores) tm_st1(tm + 16u * ch + 2u * u, d);
+                else cur.put(u, d);
             }
-            tm_st(tm + 16u * ch, cur);
+            if (!kTmRowStores) tm_st(tm + 16u * ch, cur);
             if (more) tm_wait_ld(nxt);
         }
     }
