@@ -114,6 +114,13 @@ constexpr int kTmAhead = 4;  // forward (p, rcp) look-ahead over the TMEM rows
 #define PINT_TM_ROW_STORES 1
 #endif
 constexpr bool kTmRowStores = PINT_TM_ROW_STORES;  // a tcgen05.st per row instead of per 8-row chunk
+// The TMEM rows' quotient range check in the back pass, on the values it loads, instead of the
+// forward pass, where the check's absolute value landed in the register an in-flight tcgen05.st
+// was still reading (a write-after-read wait as long as a chain step)
+#ifndef PINT_TM_BACK_CHECK
+#define PINT_TM_BACK_CHECK 1
+#endif
+constexpr bool kTmBackCheck = PINT_TM_BACK_CHECK;
 
 // ---- large n: heat_build_tmem_kernel --------------------------------------------------------
 // When a warp's state no longer fits 4 times into shared memory (n >~ 280 with the one-warp-CTA
@@ -425,7 +432,7 @@ __device__ __forceinline__ void tmem_forward(unsigned tm, int nb, const double2*
                 pv[rr % kTmAhead] = pr[kTmBody * b + rr + kTmAhead];
                 if (kTmRowStores) tm_st1(tm + 16u * ch + 2u * u, d);
                 else cur.put(u, d);
-                qmin = min(qmin, hi_abs(d) - 1u);
+                if (!kTmBackCheck) qmin = min(qmin, hi_abs(d) - 1u);
             }
             if (!kTmRowStores) tm_st(tm + 16u * ch, cur);
             if (more) tm_wait_ld(nxt);
@@ -435,7 +442,7 @@ __device__ __forceinline__ void tmem_forward(unsigned tm, int nb, const double2*
 
 // Back substitution over the TMEM rows, last chunk first; cc = c of row RR; c read kBackAhead rows
 // ahead.
-__device__ __forceinline__ void tmem_back(unsigned tm, int nb, const double* cc, double& d) {
+__device__ __forceinline__ void tmem_back(unsigned tm, int nb, const double* cc, double& d, unsigned& qmin) {
     static_assert(kTmBody % kBackAhead == 0 && kBackAhead == 8, "ring slots");
     const int nch = nb * (kTmBody / 8);
     double cv[8];
@@ -457,7 +464,9 @@ __device__ __forceinline__ void tmem_back(unsigned tm, int nb, const double* cc,
 #pragma unroll
             for (int v = 0; v < 8; ++v) {
                 const int u = 7 - v;
-                d = __dsub_rn(cur.get(u), __dmul_rn(cv[v], d));
+                const double q = cur.get(u);  // (this row's forward quotient)
+                if (kTmBackCheck) qmin = min(qmin, hi_abs(q) - 1u);
+                d = __dsub_rn(q, __dmul_rn(cv[v], d));
                 cv[v] = cc[8 * ch + u - 8];
                 if (kTmRowStores) tm_st1(tm + 16u * ch + 2u * u, d);
                 else cur.put(u, d);
@@ -577,7 +586,7 @@ __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], doub
         for (int u = 0; u < kBackAhead - 1; ++u)
             if (r - u >= 0) row(r - u, yv[u], cv[u]);
     }
-    if (kTm) tmem_back(tm, tm_bodies, CC + RR, d);
+    if (kTm) tmem_back(tm, tm_bodies, CC + RR, d, qmin);
 #pragma unroll
     for (int i = RR - 1; i >= 0; --i) {  // (RR > 0 only for n >= RR + 2: every register row is a back row)
         d = __dsub_rn(reg[i], __dmul_rn(CC[i * kS], d));  // (the register rows' quotients were checked
