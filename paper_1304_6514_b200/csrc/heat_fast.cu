@@ -231,6 +231,7 @@ struct FastPlan {
     const double* hrec;
     int* ready;  // (may be null) per-slice count of warps whose columns of the map are stored
     unsigned long long* span;  // (with ready) {first warp start, last warp end} globaltimer
+    long long wps = 0;         // warps per slice: ceil((n + 1) / CPW), or padded to whole CTAs
 };
 
 // records staged ahead: step s + ST is fetched when step s is done (and step s + ST + 1 pulled into
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(32 * W, FastCfg<R>::kMinCtas * 4 / W) heat_fas
     const int n = Q.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cg = lane / P, p = lane % P;
-    const long long wps = (n + 1 + CPW - 1) / CPW;
+    const long long wps = Q.wps;
     const long long w = static_cast<long long>(blockIdx.x) * W + warp;
     const long long w_last = min(static_cast<long long>(blockIdx.x) * W + W, Q.N * wps) - 1;
     const long long j_lo = static_cast<long long>(blockIdx.x) * W / wps, j_hi = w_last / wps;
@@ -429,7 +430,11 @@ __global__ void __launch_bounds__(32 * W, FastCfg<R>::kMinCtas * 4 / W) heat_fas
         }
     }
     // this warp's columns of slice j are stored: count it (a concurrent chain waits for all wps)
-    if (Q.ready && wlive) {
+    // (a pad warp of a slice-aligned grid owns no column and is not counted)
+    bool has_cols = false;
+#pragma unroll
+    for (int c = 0; c < C; ++c) has_cols |= kk[c] >= 0;
+    if (Q.ready && wlive && __any_sync(kFull, has_cols)) {
         __syncwarp();
         if (lane == 0) {
             __threadfence();
@@ -474,8 +479,19 @@ template <int P, int R, int W>
 int launch_fast_w(pint_ctx* ctx, FastPlan Q) {
     constexpr int NP = P * R;
     constexpr int CPW = 32 / P * FastCfg<R>::C;
-    const long long wps = (Q.n + 1 + CPW - 1) / CPW;
+    long long wps = (Q.n + 1 + CPW - 1) / CPW;
+    // slice-aligned CTAs (warps per slice padded to a multiple of W; the pad warps own no column)
+    // where a slice has many warps: each CTA then stages ONE slice's records, small enough for 4
+    // stages at 2 CTAs per SM (config 4: 129 -> 132 warps a slice, 2.3% idle; the record waits
+    // of 2 shared stages were 16% of the stall samples)
+    static const int align_env = [] {
+        const char* e = std::getenv("PINT_FAST_SLICE_CTAS");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (align_env && W > 1 && wps >= 8 * W) wps = (wps + W - 1) / W * W;
+    Q.wps = wps;
     Q.NS = static_cast<int>(std::min<long long>(W, (W + wps - 1) / wps + 1));  // slices a CTA's warps span
+    if (wps % W == 0) Q.NS = 1;
     const size_t stage_bytes = sizeof(double) * Q.NS * (fast_blk(NP) + NP);
     const bool deep = kFastStagesMax * stage_bytes + 64 <= static_cast<size_t>(W) * 25 * 1024;  // (8 warps per SM either way)
     const size_t smem = (deep ? kFastStagesMax : 2) * stage_bytes + 64;
