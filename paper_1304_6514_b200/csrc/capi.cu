@@ -105,7 +105,7 @@ class HostPool {
             fn_ = &fn;
             n_ = n;
             parts_ = parts;
-            next_.store(1);
+            next_ = 1;
             pending_ = parts - 1;
             ++generation_;
         }
@@ -129,19 +129,23 @@ class HostPool {
         cv_.notify_all();
         for (auto& t : workers_) t.join();
     }
+    // A part is claimed under the mutex, and only while the job the worker woke for is still the
+    // current one: a worker that wakes late never runs a finished job's function (whose caller
+    // has returned and destroyed it) on the next job's part indices. The caller returns only once
+    // every claimed part has finished (pending_).
     void run() {
         uint64_t seen = 0;
+        std::unique_lock<std::mutex> l(m_);
         for (;;) {
-            std::unique_lock<std::mutex> l(m_);
             cv_.wait(l, [&] { return stop_ || generation_ != seen; });
             if (stop_) return;
             seen = generation_;
-            const auto* fn = fn_;
-            const int64_t n = n_, parts = parts_;
-            l.unlock();
-            for (int64_t k = next_.fetch_add(1); k < parts; k = next_.fetch_add(1)) {
+            while (fn_ && generation_ == seen && next_ < parts_) {
+                const int64_t k = next_++, n = n_, parts = parts_;
+                const auto* fn = fn_;
+                l.unlock();
                 (*fn)(n * k / parts, n * (k + 1) / parts);
-                std::lock_guard<std::mutex> g(m_);
+                l.lock();
                 if (--pending_ == 0) done_cv_.notify_one();
             }
         }
@@ -150,8 +154,7 @@ class HostPool {
     std::mutex m_, job_mutex_;
     std::condition_variable cv_, done_cv_;
     const std::function<void(int64_t, int64_t)>* fn_ = nullptr;
-    int64_t n_ = 0, parts_ = 0, pending_ = 0;
-    std::atomic<int64_t> next_{0};
+    int64_t n_ = 0, parts_ = 0, pending_ = 0, next_ = 0;
     uint64_t generation_ = 0;
     bool stop_ = false;
 };

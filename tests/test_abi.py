@@ -92,3 +92,42 @@ def test_heat_coefficient_tables_match_reference_arithmetic():
 
 def test_affine_ldm():
     assert [capi.load().pint_affine_ldm(n) for n in (1, 3, 4, 9, 128, 512)] == [4, 4, 8, 12, 132, 516]
+
+
+def test_host_pool_back_to_back_jobs_from_threads():
+    """The host thread pool behind the table fills (capi.cu HostPool): many back-to-back
+    parallel_for jobs, from several caller threads at once, each result identical to a serial
+    reference — a worker waking late must never run a finished job's function."""
+    import ctypes as C
+    import threading
+
+    dx, T, N = 1.0 / 129, 10.0, 512
+    dt = T / (N * 16)
+    dec = pint.decompose(0.0, T, N, dt)
+    arr = (capi.Slice * N)(*[s.c() for s in dec.slices])
+    Q = sum(s.steps for s in dec.slices)  # >= 4096 steps: the pool path
+
+    def fill():
+        off = np.empty(N + 1, dtype=np.int64)
+        r, fa, fb = (np.empty(Q) for _ in range(3))
+        sx = np.empty(128)
+        n = C.c_int64()
+        assert capi.load().pint_heat_coefficients(dx, arr, N, capi.ptr(off), capi.ptr(r), capi.ptr(fa),
+                                                  capi.ptr(fb), capi.ptr(sx), C.byref(n)) == 0
+        return r, fa, fb
+
+    ref = fill()
+    bad = []
+
+    def worker():
+        for _ in range(60):
+            got = fill()
+            if not all(np.array_equal(a, b) for a, b in zip(got, ref)):
+                bad.append(1)
+
+    ts = [threading.Thread(target=worker) for _ in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not bad

@@ -46,12 +46,12 @@ if __name__ == "__main__" and (len(sys.argv) == 1 or sys.argv[1] in ("c2", "c4")
     main()
 
 
-def host_tables_ms(reps: int = 20) -> float:
+def host_tables_ms(reps: int = 20, c4: bool = False) -> float:
     """Host-only time of pint_heat_coefficients for the bench's slices (the glibc sin/cos tables)."""
     from paper_1304_6514_b200 import capi, pint
     from paper_1304_6514_b200.dist import closure_slices
 
-    n, N, S, T = 128, 256, 256, 10.0
+    n, N, S, T = (512, 4096, 16, 10.0) if c4 else (128, 256, 256, 10.0)
     dx, dt = 1.0 / (n + 1), T / (N * S)
     sl = closure_slices(pint.decompose(0.0, T, N, dt), dt)
     arr = (capi.Slice * N)(*sl)
@@ -69,4 +69,4 @@ def host_tables_ms(reps: int = 20) -> float:
 
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "--host":
-    print(json.dumps({"host_tables_ms": host_tables_ms()}))
+    print(json.dumps({"host_tables_ms": host_tables_ms(c4="c4" in sys.argv)}))
