@@ -1112,6 +1112,9 @@ int heat_build_chain(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64
     }
     if (fast) heat_fast_prepare(n);
     else heat_build_prepare(n);
+    if (!fast)  // (the forced columns ahead of the chain: nothing may sit between it and the build)
+        if (const int rc = launch_heat_forced_first(ctx, n, N, S, step_off, records, maps, per_slice_ns, guarded))
+            return rc;
     cudaMemsetAsync(ready, 0, ready_bytes, ctx->stream);
     cudaMemsetAsync(reinterpret_cast<char*>(ready) + ready_bytes, 0xff, 8, ctx->stream);  // (min start)
     cudaMemsetAsync(reinterpret_cast<char*>(ready) + ready_bytes + 8, 0, 16, ctx->stream);

@@ -306,6 +306,7 @@ __device__ __forceinline__ double div_guarded(double x, double2 pr) {
 struct alignas(64) BuildPlan {
     CUtensorMap tm_pr;  // kBasisGroup: pr2 of the slice-group blocks as [blocks][n16+1][64] doubles
     CUtensorMap tm_cc;  // kBasisGroup: c of the slice-group blocks as [blocks][n16][32] doubles
+    CUtensorMap tm_hb;  // (heat_forced_lanes_kernel: tm_pr / tm_hb / tm_cc over the slice-major records)
     int n;
     int N;
     long long S;        // max steps per slice (record layout)
@@ -923,6 +924,212 @@ __global__ void __launch_bounds__(160, 1) heat_build_tmem_kernel(const __grid_co
     }
 }
 
+// ---- forced columns apart (TMEM range): one lane per slice --------------------------------------
+// Column n of every slice's map (the forced run from 0, pde_problems.cpp:91-94) for the TMEM build,
+// which then builds the basis columns only: a 5th warp in CTA 0 of every slice shared sub-partition
+// 0 with basis warp 0 and made CTA 0 the slowest of its slice (basis-only build 32.4 against
+// 34.6 ms). Here lane l of a one-warp CTA runs slice 32 blockIdx + l: the operations, in the
+// order, of the in-CTA forced warp (column_forward / column_back in kForcedSingle mode), its state
+// in registers (rows 0 .. kFlRegRows-1) and lane-interleaved shared memory. The 32 slices' records
+// stream through a two-slot shared ring in 64-row chunks by TMA: the slice-major records seen as
+// 4-D tensors {16 doubles, slices, 16-double blocks, steps} (strides S·RS, 128 B, RS: RS = record
+// doubles) over their (p, rcp), h b and c regions, one box {16, 32, blocks, 1} per region and
+// chunk with the 128-byte swizzle — [block][lane][16], so lane l's row r sits at 16-byte chunk
+// (r % 8) ^ (l % 8) of its line: conflict-free. (Per-lane loads from global memory left the chain
+// waiting on DRAM, 1.4 ms; per-lane bulk copies needed a 32-way issue loop each, 1.1 ms.)
+constexpr int kFlRegRows = 64, kFlChunk = 64;
+constexpr unsigned kFlPrBytes = 16 * 32 * 8 * 8, kFlHbBytes = 16 * 32 * 4 * 8;  // a chunk's boxes
+constexpr unsigned kFlSlot = kFlPrBytes + kFlHbBytes;                            // 48 KB
+
+__host__ __device__ constexpr int fl_chunks(long long n) { return static_cast<int>((n16(n) + kFlChunk - 1) / kFlChunk); }
+size_t forced_lanes_smem(long long n) {
+    return 1024 + 2 * kFlSlot + sizeof(double) * 32 * static_cast<size_t>(n - kFlRegRows) + 16;
+}
+
+template <bool kGuard>
+__global__ void __launch_bounds__(32, 1) heat_forced_lanes_kernel(const __grid_constant__ BuildPlan P) {
+    extern __shared__ __align__(1024) unsigned char fl_raw[];
+    unsigned char* fl = fl_raw + ((((smem_u32(fl_raw) + 1023u) & ~1023u) - smem_u32(fl_raw)));
+    const int n = P.n, lane = threadIdx.x;
+    const long long slice = static_cast<long long>(blockIdx.x) * 32 + lane;
+    const bool live = slice < P.N;
+    const long long steps = live ? P.step_off[slice + 1] - P.step_off[slice] : 0;
+    const unsigned long long t_start = pint_dev::globaltimer();
+    const RecView V = rec_view(P.rec, n, P.N, P.S);
+    const unsigned ring0 = smem_u32(fl);                                            // [2][48 KB]
+    double* st = reinterpret_cast<double*>(fl + 2 * kFlSlot) + lane;                // row i at st[32 (i - RR)]
+    const unsigned bar0 = smem_u32(fl + 2 * kFlSlot + sizeof(double) * 32 * static_cast<size_t>(n - kFlRegRows));
+    if (lane == 0) {
+        mbar_init(bar0);
+        mbar_init(bar0 + 8);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    long long max_steps = steps;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) max_steps = max(max_steps, __shfl_xor_sync(0xffffffffu, max_steps, o));
+    const int nch = fl_chunks(n);
+    const int sl0 = static_cast<int>(blockIdx.x) * 32;
+    // task t of a step: t < nch forward chunk t, else back chunk 2 nch - 1 - t; task q = s 2 nch + t
+    // runs through slot q % 2
+    auto issue = [&](long long q) {  // (lane 0)
+        const long long s = q / (2 * nch);
+        const int t = static_cast<int>(q - s * 2 * nch);
+        const bool fwd = t < nch;
+        const int c = fwd ? t : 2 * nch - 1 - t;
+        const unsigned bar = bar0 + 8u * static_cast<unsigned>(q & 1), dst = ring0 + static_cast<unsigned>(q & 1) * kFlSlot;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // (the slot's earlier reads)
+        asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(bar),
+                     "r"(fwd ? kFlSlot : kFlHbBytes)
+                     : "memory");
+        auto tma = [&](const CUtensorMap* m, unsigned d, int blk) {
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                "%3, %4, %5}], [%6];\n" ::"r"(d),
+                "l"(reinterpret_cast<unsigned long long>(m)), "r"(0), "r"(sl0), "r"(blk), "r"(static_cast<int>(s)),
+                "r"(bar)
+                : "memory");
+        };
+        if (fwd) {
+            tma(&P.tm_pr, dst, 8 * c);
+            tma(&P.tm_hb, dst + kFlPrBytes, 4 * c);
+        } else {
+            tma(&P.tm_cc, dst, 4 * c);
+        }
+    };
+    const int sw = lane & 7;
+    // a chunk's row r: (p, rcp) at [r / 8][lane][(r % 8) ^ sw]; h b, c at [r / 16][lane][((r % 16) / 2) ^ sw] + r % 2
+    auto pr_at = [&](const unsigned char* T, int r) {
+        return *reinterpret_cast<const double2*>(T + ((r >> 3) * 32 + lane) * 128 + (((r & 7) ^ sw) << 4));
+    };
+    auto v_at = [&](const unsigned char* T, int r) {
+        return *reinterpret_cast<const double*>(T + ((r >> 4) * 32 + lane) * 128 + ((((r & 15) >> 1) ^ sw) << 4) +
+                                                ((r & 1) << 3));
+    };
+    double reg[kFlRegRows];
+#pragma unroll
+    for (int i = 0; i < kFlRegRows; ++i) reg[i] = 0.0;  // the forced run starts at 0
+    for (int i = kFlRegRows; i < n; ++i) st[32 * (i - kFlRegRows)] = 0.0;
+    unsigned qmin = 0xffffffffu;
+    auto divide = [&](double num, double2 pr) { return kGuard ? div_guarded(num, pr) : div_fast(num, pr); };
+    const long long total = max_steps * 2 * nch;
+    if (lane == 0) {
+        if (total > 0) issue(0);
+        if (total > 1) issue(1);
+    }
+    long long q = 0;
+    auto wait_task = [&]() -> const unsigned char* {  // task q's slot (landed)
+        mbar_wait(bar0 + 8u * static_cast<unsigned>(q & 1), static_cast<unsigned>((q >> 1) & 1));
+        return fl + static_cast<size_t>(q & 1) * kFlSlot;
+    };
+    auto done_task = [&]() {  // the slot is consumed: load task q + 2 into it
+        __syncwarp();
+        if (lane == 0 && q + 2 < total) issue(q + 2);
+        ++q;
+    };
+    for (long long s = 0; s < max_steps; ++s) {
+        const bool act = s < steps;  // (a shorter slice's lane computes nothing at the tail)
+        const double negr = act ? V.rec(slice, s)[0] : 0.0;
+        // forward (linalg.cpp:84-90) with the forcing increment x + h b first (pde_problems.cpp:93)
+        double d = -0.0;
+        for (int c = 0; c < nch; ++c) {
+            const unsigned char* T = wait_task();
+            const unsigned char* H = T + kFlPrBytes;
+            const int r0 = c * kFlChunk, r1 = min(n, r0 + kFlChunk);
+            if (act) {
+                if (r0 < kFlRegRows) {  // (the register rows: chunk 0, kFlRegRows == kFlChunk)
+#pragma unroll
+                    for (int i = 0; i < kFlRegRows; ++i) {
+                        const double x = __dadd_rn(reg[i], v_at(H, i));
+                        d = divide((i == 0) ? x : __dsub_rn(x, __dmul_rn(negr, d)), pr_at(T, i));
+                        reg[i] = d;
+                        qmin = min(qmin, hi_abs(d) - 1u);
+                    }
+                } else if (r1 - r0 == kFlChunk) {  // a full chunk: straight-line, every address fixed
+                    const unsigned char* pk[8];  // this lane's swizzled 16-byte chunk k of a 128-byte line
+                    const unsigned char* hk[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) pk[k] = T + lane * 128 + ((k ^ sw) << 4), hk[k] = H + lane * 128 + ((k ^ sw) << 4);
+                    auto PRr = [&](int r) { return *reinterpret_cast<const double2*>(pk[r & 7] + (r >> 3) * 4096); };
+                    auto HBr = [&](int r) {
+                        return *reinterpret_cast<const double*>(hk[(r & 15) >> 1] + (r >> 4) * 4096 + (r & 1) * 8);
+                    };
+                    double* sp = st + 32 * (r0 - kFlRegRows);
+                    constexpr int A = 4;  // operands A rows ahead, each loaded before the store in front of it
+                    double2 pv[A];
+                    double hv[A], xv[A];
+#pragma unroll
+                    for (int u = 0; u < A; ++u) pv[u] = PRr(u), hv[u] = HBr(u), xv[u] = sp[32 * u];
+#pragma unroll
+                    for (int r = 0; r < kFlChunk; ++r) {
+                        const int u = r % A;
+                        const double x = __dadd_rn(xv[u], hv[u]);
+                        d = divide(__dsub_rn(x, __dmul_rn(negr, d)), pv[u]);
+                        if (r + A < kFlChunk) pv[u] = PRr(r + A), hv[u] = HBr(r + A), xv[u] = sp[32 * (r + A)];
+                        sp[32 * r] = d;
+                        qmin = min(qmin, hi_abs(d) - 1u);
+                    }
+                } else {  // (a partial last chunk)
+                    for (int i = r0; i < r1; ++i) {
+                        const double x = __dadd_rn(st[32 * (i - kFlRegRows)], v_at(H, i - r0));
+                        d = divide(__dsub_rn(x, __dmul_rn(negr, d)), pr_at(T, i - r0));
+                        st[32 * (i - kFlRegRows)] = d;
+                        qmin = min(qmin, hi_abs(d) - 1u);
+                    }
+                }
+            }
+            done_task();
+        }
+        // back substitution (linalg.cpp:91): x_{n-1} = q_{n-1}; x_i = q_i - c_i x_{i+1}
+        for (int c = nch - 1; c >= 0; --c) {
+            const unsigned char* T = wait_task();
+            const int r0 = c * kFlChunk, r1 = min(n - 2, r0 + kFlChunk - 1);  // rows r1 .. r0, top n - 2
+            if (act) {
+                if (r0 < kFlRegRows) {
+#pragma unroll
+                    for (int k = kFlRegRows - 1; k >= 0; --k) {
+                        d = __dsub_rn(reg[k], __dmul_rn(v_at(T, k), d));
+                        reg[k] = d;
+                    }
+                } else if (r1 - r0 == kFlChunk - 1) {  // a full chunk: straight-line, every address fixed
+                    const unsigned char* ck[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) ck[k] = T + lane * 128 + ((k ^ sw) << 4);
+                    auto CCr = [&](int r) {
+                        return *reinterpret_cast<const double*>(ck[(r & 15) >> 1] + (r >> 4) * 4096 + (r & 1) * 8);
+                    };
+                    double* sp = st + 32 * (r0 - kFlRegRows);
+                    constexpr int A = 8;
+                    double yv[A], cv[A];
+#pragma unroll
+                    for (int u = 0; u < A; ++u) yv[u] = sp[32 * (kFlChunk - 1 - u)], cv[u] = CCr(kFlChunk - 1 - u);
+#pragma unroll
+                    for (int r = kFlChunk - 1; r >= 0; --r) {
+                        const int u = (kFlChunk - 1 - r) % A;
+                        d = __dsub_rn(yv[u], __dmul_rn(cv[u], d));
+                        if (r - A >= 0) yv[u] = sp[32 * (r - A)], cv[u] = CCr(r - A);
+                        sp[32 * r] = d;
+                    }
+                } else {  // (a partial chunk: the top one, ending at row n - 2)
+                    for (int i = r1; i >= r0; --i) {
+                        d = __dsub_rn(st[32 * (i - kFlRegRows)], __dmul_rn(v_at(T, i - r0), d));
+                        st[32 * (i - kFlRegRows)] = d;
+                    }
+                }
+            }
+            done_task();
+        }
+    }
+    if (live) {
+        double* gp = P.maps + slice * n * P.ldm + n;
+#pragma unroll
+        for (int k = 0; k < kFlRegRows; ++k) gp[k * P.ldm] = reg[k];
+        for (int k = kFlRegRows; k < n; ++k) gp[k * P.ldm] = st[32 * (k - kFlRegRows)];
+        if (!kGuard && qmin < kQuotLo - 1u) record_failure(P.fail, kRetryIndex + slice, PINT_E_RANGE_RETRY, 0.0);
+        if (P.per_slice_ns) atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
+    }
+}
+
 // ---- integrate: K caller columns through consecutive steps of ONE slice ------------------------
 // The integrate closure (pde_problems.cpp:86-98) and run_serial (nievergelt.cpp:126-143): the same
 // bit-exact row recurrence as the build, one warp per 32 caller columns (lane = column; a single
@@ -1130,6 +1337,29 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
+// heat_forced_lanes_kernel's tensors: the slice-major records (record j * S + s at j S RS + s RS
+// doubles) seen per region as {16 doubles, slices, 16-double blocks, steps}
+int make_fl_maps(pint_ctx* ctx, BuildPlan& P) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return pint_set_error(ctx, PINT_E_CUDA, "heat_forced_lanes: cuTensorMapEncodeTiled unavailable");
+    const long long RS = record_stride(P.n);
+    const cuuint32_t e1[4] = {1, 1, 1, 1};
+    auto make = [&](CUtensorMap* m, long long off, long long blocks, cuuint32_t box_blocks) {
+        const cuuint64_t dims[4] = {16, static_cast<cuuint64_t>(P.N), static_cast<cuuint64_t>(blocks),
+                                    static_cast<cuuint64_t>(P.S)};
+        const cuuint64_t str[3] = {static_cast<cuuint64_t>(8 * P.S * RS), 128, static_cast<cuuint64_t>(8 * RS)};
+        const cuuint32_t box[4] = {16, 32, box_blocks, 1};
+        return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(P.rec + off), dims, str, box, e1,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    const long long nb = n16(P.n) / 16;
+    if (!make(&P.tm_pr, pr_offset(), 2 * nb, 8) || !make(&P.tm_hb, hb_offset(P.n), nb, 4) ||
+        !make(&P.tm_cc, cc_offset(P.n), nb, 4))
+        return pint_set_error(ctx, PINT_E_CUDA, "heat_forced_lanes: tensor map failed");
+    return PINT_OK;
+}
+
 // The kBasisGroup tiles: pr2 as [blocks][n16+1][64] doubles (box 2 x (n+1) x 1: one slice's
 // (-r, 0), (p, rcp) column) and c as [blocks][n16][32] doubles (box 2 x n x 1: two slices' c).
 int make_tile_maps(pint_ctx* ctx, BuildPlan& P) {
@@ -1243,11 +1473,46 @@ int launch_heat_build(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int6
 
 bool heat_build_segmentable(int64_t n) { return n >= 1 && !use_tmem(n); }
 
+// The TMEM build's forced columns: the lanes kernel above (PINT_FORCED_LANES=0: the in-CTA warp)
+bool tmem_forced_lanes(long long n) {
+    static const int v = [] {
+        const char* e = std::getenv("PINT_FORCED_LANES");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v != 0 && n > kFlRegRows + 2 && forced_lanes_smem(n) <= 227 * 1024;
+}
+
 void heat_build_prepare(int64_t n) {
     if (use_tmem(n)) {
         smem_attrs(heat_build_tmem_kernel<false>, 0);
         smem_attrs(heat_build_tmem_kernel<true>, 0);
+        smem_attrs(heat_forced_lanes_kernel<false>, 0);
+        smem_attrs(heat_forced_lanes_kernel<true>, 0);
     }
+}
+
+// heat_build_chain: the forced columns ahead of the chain (nothing may sit between the chain and
+// the build it waits on); returns PINT_OK without launching when the in-CTA warp builds them.
+int launch_heat_forced_first(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, const int64_t* step_off,
+                             const double* records, double* maps, unsigned long long* per_slice_ns, int guarded) {
+    if (!use_tmem(n) || !tmem_forced_lanes(n) || N == 0) return PINT_OK;
+    BuildPlan P{};
+    P.s_begin = 0;
+    P.s_end = S;
+    P.n = static_cast<int>(n);
+    P.N = static_cast<int>(N);
+    P.S = S;
+    P.wps = static_cast<int>((n + 31) / 32);
+    P.rec = records;
+    P.step_off = step_off;
+    P.maps = maps;
+    P.ldm = pint_affine_ldm(n);
+    P.per_slice_ns = per_slice_ns;
+    P.fail = ctx->d_fail;
+    if (const int rc = make_fl_maps(ctx, P)) return rc;
+    auto fk = guarded ? heat_forced_lanes_kernel<true> : heat_forced_lanes_kernel<false>;
+    fk<<<static_cast<unsigned>((N + 31) / 32), 32, forced_lanes_smem(n), ctx->stream>>>(P);
+    return pint_check_launch(ctx, "heat_forced_lanes_kernel");
 }
 
 int heat_build_ready_target(int64_t n) { return use_tmem(n) ? static_cast<int>(((n + 31) / 32 + 3) / 4) : 0; }
@@ -1281,16 +1546,32 @@ int launch_heat_build_steps(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, cons
         const size_t smem = sizeof(double) * tm_smem_doubles(n);
         auto kern = guarded ? heat_build_tmem_kernel<true> : heat_build_tmem_kernel<false>;
         smem_attrs(kern, smem);
+        int threads = 160;
+        if (tmem_forced_lanes(n) && P.only == 0) {
+            // the forced columns first, 32 slices a warp (heat_forced_lanes_kernel); the TMEM grid then
+            // runs 4 basis warps a CTA. With `ready` (the chain already waits on this stream) the
+            // caller has launched the forced kernel ahead of the chain: heat_build_chain.
+            if (!ready) {
+                auto fk = guarded ? heat_forced_lanes_kernel<true> : heat_forced_lanes_kernel<false>;
+                smem_attrs(fk, forced_lanes_smem(n));
+                BuildPlan F = P;
+                if (const int rc = make_fl_maps(ctx, F)) return rc;
+                fk<<<static_cast<unsigned>((N + 31) / 32), 32, forced_lanes_smem(n), ctx->stream>>>(F);
+                if (const int rc = pint_check_launch(ctx, "heat_forced_lanes_kernel")) return rc;
+            }
+            P.only = 1;
+            threads = 128;
+        }
         const long long ctas = N * ((P.wps + 3) / 4);
         if (!ready) {
-            kern<<<static_cast<unsigned>(ctas), 160, smem, ctx->stream>>>(P);
+            kern<<<static_cast<unsigned>(ctas), threads, smem, ctx->stream>>>(P);
             return pint_check_launch(ctx, "heat_build_tmem_kernel");
         }
         // signalling build: launched behind the waiting chain on the same stream, allowed to start
         // while it runs (programmatic stream serialization; the chain triggers at its start)
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(ctas), 1, 1);
-        cfg.blockDim = dim3(160, 1, 1);
+        cfg.blockDim = dim3(threads, 1, 1);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = ctx->stream;
         cudaLaunchAttribute attr[1];
