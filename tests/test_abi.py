@@ -97,37 +97,39 @@ def test_affine_ldm():
 def test_host_pool_back_to_back_jobs_from_threads():
     """The host thread pool behind the table fills (capi.cu HostPool): many back-to-back
     parallel_for jobs, from several caller threads at once, each result identical to a serial
-    reference — a worker waking late must never run a finished job's function."""
-    import ctypes as C
-    import threading
+    reference — a worker waking late must never run a finished job's function. (In a child
+    process: the pool's threads must not live in the pytest process, which later forks gloo ranks.)"""
+    import subprocess
+    import sys
 
-    dx, T, N = 1.0 / 129, 10.0, 512
-    dt = T / (N * 16)
-    dec = pint.decompose(0.0, T, N, dt)
-    arr = (capi.Slice * N)(*[s.c() for s in dec.slices])
-    Q = sum(s.steps for s in dec.slices)  # >= 4096 steps: the pool path
-
-    def fill():
-        off = np.empty(N + 1, dtype=np.int64)
-        r, fa, fb = (np.empty(Q) for _ in range(3))
-        sx = np.empty(128)
-        n = C.c_int64()
-        assert capi.load().pint_heat_coefficients(dx, arr, N, capi.ptr(off), capi.ptr(r), capi.ptr(fa),
-                                                  capi.ptr(fb), capi.ptr(sx), C.byref(n)) == 0
-        return r, fa, fb
-
-    ref = fill()
-    bad = []
-
-    def worker():
-        for _ in range(60):
-            got = fill()
-            if not all(np.array_equal(a, b) for a, b in zip(got, ref)):
-                bad.append(1)
-
-    ts = [threading.Thread(target=worker) for _ in range(4)]
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join()
-    assert not bad
+    code = r"""
+import ctypes as C, sys, threading
+import numpy as np
+sys.path.insert(0, ".")
+from paper_1304_6514_b200 import capi, pint
+dx, T, N = 1.0 / 129, 10.0, 512
+dt = T / (N * 16)
+dec = pint.decompose(0.0, T, N, dt)
+arr = (capi.Slice * N)(*[s.c() for s in dec.slices])
+Q = sum(s.steps for s in dec.slices)  # >= 4096 steps: the pool path
+def fill():
+    off = np.empty(N + 1, dtype=np.int64)
+    r, fa, fb = (np.empty(Q) for _ in range(3))
+    sx = np.empty(128)
+    n = C.c_int64()
+    assert capi.load().pint_heat_coefficients(dx, arr, N, capi.ptr(off), capi.ptr(r), capi.ptr(fa),
+                                              capi.ptr(fb), capi.ptr(sx), C.byref(n)) == 0
+    return r, fa, fb
+ref = fill()
+bad = []
+def worker():
+    for _ in range(60):
+        if not all(np.array_equal(a, b) for a, b in zip(fill(), ref)):
+            bad.append(1)
+ts = [threading.Thread(target=worker) for _ in range(4)]
+for t in ts: t.start()
+for t in ts: t.join()
+sys.exit(1 if bad else 0)
+"""
+    root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
+    subprocess.run([sys.executable, "-c", code], cwd=root, check=True, timeout=300)
