@@ -16,6 +16,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <pthread.h>
 #include <vector>
 
 #include "pint_internal.cuh"
@@ -95,7 +96,7 @@ class HostPool {
     unsigned size() const { return static_cast<unsigned>(workers_.size()) + 1; }
     void parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& fn) {
         const int64_t parts = std::min<int64_t>(n, size());
-        if (parts <= 1) {
+        if (parts <= 1 || forked_child().load()) {  // (a forked child has none of the workers)
             fn(0, n);
             return;
         }
@@ -117,9 +118,14 @@ class HostPool {
     }
 
   private:
+    static std::atomic<bool>& forked_child() {
+        static std::atomic<bool> f{false};
+        return f;
+    }
     HostPool() {
         const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
         for (unsigned i = 1; i < hw; ++i) workers_.emplace_back([this] { run(); });
+        pthread_atfork(nullptr, nullptr, [] { forked_child().store(true); });
     }
     ~HostPool() {
         {

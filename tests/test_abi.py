@@ -97,7 +97,8 @@ def test_affine_ldm():
 def test_host_pool_back_to_back_jobs_from_threads():
     """The host thread pool behind the table fills (capi.cu HostPool): many back-to-back
     parallel_for jobs, from several caller threads at once, each result identical to a serial
-    reference — a worker waking late must never run a finished job's function. (In a child
+    reference — a worker waking late must never run a finished job's function — and a fork of
+    the process runs the fill serially instead of waiting on workers it does not have. (In a child
     process: the pool's threads must not live in the pytest process, which later forks gloo ranks.)"""
     import subprocess
     import sys
@@ -129,7 +130,12 @@ def worker():
 ts = [threading.Thread(target=worker) for _ in range(4)]
 for t in ts: t.start()
 for t in ts: t.join()
-sys.exit(1 if bad else 0)
+import os
+pid = os.fork()  # a forked child has none of the pool's workers: it must run the fill serially
+if pid == 0:
+    os._exit(0 if all(np.array_equal(a, b) for a, b in zip(fill(), ref)) else 1)
+_, st = os.waitpid(pid, 0)
+sys.exit(1 if bad or st != 0 else 0)
 """
     root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
     subprocess.run([sys.executable, "-c", code], cwd=root, check=True, timeout=300)
