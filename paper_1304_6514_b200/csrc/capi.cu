@@ -261,7 +261,7 @@ int pint_ctx_create(int device, pint_ctx** out) {
     }
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaMalloc(&ctx->d_fail, sizeof(FailRec)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_fail, pint_ctx::kFailAlloc) != cudaSuccess ||
         cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
         cudaEventCreate(&ctx->evc) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
@@ -274,9 +274,12 @@ int pint_ctx_create(int device, pint_ctx** out) {
     }
     ctx->own_stream = true;
     FailRec init{pint_dev::kNoFail, 0, 0, 0.0};
+    cudaMemset(ctx->d_fail, 0, pint_ctx::kFailAlloc);
     cudaMemcpy(ctx->d_fail, &init, sizeof init, cudaMemcpyHostToDevice);
     cudaMemcpy(ctx->d_fail_serial, &init, sizeof init, cudaMemcpyHostToDevice);
-    if (cudaHostAlloc(&ctx->h_small, 256, cudaHostAllocDefault) != cudaSuccess) {
+    if (cudaHostAlloc(&ctx->h_small, 256, cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&ctx->h_mapped, 256, cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->d_mapped), ctx->h_mapped, 0) != cudaSuccess) {
         pint_ctx_destroy(ctx);
         return PINT_E_CUDA;
     }
@@ -295,6 +298,7 @@ void pint_ctx_destroy(pint_ctx* ctx) {
     if (ctx->d_fail) cudaFree(ctx->d_fail);
     if (ctx->d_fail_serial) cudaFree(ctx->d_fail_serial);
     if (ctx->h_small) cudaFreeHost(ctx->h_small);
+    if (ctx->h_mapped) cudaFreeHost(ctx->h_mapped);
     if (ctx->serial) cudaStreamDestroy(ctx->serial);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -737,20 +741,31 @@ int pint_run_scalar(pint_ctx* ctx, const pint_scalar_rhs* rhs, double t0, double
     double* d_w = cv.take<double>(Mn);
     double* d_lam = cv.take<double>(N);
     auto* d_ns = cv.take<unsigned long long>(N);
-    double* d_y = cv.take<double>(1);
-    auto* d_ext = cv.take<long long>(1);
+    // y, the extrapolation count and the sweep's span sit right behind the failure record: the
+    // call's small results come back in ONE copy
+    unsigned long long* d_small = ctx->d_small();
+    auto* d_y = reinterpret_cast<double*>(d_small);
+    auto* d_ext = reinterpret_cast<long long*>(d_small + 1);
     const auto* d_steps = reinterpret_cast<const int64_t*>(d_in);
     const auto* d_dt = reinterpret_cast<const double*>(d_in + b_steps);
     const void* d_nodes = d_in + b_steps + b_dt;
     const auto* d_ab = reinterpret_cast<const double*>(d_in + b_steps + b_dt + b_nodes);
 
-    cudaEventRecord(ctx->ev0, ctx->stream);
-    if (!ok(ctx, cudaMemcpyAsync(d_in, h_in, in_bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D inputs"))
-        return PINT_E_CUDA;
-    if (per_slice_seconds) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
     int rc = PINT_OK;
     const bool sweep = !serial && !f32;
-    if (sweep) {
+    // small runs (the paper's Table-3 shapes): ensemble, weights and the EXACT sweep in one launch,
+    // its inputs as kernel parameters and its results in mapped host memory (no copies)
+    const bool fused = sweep && sweep_mode == PINT_SWEEP_EXACT && !per_slice_seconds &&
+                       scalar_small_run_fits(rhs, N, M, weight_kind);
+    cudaEventRecord(ctx->ev0, ctx->stream);
+    if (!fused && !ok(ctx, cudaMemcpyAsync(d_in, h_in, in_bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D inputs"))
+        return PINT_E_CUDA;
+    if (per_slice_seconds) cudaMemsetAsync(d_ns, 0, sizeof(unsigned long long) * N, ctx->stream);
+    if (fused) {
+        rc = launch_scalar_small_run(ctx, rhs, N, M, t0, T, dt, nodes.data(), static_cast<double*>(d_ends), d_w,
+                                     weight_kind, a, b, y0, d_lam, ctx->d_mapped);
+        if (rc) return rc;
+    } else if (sweep) {
         // the weights depend on the nodes only: side stream, overlapping the ensemble
         cudaEventRecord(ctx->ev_fork, ctx->stream);
         cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
@@ -761,14 +776,17 @@ int pint_run_scalar(pint_ctx* ctx, const pint_scalar_rhs* rhs, double t0, double
         if (rc) return rc;
         cudaEventRecord(ctx->ev_join, ctx->side);
     }
-    rc = launch_scalar_ensemble(ctx, rhs, N, Mn, d_steps, d_dt, d_nodes, d_ends, per_slice_seconds ? d_ns : nullptr);
-    if (rc) return rc;
+    if (!fused) {
+        rc = launch_scalar_ensemble(ctx, rhs, N, Mn, d_steps, d_dt, d_nodes, d_ends,
+                                    per_slice_seconds ? d_ns : nullptr);
+        if (rc) return rc;
+    }
     long long ext = 0;
     double y = 0.0;
     if (serial) {
         if (!ok(ctx, cudaMemcpyAsync(d_y, d_ends, esz, cudaMemcpyDeviceToDevice, ctx->stream), "copy"))
             return PINT_E_CUDA;
-    } else {
+    } else if (!fused) {
         if (f32) return pint_set_error(ctx, PINT_E_INVALID, "FP32 runs support the ensemble only; sweep in FP64");
         cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);  // (the weights, from the side stream)
         cudaEventRecord(ctx->evc, ctx->stream);
@@ -778,16 +796,14 @@ int pint_run_scalar(pint_ctx* ctx, const pint_scalar_rhs* rhs, double t0, double
     }
     cudaEventRecord(ctx->ev1, ctx->stream);
     int64_t d2h = 0;
-    // y, the extrapolation count and the failure record land in the pinned small block: one batch
-    auto* hs = static_cast<char*>(ctx->h_small);
-    if (!ok(ctx, cudaMemcpyAsync(hs, d_y, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H y"))
+    // the failure record, y, the extrapolation count and the sweep span: ONE copy into the pinned
+    // small block
+    auto* hs = static_cast<char*>(fused ? ctx->h_mapped : ctx->h_small);
+    if (!fused &&
+        !ok(ctx, cudaMemcpyAsync(hs, ctx->d_fail, pint_ctx::kFailBlock, cudaMemcpyDeviceToHost, ctx->stream),
+            "D2H results"))
         return PINT_E_CUDA;
-    d2h += sizeof(double);
-    if (!serial) {
-        cudaMemcpyAsync(hs + 8, d_ext, sizeof ext, cudaMemcpyDeviceToHost, ctx->stream);
-        d2h += sizeof ext;
-    }
-    cudaMemcpyAsync(hs + 16, ctx->d_fail, sizeof(FailRec), cudaMemcpyDeviceToHost, ctx->stream);
+    d2h += pint_ctx::kFailBlock;  // (fused: written by the kernel into mapped host memory)
     if (endpoints_out) {
         cudaMemcpyAsync(endpoints_out, d_ends, esz * N * Mn, cudaMemcpyDeviceToHost, ctx->stream);
         d2h += esz * N * Mn;
@@ -802,11 +818,12 @@ int pint_run_scalar(pint_ctx* ctx, const pint_scalar_rhs* rhs, double t0, double
         cudaMemcpyAsync(ns.data(), d_ns, sizeof(unsigned long long) * N, cudaMemcpyDeviceToHost, ctx->stream);
     }
     if (!ok(ctx, cudaStreamSynchronize(ctx->stream), "run_scalar sync")) return PINT_E_CUDA;
-    std::memcpy(&y, hs, sizeof y);
-    if (!serial) std::memcpy(&ext, hs + 8, sizeof ext);
+    const char* hres = hs + pint_ctx::kSmallOff;
+    std::memcpy(&y, hres, sizeof y);
+    if (!serial) std::memcpy(&ext, hres + 8, sizeof ext);
     if (f32) y = static_cast<double>(*reinterpret_cast<float*>(&y));
     FailRec frec;
-    std::memcpy(&frec, hs + 16, sizeof frec);
+    std::memcpy(&frec, hs, sizeof frec);
     pint_fail fr{-1, 0, 0, 0.0};
     if (frec.index != pint_dev::kNoFail) {  // (rare) read it properly, which also clears it
         if ((rc = pint_fail_read(ctx, &fr))) return rc;
@@ -833,10 +850,16 @@ int pint_run_scalar(pint_ctx* ctx, const pint_scalar_rhs* rhs, double t0, double
         report->traj_steps = 0;
         for (int64_t j = 0; j < N; ++j) report->traj_steps += sl[j].steps * Mn;
         report->gpu_launches = ctx->launches - launches0;
-        report->h2d_bytes = static_cast<int64_t>(in_bytes);
+        report->h2d_bytes = static_cast<int64_t>(fused ? scalar_small_run_param_bytes() : in_bytes);
         report->d2h_bytes = d2h;
         float cms = 0.f;
-        if (!serial) cudaEventElapsedTime(&cms, ctx->evc, ctx->ev1);
+        if (fused) {
+            unsigned long long span[2];
+            std::memcpy(span, hres + 16, sizeof span);
+            cms = static_cast<float>(static_cast<double>(span[1] - span[0]) * 1e-6);
+        } else if (!serial) {
+            cudaEventElapsedTime(&cms, ctx->evc, ctx->ev1);
+        }
         report->compose_ms = cms;
         report->total_ms = wall.ms();
     }

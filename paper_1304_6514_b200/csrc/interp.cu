@@ -494,7 +494,8 @@ scalar_sweep_exact_kernel(long long N, long long M, const double* __restrict__ n
 // per lane, in parallel), the snap as a ballot (lowest lane = lowest node), and the reference-order
 // sums over the M terms by shuffles — every lane runs the same sums and gets the same y, so no
 // barrier and no broadcast between slices. Bit-identical to the 512-thread kernel above (same
-// operations in the same order); ~0.94 -> ~0.15 us per slice at M = 4.
+// operations in the same order); ~0.94 -> ~0.25 us per slice at M = 4. The slice itself is
+// pint_dev::slice_eval_small, shared with the one-launch small run (ensemble.cu).
 constexpr int kSmallM = 32;
 template <int MM>  // M rounded up to a power of 2: the sums run over MM terms, the pad ones -0.0
 __global__ void __launch_bounds__(32)
@@ -519,34 +520,12 @@ scalar_sweep_exact_small_kernel(long long N, long long M, const double* __restri
         }
     for (long long j = lane; j < N; j += 32) A[j] = a_arr[j * ab_stride], B[j] = b_arr[j * ab_stride];
     __syncwarp();
-    const bool live = lane < M;
     double y = y0;
     long long ext = 0;
     for (long long j = 0; j < N; ++j) {
         if (y < A[j] || y > B[j]) ++ext;  // nievergelt.cpp:83
         const long long so = node_stride ? j * M : 0;
-        const double xk = live ? X[so + lane] : 0.0, wk = live ? Wt[so + lane] : 0.0;
-        const double vk = live ? V[j * M + lane] : 0.0;
-        const double diff = __dsub_rn(y, xk);
-        const unsigned snap = __ballot_sync(0xffffffffu, live && fabs(diff) <= __dmul_rn(1e-14, fmax(1.0, fabs(xk))));
-        // (pad lanes: -0.0, the exact identity of a round-to-nearest sum: x + -0.0 == x for every x,
-        // +0.0 included, so the MM-term sums are the M-term sums bit for bit)
-        const double r = live ? __ddiv_rn(wk, diff) : -0.0;
-        const double rv = live ? __dmul_rn(r, vk) : -0.0;
-        if (snap) {  // node snap (interp.cpp:70-72): the lowest node's value
-            y = __shfl_sync(0xffffffffu, vk, __ffs(snap) - 1);
-        } else {
-            double num = 0.0, den = 0.0;  // num += r*v, den += r for k = 0..M-1, in order
-            double tn[MM], td[MM];
-#pragma unroll
-            for (int k = 0; k < MM; ++k) tn[k] = __shfl_sync(0xffffffffu, rv, k), td[k] = __shfl_sync(0xffffffffu, r, k);
-#pragma unroll
-            for (int k = 0; k < MM; ++k) {
-                num = __dadd_rn(num, tn[k]);
-                den = __dadd_rn(den, td[k]);
-            }
-            y = __ddiv_rn(num, den);
-        }
+        y = pint_dev::slice_eval_small<MM>(y, X + so, Wt + so, V + j * M, static_cast<int>(M), lane);
         if (lane == 0 && lambdas) lambdas[j] = y;
     }
     if (lane == 0) {
