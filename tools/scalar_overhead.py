@@ -48,7 +48,16 @@ def main():
     rows = [(0.5 / N, N, 4) for N in (32, 128)] + [(6.103515625e-05, N, 4) for N in (32, 64, 128)] + \
            [(1.52587890625e-05, N, 7) for N in (32, 64, 128)]
     for dt, N, M in rows:
-        print(f"run_scalar dt={dt:.3g} N={N} M={M} S={round(0.5 / dt / N)}: {med(lambda: call(dt, N, M), a.reps):.1f} us")
+        tot, dev = [], []
+
+        def rec():
+            call(dt, N, M)
+            tot.append(rep.total_ms * 1e3)
+            dev.append(rep.device_ms * 1e3)
+
+        w = med(rec, a.reps)
+        print(f"run_scalar dt={dt:.3g} N={N} M={M} S={round(0.5 / dt / N)}: {w:.1f} us "
+              f"(inside the C call {statistics.median(tot):.1f}, device events {statistics.median(dev):.1f})")
     h = torch.empty(64, dtype=torch.float64, pin_memory=True)
     d = torch.empty(64, dtype=torch.float64, device="cuda")
     s = torch.cuda.current_stream()

@@ -1,145 +1,65 @@
-// Per-slice cost of the one-warp EXACT sweep variants (M <= 8), clock64 around the slice loop.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -std=c++17 -I../include
-//        -I../paper_1304_6514_b200/csrc tools/sweep_micro.cu -o tools/_sweep_micro
-// V0: lane k = node k, __ddiv_rn, ballot + shuffles (pint_dev::slice_eval_small)
-// V2: lane k = node k, div_rn_scaled below (branch-free, scaled), ballot + shuffles
-// V7: a shuffle + add round alone; V8 / V9: one dependent __ddiv_rn / div_rn_scaled alone
-// Measured on B200 (cycles a slice, M = 4 / 7): V0 ~480 / 563, V2 481 / 619, V7 134, V8 136, V9 130;
-// every lane computing all M terms with div_rn_scaled (no shuffles, no ballot): 632 / 1343.
+// Section timing of the EXACT scalar sweep (clock64 marks compiled in with -DPINT_SWEEP_PROF):
+// thread 0's cycles per slice in {terms + barrier, ordered sum, barrier}.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -DPINT_SWEEP_PROF -std=c++17 \
+//        -Iinclude -Ipaper_1304_6514_b200/csrc tools/sweep_micro.cu -o tools/_sweep_micro
+//   tools/_sweep_micro N M
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
-#include <cmath>
 #include <vector>
 
-#include "pint_internal.cuh"
+#include "../paper_1304_6514_b200/csrc/interp.cu"
 
-// a / b for any b: both scaled by the power of 2 that brings |b| into [1, 2), then
-// pint_dev::div_rn_fast; ok cleared outside its window
-__device__ __forceinline__ double div_rn_scaled(double a, double b, bool& ok) {
-    const unsigned eb = (static_cast<unsigned>(__double2hiint(b)) >> 20) & 0x7ffu;
-    const double sc = __hiloint2double(static_cast<int>((2046u - eb) << 20), 0);
-    const double as = __dmul_rn(a, sc), bs = __dmul_rn(b, sc);
-    const unsigned ah = static_cast<unsigned>(__double2hiint(as)) & 0x7fffffffu;
-    ok &= (eb - 1u < 2045u) & (ah - ((1023u - 900u) << 20) < (1800u << 20));
-    return pint_dev::div_rn_fast(as, bs);
+int pint_set_error(pint_ctx*, int code, const std::string& msg) {
+    std::fprintf(stderr, "error %d: %s\n", code, msg.c_str());
+    return code;
+}
+int pint_check_launch(pint_ctx*, const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) std::fprintf(stderr, "%s: %s\n", what, cudaGetErrorString(e));
+    return e == cudaSuccess ? 0 : PINT_E_CUDA;
 }
 
-template <int MM, int V>
-__global__ void sweep(int N, int M, const double* X, const double* W, const double* Vals, double y0, double* lam,
-                      long long* cyc) {
-    extern __shared__ double sm[];  // (staged like the library kernels: X | W | V)
-    const int lane = threadIdx.x;
-    for (int i = lane; i < M; i += 32) sm[i] = X[i], sm[M + i] = W[i];
-    for (int i = lane; i < N * M; i += 32) sm[2 * M + i] = Vals[i];
-    __syncwarp();
-    X = sm;
-    W = sm + M;
-    Vals = sm + 2 * M;
-    const bool live = lane < M;
-    double y = y0;
-    const long long c0 = clock64();
-    for (int j = 0; j < N; ++j) {
-        const double* V_ = Vals + j * M;
-        if (V == 8 || V == 9) {  // one dependent quotient per slice: the division latency alone
-            bool ok = true;
-            const double d = __dsub_rn(y, 3.0);
-            y = V == 8 ? __ddiv_rn(1.5, d) : div_rn_scaled(1.5, d, ok);
-            if (!ok) y = 0.0;
-        } else if (V == 7) {  // the slice's adds and a shuffle round, no division
-            const double vk = live ? V_[lane] : 0.0;
-            const double rv = __dsub_rn(y, vk);
-            double num = 0.0;
-#pragma unroll
-            for (int k = 0; k < MM; ++k) num = __dadd_rn(num, __shfl_sync(0xffffffffu, rv, k));
-            y = __dmul_rn(num, 0.25);
-        } else if (V == 0) {
-            y = pint_dev::slice_eval_small<MM>(y, X, W, V_, M, lane);
-        } else {
-            const double xk = live ? X[lane] : 0.0, wk = live ? W[lane] : 0.0, vk = live ? V_[lane] : 0.0;
-            const double diff = __dsub_rn(y, xk);
-            const unsigned snap =
-                __ballot_sync(0xffffffffu, live && fabs(diff) <= __dmul_rn(1e-14, fmax(1.0, fabs(xk))));
-            double r;
-            bool ok = true;
-            if (V == 0) r = live ? __ddiv_rn(wk, diff) : -0.0;
-            else r = live ? div_rn_scaled(wk, diff, ok) : -0.0;
-            const double rv = live ? __dmul_rn(r, vk) : -0.0;
-            if (snap) {
-                y = __shfl_sync(0xffffffffu, vk, __ffs(snap) - 1);
-            } else {
-                double num = 0.0, den = 0.0;
-                double tn[MM], td[MM];
-#pragma unroll
-                for (int k = 0; k < MM; ++k)
-                    tn[k] = __shfl_sync(0xffffffffu, rv, k), td[k] = __shfl_sync(0xffffffffu, r, k);
-#pragma unroll
-                for (int k = 0; k < MM; ++k) {
-                    num = __dadd_rn(num, tn[k]);
-                    den = __dadd_rn(den, td[k]);
-                }
-                if (V == 0) {
-                    y = __ddiv_rn(num, den);
-                } else {
-                    const double q = div_rn_scaled(num, den, ok);
-                    const bool all = __all_sync(0xffffffffu, ok || !live);
-                    y = all ? q : __ddiv_rn(num, den);  // (not exact when a term was not: test only)
-                }
-            }
-        }
-        if (lane == 0) lam[j] = y;
+void* pint_scratch(pint_ctx*, int, size_t) { return nullptr; }
+void pint_kernel_attrs(const void* fn) { cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); }
+
+int main(int argc, char** argv) {
+    const int N = argc > 1 ? std::atoi(argv[1]) : 64;
+    const int M = argc > 2 ? std::atoi(argv[2]) : 1024;
+    std::vector<double> x(M), w(M), v(static_cast<size_t>(N) * M), ab{0.0, 1.25};
+    for (int k = 0; k < M; ++k) {
+        x[k] = 0.625 * (1.0 - std::cos(M_PI * k / (M - 1)));
+        w[k] = ((k & 1) ? -1.0 : 1.0) * ((k == 0 || k == M - 1) ? 0.5 : 1.0);
     }
-    if (lane == 0) *cyc = clock64() - c0;
-}
-
-template <int MM, int V>
-void run(int N, int M, const double* dX, const double* dW, const double* dV, double* dl, long long* dc,
-         std::vector<double>& out) {
-    for (int rep = 0; rep < 3; ++rep) sweep<MM, V><<<1, 32, 8 * (2 * M + N * M)>>>(N, M, dX, dW, dV, 1.0, dl, dc);
-    long long c;
-    cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
-    out.resize(N);
-    cudaMemcpy(out.data(), dl, 8 * N, cudaMemcpyDeviceToHost);
-    std::printf("  V%d MM=%d: %.0f cycles per slice\n", V, MM, double(c) / N);
-}
-
-int main() {
-    const int N = 512;
-    for (int M : {4, 7}) {
-        std::vector<double> x(M), w(M), v(N * M);
-        for (int k = 0; k < M; ++k) x[k] = 1.0 - std::cos(M_PI * k / (M - 1));  // [0, 2]
-        for (int k = 0; k < M; ++k) {
-            double acc = 1.0;
-            for (int j = 0; j < M; ++j)
-                if (j != k) acc /= (x[k] - x[j]);
-            w[k] = acc;
-        }
-        for (int j = 0; j < N; ++j)
-            for (int k = 0; k < M; ++k) v[j * M + k] = 0.1 + 0.9 * x[k] + 0.05 * std::sin(3 * x[k] + j);
-        double *dX, *dW, *dV, *dl;
-        long long* dc;
-        cudaMalloc(&dX, 8 * M);
-        cudaMalloc(&dW, 8 * M);
-        cudaMalloc(&dV, 8 * N * M);
-        cudaMalloc(&dl, 8 * N);
-        cudaMalloc(&dc, 8);
-        cudaMemcpy(dX, x.data(), 8 * M, cudaMemcpyHostToDevice);
-        cudaMemcpy(dW, w.data(), 8 * M, cudaMemcpyHostToDevice);
-        cudaMemcpy(dV, v.data(), 8 * N * M, cudaMemcpyHostToDevice);
-        std::printf("M = %d, N = %d\n", M, N);
-        std::vector<double> l0, l2;
-        if (M <= 4) {
-            run<4, 0>(N, M, dX, dW, dV, dl, dc, l0);
-            run<4, 2>(N, M, dX, dW, dV, dl, dc, l2);
-        } else {
-            run<8, 0>(N, M, dX, dW, dV, dl, dc, l0);
-            run<8, 2>(N, M, dX, dW, dV, dl, dc, l2);
-        }
-        std::printf("  V2 == V0: %d\n", l2 == l0);
-        std::vector<double> l8, l9, l7;
-        run<4, 8>(N, M, dX, dW, dV, dl, dc, l8);
-        run<4, 9>(N, M, dX, dW, dV, dl, dc, l9);
-        run<8, 7>(N, M, dX, dW, dV, dl, dc, l7);
-        std::printf("  V9 == V8: %d\n", l8 == l9);
+    for (size_t q = 0; q < v.size(); ++q) v[q] = 0.3 + 0.5 * x[q % M] * (1.0 - 0.1 * std::sin(0.01 * q));
+    double *d_x, *d_w, *d_v, *d_ab, *d_y;
+    long long* d_e;
+    cudaMalloc(&d_x, 8 * M);
+    cudaMalloc(&d_w, 8 * M);
+    cudaMalloc(&d_v, 8 * v.size());
+    cudaMalloc(&d_ab, 16);
+    cudaMalloc(&d_y, 8 * (N + 1));
+    cudaMalloc(&d_e, 8);
+    cudaMemcpy(d_x, x.data(), 8 * M, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_w, w.data(), 8 * M, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_v, v.data(), 8 * v.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(d_ab, ab.data(), 16, cudaMemcpyHostToDevice);
+    pint_ctx ctx{};
+    for (int rep = 0; rep < 3; ++rep) {
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, ctx.stream);
+        launch_scalar_sweep(&ctx, PINT_SWEEP_EXACT, N, M, d_x, 0, d_w, d_v, d_ab, d_ab + 1, 0, 0.1, d_y, d_y + N, d_e);
+        cudaEventRecord(e1, ctx.stream);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        unsigned long long p[3];
+        cudaMemcpyFromSymbol(p, g_sweep_prof, sizeof p);
+        std::printf("{\"N\": %d, \"M\": %d, \"ms\": %.4f, \"per_slice_cycles\": {\"terms\": %.0f, \"sum\": %.0f, "
+                    "\"barrier\": %.0f}, \"sum_cycles_per_term\": %.2f}\n",
+                    N, M, ms, double(p[0]) / N, double(p[1]) / N, double(p[2]) / N, double(p[1]) / N / M);
     }
     return 0;
 }
