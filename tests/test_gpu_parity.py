@@ -116,6 +116,19 @@ def test_small_run_one_launch_matches_separate_kernels(ctx, monkeypatch, prob, N
         assert np.array_equal(e1, want) and np.array_equal(l1, lo) and y1 == yo and x1 == eo
 
 
+@pytest.mark.parametrize("N,M,S,a,b", [(16, 512, 500, -3.0, 2.0), (4, 1024, 2000, 0.0, 2.0), (2, 7, 5000, -1.0, 2.0)])
+def test_riccati_early_seed_steps_bit_exact(ctx, N, M, S, a, b):
+    """Latency-bound ensembles take the early-seeded Riccati step (ensemble.cu step_fast_early: each
+    MUFU seed from an earlier approximation with the same high word, a mismatch redoing the
+    trajectory): every endpoint bit-exact against the oracle's reference step."""
+    dt = 0.5 / (N * S)
+    rc, y, ends, lam, _, _ = run_scalar(ctx, pint.make_model_problem(), N, dt, M, a, b, weights=capi.WEIGHTS_CLOSED2)
+    assert rc == 0
+    _, _, st, h = O.decompose(0.0, 0.5, N, dt)
+    want, _, _ = O.riccati_ensemble(st, h, O.cheb_nodes(M, a, b))
+    assert np.array_equal(ends, want)
+
+
 def test_small_run_failure_is_the_lowest_task(ctx):
     """NoRealRoot inside the one-launch small run: the lowest failing task index and its value,
     as the separate ensemble kernel reports them (exec_harness.hpp:88-99)."""
