@@ -403,6 +403,43 @@ __device__ __forceinline__ void tm_st1(unsigned addr, double v) {
                  : "memory");
 }
 
+#ifdef PINT_HEAT_PROF  // section timing for tools/heat_micro.cu only (never in the library build)
+__device__ unsigned long long g_heat_prof[1 << 14][6];
+__device__ unsigned long long g_heat_prof_f[1 << 10][6];  // forced grid
+__device__ unsigned long long g_heat_span[2][1 << 14][2];  // [forced][cta] = {start, end} globaltimer
+#define HEAT_PROF_MARK(k)                           \
+    do {                                            \
+        const long long t_ = clock64();             \
+        prof[k] += static_cast<unsigned long long>(t_ - t_prev); \
+        t_prev = t_;                                \
+    } while (0)
+#else
+#define HEAT_PROF_MARK(k) \
+    do {                  \
+    } while (0)
+#endif
+#ifdef PINT_HEAT_PROF
+// per-CTA segment cycles of thread 0's column (TMEM build): forward {reg, TMEM, shared} rows, back
+// {shared, TMEM, reg} rows
+__device__ unsigned long long g_heat_seg[1 << 14][8];
+#define HEAT_SEG_START long long seg_prev_ = clock64()
+#define HEAT_SEG_MARK(k)                                                            \
+    do {                                                                            \
+        if (threadIdx.x == 0) {                                                     \
+            const long long t_ = clock64();                                         \
+            g_heat_seg[blockIdx.x & 16383][k] += static_cast<unsigned long long>(t_ - seg_prev_); \
+            seg_prev_ = t_;                                                         \
+        }                                                                           \
+    } while (0)
+#else
+#define HEAT_SEG_START \
+    do {               \
+    } while (0)
+#define HEAT_SEG_MARK(k) \
+    do {                 \
+    } while (0)
+#endif
+
 // Forward rows [RR, RR + 16 nb) from TMEM (base row RR at column 0): chunk c + 1 is loaded while
 // chunk c is eliminated, (p, rcp) read kTmAhead rows ahead. Quotients are range-checked here.
 template <bool kGuard>
@@ -498,6 +535,7 @@ __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1],
     // RR == 0: row 0 goes through the generic x - negr*d with d = -0.0, where negr*d is +0 (negr
     // <= 0) and x - (+0) == x bit-for-bit (even for x = -0), so the loop needs no row-0 select
     double d = -0.0;
+    HEAT_SEG_START;
 #pragma unroll
     for (int i = 0; i < RR; ++i) {
         const double x = kForced ? __dadd_rn(reg[i], HB[i * kS]) : reg[i];
@@ -507,7 +545,9 @@ __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1],
     }
     dm1 = d;
     const int B = RR + (kTm ? kTmBody * tm_bodies : 0);  // first shared row
+    if (kTm) HEAT_SEG_MARK(0);
     if (kTm) tmem_forward<kGuard>(tm, tm_bodies, PR + RR, negr, d, qmin);
+    if (kTm) HEAT_SEG_MARK(1);
     const int last = n - 1 - B;  // last shared row (>= 0)
     const double2* pr = PR + B * kS;
     const double* hb = HB + B * kS;
@@ -542,6 +582,7 @@ __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1],
 #pragma unroll
     for (int u = 0; u < kFwdAhead - 1; ++u)
         if (r + u <= last) row(r + u, pv[u], xv[u], hv[u]);
+    if (kTm) HEAT_SEG_MARK(2);
     return d;
 }
 
@@ -559,6 +600,7 @@ __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], doub
     const double* CC = V.cc();
     const int B = RR + (kTm ? kTmBody * tm_bodies : 0);  // first shared row
     const int top = n - 2 - B;                           // first shared row of the back pass
+    HEAT_SEG_START;
     if (top >= 0) {
         double yv[kBackAhead], cv[kBackAhead];
         const double* cc = CC + B * kS;
@@ -587,29 +629,17 @@ __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], doub
         for (int u = 0; u < kBackAhead - 1; ++u)
             if (r - u >= 0) row(r - u, yv[u], cv[u]);
     }
+    if (kTm) HEAT_SEG_MARK(3);
     if (kTm) tmem_back(tm, tm_bodies, CC + RR, d, qmin);
+    if (kTm) HEAT_SEG_MARK(4);
 #pragma unroll
     for (int i = RR - 1; i >= 0; --i) {  // (RR > 0 only for n >= RR + 2: every register row is a back row)
         d = __dsub_rn(reg[i], __dmul_rn(CC[i * kS], d));  // (the register rows' quotients were checked
         reg[i] = d;                                         //  by column_forward, where they are made)
     }
+    if (kTm) HEAT_SEG_MARK(5);
 }
 
-#ifdef PINT_HEAT_PROF  // section timing for tools/heat_micro.cu only (never in the library build)
-__device__ unsigned long long g_heat_prof[1 << 14][6];
-__device__ unsigned long long g_heat_prof_f[1 << 10][6];  // forced grid
-__device__ unsigned long long g_heat_span[2][1 << 14][2];  // [forced][cta] = {start, end} globaltimer
-#define HEAT_PROF_MARK(k)                           \
-    do {                                            \
-        const long long t_ = clock64();             \
-        prof[k] += static_cast<unsigned long long>(t_ - t_prev); \
-        t_prev = t_;                                \
-    } while (0)
-#else
-#define HEAT_PROF_MARK(k) \
-    do {                  \
-    } while (0)
-#endif
 
 // 2-D/3-D tile copies (TMA tensor) of a slice's columns out of the slice-group blocks.
 __device__ __forceinline__ void tile_load(unsigned dst, const CUtensorMap* tm, int c0, int c1, int c2,
@@ -857,22 +887,30 @@ __global__ void __launch_bounds__(160, 1) heat_build_tmem_kernel(const __grid_co
     unsigned qmin = 0xffffffffu;
     const StagedStep<kBasis> SB{R, n, lane, 0};
     const StagedStep<kForcedSingle> SF{R, n, lane, 0};
+#ifdef PINT_HEAT_PROF
+    unsigned long long prof[6] = {0, 0, 0, 0, 0, 0};
+    long long t_prev = clock64();
+#endif
     if (wlive) {
         for (long long s = 0; s < steps; ++s) {
             const unsigned parity = static_cast<unsigned>(s & 1);
             mbar_wait(bar_f, parity);
+            HEAT_PROF_MARK(0);
             double d, dm1 = 0.0;
             if (forced) d = column_forward<RR, kForcedSingle, kGuard>(reg, st, SF, dm1, qmin);
             else d = column_forward<RR, kBasis, kGuard, 32, true>(reg, st, SB, dm1, qmin, tm, nb);
             qmin = min(qmin, hi_abs(d) - 1u);
+            HEAT_PROF_MARK(1);
             __syncwarp();
             if (lane == 0) {  // the last of the CTA's live warps to finish the forward half refills it
                 __threadfence_block();
                 if (atomicAdd(cnt, 1u) % nlive == static_cast<unsigned>(nlive - 1) && s + 1 < steps) load_fwd(s + 1);
             }
             mbar_wait(bar_b, parity);
+            HEAT_PROF_MARK(2);
             if (forced) column_back<RR, kForcedSingle>(reg, st, SF, d, dm1, qmin);
             else column_back<RR, kBasis, 32, true>(reg, st, SB, d, dm1, qmin, tm, nb);
+            HEAT_PROF_MARK(3);
             __syncwarp();
             if (lane == 0) {
                 __threadfence_block();
@@ -881,7 +919,15 @@ __global__ void __launch_bounds__(160, 1) heat_build_tmem_kernel(const __grid_co
                     if (s + 2 < steps) prefetch_l2(V.rec(slice, s + 2), 8u * static_cast<unsigned>(record_stride(n)));
                 }
             }
+            HEAT_PROF_MARK(4);
         }
+#ifdef PINT_HEAT_PROF
+        if (threadIdx.x == 0 && blockIdx.x < (1 << 14)) {
+            for (int q = 0; q < 5; ++q) g_heat_prof[blockIdx.x][q] = prof[q];
+            g_heat_span[0][blockIdx.x][0] = t_start;
+            g_heat_span[0][blockIdx.x][1] = pint_dev::globaltimer();
+        }
+#endif
         const bool live = forced ? lane == 0 : k < n;
         double* gp = P.maps + slice * n * P.ldm + k;
         if (live) {

@@ -21,6 +21,11 @@ int pint_check_launch(pint_ctx*, const char* what) {
     return e == cudaSuccess ? 0 : PINT_E_CUDA;
 }
 void* pint_scratch(pint_ctx*, int, size_t) { return nullptr; }
+void pint_kernel_attrs(const void* fn) {
+    cudaFuncAttributes a{};
+    cudaFuncGetAttributes(&a, fn);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - static_cast<int>(a.sharedSizeBytes));
+}
 extern "C" int64_t pint_affine_ldm(int64_t n) { return (n + 1 + 3) / 4 * 4; }
 
 int main(int argc, char** argv) {
@@ -108,6 +113,22 @@ int main(int argc, char** argv) {
             tot += acc[q] / cnt;
         }
         std::printf("  per-row=%.1f (worst warp %.1f)\n", tot / S / n, worst / S / n);
+    }
+    if (n >= 282) {  // TMEM build: thread 0's segments per step
+        std::vector<unsigned long long> seg(static_cast<size_t>(1 << 14) * 8);
+        cudaMemcpyFromSymbol(seg.data(), g_heat_seg, seg.size() * 8);
+        const int ctas = N * ((wps + 3) / 4);
+        const char* sn[6] = {"fwd_reg", "fwd_tmem", "fwd_smem", "back_smem", "back_tmem", "back_reg"};
+        double acc[6] = {0, 0, 0, 0, 0, 0};
+        for (int b = 0; b < ctas && b < (1 << 14); ++b)
+            for (int q = 0; q < 6; ++q) acc[q] += seg[b * 8 + q];
+        std::printf("TMEM segments, cycles per step (per row):");
+        const int rows[6] = {64, 256, n - 320, n - 320 - 1, 256, 64};
+        for (int q = 0; q < 6; ++q) {
+            const double c = acc[q] / ctas / S / 2;  // (two launches accumulate)
+            std::printf(" %s=%.0f (%.1f)", sn[q], c, c / rows[q]);
+        }
+        std::printf("\n");
     }
     return 0;
 }
