@@ -521,13 +521,18 @@ __device__ __forceinline__ void tmem_back(unsigned tm, int nb, const double* cc,
 // (every load is issued before the stores in front of it: the compiler cannot hoist a shared load
 // above a shared store it cannot disambiguate). Quotients are range-checked off the chain: the
 // register rows here, the shared rows in column_back. Returns q_{n-1}; dm1 = q_{n-2}.
-template <int RR, int kMode, bool kGuard, int kLS = lane_stride(kMode), bool kTm = false>
+template <int RR, int kMode, bool kGuard, int kLS = lane_stride(kMode), bool kTm = false, int kNs = 0>
 __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1], double* st,
                                                  const StagedStep<kMode>& V, double& dm1, unsigned& qmin,
                                                  unsigned tm = 0, int tm_bodies = 0) {
     constexpr int kS = StagedStep<kMode>::kS;
     constexpr bool kForced = StagedStep<kMode>::kForced;
-    const int n = V.n;
+    // kNs > 0: n known at compile time (the TMEM build at n = kNs), so the shared-row loops unroll
+    // completely and ptxas places every look-ahead load where it hides its latency (with a runtime
+    // trip count it sank a whole ring's refills to the end of each iteration, right in front of
+    // their first use: ~9 cycles a row)
+    const int n = kNs ? kNs : V.n;
+    if (kNs) tm_bodies = tm_rows(kNs) / kTmBody;
     const double negr = V.negr();
     const double2* PR = V.pr();
     const double* HB = V.hb();
@@ -569,7 +574,8 @@ __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1],
         st[kLS * rr] = d;
     };
     int r = 0;
-#pragma unroll 1
+    constexpr int kFwdUnroll = kNs ? (kNs - RR - tm_rows(kNs) + kFwdAhead) / kFwdAhead : 1;
+#pragma unroll kFwdUnroll
     for (; r + kFwdAhead - 1 <= last; r += kFwdAhead) {
 #pragma unroll
         for (int u = 0; u < kFwdAhead; ++u) {  // consume, then refill the slot in place
@@ -591,12 +597,13 @@ __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1],
 // forward quotients (zero wraps to the maximum, so exact zeros pass): a quotient below 2^-950
 // means its dividend may have left Markstein's range (one VIADDMNMX per row) — for the shared
 // rows here, as they are read back anyway; for the register rows in column_forward.
-template <int RR, int kMode, int kLS = lane_stride(kMode), bool kTm = false>
+template <int RR, int kMode, int kLS = lane_stride(kMode), bool kTm = false, int kNs = 0>
 __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], double* st, const StagedStep<kMode>& V,
                                             double d, double dm1, unsigned& qmin, unsigned tm = 0,
                                             int tm_bodies = 0) {
     constexpr int kS = StagedStep<kMode>::kSc;
-    const int n = V.n;
+    const int n = kNs ? kNs : V.n;  // (kNs: see column_forward)
+    if (kNs) tm_bodies = tm_rows(kNs) / kTmBody;
     const double* CC = V.cc();
     const int B = RR + (kTm ? kTmBody * tm_bodies : 0);  // first shared row
     const int top = n - 2 - B;                           // first shared row of the back pass
@@ -616,7 +623,8 @@ __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], doub
             st[kLS * rr] = d;
         };
         int r = top;
-#pragma unroll 1
+        constexpr int kBackUnroll = kNs ? (kNs - RR - tm_rows(kNs) + kBackAhead) / kBackAhead : 1;
+#pragma unroll kBackUnroll
         for (; r >= kBackAhead - 1; r -= kBackAhead) {
 #pragma unroll
             for (int u = 0; u < kBackAhead; ++u) {  // consume, then refill the slot in place
@@ -818,12 +826,12 @@ __global__ void __maxnreg__(255) heat_build_kernel(const __grid_constant__ Build
     if (!kForced) asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
-template <bool kGuard>
+template <bool kGuard, int kNs = 0>  // kNs > 0: built for n = kNs only (column_forward)
 __global__ void __launch_bounds__(160, 1) heat_build_tmem_kernel(const __grid_constant__ BuildPlan P) {
     constexpr int RR = kTmRegRows;
     extern __shared__ __align__(128) double smem[];
     const unsigned long long t_start = pint_dev::globaltimer();
-    const int n = P.n;
+    const int n = kNs ? kNs : P.n;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int cps = (P.wps + 3) / 4;  // CTAs per slice
     const long long slice = blockIdx.x / cps;
@@ -898,7 +906,7 @@ __global__ void __launch_bounds__(160, 1) heat_build_tmem_kernel(const __grid_co
             HEAT_PROF_MARK(0);
             double d, dm1 = 0.0;
             if (forced) d = column_forward<RR, kForcedSingle, kGuard>(reg, st, SF, dm1, qmin);
-            else d = column_forward<RR, kBasis, kGuard, 32, true>(reg, st, SB, dm1, qmin, tm, nb);
+            else d = column_forward<RR, kBasis, kGuard, 32, true, kNs>(reg, st, SB, dm1, qmin, tm, nb);
             qmin = min(qmin, hi_abs(d) - 1u);
             HEAT_PROF_MARK(1);
             __syncwarp();
@@ -909,7 +917,7 @@ __global__ void __launch_bounds__(160, 1) heat_build_tmem_kernel(const __grid_co
             mbar_wait(bar_b, parity);
             HEAT_PROF_MARK(2);
             if (forced) column_back<RR, kForcedSingle>(reg, st, SF, d, dm1, qmin);
-            else column_back<RR, kBasis, 32, true>(reg, st, SB, d, dm1, qmin, tm, nb);
+            else column_back<RR, kBasis, 32, true, kNs>(reg, st, SB, d, dm1, qmin, tm, nb);
             HEAT_PROF_MARK(3);
             __syncwarp();
             if (lane == 0) {
@@ -1532,6 +1540,8 @@ void heat_build_prepare(int64_t n) {
     if (use_tmem(n)) {
         smem_attrs(heat_build_tmem_kernel<false>, 0);
         smem_attrs(heat_build_tmem_kernel<true>, 0);
+        smem_attrs(heat_build_tmem_kernel<false, 512>, 0);
+        smem_attrs(heat_build_tmem_kernel<true, 512>, 0);
         smem_attrs(heat_forced_lanes_kernel<false>, 0);
         smem_attrs(heat_forced_lanes_kernel<true>, 0);
     }
@@ -1590,7 +1600,13 @@ int launch_heat_build_steps(pint_ctx* ctx, int64_t n, int64_t N, int64_t S, cons
     P.span = ready ? reinterpret_cast<unsigned long long*>(ready + ((N + 1) & ~1ll)) : nullptr;
     if (use_tmem(n)) {
         const size_t smem = sizeof(double) * tm_smem_doubles(n);
-        auto kern = guarded ? heat_build_tmem_kernel<true> : heat_build_tmem_kernel<false>;
+        static const bool static512 = [] {  // PINT_TM_STATIC=0: the runtime-n kernel at n = 512 too
+            const char* e = std::getenv("PINT_TM_STATIC");
+            return !e || std::atoi(e) != 0;
+        }();
+        auto kern = (n == 512 && static512)
+                        ? (guarded ? heat_build_tmem_kernel<true, 512> : heat_build_tmem_kernel<false, 512>)
+                        : (guarded ? heat_build_tmem_kernel<true> : heat_build_tmem_kernel<false>);
         smem_attrs(kern, smem);
         int threads = 160;
         if (tmem_forced_lanes(n) && P.only == 0) {
