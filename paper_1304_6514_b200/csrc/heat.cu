@@ -442,9 +442,14 @@ __device__ unsigned long long g_heat_seg[1 << 14][8];
 
 // Forward rows [RR, RR + 16 nb) from TMEM (base row RR at column 0): chunk c + 1 is loaded while
 // chunk c is eliminated, (p, rcp) read kTmAhead rows ahead. Quotients are range-checked here.
-template <bool kGuard>
+#ifndef PINT_TM_BODY_UNROLL
+#define PINT_TM_BODY_UNROLL 2
+#endif
+template <bool kGuard, int kNb = 0>  // kNb > 0: nb = kNb, the body loop unrolled PINT_TM_BODY_UNROLL times
 __device__ __forceinline__ void tmem_forward(unsigned tm, int nb, const double2* pr, double negr, double& d,
                                              unsigned& qmin) {
+    if (kNb) nb = kNb;
+    constexpr int kU = kNb ? PINT_TM_BODY_UNROLL : 1;
     auto divide = [&](double num, double2 p) { return kGuard ? div_guarded(num, p) : div_fast(num, p); };
     static_assert(kTmBody % kTmAhead == 0 && kTmBody % 16 == 0, "ring slots");
     double2 pv[kTmAhead];
@@ -454,7 +459,7 @@ __device__ __forceinline__ void tmem_forward(unsigned tm, int nb, const double2*
     tm_wait_st();  // the back pass's stores
     tm_ld(tm, A);
     tm_wait_ld(A);
-#pragma unroll 1
+#pragma unroll kU
     for (int b = 0; b < nb; ++b) {
 #pragma unroll
         for (int c = 0; c < kTmBody / 8; ++c) {
@@ -480,7 +485,10 @@ __device__ __forceinline__ void tmem_forward(unsigned tm, int nb, const double2*
 
 // Back substitution over the TMEM rows, last chunk first; cc = c of row RR; c read kBackAhead rows
 // ahead.
+template <int kNb = 0>  // (see tmem_forward)
 __device__ __forceinline__ void tmem_back(unsigned tm, int nb, const double* cc, double& d, unsigned& qmin) {
+    if (kNb) nb = kNb;
+    constexpr int kU = kNb ? PINT_TM_BODY_UNROLL : 1;
     static_assert(kTmBody % kBackAhead == 0 && kBackAhead == 8, "ring slots");
     const int nch = nb * (kTmBody / 8);
     double cv[8];
@@ -490,7 +498,7 @@ __device__ __forceinline__ void tmem_back(unsigned tm, int nb, const double* cc,
     tm_wait_st();  // the forward pass's stores
     tm_ld(tm + 16u * (nch - 1), A);
     tm_wait_ld(A);
-#pragma unroll 1
+#pragma unroll kU
     for (int b = 0; b < nb; ++b) {
 #pragma unroll
         for (int c = 0; c < kTmBody / 8; ++c) {
@@ -551,7 +559,7 @@ __device__ __forceinline__ double column_forward(double (&reg)[RR > 0 ? RR : 1],
     dm1 = d;
     const int B = RR + (kTm ? kTmBody * tm_bodies : 0);  // first shared row
     if (kTm) HEAT_SEG_MARK(0);
-    if (kTm) tmem_forward<kGuard>(tm, tm_bodies, PR + RR, negr, d, qmin);
+    if (kTm) tmem_forward<kGuard, kNs ? tm_rows(kNs) / kTmBody : 0>(tm, tm_bodies, PR + RR, negr, d, qmin);
     if (kTm) HEAT_SEG_MARK(1);
     const int last = n - 1 - B;  // last shared row (>= 0)
     const double2* pr = PR + B * kS;
@@ -638,7 +646,7 @@ __device__ __forceinline__ void column_back(double (&reg)[RR > 0 ? RR : 1], doub
             if (r - u >= 0) row(r - u, yv[u], cv[u]);
     }
     if (kTm) HEAT_SEG_MARK(3);
-    if (kTm) tmem_back(tm, tm_bodies, CC + RR, d, qmin);
+    if (kTm) tmem_back<kNs ? tm_rows(kNs) / kTmBody : 0>(tm, tm_bodies, CC + RR, d, qmin);
     if (kTm) HEAT_SEG_MARK(4);
 #pragma unroll
     for (int i = RR - 1; i >= 0; --i) {  // (RR > 0 only for n >= RR + 2: every register row is a back row)
