@@ -122,6 +122,18 @@ int main(int argc, char** argv) {
         double acc[6] = {0, 0, 0, 0, 0, 0};
         for (int b = 0; b < ctas && b < (1 << 14); ++b)
             for (int q = 0; q < 6; ++q) acc[q] += seg[b * 8 + q];
+        {  // CTA lifetime against its step loop (the last launch's spans; prof accumulates both)
+            std::vector<unsigned long long> span(2 * (1 << 14) * 2), pr(static_cast<size_t>(1 << 14) * 6);
+            cudaMemcpyFromSymbol(span.data(), g_heat_span, span.size() * 8);
+            cudaMemcpyFromSymbol(pr.data(), g_heat_prof, pr.size() * 8);
+            double life = 0, loop = 0;
+            for (int b = 0; b < ctas && b < (1 << 14); ++b) {
+                life += double(span[b * 2 + 1] - span[b * 2]);
+                for (int q = 0; q < 5; ++q) loop += double(pr[b * 6 + q]);
+            }
+            std::printf("CTA lifetime %.1f us, step loop %.1f us (at 1.965 GHz)\n", life / ctas * 1e-3,
+                        loop / ctas / 1.965e3);
+        }
         std::printf("TMEM segments, cycles per step (per row):");
         const int rows[6] = {64, 256, n - 320, n - 320 - 1, 256, 64};
         for (int q = 0; q < 6; ++q) {
