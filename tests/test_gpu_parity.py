@@ -496,12 +496,12 @@ def test_heat_large_n_build_paths(ctx, n):
         assert np.array_equal(G[j], Gw) and np.array_equal(c[j], cw)
 
 
-@pytest.mark.parametrize("n", [128, 300])
+@pytest.mark.parametrize("n", [128, 300, 512])
 def test_heat_underflow_retries_guarded(ctx, n):
     """dt = 1e-9: r ~ 2e-5 (n = 128), so a basis column decays like r^|i-k| and runs through the
     subnormal range inside the first step. The fast build must notice (range check off the chain
     -> PINT_E_RANGE_RETRY) and the guarded build must then match the reference bit-for-bit
-    (n = 300: the TMEM build's guarded variant)."""
+    (n = 300: the TMEM build's guarded variant; n = 512: its compile-time-n instance)."""
     import torch
 
     from paper_1304_6514_b200.dist import HeatPlan
