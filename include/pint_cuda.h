@@ -239,7 +239,10 @@ int pint_bilinear_sweep_dev(pint_ctx* ctx, int64_t N, int64_t Mu, int64_t Mv, co
 
 /* ---- full runs with HOST buffers (run_nievergelt, nievergelt.cpp:145-265) ---- */
 /* Scalar: decompose, sample nodes, K1, weights, K2 sweep. y_out[0] = final state.
- * endpoints_out (N*M, may be NULL) receives the ensemble; lambdas_out (N, may be NULL). */
+ * endpoints_out (N*M, may be NULL) receives the ensemble; lambdas_out (N, may be NULL).
+ * Small runs (FP64, EXACT sweep, M <= 32, N*M <= 8192, per_slice_seconds NULL) run as ONE kernel
+ * launch with no input copy (set PINT_SMALL_RUN=0 for the separate kernels); results and errors
+ * are identical either way. */
 int pint_run_scalar(pint_ctx* ctx, const pint_scalar_rhs* rhs, double t0, double T, double y0,
                     int64_t N, double dt, int node_kind, int64_t M, double a, double b,
                     int weight_kind, int sweep_mode, double* y_out, double* endpoints_out,
