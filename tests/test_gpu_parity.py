@@ -81,6 +81,7 @@ SMALL_RUNS = [  # (problem, N, S or dt, M, a, b, weights): the one-launch small 
     ("riccati", 124, 0.5 / (124 * 40), 8, 0.0, 2.0, capi.WEIGHTS_PRODUCT),   # N*M = 992, the limit
     ("riccati", 4, 1e-3, 5, 0.0, 0.5, capi.WEIGHTS_PRODUCT),                 # extrapolations
     ("riccati", 2, 0.01, 3, 0.0, 2.0, capi.WEIGHTS_CLOSED2),
+    ("riccati", 8, 1e-3, 1, 0.0, 2.0, capi.WEIGHTS_PRODUCT),                 # one node: every slice snaps
     ("riccati", 16, 1e-3, 6, -1.0, 2.0, capi.WEIGHTS_PRODUCT),
     ("riccati", 16, 1e-3, 17, 0.0, 2.0, capi.WEIGHTS_PRODUCT),
     ("riccati", 31, 0.5 / (31 * 20), 32, 0.0, 2.0, capi.WEIGHTS_CLOSED2),    # M = 32, the limit
