@@ -969,6 +969,9 @@ __global__ void __launch_bounds__(160, 1) heat_build_tmem_kernel(const __grid_co
             if (!kGuard && qmin < kQuotLo - 1u) record_failure(P.fail, kRetryIndex + slice, PINT_E_RANGE_RETRY, 0.0);
         }
         if (P.per_slice_ns && lane == 0) atomicAdd(P.per_slice_ns + slice, pint_dev::globaltimer() - t_start);
+#ifdef PINT_HEAT_PROF
+        if (threadIdx.x == 0 && blockIdx.x < (1 << 14)) g_heat_span[1][blockIdx.x][0] = pint_dev::globaltimer();  // epilogue end
+#endif
     }
     tm_wait_st();
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -984,6 +987,9 @@ __global__ void __launch_bounds__(160, 1) heat_build_tmem_kernel(const __grid_co
         atomicMin(P.span, t_start);
         atomicMax(P.span + 1, pint_dev::globaltimer());
     }
+#ifdef PINT_HEAT_PROF
+    if (threadIdx.x == 0 && blockIdx.x < (1 << 14)) g_heat_span[1][blockIdx.x][1] = pint_dev::globaltimer();  // CTA end
+#endif
 }
 
 // ---- forced columns apart (TMEM range): one lane per slice --------------------------------------

@@ -131,8 +131,21 @@ int main(int argc, char** argv) {
                 life += double(span[b * 2 + 1] - span[b * 2]);
                 for (int q = 0; q < 5; ++q) loop += double(pr[b * 6 + q]);
             }
-            std::printf("CTA lifetime %.1f us, step loop %.1f us (at 1.965 GHz)\n", life / ctas * 1e-3,
-                        loop / ctas / 1.965e3);
+            double epi = 0, tail = 0;
+            unsigned long long t0 = ~0ull, t1 = 0;
+            const size_t o = size_t(1) << 15;  // g_heat_span[1]: {epilogue end, CTA end}
+            for (int b = 0; b < ctas && b < (1 << 14); ++b) {
+                epi += double(span[o + b * 2] - span[b * 2 + 1]);
+                tail += double(span[o + b * 2 + 1] - span[o + b * 2]);
+                t0 = std::min(t0, span[b * 2]);
+                t1 = std::max(t1, span[o + b * 2 + 1]);
+            }
+            int sms = 0;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+            std::printf("CTA lifetime %.1f us, step loop %.1f us (at 1.965 GHz), epilogue %.1f us, dealloc+ready %.1f us; "
+                        "launch span %.3f ms = %.1f us per CTA slot on %d SMs\n", life / ctas * 1e-3,
+                        loop / ctas / 1.965e3, epi / ctas * 1e-3, tail / ctas * 1e-3, (t1 - t0) * 1e-6,
+                        (t1 - t0) * 1e-3 / (double(ctas) / sms), sms);
         }
         std::printf("TMEM segments, cycles per step (per row):");
         const int rows[6] = {64, 256, n - 320, n - 320 - 1, 256, 64};
